@@ -1,0 +1,194 @@
+/* geoshoot_b200.h — C ABI of the B200-native Euler–Poincaré N-particle hot path.
+ *
+ * The reference (arXiv 1510.03816, package `geoshoot`, /root/reference/pkg/src/geoshoot)
+ * is pure Python/NumPy and has no FFI or plugin registry: its drop-in boundary is the
+ * Python function API.  Each entry point below replaces one reference function; the
+ * Python shim `paper_1510_03816_b200` binds them with ctypes and re-exposes the
+ * reference signatures.
+ *
+ *   gs_rhs          <- geoshoot.particles.rhs            particles.py:109-117 (+ _interaction_terms :79-106)
+ *   gs_rhs_rows     <- rows [row0,row1) of the same (target-row sharding)
+ *   gs_hamiltonian  <- geoshoot.particles.hamiltonian    particles.py:120-131
+ *   gs_evolve       <- geoshoot.integrator.evolve        integrator.py:66-121
+ *   gs_match        <- geoshoot.shooting.match, momentum update branch
+ *                                                        shooting.py:218-301 (update :266-267)
+ *   gs_stage_*      <- one RK4 stage of integrator.py:98-114 for a row range; the
+ *                      building blocks of the multi-GPU driver (paper_1510_03816_b200/sharded.py)
+ *
+ * Conventions
+ *   - All arrays are fp64.  (n,2) arrays are C-order AoS (x0,y0,x1,y1,...) exactly as the
+ *     reference's NumPy arrays.  Pointers documented "device" must be device memory of the
+ *     context's GPU; "host" pointers are ordinary host memory.
+ *   - All GPU work is ordered on the caller's `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  Functions that must report a numerical outcome
+ *     (status, match result) synchronise that stream before returning; gs_rhs_async and
+ *     the gs_stage_* calls never synchronise.
+ *   - The library owns only the workspaces inside a gs_context; the caller owns every
+ *     buffer it passes.  One context per concurrent caller; no global mutable state
+ *     beyond a thread-local last-error string.
+ *   - Every function returns a GS_* code; numerical failures are also described in a
+ *     gs_status_t so the shim can rebuild the reference's exception messages:
+ *       GS_ERR_COINCIDENT      -> DegenerateConfigurationError  particles.py:92-98,
+ *                                 integrator.py:102-105 ("(during step k, t in [a, b])")
+ *       GS_ERR_NONFINITE_STAGE -> DivergenceError "non-finite intermediate at step k"
+ *                                 integrator.py:106-112
+ *       GS_ERR_NONFINITE_STATE -> DivergenceError "non-finite state at step k"
+ *                                 integrator.py:58-63
+ *       GS_ERR_INVALID         -> ConfigurationError / ValueError
+ */
+#ifndef GEOSHOOT_B200_H
+#define GEOSHOOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+
+#define GS_OK 0
+#define GS_ERR_INVALID 1
+#define GS_ERR_COINCIDENT 2
+#define GS_ERR_NONFINITE_STAGE 3
+#define GS_ERR_NONFINITE_STATE 4
+#define GS_ERR_CUDA 5
+#define GS_ERR_UNSUPPORTED 6
+
+/* kernels.py:44-47 KernelFamily (bessel is not provided on the device) */
+#define GS_FAMILY_CONICAL 0
+#define GS_FAMILY_GAUSSIAN 1
+
+/* pair-sum strategy */
+#define GS_PATH_AUTO 0   /* cell list when the support radius is small against the point cloud */
+#define GS_PATH_DENSE 1  /* all N^2 pairs, the reference's own semantics (no truncation) */
+#define GS_PATH_CELL 2   /* pairs with d_ij < cutoff only (KD-1: G(cutoff) = 2^-53) */
+
+/* shooting.py:56-63 */
+#define GS_STOP_TARGET_RESIDUAL 0
+#define GS_STOP_MOMENTUM_DELTA 1
+#define GS_NORM_MAX 0
+#define GS_NORM_L2 1
+
+/* match outcomes (MatchResult.converged / diagnosis, shooting.py:251-301) */
+#define GS_MATCH_CONVERGED 0
+#define GS_MATCH_CAP 1          /* "iteration cap reached before the stopping rule" */
+#define GS_MATCH_BLOWUP 2       /* "step too large" (non-finite or > 1e6 x initial norm) */
+#define GS_MATCH_EVOLVE_FAILED 3/* "step too large (<evolve exception>)", see status */
+
+/* SystemSpec + KernelSpec (particles.py:67-76, kernels.py:50-88) */
+typedef struct {
+    int32_t family;      /* GS_FAMILY_* */
+    int32_t normalized;  /* KernelSpec.normalized: G(0) = 1, else x 1/(2 pi alpha^2) */
+    double alpha;        /* KernelSpec.alpha > 0 */
+    double sigma2;       /* SystemSpec.sigma2 >= 0 */
+    double cutoff;       /* support radius for GS_PATH_CELL/AUTO; <= 0 disables the cell path */
+    int32_t path;        /* GS_PATH_* */
+    int32_t reserved;
+} gs_system_t;
+
+typedef struct {
+    int32_t code;        /* GS_* of the first failure */
+    int32_t step;        /* 1-based RK4 step of the failure (evolve / match), 0 otherwise */
+    int64_t i, j;        /* coincident pair, first in row-major order (GS_ERR_COINCIDENT) */
+    int32_t iteration;   /* match iteration whose shoot failed (0 = the initial zero-momentum shoot) */
+    int32_t event;       /* position of the failure inside its step, 0..7: 2s = coincidence in the RHS of
+                            stage s, 2s+1 = non-finite input of stage s+1, 7 = non-finite state; lets a
+                            multi-GPU driver order failures seen by different ranks */
+} gs_status_t;
+
+/* ShootingConfig (shooting.py:66-100) restricted to the momentum update */
+typedef struct {
+    double h;
+    double epsilon;
+    int32_t max_iter;
+    int32_t stop_rule;   /* GS_STOP_* */
+    int32_t norm;        /* GS_NORM_* */
+    int32_t steps;       /* EvolveConfig.steps */
+    double t_final;      /* EvolveConfig.t_final */
+} gs_match_config_t;
+
+typedef struct {
+    int32_t outcome;         /* GS_MATCH_* */
+    int32_t iterations;      /* len(residual_history) */
+    double hamiltonian;      /* H(q0, p0), particles.py:120-131 */
+    double final_residual;   /* _norm(target - endpoint) */
+    gs_status_t status;      /* evolve failure details when outcome == GS_MATCH_EVOLVE_FAILED */
+    double seconds_device;   /* device time of the whole match (CUDA events) */
+} gs_match_result_t;
+
+typedef struct gs_context gs_context;
+
+const char* gs_version(void);
+int gs_abi_version(void);
+const char* gs_last_error(void);
+
+int gs_create(gs_context** ctx, int device);
+int gs_destroy(gs_context* ctx);
+
+/* particles.rhs: dq, dp (device, n x 2) from q, p (device, n x 2).  Synchronises to fill status. */
+int gs_rhs(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
+           double* dq, double* dp, gs_status_t* status, void* stream);
+/* Rows [row0, row1) only: dq, dp are (row1-row0) x 2.  Does not synchronise; a coincidence is
+ * reported by the next gs_status_fetch on this context. */
+int gs_rhs_rows(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
+                int64_t row0, int64_t row1, double* dq, double* dp, void* stream);
+int gs_status_fetch(gs_context* ctx, gs_status_t* status, void* stream);
+int gs_status_reset(gs_context* ctx, void* stream);
+
+/* particles.hamiltonian: *h_out (host) = sum_ij (p_i . p_j) G(d_ij).  Synchronises. */
+int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
+                   double* h_out, void* stream);
+
+/* integrator.evolve: q, p (device, n x 2) are advanced in place over [0, t_final] with `steps`
+ * classical RK4 steps.  If capture_every > 0 and frames != NULL, frames (device) receives
+ * (1 + steps/capture_every + [steps % capture_every != 0]) records of n x 4 doubles
+ * (x, y, px, py) at the reference's capture times (integrator.py:84-86, 116-119).
+ * Synchronises; on failure q, p hold the state of the failing step (unspecified). */
+int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final, int32_t steps,
+              int32_t capture_every, double* q, double* p, double* frames, gs_status_t* status,
+              void* stream);
+
+/* shooting.match with UpdateSpace.MOMENTUM: q0, target (device, n x 2).  Outputs p0_out and
+ * endpoint_out (device, n x 2), history_out (host, >= max_iter doubles) and *result (host).
+ * The whole feedback loop runs on the device; the host reads two scalars per iteration
+ * (one persistent kernel for n <= 1024).  Synchronises. */
+int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* cfg, int64_t n,
+             const double* q0, const double* target, double* p0_out, double* endpoint_out,
+             double* history_out, gs_match_result_t* result, void* stream);
+
+/* ---- stage-level API (multi-GPU driver; one rank owns rows [row0, row1)) -----------------
+ * The context keeps a packed stage state S (n x 4: x, y, px, py, device) that every rank
+ * holds in full, plus the rank's own RK4 base/accumulator rows.
+ *   gs_stage_begin  : S <- (q, p) (device, n x 2, full), base rows <- S rows, resets status;
+ *                     S has room for n + 64 records (padding rows are zero) so that equal-size
+ *                     per-rank slices can be all-gathered in place
+ *   gs_stage_run    : one RK4 stage (0..3) of step `step` (1-based) for rows [row0,row1):
+ *                     evaluates the RHS of those rows against all n sources in S and writes
+ *                     the next stage input (or, after stage 3, the new state) into S's rows
+ *   gs_stage_state  : device pointer to S (n x 4 doubles), for the all-gather of S's rows
+ *   gs_stage_end    : copies the base rows out as (q, p) rows (device, (row1-row0) x 2)
+ */
+int gs_stage_begin(gs_context* ctx, int64_t n, const double* q, const double* p, int64_t row0,
+                   int64_t row1, void* stream);
+int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt,
+                 void* stream);
+double* gs_stage_state(gs_context* ctx);
+int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream);
+
+/* Profiling: with profiling enabled, every launch of the pair kernel (the dense or cell-list
+ * RHS sweep, or the persistent small-N kernel) is bracketed by CUDA events on its stream;
+ * gs_profile_read returns their summed device time (ms), the number of pair-kernel launches
+ * and of all kernel launches since the last reset.  Synchronises on the last event. */
+int gs_profile_enable(gs_context* ctx, int32_t on);
+int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int32_t reset);
+
+/* micro-benchmark used by bench.py for the FP64 roofline denominator: `iters` dependent
+ * DFMA chains per thread on a full grid; returns the device time in *ms (host). */
+int gs_fp64_peak_probe(gs_context* ctx, int32_t iters, double* ms, double* flops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEOSHOOT_B200_H */

@@ -1,0 +1,719 @@
+// gs_api.cu — C ABI of libgs_b200.so (include/geoshoot_b200.h).
+//
+// Host-side orchestration of the device path: argument validation with the reference's
+// error contract, workspaces owned by an opaque context, the RK4 stage loop
+// (integrator.py:95-119) and the feedback loop (shooting.py:259-301, momentum update).
+// The numerics all run in the kernels of gs_dense.cu / gs_small.cu / gs_cell.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/geoshoot_b200.h"
+#include "gs_kernels.cuh"
+
+using namespace gsb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define GS_CUDA(call)                                                                                   \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(GS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));               \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct gs_context {
+    int device = 0;
+    int sm_count = 148;
+    DevBuf<double> tbl;
+    DevBuf<DevStatus> st;
+    DevStatus* st_host = nullptr;   // pinned
+    double* scal_host = nullptr;    // pinned scratch (16 doubles)
+    // stage session
+    DevBuf<double4> S, B, A, part;
+    int64_t n = 0, row0 = 0, row1 = 0;
+    // match / reductions
+    DevBuf<double> q0, tgt, p, resid, red, ham, hist, scal;
+    DevBuf<SmallResult> small_res;
+    // profiling: CUDA events around every pair-kernel launch, kernel launch counter
+    int prof_on = 0;
+    std::vector<cudaEvent_t> prof_events;
+    size_t prof_used = 0;
+    long long launches = 0;
+    long long pair_launches = 0;
+};
+
+namespace {
+
+constexpr int kRedBlocks = 512;
+constexpr int64_t kStatePad = 64;  // spare records after S for equal-size all-gather slices
+
+int check_system(const gs_system_t* sys) {
+    if (!sys) return fail(GS_ERR_INVALID, "system is NULL");
+    if (sys->family != GS_FAMILY_CONICAL && sys->family != GS_FAMILY_GAUSSIAN)
+        return fail(GS_ERR_UNSUPPORTED, "kernel family not available on the device (conical, gaussian only)");
+    if (!(sys->alpha > 0.0) || !std::isfinite(sys->alpha))
+        return fail(GS_ERR_INVALID, "alpha must be positive");
+    if (!(sys->sigma2 >= 0.0) || !std::isfinite(sys->sigma2))
+        return fail(GS_ERR_INVALID, "sigma2 must be nonnegative");
+    if (sys->path != GS_PATH_AUTO && sys->path != GS_PATH_DENSE && sys->path != GS_PATH_CELL)
+        return fail(GS_ERR_INVALID, "unknown path");
+    return GS_OK;
+}
+
+SysConst make_const(const gs_system_t* sys) {
+    SysConst c;
+    c.fam = sys->family;
+    const double a = sys->alpha;
+    const double peak = sys->normalized ? 1.0 : 1.0 / (2.0 * M_PI * a * a);   // kernels.py:83-88
+    if (c.fam == kFamConical) {
+        c.k1 = -(double)kTbl / (a * kLn2);
+        c.scale_p = peak / a;
+    } else {
+        c.k1 = -(double)kTbl / (2.0 * a * a * kLn2);
+        c.scale_p = peak / (a * a);
+    }
+    c.scale_q = peak;
+    c.sigma2 = sys->sigma2;
+    c.cutoff = sys->cutoff;
+    return c;
+}
+
+// ---- small elementwise kernels -----------------------------------------------------------
+__global__ void k_pack(const double* __restrict__ q, const double* __restrict__ p, int64_t n, double4* S,
+                       DevStatus* st, int check) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double4 v = make_double4(q[2 * i], q[2 * i + 1], p[2 * i], p[2 * i + 1]);
+    S[i] = v;
+    if (check && !finite4(v.x, v.y, v.z, v.w)) record_event(st, 0ull, kNoEvent);
+}
+
+__global__ void k_copy_rows(const double4* __restrict__ S, int64_t row0, int64_t nrows, double4* B) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li < nrows) B[li] = S[row0 + li];
+}
+
+__global__ void k_unpack(const double4* __restrict__ B, int64_t nrows, double* q, double* p) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= nrows) return;
+    const double4 v = B[li];
+    q[2 * li] = v.x; q[2 * li + 1] = v.y;
+    if (p) { p[2 * li] = v.z; p[2 * li + 1] = v.w; }
+}
+
+__global__ void k_status_reset(DevStatus* st) {
+    st->first_event = kNoEvent;
+    st->pair_key = kNoEvent;
+}
+
+// match: p <- p + h r (shooting.py:266-267); S = B = (q0, p) (evolve's input copy, integrator.py:81-82)
+__global__ void k_match_begin(const double* __restrict__ q0, double* p, const double* __restrict__ resid, double h,
+                              int64_t n, double4* S, double4* B) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double px = p[2 * i], py = p[2 * i + 1];
+    if (h != 0.0) {
+        px = __dadd_rn(px, __dmul_rn(h, resid[2 * i]));
+        py = __dadd_rn(py, __dmul_rn(h, resid[2 * i + 1]));
+        p[2 * i] = px; p[2 * i + 1] = py;
+    }
+    const double4 v = make_double4(q0[2 * i], q0[2 * i + 1], px, py);
+    S[i] = v;
+    B[i] = v;
+}
+
+__device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
+
+// residual = target - endpoint (shooting.py:277) and per-block partial of the norm
+// (shooting.py:124-135).  `src` is either the evolved base state (B, stride 4) or an
+// endpoint array (stride 2).  Skipped when the evolve failed (endpoint keeps the last
+// finite shoot, shooting.py:271-276).
+__global__ void k_residual(const double* __restrict__ src, int stride, const double* __restrict__ tgt, int64_t n,
+                           double* endpoint, double* resid, int kind, double* red, DevStatus* st) {
+    __shared__ double s[256];
+    if (st && *((volatile unsigned long long*)&st->first_event) != kNoEvent) return;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double ex = src[stride * i], ey = src[stride * i + 1];
+        if (endpoint) { endpoint[2 * i] = ex; endpoint[2 * i + 1] = ey; }
+        const double rx = __dsub_rn(tgt[2 * i], ex), ry = __dsub_rn(tgt[2 * i + 1], ey);
+        resid[2 * i] = rx; resid[2 * i + 1] = ry;
+        if (kind == GS_NORM_MAX) acc = nanmax(acc, hypot(rx, ry));
+        else acc += __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry));
+    }
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (threadIdx.x < w)
+            s[threadIdx.x] = (kind == GS_NORM_MAX) ? nanmax(s[threadIdx.x], s[threadIdx.x + w])
+                                                   : s[threadIdx.x] + s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) red[blockIdx.x] = s[0];
+}
+
+// deterministic final reduction of `m` partials; kind: 0 max, 1 sum -> sqrt, 2 plain sum
+__global__ void k_reduce_final(const double* __restrict__ red, int m, int kind, double* out, DevStatus* st) {
+    __shared__ double s[512];
+    if (st && *((volatile unsigned long long*)&st->first_event) != kNoEvent) return;
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < m; t += blockDim.x) acc = (kind == 0) ? nanmax(acc, red[t]) : acc + red[t];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] = (kind == 0) ? nanmax(s[threadIdx.x], s[threadIdx.x + w]) : s[threadIdx.x] + s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = (kind == 1) ? sqrt(s[0]) : s[0];
+}
+
+__global__ void k_sum_partial(const double* __restrict__ v, int64_t n, double* red) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += v[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) red[blockIdx.x] = s[0];
+}
+
+__global__ void k_fp64_probe(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double m = 0.999999999, c = 1e-12;
+    for (int k = 0; k < iters; ++k) {
+        a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+        a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+    const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == 12345.678) out[0] = r;  // never true; keeps the chains alive
+}
+
+inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+int ensure_session(gs_context* ctx, int64_t n, int64_t nrows) {
+    const DensePlan plan = dense_plan(n, ctx->sm_count);
+    GS_CUDA(ctx->S.ensure(n + kStatePad));
+    GS_CUDA(ctx->B.ensure(nrows));
+    GS_CUDA(ctx->A.ensure(nrows));
+    GS_CUDA(ctx->part.ensure((size_t)plan.nchunks * nrows));
+    return GS_OK;
+}
+
+void decode_status(const DevStatus& d, int64_t n, gs_status_t* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->i = out->j = -1;
+    if (d.first_event == kNoEvent) { out->code = GS_OK; return; }
+    const unsigned long long step = d.first_event / 8, ev = d.first_event % 8;
+    out->step = (int32_t)step;
+    out->event = (int32_t)ev;
+    if (d.first_event == 0) out->code = GS_ERR_INVALID;
+    else if (ev % 2 == 0) {
+        out->code = GS_ERR_COINCIDENT;
+        out->i = (int64_t)(d.pair_key / (unsigned long long)n);
+        out->j = (int64_t)(d.pair_key % (unsigned long long)n);
+    } else if (ev == 7) out->code = GS_ERR_NONFINITE_STATE;
+    else out->code = GS_ERR_NONFINITE_STAGE;
+}
+
+int fetch_status(gs_context* ctx, cudaStream_t s, int64_t n, gs_status_t* out) {
+    GS_CUDA(cudaMemcpyAsync(ctx->st_host, ctx->st.ptr, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    gs_status_t tmp;
+    decode_status(*ctx->st_host, n, &tmp);
+    if (out) *out = tmp;
+    return tmp.code;
+}
+
+cudaEvent_t prof_event(gs_context* ctx) {
+    if (ctx->prof_used == ctx->prof_events.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->prof_events.push_back(e);
+    }
+    return ctx->prof_events[ctx->prof_used++];
+}
+
+// The pair kernel (the hot spot) of every RHS goes through here: timed when profiling is on.
+void pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
+                 const DensePlan& plan, double4* part, unsigned long long ev, cudaStream_t stream) {
+    if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+    launch_dense_partial(sc, S, n, row0, nrows, plan, part, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
+    if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+    ctx->launches++;
+    ctx->pair_launches++;
+}
+
+// One RK4 stage for the session's rows (dense partial + finish epilogue).
+void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cudaStream_t stream) {
+    const int64_t n = ctx->n, nrows = ctx->row1 - ctx->row0;
+    const DensePlan plan = dense_plan(n, ctx->sm_count);
+    const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)s;
+    pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
+    ctx->launches++;  // finish
+    FinishArgs fa{};
+    fa.part = ctx->part.ptr; fa.nchunks = plan.nchunks; fa.nrows = nrows; fa.row0 = ctx->row0;
+    fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr;
+    fa.stage = s; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
+    launch_finish(kFinStage, sc, fa, stream);
+}
+
+// integrator.py:95-119 over the session rows (single rank: rows = all).
+int run_evolve(gs_context* ctx, const SysConst& sc, double t_final, int steps, int capture_every, double* frames,
+               cudaStream_t stream) {
+    const double dt = t_final / steps;
+    const int64_t nrows = ctx->row1 - ctx->row0;
+    int f = 0;
+    if (capture_every > 0 && frames)
+        GS_CUDA(cudaMemcpyAsync(frames, ctx->B.ptr, nrows * sizeof(double4), cudaMemcpyDeviceToDevice, stream));
+    if (capture_every > 0) f = 1;
+    for (int step = 1; step <= steps; ++step) {
+        for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, stream);
+        if (capture_every > 0 && (step % capture_every == 0 || step == steps)) {
+            if (frames)
+                GS_CUDA(cudaMemcpyAsync(frames + (size_t)f * nrows * 4, ctx->B.ptr, nrows * sizeof(double4),
+                                        cudaMemcpyDeviceToDevice, stream));
+            ++f;
+        }
+    }
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int small_split(int64_t n) {
+    int split = 1;
+    while (split < 32 && n * split * 2 <= kSmallThreads) split *= 2;
+    return split;
+}
+
+bool use_small(const gs_system_t* sys, int64_t n) {
+    return n <= kSmallMax && sys->path != GS_PATH_CELL;
+}
+
+}  // namespace
+
+// ======================================================================================
+extern "C" {
+
+const char* gs_version(void) { return "geoshoot-b200 0.1.0 (sm_100a, fp64)"; }
+int gs_abi_version(void) { return GS_ABI_VERSION; }
+const char* gs_last_error(void) { return g_last_error.c_str(); }
+
+int gs_create(gs_context** out, int device) {
+    if (!out) return fail(GS_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    GS_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(GS_ERR_INVALID, "bad device ordinal");
+    GS_CUDA(cudaSetDevice(device));
+    gs_context* ctx = new gs_context();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    // 2^(j/256), j = 0..255, rounded from long double
+    std::vector<double> t(kTbl);
+    for (int j = 0; j < kTbl; ++j) t[j] = (double)exp2l((long double)j / (long double)kTbl);
+    cudaError_t e = ctx->tbl.ensure(kTbl);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->tbl.ptr, t.data(), kTbl * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = ctx->st.ensure(1);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->st_host, sizeof(DevStatus));
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->scal_host, 16 * sizeof(double));
+    if (e == cudaSuccess) e = ctx->scal.ensure(16);
+    if (e == cudaSuccess) e = ctx->small_res.ensure(1);
+    if (e != cudaSuccess) {
+        gs_destroy(ctx);
+        return fail(GS_ERR_CUDA, std::string("gs_create: ") + cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return GS_OK;
+}
+
+int gs_destroy(gs_context* ctx) {
+    if (!ctx) return GS_OK;
+    cudaSetDevice(ctx->device);
+    ctx->tbl.release(); ctx->st.release(); ctx->S.release(); ctx->B.release(); ctx->A.release();
+    ctx->part.release(); ctx->q0.release(); ctx->tgt.release(); ctx->p.release(); ctx->resid.release();
+    ctx->red.release(); ctx->ham.release(); ctx->hist.release(); ctx->scal.release(); ctx->small_res.release();
+    if (ctx->st_host) cudaFreeHost(ctx->st_host);
+    if (ctx->scal_host) cudaFreeHost(ctx->scal_host);
+    delete ctx;
+    return GS_OK;
+}
+
+int gs_status_reset(gs_context* ctx, void* stream) {
+    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
+    k_status_reset<<<1, 1, 0, (cudaStream_t)stream>>>(ctx->st.ptr);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_status_fetch(gs_context* ctx, gs_status_t* status, void* stream) {
+    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
+    const int rc = fetch_status(ctx, (cudaStream_t)stream, ctx->n > 0 ? ctx->n : 1, status);
+    return rc == GS_ERR_CUDA ? rc : GS_OK;
+}
+
+static int rhs_impl(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
+                    int64_t row0, int64_t row1, double* dq, double* dp, cudaStream_t s) {
+    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (n < 1 || !q || !p || !dq || !dp) return fail(GS_ERR_INVALID, "q and p must have shape (N, 2), N >= 1");
+    if (row0 < 0 || row1 > n || row0 > row1) return fail(GS_ERR_INVALID, "bad row range");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const int64_t nrows = row1 - row0;
+    if ((rc = ensure_session(ctx, n, nrows))) return rc;
+    ctx->n = n; ctx->row0 = row0; ctx->row1 = row1;
+    const SysConst sc = make_const(sys);
+    k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+    k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 1);
+    const DensePlan plan = dense_plan(n, ctx->sm_count);
+    pair_kernel(ctx, sc, ctx->S.ptr, n, row0, nrows, plan, ctx->part.ptr, 2ull, s);
+    ctx->launches += 3;  // reset, pack, finish
+    FinishArgs fa{};
+    fa.part = ctx->part.ptr; fa.nchunks = plan.nchunks; fa.nrows = nrows; fa.row0 = row0; fa.S = ctx->S.ptr;
+    fa.dq = dq; fa.dp = dp; fa.st = ctx->st.ptr; fa.event = 3ull;
+    launch_finish(kFinRhs, sc, fa, s);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_rhs_rows(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p, int64_t row0,
+                int64_t row1, double* dq, double* dp, void* stream) {
+    return rhs_impl(ctx, sys, n, q, p, row0, row1, dq, dp, (cudaStream_t)stream);
+}
+
+int gs_rhs(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p, double* dq,
+           double* dp, gs_status_t* status, void* stream) {
+    int rc = rhs_impl(ctx, sys, n, q, p, 0, n, dq, dp, (cudaStream_t)stream);
+    if (rc) return rc;
+    gs_status_t st;
+    rc = fetch_status(ctx, (cudaStream_t)stream, n, &st);
+    if (status) *status = st;
+    if (rc == GS_ERR_INVALID) return fail(rc, "state contains non-finite entries");
+    return rc;
+}
+
+int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
+                   double* h_out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !h_out) return fail(GS_ERR_INVALID, "NULL argument");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (n < 1 || !q || !p) return fail(GS_ERR_INVALID, "q and p must have shape (N, 2), N >= 1");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    if ((rc = ensure_session(ctx, n, n))) return rc;
+    GS_CUDA(ctx->ham.ensure(n));
+    GS_CUDA(ctx->red.ensure(kRedBlocks));
+    ctx->n = n; ctx->row0 = 0; ctx->row1 = n;
+    const SysConst sc = make_const(sys);
+    k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+    k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+    const DensePlan plan = dense_plan(n, ctx->sm_count);
+    // coincident pairs are irrelevant to H (particles.py:127-128 has no check): use an event id
+    // that is never reported
+    pair_kernel(ctx, sc, ctx->S.ptr, n, 0, n, plan, ctx->part.ptr, 2ull, s);
+    ctx->launches += 5;  // reset, pack, finish, 2 reductions
+    FinishArgs fa{};
+    fa.part = ctx->part.ptr; fa.nchunks = plan.nchunks; fa.nrows = n; fa.row0 = 0; fa.S = ctx->S.ptr;
+    fa.ham = ctx->ham.ptr; fa.st = ctx->st.ptr; fa.event = 0ull;  // never skipped
+    launch_finish(kFinHam, sc, fa, s);
+    const int nb = (int)std::min<int64_t>(kRedBlocks, (n + 255) / 256);
+    k_sum_partial<<<nb, 256, 0, s>>>(ctx->ham.ptr, n, ctx->red.ptr);
+    k_reduce_final<<<1, 512, 0, s>>>(ctx->red.ptr, nb, 2, ctx->scal.ptr, nullptr);
+    GS_CUDA(cudaMemcpyAsync(ctx->scal_host, ctx->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    *h_out = ctx->scal_host[0];
+    return GS_OK;
+}
+
+int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final, int32_t steps,
+              int32_t capture_every, double* q, double* p, double* frames, gs_status_t* status, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (n < 1 || !q || !p) return fail(GS_ERR_INVALID, "q and p must have shape (N, 2), N >= 1");
+    if (!(t_final > 0.0) || !std::isfinite(t_final)) return fail(GS_ERR_INVALID, "t_final must be positive");
+    if (steps < 1) return fail(GS_ERR_INVALID, "steps must be >= 1");
+    if (capture_every < 0) return fail(GS_ERR_INVALID, "capture_every must be >= 0");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const SysConst sc = make_const(sys);
+    ctx->n = n;
+    if (use_small(sys, n)) {
+        SmallArgs a{};
+        a.n = n; a.split = small_split(n); a.mode = 0; a.t_final = t_final; a.steps = steps;
+        a.capture_every = capture_every; a.q_in = q; a.p_in = p; a.q_out = q; a.p_out = p; a.frames = frames;
+        a.st = ctx->st.ptr;
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        launch_small(sc, a, ctx->tbl.ptr, s);
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        ctx->launches++;
+        ctx->pair_launches++;
+        GS_CUDA(cudaGetLastError());
+    } else {
+        if ((rc = ensure_session(ctx, n, n))) return rc;
+        ctx->row0 = 0; ctx->row1 = n;
+        ctx->launches += 4;  // reset, pack, copy, unpack
+        k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+        k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+        k_copy_rows<<<nblk(n), 256, 0, s>>>(ctx->S.ptr, 0, n, ctx->B.ptr);
+        if ((rc = run_evolve(ctx, sc, t_final, steps, capture_every, frames, s))) return rc;
+        k_unpack<<<nblk(n), 256, 0, s>>>(ctx->B.ptr, n, q, p);
+        GS_CUDA(cudaGetLastError());
+    }
+    gs_status_t st;
+    rc = fetch_status(ctx, s, n, &st);
+    if (status) *status = st;
+    return rc;
+}
+
+int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* cfg, int64_t n, const double* q0,
+             const double* target, double* p0_out, double* endpoint_out, double* history_out,
+             gs_match_result_t* result, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !cfg || !result || !history_out) return fail(GS_ERR_INVALID, "NULL argument");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (n < 1 || !q0 || !target || !p0_out || !endpoint_out)
+        return fail(GS_ERR_INVALID, "templates must have shape (N, 2), N >= 1");
+    if (!(cfg->h > 0.0) || !std::isfinite(cfg->h)) return fail(GS_ERR_INVALID, "h must be positive");
+    if (!(cfg->epsilon > 0.0) || !std::isfinite(cfg->epsilon)) return fail(GS_ERR_INVALID, "epsilon must be positive");
+    if (cfg->max_iter < 1) return fail(GS_ERR_INVALID, "max_iter must be >= 1");
+    if (cfg->steps < 1 || !(cfg->t_final > 0.0)) return fail(GS_ERR_INVALID, "bad evolve config");
+    if (sys->sigma2 > 0.0 && cfg->stop_rule != GS_STOP_MOMENTUM_DELTA)
+        return fail(GS_ERR_INVALID, "inexact matching (sigma2 > 0) cannot stop on the endpoint residual; "
+                                    "use stop_rule = MomentumDelta");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const SysConst sc = make_const(sys);
+    std::memset(result, 0, sizeof(*result));
+    result->status.i = result->status.j = -1;
+    cudaEvent_t e0, e1;
+    GS_CUDA(cudaEventCreate(&e0));
+    GS_CUDA(cudaEventCreate(&e1));
+    GS_CUDA(cudaEventRecord(e0, s));
+    ctx->n = n;
+
+    if (use_small(sys, n)) {
+        GS_CUDA(ctx->hist.ensure(cfg->max_iter));
+        SmallArgs a{};
+        a.n = n; a.split = small_split(n); a.mode = 1; a.t_final = cfg->t_final; a.steps = cfg->steps;
+        a.q_in = q0; a.target = target; a.q_out = endpoint_out; a.p_out = p0_out;
+        a.h = cfg->h; a.epsilon = cfg->epsilon; a.max_iter = cfg->max_iter; a.stop_rule = cfg->stop_rule;
+        a.norm = cfg->norm; a.history = ctx->hist.ptr; a.result = ctx->small_res.ptr; a.st = ctx->st.ptr;
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        launch_small(sc, a, ctx->tbl.ptr, s);
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        ctx->launches++;
+        ctx->pair_launches++;
+        GS_CUDA(cudaGetLastError());
+        GS_CUDA(cudaEventRecord(e1, s));
+        SmallResult r;
+        GS_CUDA(cudaMemcpyAsync(&r, ctx->small_res.ptr, sizeof(r), cudaMemcpyDeviceToHost, s));
+        GS_CUDA(cudaStreamSynchronize(s));
+        if (r.iterations > 0)
+            GS_CUDA(cudaMemcpy(history_out, ctx->hist.ptr, r.iterations * sizeof(double), cudaMemcpyDeviceToHost));
+        result->outcome = r.outcome;
+        result->iterations = r.iterations;
+        result->hamiltonian = r.hamiltonian;
+        result->final_residual = r.final_residual;
+        if (r.outcome == GS_MATCH_EVOLVE_FAILED) {
+            DevStatus d{r.fail_event, r.pair_key};
+            decode_status(d, n, &result->status);
+            result->status.iteration = r.fail_iter;
+        }
+    } else {
+        // host-driven loop, all state on the device, two scalars read back per iteration
+        if ((rc = ensure_session(ctx, n, n))) return rc;
+        GS_CUDA(ctx->q0.ensure(2 * n)); GS_CUDA(ctx->tgt.ensure(2 * n)); GS_CUDA(ctx->p.ensure(2 * n));
+        GS_CUDA(ctx->resid.ensure(2 * n)); GS_CUDA(ctx->red.ensure(kRedBlocks)); GS_CUDA(ctx->ham.ensure(n));
+        ctx->row0 = 0; ctx->row1 = n;
+        GS_CUDA(cudaMemcpyAsync(ctx->q0.ptr, q0, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        GS_CUDA(cudaMemcpyAsync(ctx->tgt.ptr, target, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        GS_CUDA(cudaMemsetAsync(ctx->p.ptr, 0, 2 * n * sizeof(double), s));
+        // initial shoot with p = 0 leaves q0 unchanged bitwise: endpoint = q0 (shooting.py:244-247)
+        const int nb = (int)std::min<int64_t>(kRedBlocks, (n + 255) / 256);
+        const int red_kind = cfg->norm == GS_NORM_MAX ? 0 : 1;
+        k_residual<<<nb, 256, 0, s>>>(ctx->q0.ptr, 2, ctx->tgt.ptr, n, endpoint_out, ctx->resid.ptr, cfg->norm,
+                                      ctx->red.ptr, nullptr);
+        k_reduce_final<<<1, 512, 0, s>>>(ctx->red.ptr, nb, red_kind, ctx->scal.ptr, nullptr);
+        GS_CUDA(cudaMemcpyAsync(ctx->scal_host, ctx->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, s));
+        GS_CUDA(cudaStreamSynchronize(s));
+        double nrm = ctx->scal_host[0];
+        double initial = nrm;
+        bool have_initial = cfg->stop_rule == GS_STOP_TARGET_RESIDUAL;
+        int outcome = GS_MATCH_CAP, iters = 0;
+        if (cfg->stop_rule == GS_STOP_TARGET_RESIDUAL && nrm < cfg->epsilon) {
+            outcome = GS_MATCH_CONVERGED;
+        } else {
+            for (int it = 0; it < cfg->max_iter; ++it) {
+                const double delta = cfg->h * nrm;
+                k_match_begin<<<nblk(n), 256, 0, s>>>(ctx->q0.ptr, ctx->p.ptr, ctx->resid.ptr, cfg->h, n, ctx->S.ptr,
+                                                      ctx->B.ptr);
+                ctx->launches += 4;  // begin, reset, residual, reduce
+                k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+                if ((rc = run_evolve(ctx, sc, cfg->t_final, cfg->steps, 0, nullptr, s))) return rc;
+                k_residual<<<nb, 256, 0, s>>>(reinterpret_cast<const double*>(ctx->B.ptr), 4, ctx->tgt.ptr, n,
+                                              endpoint_out, ctx->resid.ptr, cfg->norm, ctx->red.ptr, ctx->st.ptr);
+                k_reduce_final<<<1, 512, 0, s>>>(ctx->red.ptr, nb, red_kind, ctx->scal.ptr, ctx->st.ptr);
+                GS_CUDA(cudaMemcpyAsync(ctx->scal_host, ctx->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, s));
+                gs_status_t st;
+                rc = fetch_status(ctx, s, n, &st);  // synchronises
+                if (rc == GS_ERR_CUDA) return rc;
+                if (st.code != GS_OK) {
+                    outcome = GS_MATCH_EVOLVE_FAILED;
+                    result->status = st;
+                    result->status.iteration = it + 1;
+                    break;
+                }
+                nrm = ctx->scal_host[0];
+                const double value = cfg->stop_rule == GS_STOP_TARGET_RESIDUAL ? nrm : delta;
+                if (!have_initial) { initial = value; have_initial = true; }
+                history_out[it] = value;
+                iters = it + 1;
+                if (!std::isfinite(value) || (initial > 0.0 && value > 1e6 * initial)) { outcome = GS_MATCH_BLOWUP; break; }
+                if (value < cfg->epsilon) { outcome = GS_MATCH_CONVERGED; break; }
+            }
+        }
+        GS_CUDA(cudaMemcpyAsync(p0_out, ctx->p.ptr, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        GS_CUDA(cudaEventRecord(e1, s));
+        double H = 0.0;
+        if ((rc = gs_hamiltonian(ctx, sys, n, q0, p0_out, &H, stream))) return rc;
+        result->outcome = outcome;
+        result->iterations = iters;
+        result->hamiltonian = H;
+        result->final_residual = nrm;
+    }
+    GS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    result->seconds_device = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return GS_OK;
+}
+
+// ---- stage API ------------------------------------------------------------------------
+int gs_stage_begin(gs_context* ctx, int64_t n, const double* q, const double* p, int64_t row0, int64_t row1,
+                   void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !q || !p || n < 1 || row0 < 0 || row1 > n || row0 > row1) return fail(GS_ERR_INVALID, "bad stage args");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    int rc = ensure_session(ctx, n, row1 - row0);
+    if (rc) return rc;
+    ctx->n = n; ctx->row0 = row0; ctx->row1 = row1;
+    k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+    GS_CUDA(cudaMemsetAsync(ctx->S.ptr + n, 0, kStatePad * sizeof(double4), s));
+    k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+    if (row1 > row0) k_copy_rows<<<nblk(row1 - row0), 256, 0, s>>>(ctx->S.ptr, row0, row1 - row0, ctx->B.ptr);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt, void* stream) {
+    if (!ctx || ctx->n < 1) return fail(GS_ERR_INVALID, "no stage session");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (stg < 0 || stg > 3 || step < 1) return fail(GS_ERR_INVALID, "bad stage index");
+    stage(ctx, make_const(sys), step, stg, dt, (cudaStream_t)stream);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+double* gs_stage_state(gs_context* ctx) { return ctx ? reinterpret_cast<double*>(ctx->S.ptr) : nullptr; }
+
+int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream) {
+    if (!ctx || !q_rows) return fail(GS_ERR_INVALID, "bad stage args");
+    const int64_t nrows = ctx->row1 - ctx->row0;
+    if (nrows > 0) k_unpack<<<nblk(nrows), 256, 0, (cudaStream_t)stream>>>(ctx->B.ptr, nrows, q_rows, p_rows);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_profile_enable(gs_context* ctx, int32_t on) {
+    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
+    ctx->prof_on = on ? 1 : 0;
+    ctx->prof_used = 0;
+    return GS_OK;
+}
+
+int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int32_t reset) {
+    if (!ctx || !pair_ms || !pair_launches || !launches) return fail(GS_ERR_INVALID, "NULL argument");
+    double total = 0.0;
+    if (ctx->prof_used >= 2) {
+        GS_CUDA(cudaEventSynchronize(ctx->prof_events[ctx->prof_used - 1]));
+        for (size_t k = 0; k + 1 < ctx->prof_used; k += 2) {
+            float t = 0.f;
+            GS_CUDA(cudaEventElapsedTime(&t, ctx->prof_events[k], ctx->prof_events[k + 1]));
+            total += t;
+        }
+    }
+    *pair_ms = total;
+    *pair_launches = ctx->pair_launches;
+    *launches = ctx->launches;
+    if (reset) {
+        ctx->prof_used = 0;
+        ctx->pair_launches = 0;
+        ctx->launches = 0;
+    }
+    return GS_OK;
+}
+
+int gs_fp64_peak_probe(gs_context* ctx, int32_t iters, double* ms, double* flops, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !ms || !flops || iters < 1) return fail(GS_ERR_INVALID, "bad probe args");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const int blocks = ctx->sm_count * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    GS_CUDA(cudaEventCreate(&e0));
+    GS_CUDA(cudaEventCreate(&e1));
+    k_fp64_probe<<<blocks, threads, 0, s>>>(ctx->scal.ptr, iters);  // warm-up
+    GS_CUDA(cudaEventRecord(e0, s));
+    k_fp64_probe<<<blocks, threads, 0, s>>>(ctx->scal.ptr, iters);
+    GS_CUDA(cudaEventRecord(e1, s));
+    GS_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms = t;
+    *flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return GS_OK;
+}
+
+}  // extern "C"

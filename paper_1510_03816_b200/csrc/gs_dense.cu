@@ -1,0 +1,164 @@
+// gs_dense.cu — all-pairs (dense) fp64 RHS of the Euler–Poincaré N-particle system.
+//
+// Replaces particles._interaction_terms + rhs (particles.py:79-117) and the N x N
+// temporaries of kernels.pairwise_distances / kernel_value / kernel_derivative
+// (kernels.py:121-178): nothing of size N^2 is ever materialised.
+//
+// Grid: (row blocks of kDB targets) x (source chunks).  Each thread owns one target row,
+// keeps its (x, y, px, py) and four fp64 accumulators in registers, and sweeps its
+// chunk's sources through a shared-memory tile (kDT records of 32 B, read as warp-wide
+// broadcasts).  The chunk split gives the GPU enough CTAs at small N (N = 16384 has only
+// 128 row blocks) and is fixed by n alone, so a row's summation order — and its bits —
+// do not depend on how rows are sharded across GPUs.  Chunk partials are summed in chunk
+// order by the finish kernel, which also applies the kernel scale factors, the sigma2
+// term and the fused RK4 stage epilogue (integrator.py:98-114).
+//
+// Bound: FP64 pipe.  ~27 DP-pipe slots per ordered pair (2 DADD diff, 2 r^2, 5 rsqrt
+// refinement, 2 r*k1, 8 exp, 2 p.p, 4 accumulate, 2 coefficient) against the
+// libm formulation's 45.
+#include <algorithm>
+
+#include "gs_kernels.cuh"
+
+namespace gsb {
+
+DensePlan dense_plan(int64_t n, int sm_count) {
+    const int64_t row_blocks = (n + kDB - 1) / kDB;
+    const int64_t tiles = (n + kDT - 1) / kDT;
+    const int64_t want_ctas = (int64_t)sm_count * 32;
+    int64_t nc = (want_ctas + row_blocks - 1) / row_blocks;
+    nc = std::max<int64_t>(1, std::min(nc, tiles));
+    int64_t chunk_tiles = (tiles + nc - 1) / nc;
+    DensePlan p;
+    p.chunk = chunk_tiles * kDT;
+    p.nchunks = (int)((n + p.chunk - 1) / p.chunk);
+    return p;
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict__ S, int64_t n, int64_t row0,
+                                                       int64_t nrows, int64_t chunk, double k1,
+                                                       double4* __restrict__ part, DevStatus* st,
+                                                       unsigned long long event, const double* __restrict__ tbl_g) {
+    __shared__ double s_tbl[kTbl];
+    __shared__ double4 s_src[kDT];
+    if (*((volatile unsigned long long*)&st->first_event) < event) return;  // an earlier failure
+    for (int t = threadIdx.x; t < kTbl; t += kDB) s_tbl[t] = tbl_g[t];
+
+    const int64_t li = (int64_t)blockIdx.x * kDB + threadIdx.x;
+    const bool valid = li < nrows;
+    const int64_t i = row0 + (valid ? li : 0);
+    const double4 me = S[i];
+    const int64_t j0 = (int64_t)blockIdx.y * chunk;
+    const int64_t j1 = min(n, j0 + chunk);
+
+    double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
+    for (int64_t t0 = j0; t0 < j1; t0 += kDT) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kDT; t += kDB) {
+            const int64_t j = t0 + t;
+            s_src[t] = (j < j1) ? S[j] : make_double4(0.0, 0.0, 0.0, 0.0);  // zero records add exactly 0
+        }
+        __syncthreads();
+        const int m = (int)((j1 - t0) < kDT ? (j1 - t0) : kDT);
+        const int mr = (m + 3) & ~3;
+#pragma unroll 4
+        for (int jj = 0; jj < mr; ++jj) {
+            const double4 s = s_src[jj];
+            double pdot;
+            if (pair_accum<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, s_tbl, k1, aqx, aqy, apx, apy, pdot)) {
+                const int64_t j = t0 + jj;
+                if (valid && j != i && j < n && pdot != 0.0)
+                    record_event(st, event, (unsigned long long)(i * n + j));
+            }
+        }
+    }
+    if (valid) part[(int64_t)blockIdx.y * nrows + li] = make_double4(aqx, aqy, apx, apy);
+}
+
+void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
+                          const DensePlan& plan, double4* part, DevStatus* st, unsigned long long event,
+                          const double* tbl_dev, cudaStream_t stream) {
+    if (nrows <= 0) return;
+    dim3 grid((unsigned)((nrows + kDB - 1) / kDB), (unsigned)plan.nchunks);
+    if (sc.fam == kFamConical)
+        k_dense_partial<kFamConical><<<grid, kDB, 0, stream>>>(S, n, row0, nrows, plan.chunk, sc.k1, part, st,
+                                                                event, tbl_dev);
+    else
+        k_dense_partial<kFamGaussian><<<grid, kDB, 0, stream>>>(S, n, row0, nrows, plan.chunk, sc.k1, part, st,
+                                                                 event, tbl_dev);
+}
+
+// ---------------------------------------------------------------------------------------
+// Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_finish(SysConst sc, FinishArgs a) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= a.nrows) return;
+    if (*((volatile unsigned long long*)&a.st->first_event) < a.event) return;
+    const int64_t i = a.row0 + li;
+    double sqx = 0.0, sqy = 0.0, spx = 0.0, spy = 0.0;
+    for (int c = 0; c < a.nchunks; ++c) {
+        const double4 v = a.part[(int64_t)c * a.nrows + li];
+        sqx += v.x; sqy += v.y; spx += v.z; spy += v.w;
+    }
+    const double4 me = a.S[i];
+    // particles.py:113-116: dq = K p (+ sigma2 p), dp = -(sum_j a_ij (q_i - q_j))
+    double dqx = sqx * sc.scale_q, dqy = sqy * sc.scale_q;
+    if (sc.sigma2 != 0.0) {
+        dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
+        dqy = __dadd_rn(dqy, __dmul_rn(sc.sigma2, me.w));
+    }
+    const double dpx = spx * sc.scale_p, dpy = spy * sc.scale_p;
+    if (MODE == kFinRhs) {
+        a.dq[2 * li] = dqx; a.dq[2 * li + 1] = dqy;
+        a.dp[2 * li] = dpx; a.dp[2 * li + 1] = dpy;
+        return;
+    }
+    if (MODE == kFinHam) {
+        a.ham[li] = __dadd_rn(__dmul_rn(me.z, sqx * sc.scale_q), __dmul_rn(me.w, sqy * sc.scale_q));
+        return;
+    }
+    // RK4 stage epilogue in the reference's evaluation order (integrator.py:98-114):
+    //   stage inputs q + (0.5 dt) k_s, q + dt k_3; combine q + (dt/6) (((k1 + 2k2) + 2k3) + k4)
+    double4 b = a.B[li];
+    double4 acc;
+    double4 nxt;
+    if (a.stage == 0) {
+        acc = make_double4(dqx, dqy, dpx, dpy);
+    } else {
+        acc = a.A[li];
+        const double w = (a.stage == 3) ? 1.0 : 2.0;
+        acc.x = __dadd_rn(acc.x, __dmul_rn(w, dqx));
+        acc.y = __dadd_rn(acc.y, __dmul_rn(w, dqy));
+        acc.z = __dadd_rn(acc.z, __dmul_rn(w, dpx));
+        acc.w = __dadd_rn(acc.w, __dmul_rn(w, dpy));
+    }
+    if (a.stage < 3) {
+        const double c = (a.stage == 2) ? a.dt : 0.5 * a.dt;
+        nxt.x = __dadd_rn(b.x, __dmul_rn(c, dqx));
+        nxt.y = __dadd_rn(b.y, __dmul_rn(c, dqy));
+        nxt.z = __dadd_rn(b.z, __dmul_rn(c, dpx));
+        nxt.w = __dadd_rn(b.w, __dmul_rn(c, dpy));
+        a.A[li] = acc;
+    } else {
+        const double c = a.dt / 6.0;
+        nxt.x = __dadd_rn(b.x, __dmul_rn(c, acc.x));
+        nxt.y = __dadd_rn(b.y, __dmul_rn(c, acc.y));
+        nxt.z = __dadd_rn(b.z, __dmul_rn(c, acc.z));
+        nxt.w = __dadd_rn(b.w, __dmul_rn(c, acc.w));
+        a.B[li] = nxt;
+    }
+    a.S[i] = nxt;
+    if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
+}
+
+void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream) {
+    if (a.nrows <= 0) return;
+    const unsigned blocks = (unsigned)((a.nrows + 255) / 256);
+    if (mode == kFinRhs) k_finish<kFinRhs><<<blocks, 256, 0, stream>>>(sc, a);
+    else if (mode == kFinHam) k_finish<kFinHam><<<blocks, 256, 0, stream>>>(sc, a);
+    else k_finish<kFinStage><<<blocks, 256, 0, stream>>>(sc, a);
+}
+
+}  // namespace gsb

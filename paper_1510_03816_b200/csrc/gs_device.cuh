@@ -1,0 +1,120 @@
+// gs_device.cuh — fp64 pair-interaction math shared by every kernel of the B200 path.
+//
+// One ordered pair (i <- j) of the Euler–Poincaré RHS (particles.py:79-117):
+//   dq_i += G(d_ij) p_j
+//   dp_i += (p_i . p_j) (-G'(d_ij) / d_ij) (q_i - q_j)          (j != i, d_ij > 0)
+// accumulated in "raw" units; the per-row epilogue applies
+//   conical  G = exp(-r/alpha):        dq *= peak,  dp *= peak/alpha   (G'/r = -G/(alpha r))
+//   gaussian G = exp(-r^2/(2alpha^2)): dq *= peak,  dp *= peak/alpha^2 (G'/r = -G/alpha^2)
+// with peak = 1 (normalized) or 1/(2 pi alpha^2) (kernels.py:83-88, 129-136, 158-165).
+//
+// The reference evaluates exp twice per pair (kernel_value and kernel_derivative) and a
+// sqrt and a divide (kernels.py:130, 159; particles.py:100).  Here one pair costs one
+// MUFU.RSQ64H + one cubic refinement (r and 1/r), and ONE table-driven exp:
+//   2^(y/256) = T[k & 255] * 2^(k >> 8) * e^(u ln2/256),  k = rint(y), u = y - k in [-1/2, 1/2]
+// with a 256-entry table in shared memory and a degree-4 polynomial for e^x - 1 on
+// |x| <= ln2/512 (truncation 4e-17).  The whole exp is 3 DADD + 4 DFMA + 1 DMUL on the
+// FP64 pipe plus integer work; results agree with libm to a few ulp (tests/test_gpu_*.py).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gsb {
+
+constexpr int kFamConical = 0;
+constexpr int kFamGaussian = 1;
+
+constexpr int kTblBits = 8;
+constexpr int kTbl = 1 << kTblBits;
+constexpr double kLn2 = 0.69314718055994530941723212145818;
+constexpr double kC1 = kLn2 / kTbl;
+constexpr double kC2 = kC1 * kC1 / 2.0;
+constexpr double kC3 = kC1 * kC1 * kC1 / 6.0;
+constexpr double kC4 = kC1 * kC1 * kC1 * kC1 / 24.0;
+constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr int kKMin = -1020 * kTbl;                 // below: G underflows (flush to 0)
+
+constexpr uint64_t kNoEvent = ~0ull;
+
+// Device-side failure record.  `first_event` = step*8 + ev, ev in 0..7:
+//   ev = 2s   coincident interacting pair in the RHS of stage s   (particles.py:92-98)
+//   ev = 2s+1 non-finite input of stage s+1 (s < 3)               (integrator.py:106-112)
+//   ev = 7    non-finite state after the step                     (integrator.py:58-63)
+// Kernels of one launch share one event id and launches are stream-ordered, so the
+// first failure wins without a race; `pair_key` = i*n + j of the row-major-first pair.
+struct DevStatus {
+    unsigned long long first_event;
+    unsigned long long pair_key;
+};
+
+__device__ __forceinline__ double rsqrt_refined(double x) {
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+    // cubic correction: y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2
+    double h = x * y0;
+    double e = fma(-h, y0, 1.0);
+    double t = fma(e, 0.375, 0.5);
+    double ye = y0 * e;
+    return fma(ye, t, y0);
+}
+
+// 2^(y / kTbl) for y <= 0 (y = -r/alpha * kTbl/ln2); 0 below 2^-1020.
+__device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ tbl) {
+    double s = y + kRoundMagic;
+    double kd = s - kRoundMagic;
+    double u = y - kd;
+    int k = __double2loint(s);
+    int kc = max(k, kKMin);
+    double t = tbl[kc & (kTbl - 1)];
+    int n = kc >> kTblBits;
+    double tn = __hiloint2double(__double2hiint(t) + (n << 20), __double2loint(t));
+    double e1 = u * fma(fma(fma(kC4, u, kC3), u, kC2), u, kC1);
+    double g = fma(tn, e1, tn);
+    return (k < kKMin) ? 0.0 : g;
+}
+
+// Accumulates one ordered pair.  k1 = -kTbl/(alpha ln2) (conical, multiplies r) or
+// -kTbl/(2 alpha^2 ln2) (gaussian, multiplies r^2).  Returns true when d_ij == 0
+// (self pair or coincident particles): G(0)=1 enters dq, nothing enters dp, and the
+// caller checks the reference's "interacting coincident pair" condition with *pdot_out.
+template <int FAM>
+__device__ __forceinline__ bool pair_accum(double xi, double yi, double pxi, double pyi, double xj, double yj,
+                                           double pxj, double pyj, const double* __restrict__ tbl, double k1,
+                                           double& aqx, double& aqy, double& apx, double& apy,
+                                           double& pdot_out) {
+    double dx = xi - xj;
+    double dy = yi - yj;
+    double r2 = fma(dx, dx, dy * dy);
+    double pdot = fma(pxi, pxj, pyi * pyj);
+    bool z = (r2 == 0.0);
+    double g, c;
+    if (FAM == kFamConical) {
+        double r2s = z ? 1.0 : r2;
+        double rs = rsqrt_refined(r2s);
+        double r = r2s * rs;
+        g = exp2_tbl(r * k1, tbl);
+        g = z ? 1.0 : g;
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl(r2 * k1, tbl);   // exactly 1 at r2 == 0
+        c = pdot * g;
+    }
+    c = z ? 0.0 : c;
+    aqx = fma(g, pxj, aqx);
+    aqy = fma(g, pyj, aqy);
+    apx = fma(c, dx, apx);
+    apy = fma(c, dy, apy);
+    pdot_out = pdot;
+    return z;
+}
+
+__device__ __forceinline__ bool finite4(double a, double b, double c, double d) {
+    return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d);
+}
+
+__device__ __forceinline__ void record_event(DevStatus* st, unsigned long long event, unsigned long long key) {
+    atomicMin(&st->pair_key, key);
+    atomicMin(&st->first_event, event);
+}
+
+}  // namespace gsb

@@ -1,0 +1,96 @@
+// gs_kernels.cuh — kernel launchers shared between the translation units of libgs_b200.so.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gs_device.cuh"
+
+namespace gsb {
+
+// Derived per-system constants (host-computed once per call).
+struct SysConst {
+    int fam;
+    double k1;        // exponent scale, see pair_accum
+    double scale_q;   // peak (or 1)
+    double scale_p;   // peak/alpha (conical) or peak/alpha^2 (gaussian)
+    double sigma2;
+    double cutoff;    // > 0: truncate pairs with d >= cutoff (cell path)
+};
+
+// Dense tiling: DB targets per CTA (one per thread), DT sources per shared-memory tile.
+constexpr int kDB = 128;
+constexpr int kDT = 256;
+
+struct DensePlan {
+    int64_t chunk;    // sources per CTA column (multiple of kDT)
+    int nchunks;
+};
+DensePlan dense_plan(int64_t n, int sm_count);
+
+// RHS partial sums of rows [row0, row0+nrows) against all n sources of S, one
+// record (sum G p_j, sum c (q_i - q_j)) per (chunk, row): part[c * nrows + li].
+void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
+                          const DensePlan& plan, double4* part, DevStatus* st, unsigned long long event,
+                          const double* tbl_dev, cudaStream_t stream);
+
+// Finish modes
+constexpr int kFinRhs = 0;    // write dq, dp rows ((nrows, 2) AoS)
+constexpr int kFinStage = 1;  // RK4 stage epilogue (integrator.py:98-114)
+constexpr int kFinHam = 2;    // ham[li] = p_i . dq_i (sigma2 excluded)
+
+struct FinishArgs {
+    const double4* part;
+    int nchunks;
+    int64_t nrows, row0;
+    double4* S;        // stage state (all n rows)
+    double4* B;        // base rows (nrows)
+    double4* A;        // RK accumulator rows (nrows)
+    double* dq;        // kFinRhs
+    double* dp;
+    double* ham;       // kFinHam
+    int stage;
+    double dt;
+    DevStatus* st;
+    unsigned long long event;
+};
+void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream);
+
+// Small-N persistent kernel: a whole evolve or a whole match in one CTA (n <= kSmallMax).
+constexpr int kSmallMax = 512;
+constexpr int kSmallThreads = 512;
+
+struct SmallResult {
+    double hamiltonian;
+    double final_residual;
+    unsigned long long fail_event;   // kNoEvent if the shoots never failed
+    unsigned long long pair_key;
+    int outcome;                     // GS_MATCH_*
+    int iterations;
+    int fail_iter;
+    int pad;
+};
+
+struct SmallArgs {
+    int64_t n;
+    int split;             // lanes per target (power of two <= 32)
+    int mode;              // 0 evolve, 1 match
+    double t_final;
+    int steps;
+    int capture_every;
+    // evolve: q_in/p_in (n,2) in, q_out/p_out (n,2) out, frames (n x 4 per frame) or null
+    const double* q_in;
+    const double* p_in;
+    double* q_out;
+    double* p_out;
+    double* frames;
+    // match
+    const double* target;
+    double h, epsilon;
+    int max_iter, stop_rule, norm;
+    double* history;       // device, max_iter
+    SmallResult* result;   // device
+    DevStatus* st;         // evolve: failure record
+};
+void launch_small(const SysConst& sc, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream);
+
+}  // namespace gsb

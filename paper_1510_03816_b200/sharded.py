@@ -1,0 +1,258 @@
+"""Multi-GPU driver: target-row sharding with one all-gather of the stage state per RK stage.
+
+SURVEY.md §8(e).  Each rank (one process per GPU, ``torch.distributed`` over NCCL) owns the
+contiguous target rows [r0, r1) of an equal-size split (c = ceil(N / world) rows per rank,
+the last rank's tail padded), evaluates their RHS against all N sources with
+``gs_stage_run`` (the fused RHS + RK4 stage epilogue of csrc/gs_dense.cu), and the 32-byte
+(x, y, px, py) records of its rows are all-gathered so that every rank holds the next stage
+input in full.  The matching loop adds one scalar all-reduce per iteration (MAX for the
+max-norm, SUM for the squared L2 norm) and one SUM for H.
+
+Every row's sum runs over the same source chunks in the same order whatever the number of
+ranks (the chunking depends on N only), so 1/2/4/8-GPU results are bitwise identical.
+
+The orchestration is written against a small backend interface so that the same code runs
+on CPU (``gloo``) with a numpy stage backend in tests/test_sharded_gloo.py; the product
+backend is :class:`DeviceStageBackend` (libgs_b200.so).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native as N
+from . import device
+from . import errors as _errors
+
+STOP_RESIDUAL, STOP_MDELTA = "residual", "momentum-delta"
+
+
+def row_split(n: int, world: int, rank: int):
+    """Equal-size row blocks: rank owns [r0, r1) with c = ceil(n / world) rows (tail may be short)."""
+    c = (n + world - 1) // world
+    r0 = min(n, rank * c)
+    r1 = min(n, r0 + c)
+    return r0, r1, c
+
+
+def rhs_rows(spec, q, p, r0: int, r1: int):
+    """Rows [r0, r1) of particles.rhs on device tensors (gs_rhs_rows)."""
+    import torch
+
+    ctx = N.Context.get()
+    q = device.as_device(q, torch)
+    p = device.as_device(p, torch)
+    dq = torch.empty((r1 - r0, 2), dtype=torch.float64, device=q.device)
+    dp = torch.empty_like(dq)
+    sysc = device.system_struct(spec)
+    s = torch.cuda.current_stream().cuda_stream
+    N.check(ctx.lib.gs_rhs_rows(ctx.handle, ctypes.byref(sysc), q.shape[0], q.data_ptr(), p.data_ptr(), r0, r1,
+                                dq.data_ptr(), dp.data_ptr(), s), "gs_rhs_rows")
+    st = N.Status()
+    N.check(ctx.lib.gs_status_fetch(ctx.handle, ctypes.byref(st), s), "gs_status_fetch")
+    exc = device.status_exception(st)
+    if exc is not None:
+        raise exc
+    return dq, dp
+
+
+class DeviceStageBackend:
+    """gs_stage_* of libgs_b200.so on this rank's GPU."""
+
+    def __init__(self, spec):
+        import torch
+
+        self.torch = torch
+        self.ctx = N.Context.get()
+        self.sysc = device.system_struct(spec)
+        self.n = 0
+
+    def _s(self):
+        return self.torch.cuda.current_stream().cuda_stream
+
+    def begin(self, q, p, r0: int, r1: int):
+        torch = self.torch
+        q = device.as_device(q, torch)
+        p = device.as_device(p, torch)
+        self.n, self.r0, self.r1 = q.shape[0], r0, r1
+        N.check(self.ctx.lib.gs_stage_begin(self.ctx.handle, self.n, q.data_ptr(), p.data_ptr(), r0, r1, self._s()),
+                "gs_stage_begin")
+
+    def state(self, rows: int):
+        """(rows, 4) float64 CUDA tensor aliasing the library's stage state S (rows <= n + 64)."""
+        torch = self.torch
+        ptr = self.ctx.lib.gs_stage_state(self.ctx.handle)
+        n_pad = self.n + 64
+        assert rows <= n_pad
+        return _wrap_device_ptr(torch, ptr, (rows, 4))
+
+    def run(self, step: int, stage: int, dt: float):
+        N.check(self.ctx.lib.gs_stage_run(self.ctx.handle, ctypes.byref(self.sysc), step, stage, dt, self._s()),
+                "gs_stage_run")
+
+    def status(self) -> N.Status:
+        st = N.Status()
+        N.check(self.ctx.lib.gs_status_fetch(self.ctx.handle, ctypes.byref(st), self._s()), "gs_status_fetch")
+        return st
+
+
+def _wrap_device_ptr(torch, ptr: int, shape):
+    """Zero-copy float64 CUDA tensor over a library-owned device pointer."""
+    class _Holder:
+        pass
+
+    h = _Holder()
+    numel = int(np.prod(shape))
+    h.__cuda_array_interface__ = {"shape": (numel,), "typestr": "<f8", "data": (int(ptr), False), "version": 3}
+    return torch.as_tensor(h, device="cuda").view(*shape)
+
+
+def _event_key(st) -> tuple:
+    if st.code == N.GS_OK:
+        return (math.inf, 0, 0)
+    return (st.step * 8 + st.event, st.i, st.j)
+
+
+class ShardedSolver:
+    """Row-sharded evolve / match across the ranks of ``group`` (default: the world)."""
+
+    def __init__(self, spec, backend=None, group=None):
+        import torch.distributed as dist
+
+        self.spec = spec
+        self.backend = backend or DeviceStageBackend(spec)
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    # -- collectives (plumbing) -------------------------------------------------------------
+    def _allgather_rows(self, S, r0: int, c: int):
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(S[: c * self.world], S[r0:r0 + c].clone(), group=self.group)
+
+    def _allreduce(self, t, op):
+        if self.world > 1:
+            self.dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+    def _raise_first_failure(self, t_final, steps):
+        torch = _torch_of(self.backend)
+        st = self.backend.status()
+        key = _event_key(st)
+        if self.world > 1:
+            enc = torch.tensor([key[0] if key[0] != math.inf else 2.0**62, float(st.i), float(st.j), float(st.code),
+                                float(st.step), float(st.event)], dtype=torch.float64, device=_dev_of(self.backend))
+            allk = [torch.empty_like(enc) for _ in range(self.world)]
+            self.dist.all_gather(allk, enc, group=self.group)
+            rows = sorted(tuple(x.tolist()) for x in allk)
+            best = rows[0]
+            if best[0] >= 2.0**62:
+                return
+            st = N.Status(int(best[3]), int(best[4]), int(best[1]), int(best[2]), 0, int(best[5]))
+        exc = device.status_exception(st, t_final, steps)
+        if exc is not None:
+            raise exc
+
+    # -- integrator.evolve ------------------------------------------------------------------
+    def evolve(self, q, p, t_final: float, steps: int):
+        """Full (q, p) at t_final on every rank (integrator.py:66-121)."""
+        n = q.shape[0]
+        r0, r1, c = row_split(n, self.world, self.rank)
+        self.backend.begin(q, p, r0, r1)
+        S = self.backend.state(c * self.world)
+        dt = t_final / steps
+        for step in range(1, steps + 1):
+            for s in range(4):
+                self.backend.run(step, s, dt)
+                self._allgather_rows(S, r0, c)
+        self._raise_first_failure(t_final, steps)
+        return S[:n, 0:2].clone(), S[:n, 2:4].clone()
+
+    # -- shooting.match, momentum update ----------------------------------------------------
+    def match(self, q0, target, h: float, epsilon: float, max_iter: int, stop_rule: str = STOP_RESIDUAL,
+              norm: str = "max", t_final: float = 1.0, steps: int = 20) -> dict:
+        torch = _torch_of(self.backend)
+        dev = _dev_of(self.backend)
+        q0 = torch.as_tensor(np.asarray(q0) if not isinstance(q0, torch.Tensor) else q0, dtype=torch.float64,
+                             device=dev)
+        target = torch.as_tensor(np.asarray(target) if not isinstance(target, torch.Tensor) else target,
+                                 dtype=torch.float64, device=dev)
+        n = q0.shape[0]
+        r0, r1, _ = row_split(n, self.world, self.rank)
+        p = torch.zeros_like(q0)
+        endpoint = q0.clone()  # evolve(q0, 0) == q0 exactly
+        residual = target - endpoint
+
+        def norm_of(res):
+            rows = res[r0:r1]
+            if norm == "max":
+                v = torch.hypot(rows[:, 0], rows[:, 1]).max() if r1 > r0 else torch.zeros((), dtype=torch.float64,
+                                                                                          device=dev)
+                return float(self._allreduce(v.reshape(1), self.dist.ReduceOp.MAX if self.world > 1 else None)[0])
+            v = (rows * rows).sum().reshape(1)
+            return math.sqrt(float(self._allreduce(v, self.dist.ReduceOp.SUM if self.world > 1 else None)[0]))
+
+        history = []
+        nrm = norm_of(residual)
+        initial = nrm if stop_rule == STOP_RESIDUAL else None
+        diagnosis, converged = None, False
+        if stop_rule == STOP_RESIDUAL and nrm < epsilon:
+            converged = True
+        else:
+            diagnosis = "iteration cap reached before the stopping rule"
+            for _ in range(max_iter):
+                delta = h * nrm
+                p = p + h * residual
+                try:
+                    qT, _ = self.evolve(q0, p, t_final, steps)
+                except (_errors.DivergenceError, _errors.DegenerateConfigurationError) as exc:
+                    diagnosis = f"step too large ({exc})"
+                    break
+                endpoint = qT
+                residual = target - endpoint
+                nrm = norm_of(residual)
+                value = nrm if stop_rule == STOP_RESIDUAL else delta
+                if initial is None:
+                    initial = value
+                history.append(value)
+                if not math.isfinite(value) or (initial > 0 and value > 1e6 * initial):
+                    diagnosis = "step too large"
+                    break
+                if value < epsilon:
+                    diagnosis, converged = None, True
+                    break
+        H = self.hamiltonian(q0, p)
+        return dict(p0=p, endpoint=endpoint, iterations=len(history), converged=converged,
+                    residual_history=tuple(history), hamiltonian=H, final_residual=nrm, diagnosis=diagnosis)
+
+    def hamiltonian(self, q, p) -> float:
+        """particles.hamiltonian: this rank's rows of p_i . (K p)_i, SUM-reduced."""
+        torch = _torch_of(self.backend)
+        n = q.shape[0]
+        r0, r1, _ = row_split(n, self.world, self.rank)
+        part = self.backend.hamiltonian_rows(self.spec, q, p, r0, r1) if hasattr(self.backend, "hamiltonian_rows") \
+            else _device_hamiltonian_rows(self.spec, q, p, r0, r1)
+        t = torch.tensor([part], dtype=torch.float64, device=_dev_of(self.backend))
+        return float(self._allreduce(t, self.dist.ReduceOp.SUM if self.world > 1 else None)[0])
+
+
+def _device_hamiltonian_rows(spec, q, p, r0, r1) -> float:
+    if r1 <= r0:
+        return 0.0
+    dq, _ = rhs_rows(device._plain_spec(spec), q, p, r0, r1)
+    pr = device.as_device(p)[r0:r1]
+    return float((pr * dq).sum())
+
+
+def _torch_of(backend):
+    import torch
+
+    return torch
+
+
+def _dev_of(backend):
+    return getattr(backend, "device", "cuda")

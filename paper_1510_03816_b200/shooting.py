@@ -1,0 +1,214 @@
+"""Feedback-control geodesic shooting on the B200 (mirror of geoshoot/shooting.py:33-320).
+
+``match`` with ``UpdateSpace.MOMENTUM`` — the update of BASELINE.json's north_star,
+p0 <- p0 + h (Y - X(T)) (shooting.py:266-267) — runs entirely in libgs_b200.so: the
+initial shoot, every RK4 stage, the residual, its norm, the update and both stop rules,
+with one persistent kernel for N <= 512 and a device loop reading two scalars per
+iteration above that.  ``UpdateSpace.VELOCITY`` (the reference default) keeps the
+reference's host Gram/Cholesky solve between device shoots (SURVEY.md §8(f1) moves it
+to the device next).
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import device
+from . import errors as _errors
+from . import types as _types
+from .integrator import EvolveConfig
+from .kernels import family_name
+from .particles import SystemSpec
+
+__all__ = ["UpdateSpace", "StopRule", "ResidualNorm", "ShootingConfig", "MatchResult", "match",
+           "contraction_diagnostics"]
+
+_BLOWUP_FACTOR = 1e6          # shooting.py:47
+_ILL_CONDITIONED = 1e12       # shooting.py:48
+
+
+class UpdateSpace(str, enum.Enum):
+    VELOCITY = "velocity"
+    MOMENTUM = "momentum"
+
+
+class StopRule(str, enum.Enum):
+    TARGET_RESIDUAL = "residual"
+    MOMENTUM_DELTA = "momentum-delta"
+
+
+class ResidualNorm(str, enum.Enum):
+    MAX = "max"
+    L2 = "l2"
+
+
+@dataclass(frozen=True)
+class ShootingConfig:
+    """Knobs of the matching iteration (shooting.py:66-100)."""
+
+    h: float
+    epsilon: float = 1e-3
+    max_iter: int = 500
+    update_space: UpdateSpace = UpdateSpace.VELOCITY
+    stop_rule: StopRule = StopRule.TARGET_RESIDUAL
+    norm: ResidualNorm = ResidualNorm.MAX
+    evolve: EvolveConfig = field(default_factory=EvolveConfig)
+    system: SystemSpec = field(default_factory=SystemSpec)
+
+    def __post_init__(self):
+        object.__setattr__(self, "update_space", UpdateSpace(self.update_space))
+        object.__setattr__(self, "stop_rule", StopRule(self.stop_rule))
+        object.__setattr__(self, "norm", ResidualNorm(self.norm))
+        if not (self.h > 0 and math.isfinite(self.h)):
+            raise _errors.ConfigurationError(f"h must be positive, got {self.h}")
+        if not (self.epsilon > 0 and math.isfinite(self.epsilon)):
+            raise _errors.ConfigurationError(f"epsilon must be positive, got {self.epsilon}")
+        if self.max_iter < 1:
+            raise _errors.ConfigurationError(f"max_iter must be >= 1, got {self.max_iter}")
+        if self.system.sigma2 > 0 and self.stop_rule is not StopRule.MOMENTUM_DELTA:
+            raise _errors.ConfigurationError(
+                "inexact matching (sigma2 > 0) cannot stop on the endpoint "
+                "residual; use stop_rule = MomentumDelta")
+
+
+@dataclass(frozen=True)
+class MatchResult:
+    """Outcome of one matching run (shooting.py:103-121)."""
+
+    p0: np.ndarray
+    iterations: int
+    converged: bool
+    residual_history: tuple
+    hamiltonian: float
+    final_template: object
+    final_residual: float
+    diagnosis: str | None = None
+    warnings: tuple = ()
+
+
+def _enum_value(e) -> str:
+    return str(getattr(e, "value", e))
+
+
+def _norm(kind: str, vec: np.ndarray) -> float:
+    """shooting.py:124-135."""
+    arr = np.asarray(vec, dtype=float).reshape(-1, 2)
+    if kind == "max":
+        return float(np.max(np.hypot(arr[:, 0], arr[:, 1])))
+    return float(np.linalg.norm(arr.ravel()))
+
+
+def _make_result(p0, iterations, converged, history, hamiltonian, endpoint, reference, target, final_residual,
+                 diagnosis, warnings):
+    final = _types.get("LandmarkTemplate")(endpoint, f"{reference.label}>{target.label}")
+    return _types.get("MatchResult")(
+        p0=p0, iterations=iterations, converged=converged, residual_history=tuple(history),
+        hamiltonian=hamiltonian, final_template=final, final_residual=final_residual, diagnosis=diagnosis,
+        warnings=warnings)
+
+
+def _prepare(reference, target) -> None:
+    if reference.n != target.n:
+        raise _errors.ConfigurationError(
+            f"templates must have equal landmark counts: {reference.n} (reference) vs {target.n} (target)")
+
+
+def match(reference, target, cfg):
+    """Find initial momenta carrying ``reference`` onto ``target`` (shooting.py:218-301)."""
+    _prepare(reference, target)
+    if _enum_value(cfg.update_space) == "velocity":
+        return _match_velocity(reference, target, cfg)
+    r = device.match(cfg.system, reference.points, target.points, cfg.h, cfg.epsilon, cfg.max_iter,
+                     _enum_value(cfg.stop_rule), _enum_value(cfg.norm), cfg.evolve.t_final, cfg.evolve.steps)
+    return _make_result(r["p0"].cpu().numpy(), r["iterations"], r["converged"], r["residual_history"],
+                        r["hamiltonian"], r["endpoint"].cpu().numpy(), reference, target, r["final_residual"],
+                        r["diagnosis"], ())
+
+
+# --- velocity-space update: host Gram solve between device shoots ---------------------------
+def _gram(kernel, q0: np.ndarray) -> np.ndarray:
+    """kernels.gram_matrix (kernels.py:181-197) for conical/gaussian."""
+    diff = q0[:, None, :] - q0[None, :, :]
+    dist = np.sqrt(np.sum(diff * diff, axis=-1))
+    off = ~np.eye(len(q0), dtype=bool)
+    if np.any(dist[off] == 0.0):
+        i, j = np.argwhere((dist == 0.0) & off)[0]
+        raise _errors.DegenerateConfigurationError(f"points {i} and {j} coincide; Gram matrix would be singular")
+    fam = family_name(kernel)
+    k = np.exp(-dist / kernel.alpha) if fam == "conical" else np.exp(-0.5 * (dist / kernel.alpha) ** 2)
+    if not kernel.normalized:
+        k *= 1.0 / (2.0 * math.pi * kernel.alpha**2)
+    return k
+
+
+def _match_velocity(reference, target, cfg):
+    from scipy.linalg import cho_factor, cho_solve
+
+    q0 = reference.points
+    n = reference.n
+    K = _gram(cfg.system.kernel, q0)
+    cond = float(np.linalg.cond(K))
+    try:
+        factor = cho_factor(K, lower=True)
+    except np.linalg.LinAlgError as exc:
+        raise _errors.DegenerateConfigurationError(f"kernel Gram matrix is not positive definite: {exc}") from exc
+    warnings = ()
+    if not (cond < _ILL_CONDITIONED):
+        warnings = (f"Gram matrix condition number {cond:.3e} exceeds {_ILL_CONDITIONED:.0e}; "
+                    "momenta recovery may lose accuracy",)
+    norm_kind = _enum_value(cfg.norm)
+    mdelta = _enum_value(cfg.stop_rule) == "momentum-delta"
+    ev = cfg.evolve
+
+    def shoot(p):
+        q, _, _ = device.evolve(cfg.system, q0, p, ev.t_final, ev.steps, 0)
+        return q.cpu().numpy()
+
+    def result(p, history, converged, endpoint, diagnosis):
+        return _make_result(p, len(history), converged, history, device.hamiltonian(cfg.system, q0, p), endpoint,
+                            reference, target, _norm(norm_kind, target.points - endpoint), diagnosis, warnings)
+
+    u = np.zeros((n, 2))
+    p = np.zeros((n, 2))
+    endpoint = q0.copy()  # evolve(q0, 0) leaves q0 unchanged
+    residual = target.points - endpoint
+    history: list = []
+    initial = None
+    if not mdelta:
+        initial = _norm(norm_kind, residual)
+        if initial < cfg.epsilon:
+            return result(p, history, True, endpoint, None)
+    for _ in range(cfg.max_iter):
+        delta = cfg.h * _norm(norm_kind, residual)
+        u = u + cfg.h * residual
+        p = cho_solve(factor, u)
+        try:
+            endpoint_new = shoot(p)
+        except (_errors.DivergenceError, _errors.DegenerateConfigurationError) as exc:
+            return result(p, history, False, endpoint, f"step too large ({exc})")
+        endpoint = endpoint_new
+        residual = target.points - endpoint
+        value = delta if mdelta else _norm(norm_kind, residual)
+        if initial is None:
+            initial = value
+        history.append(value)
+        if not math.isfinite(value) or (initial > 0 and value > _BLOWUP_FACTOR * initial):
+            return result(p, history, False, endpoint, "step too large")
+        if value < cfg.epsilon:
+            return result(p, history, True, endpoint, None)
+    return result(p, history, False, endpoint, "iteration cap reached before the stopping rule")
+
+
+def contraction_diagnostics(result) -> list:
+    """Consecutive stopping-norm ratios |r(k+1)| / |r(k)| (shooting.py:304-320)."""
+    hist = result.residual_history
+    if len(hist) < 2:
+        return []
+    return [hist[i + 1] / hist[i] if hist[i] > 0 else math.inf for i in range(len(hist) - 1)]
+
+
+_types.register_defaults(MatchResult=MatchResult)

@@ -1,0 +1,273 @@
+"""Parity of the CUDA path (through the C ABI) with the reference's golden outputs and the oracle.
+
+Tolerances (BASELINE.json north_star): per-RHS ||x_gpu - x_ref||_inf / ||x_ref||_inf <= 1e-10 for
+dq and dp separately; matched p0 and X(T) within 1e-8 with identical iteration counts.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, cases
+
+pytestmark = pytest.mark.gpu
+
+RHS_TOL = 1e-10
+MATCH_TOL = 1e-8
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def spec_from(kp):
+    import paper_1510_03816_b200 as gs
+
+    fam = "conical" if int(kp[0]) == 0 else "gaussian"
+    return gs.SystemSpec(kernel=gs.KernelSpec(family=fam, alpha=float(kp[1]), normalized=bool(kp[2])),
+                         sigma2=float(kp[3]))
+
+
+RHS = cases("rhs_cases.npz")
+
+
+@pytest.mark.parametrize("name", sorted(RHS))
+def test_rhs_matches_reference(cuda, name):
+    import paper_1510_03816_b200 as gs
+
+    c = RHS[name]
+    spec = spec_from(c["kparams"])
+    dq, dp = gs.rhs(spec, gs.ParticleState(c["q"], c["p"]))
+    assert isinstance(dq, np.ndarray) and dq.shape == c["q"].shape
+    assert rel(dq, c["dq"]) <= RHS_TOL
+    assert rel(dp, c["dp"]) <= RHS_TOL
+    h = gs.hamiltonian(spec, gs.ParticleState(c["q"], c["p"]))
+    assert h == pytest.approx(float(c["H"]), rel=1e-12, abs=1e-300)
+
+
+def test_rhs_matches_sympy_two_particle_oracle(cuda):
+    """test_particles.py:52-71: rtol = atol = 1e-12 against the symbolic N=2 equations."""
+    import paper_1510_03816_b200 as gs
+
+    z = np.load(os.path.join(GOLDEN, "rhs_n2_sympy.npz"))
+    for t in range(len(z["q"])):
+        spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=float(z["alpha"][t])), sigma2=float(z["sigma2"][t]))
+        dq, dp = gs.rhs(spec, gs.ParticleState(z["q"][t], z["p"][t]))
+        np.testing.assert_allclose(dq, z["dq_sympy"][t], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(dp, z["dp_sympy"][t], rtol=1e-12, atol=1e-12)
+
+
+def test_rhs_config2_matches_reference(cuda):
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c2()
+    z = np.load(os.path.join(GOLDEN, "rhs_c2.npz"))
+    spec = spec_from(z["kparams"])
+    for path in ("dense", "auto"):
+        gs.set_path(path)
+        try:
+            dq, dp = gs.rhs(spec, gs.ParticleState(w.q, w.p))
+        finally:
+            gs.set_path("auto")
+        assert rel(dq, z["dq"]) <= RHS_TOL, path
+        assert rel(dp, z["dp"]) <= RHS_TOL, path
+
+
+EVO = cases("evolve_cases.npz")
+
+
+@pytest.mark.parametrize("name", sorted(EVO))
+def test_evolve_matches_reference(cuda, name):
+    import paper_1510_03816_b200 as gs
+
+    c = EVO[name]
+    spec = spec_from(c["kparams"])
+    tf, steps, cap = c["cfg"]
+    out = gs.evolve(spec, gs.ParticleState(c["q"], c["p"]),
+                    gs.EvolveConfig(t_final=float(tf), steps=int(steps), capture_every=int(cap)))
+    assert rel(out.final.q, c["qT"]) <= RHS_TOL
+    assert rel(out.final.p, c["pT"]) <= 1e-9
+    if cap:
+        np.testing.assert_array_equal(out.times, c["times"])
+        fq = np.array([s.q for _, s in out.frames])
+        assert rel(fq, c["frames_q"]) <= RHS_TOL
+    else:
+        assert out.frames == ()
+
+
+with open(os.path.join(GOLDEN, "match_cases.json")) as _f:
+    MATCH_META = json.load(_f)
+MATCH = cases("match_cases.npz")
+
+
+def _match_spec(m):
+    import paper_1510_03816_b200 as gs
+
+    return gs.SystemSpec(kernel=gs.KernelSpec(family=m["family"], alpha=m["alpha"], normalized=m["normalized"]),
+                         sigma2=m["sigma2"])
+
+
+@pytest.mark.parametrize("name", sorted(MATCH_META))
+def test_match_matches_reference(cuda, name):
+    import paper_1510_03816_b200 as gs
+
+    m, c = MATCH_META[name], MATCH[name]
+    cfg = gs.ShootingConfig(h=m["h"], epsilon=m["epsilon"], max_iter=m["max_iter"], update_space="momentum",
+                            stop_rule=m["stop_rule"], norm=m["norm"],
+                            evolve=gs.EvolveConfig(t_final=m["t_final"], steps=m["steps"]), system=_match_spec(m))
+    ref = gs.LandmarkTemplate(c["ref"], m["ref_label"])
+    tgt = gs.LandmarkTemplate(c["tgt"], m["tgt_label"])
+    res = gs.match(ref, tgt, cfg)
+    assert res.iterations == m["iterations"]
+    assert res.converged == m["converged"]
+    assert len(res.residual_history) == res.iterations
+    assert res.final_template.label == m["final_label"]
+    if m["diagnosis"] and m["diagnosis"].startswith("step too large"):
+        assert res.diagnosis == m["diagnosis"]
+        assert np.all(np.isfinite(res.p0))
+        return
+    assert res.diagnosis == m["diagnosis"]
+    scale = max(np.abs(c["p0"]).max(), 1e-300)
+    assert np.abs(res.p0 - c["p0"]).max() / scale <= MATCH_TOL
+    assert np.abs(res.final_template.points - c["endpoint"]).max() <= MATCH_TOL * max(1.0, np.abs(c["endpoint"]).max())
+    assert res.hamiltonian == pytest.approx(m["hamiltonian"], rel=MATCH_TOL, abs=1e-300)
+    hist = np.array(res.residual_history)
+    if hist.size:
+        np.testing.assert_allclose(hist, c["history"], rtol=1e-6, atol=1e-12)
+    assert res.final_residual == pytest.approx(m["final_residual"], rel=1e-6, abs=1e-12)
+
+
+def test_error_messages_match_reference(cuda):
+    import paper_1510_03816_b200 as gs
+
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msgs = json.load(f)
+    q = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 1.0]])
+    p = np.array([[1.0, 0.0], [1.0, 0.0], [0.0, 0.0]])
+    with pytest.raises(gs.DegenerateConfigurationError) as e:
+        gs.rhs(gs.SystemSpec(), gs.ParticleState(q, p))
+    assert str(e.value) == msgs["rhs_coincident"]
+    q = np.array([[0.0, 0.0], [0.0, 0.0], [2.0, 0.0]])
+    p = np.array([[0.0, 1.0], [0.0, 1.0], [0.0, 0.0]])
+    with pytest.raises(gs.DegenerateConfigurationError) as e:
+        gs.evolve(gs.SystemSpec(), gs.ParticleState(q, p), gs.EvolveConfig(steps=10))
+    assert str(e.value) == msgs["evolve_coincident"]
+    q = np.array([[-0.5, 0.0], [0.5, 0.0]])
+    p = np.array([[1e200, 0.0], [-1e200, 0.0]])
+    with pytest.raises(gs.DivergenceError) as e:
+        gs.evolve(gs.SystemSpec(), gs.ParticleState(q, p), gs.EvolveConfig(steps=4))
+    assert str(e.value) == msgs["evolve_divergence"]
+    q = np.array([[0.0, 0.0], [1.0, 0.0], [5.0, 5.0], [1.0, 0.0], [0.0, 0.0]])
+    p = np.array([[1.0, 0.0], [0.0, 2.0], [1.0, 0.0], [0.0, 1.0], [3.0, 0.0]])
+    with pytest.raises(gs.DegenerateConfigurationError) as e:
+        gs.rhs(gs.SystemSpec(), gs.ParticleState(q, p))
+    assert str(e.value) == msgs["rhs_coincident_two_groups"]
+    q = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 1.0]])
+    p = np.array([[1.0, 0.0], [0.0, 0.0], [0.0, 1.0]])
+    dq, dp = gs.rhs(gs.SystemSpec(), gs.ParticleState(q, p))   # inert coincident pair tolerated
+    assert np.all(np.isfinite(dq)) and np.all(np.isfinite(dp))
+
+
+def test_errors_on_the_general_path(cuda):
+    """Coincidence / divergence detection inside the multi-kernel path (N > 512)."""
+    import paper_1510_03816_b200 as gs
+
+    rng = np.random.default_rng(5)
+    n = 700
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 0.1, (n, 2))
+    q[431] = q[17]
+    with pytest.raises(gs.DegenerateConfigurationError, match="particles 17 and 431 coincide"):
+        gs.rhs(gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.05)), gs.ParticleState(q, p))
+    with pytest.raises(gs.DegenerateConfigurationError, match=r"\(during step 1, t in \[0, 0.1\]\)"):
+        gs.evolve(gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.05)), gs.ParticleState(q, p), gs.EvolveConfig(steps=10))
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 1e200, (n, 2))
+    with pytest.raises(gs.DivergenceError, match=r"step 1 "):
+        gs.evolve(gs.SystemSpec(), gs.ParticleState(q, p), gs.EvolveConfig(steps=4))
+
+
+def test_zero_momentum_is_a_fixed_point_bitwise(cuda):
+    import paper_1510_03816_b200 as gs
+
+    for n in (6, 2000):
+        q = np.random.default_rng(n).uniform(-1, 1, (n, 2))
+        out = gs.evolve(gs.SystemSpec(), gs.ParticleState(q, np.zeros((n, 2))), gs.EvolveConfig(steps=10))
+        np.testing.assert_array_equal(out.final.q, q)
+        np.testing.assert_array_equal(out.final.p, np.zeros((n, 2)))
+
+
+# ---- beyond the reference's reach: the C oracle (pinned in tests/test_oracle.py) ----------------
+def _kern(spec):
+    from oracle.restate import Kernel
+
+    return Kernel(0 if spec.kernel.family.value == "conical" else 1, spec.kernel.alpha, spec.kernel.normalized)
+
+
+def test_general_path_evolve_matches_oracle(cuda):
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+
+    rng = np.random.default_rng(42)
+    n = 3000
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 0.05, (n, 2))
+    for spec in (gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.1 / gs.LAMBDA)),
+                 gs.SystemSpec(kernel=gs.KernelSpec(family="gaussian", alpha=0.03, normalized=False), sigma2=0.2)):
+        out = gs.evolve(spec, gs.ParticleState(q, p), gs.EvolveConfig(steps=3))
+        qo, po = native.evolve(_kern(spec), spec.sigma2, q, p, 1.0, 3)
+        assert rel(out.final.q, qo) <= RHS_TOL
+        assert rel(out.final.p, po) <= RHS_TOL
+
+
+def test_general_path_match_matches_oracle(cuda):
+    """N = 1024 > 512 exercises the multi-kernel device loop of gs_match."""
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+
+    n = 1024
+    ref = gs.circle(1.0, n=n)
+    tgt = gs.ellipse_rot_shift(1.3, 0.7, 0.0, n=n)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.03 / gs.LAMBDA))
+    cfg = gs.ShootingConfig(h=0.5, epsilon=1e-6, max_iter=60, update_space="momentum",
+                            evolve=gs.EvolveConfig(steps=10), system=spec)
+    res = gs.match(ref, tgt, cfg)
+    o = native.match_momentum(_kern(spec), 0.0, ref.points, tgt.points, 0.5, 1e-6, 60, "residual", "max", 1.0, 10)
+    assert res.iterations == o["iterations"] and res.converged == o["converged"]
+    assert np.abs(res.p0 - o["p0"]).max() / np.abs(o["p0"]).max() <= MATCH_TOL
+    assert res.hamiltonian == pytest.approx(o["hamiltonian"], rel=MATCH_TOL)
+
+
+def test_config3_dense_rhs_sampled_rows_match_oracle(cuda):
+    """Full C3 size (N = 131072, every pair interacts): sampled rows against the oracle,
+    plus size-independent properties: bitwise determinism, row-sharding invariance,
+    momentum conservation sum_i dp_i = 0 and translation invariance."""
+    import torch
+
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+    from paper_1510_03816_b200 import configs, device
+
+    w = configs.c3()
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
+    dq, dp = device.rhs(spec, w.q, w.p)
+    dq2, dp2 = device.rhs(spec, w.q, w.p)
+    assert torch.equal(dq, dq2) and torch.equal(dp, dp2)
+    dqh, dph = dq.cpu().numpy(), dp.cpu().numpy()
+    for r0 in (0, 65536 + 123, w.n - 256):
+        oq, op = native.rhs(_kern(spec), 0.0, w.q, w.p, rows=(r0, r0 + 256))
+        assert rel(dqh[r0:r0 + 256], oq) <= RHS_TOL
+        assert rel(dph[r0:r0 + 256], op) <= RHS_TOL
+    # momentum equation antisymmetry: sum_i dp_i = 0 up to rounding of N^2 terms
+    assert np.abs(dph.sum(axis=0)).max() <= 1e-9 * np.abs(dph).sum()
+    # translation invariance (positions shifted by a dyadic constant: exact differences)
+    dq3, dp3 = device.rhs(spec, w.q + 0.5, w.p)
+    assert rel(dq3.cpu().numpy(), dqh) <= 1e-13 and rel(dp3.cpu().numpy(), dph) <= 1e-12
+    # row sharding (the multi-GPU split) gives the same bits as the single-GPU rows
+    from paper_1510_03816_b200 import sharded
+
+    rows = sharded.rhs_rows(spec, torch.from_numpy(w.q).cuda(), torch.from_numpy(w.p).cuda(), 40000, 70001)
+    assert torch.equal(rows[0], dq[40000:70001]) and torch.equal(rows[1], dp[40000:70001])

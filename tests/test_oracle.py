@@ -1,0 +1,145 @@
+"""Pin the CPU oracle (oracle/) against the golden fixtures produced by the unmodified reference.
+
+CPU-only.  Both restatements must reproduce the reference: the numpy restatement to the
+last bit on the RHS (same formula, same BLAS calls), the C restatement (direct-difference
+dp) to the reference's own cancellation floor.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, cases
+from oracle import native, restate
+from oracle.restate import Kernel, OracleDegenerate, OracleDivergence
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+RHS = cases("rhs_cases.npz")
+
+
+@pytest.mark.parametrize("name", sorted(RHS))
+def test_restate_rhs_matches_reference(name):
+    c = RHS[name]
+    k = Kernel.from_params(c["kparams"])
+    dq, dp = restate.rhs(k, c["kparams"][3], c["q"], c["p"])
+    assert rel(dq, c["dq"]) <= 1e-15
+    assert rel(dp, c["dp"]) <= 1e-14
+    assert restate.hamiltonian(k, c["q"], c["p"]) == pytest.approx(float(c["H"]), rel=1e-13, abs=1e-300)
+
+
+@pytest.mark.parametrize("name", sorted(RHS))
+def test_native_oracle_rhs_matches_reference(name):
+    c = RHS[name]
+    k = Kernel.from_params(c["kparams"])
+    dq, dp = native.rhs(k, c["kparams"][3], c["q"], c["p"])
+    assert rel(dq, c["dq"]) <= 1e-13
+    assert rel(dp, c["dp"]) <= 1e-11  # reference's own a.sum*q - a@q cancellation
+    assert native.hamiltonian(k, c["q"], c["p"]) == pytest.approx(float(c["H"]), rel=1e-12, abs=1e-300)
+
+
+def test_oracles_match_sympy_two_particle_oracle():
+    z = np.load(os.path.join(GOLDEN, "rhs_n2_sympy.npz"))
+    for t in range(len(z["q"])):
+        k = Kernel(0, float(z["alpha"][t]), True)
+        for impl in (restate, native):
+            dq, dp = impl.rhs(k, float(z["sigma2"][t]), z["q"][t], z["p"][t])
+            np.testing.assert_allclose(dq, z["dq_sympy"][t], rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(dp, z["dp_sympy"][t], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(z["dq"][t], z["dq_sympy"][t], rtol=1e-12, atol=1e-12)
+
+
+def test_native_rhs_c2_matches_reference():
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c2()
+    z = np.load(os.path.join(GOLDEN, "rhs_c2.npz"))
+    k = Kernel.from_params(z["kparams"])
+    dq, dp = native.rhs(k, 0.0, w.q, w.p)
+    assert rel(dq, z["dq"]) <= 1e-13
+    assert rel(dp, z["dp"]) <= 1e-11
+    # KD-1: the truncated (cell-list) sum differs from the dense reference by ~1e-15
+    dqc, dpc = native.rhs(k, 0.0, w.q, w.p, cutoff=w.sigma)
+    assert rel(dqc, z["dq"]) <= 1e-13
+    assert rel(dpc, z["dp"]) <= 1e-11
+
+
+EVO = cases("evolve_cases.npz")
+
+
+@pytest.mark.parametrize("name", sorted(EVO))
+def test_oracle_evolve_matches_reference(name):
+    c = EVO[name]
+    k = Kernel.from_params(c["kparams"])
+    tf, steps, cap = c["cfg"]
+    q, p, frames = restate.evolve(k, c["kparams"][3], c["q"], c["p"], tf, int(steps), int(cap))
+    assert rel(q, c["qT"]) <= 1e-14
+    assert rel(p, c["pT"]) <= 1e-13
+    if cap:
+        np.testing.assert_allclose([f[0] for f in frames], c["times"], rtol=0, atol=0)
+    qn, pn = native.evolve(k, c["kparams"][3], c["q"], c["p"], tf, int(steps))
+    assert rel(qn, c["qT"]) <= 1e-12
+    assert rel(pn, c["pT"]) <= 1e-10
+
+
+with open(os.path.join(GOLDEN, "match_cases.json")) as _f:
+    MATCH_META = json.load(_f)
+MATCH = cases("match_cases.npz")
+
+
+def _kernel(meta):
+    return Kernel(0 if meta["family"] == "conical" else 1, meta["alpha"], meta["normalized"])
+
+
+@pytest.mark.parametrize("name", sorted(MATCH_META))
+def test_oracle_match_matches_reference(name):
+    m, c = MATCH_META[name], MATCH[name]
+    out = native.match_momentum(_kernel(m), m["sigma2"], c["ref"], c["tgt"], m["h"], m["epsilon"], m["max_iter"],
+                                m["stop_rule"], m["norm"], m["t_final"], m["steps"])
+    assert out["iterations"] == m["iterations"]
+    assert out["converged"] == m["converged"]
+    if m["diagnosis"] and m["diagnosis"].startswith("step too large"):
+        # divergent runs: the blow-up amplifies rounding chaotically; only the outcome is pinned
+        assert out["diagnosis"] == m["diagnosis"]
+        return
+    scale = max(np.abs(c["p0"]).max(), 1e-300)
+    assert np.abs(out["p0"] - c["p0"]).max() / scale <= 1e-8
+    assert np.abs(out["endpoint"] - c["endpoint"]).max() <= 1e-8 * max(1.0, np.abs(c["endpoint"]).max())
+    assert out["hamiltonian"] == pytest.approx(m["hamiltonian"], rel=1e-8, abs=1e-300)
+    if m["diagnosis"] is None:
+        assert out["diagnosis"] is None
+    else:
+        assert out["diagnosis"].split(" (")[0] == m["diagnosis"].split(" (")[0]
+
+
+def test_oracle_error_messages_match_reference():
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msgs = json.load(f)
+    k = Kernel()
+    q = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 1.0]])
+    p = np.array([[1.0, 0.0], [1.0, 0.0], [0.0, 0.0]])
+    for impl in (restate, native):
+        with pytest.raises(OracleDegenerate) as e:
+            impl.rhs(k, 0.0, q, p)
+        assert str(e.value) == msgs["rhs_coincident"]
+    q = np.array([[0.0, 0.0], [0.0, 0.0], [2.0, 0.0]])
+    p = np.array([[0.0, 1.0], [0.0, 1.0], [0.0, 0.0]])
+    with pytest.raises(OracleDegenerate) as e:
+        native.evolve(k, 0.0, q, p, 1.0, 10)
+    assert str(e.value) == msgs["evolve_coincident"]
+    q = np.array([[-0.5, 0.0], [0.5, 0.0]])
+    p = np.array([[1e200, 0.0], [-1e200, 0.0]])
+    for ev in (lambda: restate.evolve(k, 0.0, q, p, 1.0, 4), lambda: native.evolve(k, 0.0, q, p, 1.0, 4)):
+        with pytest.raises(OracleDivergence) as e:
+            ev()
+        assert str(e.value) == msgs["evolve_divergence"]
+    q = np.array([[0.0, 0.0], [1.0, 0.0], [5.0, 5.0], [1.0, 0.0], [0.0, 0.0]])
+    p = np.array([[1.0, 0.0], [0.0, 2.0], [1.0, 0.0], [0.0, 1.0], [3.0, 0.0]])
+    with pytest.raises(OracleDegenerate) as e:
+        native.rhs(k, 0.0, q, p)
+    assert str(e.value) == msgs["rhs_coincident_two_groups"]
