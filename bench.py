@@ -216,8 +216,8 @@ def main():
     import ctypes
 
     lib.gs_profile_enable(ctx.handle, 1)
-    pm, pl, ll = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
-    lib.gs_profile_read(ctx.handle, ctypes.byref(pm), ctypes.byref(pl), ctypes.byref(ll), 1)
+    pm, pl, ll, pp = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    lib.gs_profile_read(ctx.handle, ctypes.byref(pm), ctypes.byref(pl), ctypes.byref(ll), ctypes.byref(pp), 1)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     if world > 1:
@@ -232,21 +232,23 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    lib.gs_profile_read(ctx.handle, ctypes.byref(pm), ctypes.byref(pl), ctypes.byref(ll), 1)
+    lib.gs_profile_read(ctx.handle, ctypes.byref(pm), ctypes.byref(pl), ctypes.byref(ll), ctypes.byref(pp), 1)
     lib.gs_profile_enable(ctx.handle, 0)
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, float(pp.value)], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tp = t[1:].clone()
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tp, op=dist.ReduceOp.SUM)
+        t[1] = tp[0]
     ms_max = float(t[0])
-    pairs_per_rhs = float(w.n) * w.n
-    total_pairs = a.steps * 4 * a.rk_steps * pairs_per_rhs
+    total_pairs = float(t[1])          # evaluated ordered pairs, counted by the library (all ranks)
+    pairs_per_rhs = total_pairs / (a.steps * 4 * a.rk_steps)
     value = total_pairs / (ms_max / 1e3)
 
     # roofline of the dominant kernel (pair kernel), measured live with CUDA events
     pair_ms_avg = pm.value / max(1, pl.value)
-    rows_local = sharded.row_split(w.n, world, rank)[1] - sharded.row_split(w.n, world, rank)[0]
-    pairs_per_launch = rows_local * float(w.n)
+    pairs_per_launch = float(pp.value) / max(1, pl.value)
     ach_pairs = pairs_per_launch / (pair_ms_avg / 1e3)
     ach_tflops = ach_pairs * 2 * W_ALG / 1e12
     peak = None

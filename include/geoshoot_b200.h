@@ -178,10 +178,13 @@ int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream);
 
 /* Profiling: with profiling enabled, every launch of the pair kernel (the dense or cell-list
  * RHS sweep, or the persistent small-N kernel) is bracketed by CUDA events on its stream;
- * gs_profile_read returns their summed device time (ms), the number of pair-kernel launches
- * and of all kernel launches since the last reset.  Synchronises on the last event. */
+ * gs_profile_read returns their summed device time (ms), the number of pair-kernel launches,
+ * of all kernel launches and of evaluated ordered pairs (dense: rows x n per RHS; cell list:
+ * pairs with d < cutoff incl. self, counted on the device while profiling) since the last
+ * reset.  Synchronises. */
 int gs_profile_enable(gs_context* ctx, int32_t on);
-int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int32_t reset);
+int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int64_t* pairs,
+                    int32_t reset);
 
 /* micro-benchmark used by bench.py for the FP64 roofline denominator: `iters` dependent
  * DFMA chains per thread on a full grid; returns the device time in *ms (host). */

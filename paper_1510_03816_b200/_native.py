@@ -110,8 +110,8 @@ def load(path: str = LIB_PATH):
             "gs_stage_end": ([_vp, _dp, _dp, _vp], ctypes.c_int),
             "gs_fp64_peak_probe": ([_vp, ctypes.c_int32, P(ctypes.c_double), P(ctypes.c_double), _vp], ctypes.c_int),
             "gs_profile_enable": ([_vp, ctypes.c_int32], ctypes.c_int),
-            "gs_profile_read": ([_vp, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_int64), ctypes.c_int32],
-                                ctypes.c_int),
+            "gs_profile_read": ([_vp, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64),
+                                 ctypes.c_int32], ctypes.c_int),
         }
         for name, (args, res) in proto.items():
             fn = getattr(lib, name)

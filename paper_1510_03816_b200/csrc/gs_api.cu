@@ -6,11 +6,13 @@
 // The numerics all run in the kernels of gs_dense.cu / gs_small.cu / gs_cell.cu.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/geoshoot_b200.h"
+#include "gs_cell.cuh"
 #include "gs_kernels.cuh"
 
 using namespace gsb;
@@ -72,6 +74,28 @@ struct gs_context {
     size_t prof_used = 0;
     long long launches = 0;
     long long pair_launches = 0;
+    long long host_pairs = 0;     // dense / small-kernel pair count (known on the host)
+    // cell list (gs_cell.cu)
+    DevBuf<unsigned> c_keys, c_keys_sorted, c_vals, c_perm;
+    DevBuf<int> c_start;
+    DevBuf<double4> c_Ss;
+    DevBuf<double> c_bbox;
+    DevBuf<GridParams> c_gp;
+    DevBuf<unsigned char> c_cub;
+    DevBuf<unsigned long long> c_acc;   // accepted pairs (profiling)
+    size_t c_cub_bytes = 0;
+    int cell_on = 0;                    // path of the current call
+    // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        std::vector<double> key;
+        std::vector<cudaEvent_t> ev;    // profiling events captured inside the graph
+        long long launches = 0, pair_launches = 0, host_pairs = 0;
+    } graph;
+    std::vector<cudaEvent_t>* capture_events = nullptr;  // non-null while capturing
+    cudaStream_t cap_stream = nullptr;
+    int graphs_on = 1;
+    double prof_ms_acc = 0.0;           // pair-kernel time already harvested (graph replays)
 };
 
 namespace {
@@ -262,6 +286,12 @@ int fetch_status(gs_context* ctx, cudaStream_t s, int64_t n, gs_status_t* out) {
 }
 
 cudaEvent_t prof_event(gs_context* ctx) {
+    if (ctx->capture_events) {  // recorded as an event node of the graph being captured
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->capture_events->push_back(e);
+        return e;
+    }
     if (ctx->prof_used == ctx->prof_events.size()) {
         cudaEvent_t e;
         cudaEventCreate(&e);
@@ -270,17 +300,79 @@ cudaEvent_t prof_event(gs_context* ctx) {
     return ctx->prof_events[ctx->prof_used++];
 }
 
+CellWs cell_ws(gs_context* ctx) {
+    CellWs w;
+    w.keys = ctx->c_keys.ptr; w.keys_sorted = ctx->c_keys_sorted.ptr; w.vals = ctx->c_vals.ptr;
+    w.perm = ctx->c_perm.ptr; w.start = ctx->c_start.ptr; w.Ss = ctx->c_Ss.ptr; w.bbox_red = ctx->c_bbox.ptr;
+    w.gp = ctx->c_gp.ptr; w.cub_temp = ctx->c_cub.ptr; w.cub_bytes = ctx->c_cub_bytes;
+    return w;
+}
+
+int ensure_cell(gs_context* ctx, int64_t n) {
+    GS_CUDA(ctx->c_keys.ensure(n)); GS_CUDA(ctx->c_keys_sorted.ensure(n)); GS_CUDA(ctx->c_vals.ensure(n));
+    GS_CUDA(ctx->c_perm.ensure(n)); GS_CUDA(ctx->c_Ss.ensure(n));
+    GS_CUDA(ctx->c_start.ensure(cell_cap(n) + 1));
+    GS_CUDA(ctx->c_bbox.ensure(4 * kCellBboxBlocks));
+    GS_CUDA(ctx->c_gp.ensure(1));
+    GS_CUDA(ctx->c_acc.ensure(1));
+    const size_t bytes = cell_cub_bytes(n);
+    GS_CUDA(ctx->c_cub.ensure(bytes));
+    ctx->c_cub_bytes = ctx->c_cub.cap;
+    return GS_OK;
+}
+
+// Pair-sum strategy of one API call (gs_system_t.path).  AUTO takes the cell list when the
+// support radius is small against the point cloud of S (one bbox reduction + 8-byte read).
+constexpr int64_t kCellMinN = 2048;
+constexpr int kCellMinCells = 25;
+
+int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s) {
+    ctx->cell_on = 0;
+    if (sys->path == GS_PATH_DENSE) return GS_OK;
+    if (sys->path == GS_PATH_CELL && !(sys->cutoff > 0.0))
+        return fail(GS_ERR_INVALID, "the cell-list path needs a positive cutoff (support radius)");
+    if (!(sys->cutoff > 0.0) || (sys->path == GS_PATH_AUTO && n < kCellMinN)) return GS_OK;
+    int rc = ensure_cell(ctx, n);
+    if (rc) return rc;
+    if (sys->path == GS_PATH_CELL) {
+        ctx->cell_on = 1;
+        return GS_OK;
+    }
+    // AUTO: grid size at cell edge = cutoff
+    CellWs w = cell_ws(ctx);
+    if (cell_build(w, S, n, sys->cutoff, s) != 0) return fail(GS_ERR_CUDA, "cell_build failed");
+    GridParams g;
+    GS_CUDA(cudaMemcpyAsync(&g, ctx->c_gp.ptr, sizeof(g), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    ctx->cell_on = (int64_t)g.nx * g.ny >= kCellMinCells;
+    return GS_OK;
+}
+
 // The pair kernel (the hot spot) of every RHS goes through here: timed when profiling is on.
+// Dense: part holds plan.nchunks chunk partials; cell list: one record per row.
 void pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
                  const DensePlan& plan, double4* part, unsigned long long ev, cudaStream_t stream) {
-    if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
-    launch_dense_partial(sc, S, n, row0, nrows, plan, part, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
-    if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+    if (ctx->cell_on) {
+        CellWs w = cell_ws(ctx);
+        cell_build(w, S, n, sc.cutoff, stream);
+        ctx->launches += 6;  // bbox, params, keys, 2x radix passes (approx.), start/permute
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        launch_cell_pair(sc, w, n, row0, row0 + nrows, part, ctx->st.ptr, ev, ctx->tbl.ptr,
+                         ctx->prof_on ? ctx->c_acc.ptr : nullptr, stream);
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+    } else {
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        launch_dense_partial(sc, S, n, row0, nrows, plan, part, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        ctx->host_pairs += nrows * n;
+    }
     ctx->launches++;
     ctx->pair_launches++;
 }
 
-// One RK4 stage for the session's rows (dense partial + finish epilogue).
+inline int pair_chunks(gs_context* ctx, const DensePlan& plan) { return ctx->cell_on ? 1 : plan.nchunks; }
+
+// One RK4 stage for the session's rows (pair kernel + finish epilogue).
 void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cudaStream_t stream) {
     const int64_t n = ctx->n, nrows = ctx->row1 - ctx->row0;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
@@ -288,15 +380,76 @@ void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cuda
     pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
     ctx->launches++;  // finish
     FinishArgs fa{};
-    fa.part = ctx->part.ptr; fa.nchunks = plan.nchunks; fa.nrows = nrows; fa.row0 = ctx->row0;
+    fa.part = ctx->part.ptr; fa.nchunks = pair_chunks(ctx, plan); fa.nrows = nrows; fa.row0 = ctx->row0;
     fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr;
     fa.stage = s; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
     launch_finish(kFinStage, sc, fa, stream);
 }
 
+void graph_reset(gs_context* ctx) {
+    if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
+    for (cudaEvent_t e : ctx->graph.ev) cudaEventDestroy(e);
+    ctx->graph = gs_context::Graph();
+}
+
+// Everything the captured kernels bake in: sizes, constants, buffer addresses, path, profiling.
+std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, int steps) {
+    auto P = [](const void* p) { return (double)(uintptr_t)p; };
+    return {(double)ctx->n, (double)ctx->row0, (double)ctx->row1, (double)steps, dt, (double)ctx->cell_on,
+            (double)ctx->prof_on, (double)sc.fam, sc.k1, sc.scale_q, sc.scale_p, sc.sigma2, sc.cutoff,
+            P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr),
+            P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr)};
+}
+
+// integrator.py:95-119 as one CUDA graph (4 x steps stages, ~2 kernels per dense stage and
+// ~10 per cell-list stage) captured once per configuration and replayed on the caller's
+// stream: no per-launch CPU overhead inside a shoot.
+int run_evolve_graph(gs_context* ctx, const SysConst& sc, double t_final, int steps, cudaStream_t stream) {
+    const double dt = t_final / steps;
+    std::vector<double> key = graph_key(ctx, sc, dt, steps);
+    if (!ctx->graph.exec || ctx->graph.key != key) {
+        graph_reset(ctx);
+        if (!ctx->cap_stream) GS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        const long long l0 = ctx->launches, pl0 = ctx->pair_launches, hp0 = ctx->host_pairs;
+        ctx->capture_events = &ctx->graph.ev;
+        GS_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+        for (int step = 1; step <= steps; ++step)
+            for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, ctx->cap_stream);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
+        ctx->capture_events = nullptr;
+        if (e != cudaSuccess) return fail(GS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&ctx->graph.exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(GS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        ctx->graph.key = key;
+        ctx->graph.launches = ctx->launches - l0;
+        ctx->graph.pair_launches = ctx->pair_launches - pl0;
+        ctx->graph.host_pairs = ctx->host_pairs - hp0;
+        ctx->launches = l0; ctx->pair_launches = pl0; ctx->host_pairs = hp0;  // counted per replay below
+    }
+    GS_CUDA(cudaGraphLaunch(ctx->graph.exec, stream));
+    ctx->launches += ctx->graph.launches;
+    ctx->pair_launches += ctx->graph.pair_launches;
+    ctx->host_pairs += ctx->graph.host_pairs;
+    return GS_OK;
+}
+
+// Harvest the pair-kernel times of the last graph replay (call after the stream is synced).
+int graph_harvest(gs_context* ctx) {
+    if (!ctx->prof_on || ctx->graph.ev.size() < 2) return GS_OK;
+    for (size_t k = 0; k + 1 < ctx->graph.ev.size(); k += 2) {
+        float t = 0.f;
+        GS_CUDA(cudaEventElapsedTime(&t, ctx->graph.ev[k], ctx->graph.ev[k + 1]));
+        ctx->prof_ms_acc += t;
+    }
+    return GS_OK;
+}
+
 // integrator.py:95-119 over the session rows (single rank: rows = all).
 int run_evolve(gs_context* ctx, const SysConst& sc, double t_final, int steps, int capture_every, double* frames,
                cudaStream_t stream) {
+    if (capture_every == 0 && ctx->graphs_on) return run_evolve_graph(ctx, sc, t_final, steps, stream);
     const double dt = t_final / steps;
     const int64_t nrows = ctx->row1 - ctx->row0;
     int f = 0;
@@ -344,6 +497,7 @@ int gs_create(gs_context** out, int device) {
     GS_CUDA(cudaSetDevice(device));
     gs_context* ctx = new gs_context();
     ctx->device = device;
+    if (const char* g = std::getenv("GS_B200_GRAPHS")) ctx->graphs_on = std::atoi(g) != 0;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
     std::vector<double> t(kTbl);
@@ -371,6 +525,12 @@ int gs_destroy(gs_context* ctx) {
     ctx->red.release(); ctx->ham.release(); ctx->hist.release(); ctx->scal.release(); ctx->small_res.release();
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
     if (ctx->scal_host) cudaFreeHost(ctx->scal_host);
+    graph_reset(ctx);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+    ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
+    ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
+    ctx->c_acc.release();
     delete ctx;
     return GS_OK;
 }
@@ -402,11 +562,12 @@ static int rhs_impl(gs_context* ctx, const gs_system_t* sys, int64_t n, const do
     const SysConst sc = make_const(sys);
     k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
     k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 1);
+    if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
     pair_kernel(ctx, sc, ctx->S.ptr, n, row0, nrows, plan, ctx->part.ptr, 2ull, s);
     ctx->launches += 3;  // reset, pack, finish
     FinishArgs fa{};
-    fa.part = ctx->part.ptr; fa.nchunks = plan.nchunks; fa.nrows = nrows; fa.row0 = row0; fa.S = ctx->S.ptr;
+    fa.part = ctx->part.ptr; fa.nchunks = pair_chunks(ctx, plan); fa.nrows = nrows; fa.row0 = row0; fa.S = ctx->S.ptr;
     fa.dq = dq; fa.dp = dp; fa.st = ctx->st.ptr; fa.event = 3ull;
     launch_finish(kFinRhs, sc, fa, s);
     GS_CUDA(cudaGetLastError());
@@ -444,13 +605,14 @@ int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const dou
     const SysConst sc = make_const(sys);
     k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
     k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+    if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
     // coincident pairs are irrelevant to H (particles.py:127-128 has no check): use an event id
     // that is never reported
     pair_kernel(ctx, sc, ctx->S.ptr, n, 0, n, plan, ctx->part.ptr, 2ull, s);
     ctx->launches += 5;  // reset, pack, finish, 2 reductions
     FinishArgs fa{};
-    fa.part = ctx->part.ptr; fa.nchunks = plan.nchunks; fa.nrows = n; fa.row0 = 0; fa.S = ctx->S.ptr;
+    fa.part = ctx->part.ptr; fa.nchunks = pair_chunks(ctx, plan); fa.nrows = n; fa.row0 = 0; fa.S = ctx->S.ptr;
     fa.ham = ctx->ham.ptr; fa.st = ctx->st.ptr; fa.event = 0ull;  // never skipped
     launch_finish(kFinHam, sc, fa, s);
     const int nb = (int)std::min<int64_t>(kRedBlocks, (n + 255) / 256);
@@ -480,6 +642,7 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
         a.n = n; a.split = small_split(n); a.mode = 0; a.t_final = t_final; a.steps = steps;
         a.capture_every = capture_every; a.q_in = q; a.p_in = p; a.q_out = q; a.p_out = p; a.frames = frames;
         a.st = ctx->st.ptr;
+        ctx->host_pairs += 4LL * steps * n * n;
         if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
         launch_small(sc, a, ctx->tbl.ptr, s);
         if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
@@ -492,6 +655,7 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
         ctx->launches += 4;  // reset, pack, copy, unpack
         k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
         k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+        if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
         k_copy_rows<<<nblk(n), 256, 0, s>>>(ctx->S.ptr, 0, n, ctx->B.ptr);
         if ((rc = run_evolve(ctx, sc, t_final, steps, capture_every, frames, s))) return rc;
         k_unpack<<<nblk(n), 256, 0, s>>>(ctx->B.ptr, n, q, p);
@@ -500,6 +664,10 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
     gs_status_t st;
     rc = fetch_status(ctx, s, n, &st);
     if (status) *status = st;
+    if (rc != GS_ERR_CUDA) {
+        const int hr = graph_harvest(ctx);
+        if (hr) return hr;
+    }
     return rc;
 }
 
@@ -548,6 +716,8 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         GS_CUDA(cudaStreamSynchronize(s));
         if (r.iterations > 0)
             GS_CUDA(cudaMemcpy(history_out, ctx->hist.ptr, r.iterations * sizeof(double), cudaMemcpyDeviceToHost));
+        ctx->host_pairs += (long long)(r.iterations + (r.outcome == GS_MATCH_EVOLVE_FAILED)) * 4LL * cfg->steps * n * n +
+                           n * n;
         result->outcome = r.outcome;
         result->iterations = r.iterations;
         result->hamiltonian = r.hamiltonian;
@@ -566,6 +736,8 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         GS_CUDA(cudaMemcpyAsync(ctx->q0.ptr, q0, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
         GS_CUDA(cudaMemcpyAsync(ctx->tgt.ptr, target, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
         GS_CUDA(cudaMemsetAsync(ctx->p.ptr, 0, 2 * n * sizeof(double), s));
+        k_match_begin<<<nblk(n), 256, 0, s>>>(ctx->q0.ptr, ctx->p.ptr, ctx->resid.ptr, 0.0, n, ctx->S.ptr, ctx->B.ptr);
+        if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
         // initial shoot with p = 0 leaves q0 unchanged bitwise: endpoint = q0 (shooting.py:244-247)
         const int nb = (int)std::min<int64_t>(kRedBlocks, (n + 255) / 256);
         const int red_kind = cfg->norm == GS_NORM_MAX ? 0 : 1;
@@ -595,6 +767,7 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
                 gs_status_t st;
                 rc = fetch_status(ctx, s, n, &st);  // synchronises
                 if (rc == GS_ERR_CUDA) return rc;
+                if ((rc = graph_harvest(ctx))) return rc;
                 if (st.code != GS_OK) {
                     outcome = GS_MATCH_EVOLVE_FAILED;
                     result->status = st;
@@ -650,6 +823,7 @@ int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
     int rc = check_system(sys);
     if (rc) return rc;
     if (stg < 0 || stg > 3 || step < 1) return fail(GS_ERR_INVALID, "bad stage index");
+    if (step == 1 && stg == 0 && (rc = choose_path(ctx, sys, ctx->S.ptr, ctx->n, (cudaStream_t)stream))) return rc;
     stage(ctx, make_const(sys), step, stg, dt, (cudaStream_t)stream);
     GS_CUDA(cudaGetLastError());
     return GS_OK;
@@ -672,9 +846,17 @@ int gs_profile_enable(gs_context* ctx, int32_t on) {
     return GS_OK;
 }
 
-int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int32_t reset) {
-    if (!ctx || !pair_ms || !pair_launches || !launches) return fail(GS_ERR_INVALID, "NULL argument");
-    double total = 0.0;
+int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int64_t* pairs,
+                    int32_t reset) {
+    if (!ctx || !pair_ms || !pair_launches || !launches || !pairs) return fail(GS_ERR_INVALID, "NULL argument");
+    unsigned long long acc = 0;
+    if (ctx->c_acc.ptr) {
+        GS_CUDA(cudaMemcpy(&acc, ctx->c_acc.ptr, sizeof(acc), cudaMemcpyDeviceToHost));
+        if (reset) GS_CUDA(cudaMemset(ctx->c_acc.ptr, 0, sizeof(acc)));
+    }
+    *pairs = (int64_t)acc + ctx->host_pairs;
+    if (reset) ctx->host_pairs = 0;
+    double total = ctx->prof_ms_acc;
     if (ctx->prof_used >= 2) {
         GS_CUDA(cudaEventSynchronize(ctx->prof_events[ctx->prof_used - 1]));
         for (size_t k = 0; k + 1 < ctx->prof_used; k += 2) {
@@ -687,6 +869,7 @@ int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, in
     *pair_launches = ctx->pair_launches;
     *launches = ctx->launches;
     if (reset) {
+        ctx->prof_ms_acc = 0.0;
         ctx->prof_used = 0;
         ctx->pair_launches = 0;
         ctx->launches = 0;

@@ -1,0 +1,251 @@
+// gs_cell.cu — cell-list fp64 RHS for the numerically compact kernels (KD-1).
+//
+// The reference sums all N^2 pairs (particles.py:79-117).  With the conical kernel at
+// alpha = sigma / (53 ln 2) every pair beyond the support radius sigma contributes less
+// than 2^-53 of a neighbour's term, so the device may sum only pairs with d_ij < cutoff
+// (the truncation changes results by ~1e-15 relative).  Per RHS:
+//
+//   1. bounding box of the stage positions (block partials + one-block finish) and the
+//      grid parameters (cell edge >= cutoff; coarsened if the grid would exceed the cap),
+//      all on the device — no host round trip;
+//   2. cell key per particle, stable LSD radix sort of (key, index) with CUB, cell start
+//      offsets (start[c] = first sorted position with key >= c), permuted copy of the
+//      32-byte (x, y, px, py) records so that a cell's particles are contiguous;
+//   3. the pair kernel: one thread per target in sorted order; the 3 stencil rows of its
+//      cell are 3 contiguous sorted ranges.  Candidates are filtered (4 FP64 ops) into a
+//      per-lane list in shared memory, then the accepted pairs run the full pair body of
+//      gs_device.cuh — lanes do not idle on rejected candidates.  Each target's sum runs
+//      over its candidates in a fixed order (row, then sorted position), so results are
+//      deterministic.  Raw sums are written at the target's original index; the shared
+//      finish kernel (gs_dense.cu) applies scales, sigma2 and the RK4 stage epilogue.
+//
+// Bound: FP64 pipe for the pair kernel (~90 DP slots per HBM byte at config 5); the build
+// kernels (sort / scan / permute) are HBM/latency bound and are measured separately.
+#include <cub/cub.cuh>
+
+#include "gs_cell.cuh"
+
+namespace gsb {
+
+namespace {
+
+constexpr int kBB = 256;        // bbox block
+constexpr int kCB = 128;        // pair-kernel threads per CTA
+constexpr int kCL = 64;         // candidate chunk (per-lane list capacity)
+
+__global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double* red) {
+    __shared__ double s[4][kBB];
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * kBB + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBB) {
+        const double4 v = S[i];
+        bad |= !(isfinite(v.x) && isfinite(v.y));
+        mnx = fmin(mnx, v.x); mxx = fmax(mxx, v.x);
+        mny = fmin(mny, v.y); mxy = fmax(mxy, v.y);
+    }
+    if (bad) { mnx = NAN; }
+    s[0][threadIdx.x] = mnx; s[1][threadIdx.x] = mny; s[2][threadIdx.x] = mxx; s[3][threadIdx.x] = mxy;
+    __syncthreads();
+    for (int w = kBB / 2; w; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            const bool nan0 = s[0][threadIdx.x] != s[0][threadIdx.x] || s[0][o] != s[0][o];
+            s[0][threadIdx.x] = nan0 ? NAN : fmin(s[0][threadIdx.x], s[0][o]);
+            s[1][threadIdx.x] = fmin(s[1][threadIdx.x], s[1][o]);
+            s[2][threadIdx.x] = fmax(s[2][threadIdx.x], s[2][o]);
+            s[3][threadIdx.x] = fmax(s[3][threadIdx.x], s[3][o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) red[4 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, GridParams* gp) {
+    if (threadIdx.x != 0) return;
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    bool bad = false;
+    for (int b = 0; b < nb; ++b) {
+        bad |= red[4 * b] != red[4 * b];
+        mnx = fmin(mnx, red[4 * b]); mny = fmin(mny, red[4 * b + 1]);
+        mxx = fmax(mxx, red[4 * b + 2]); mxy = fmax(mxy, red[4 * b + 3]);
+    }
+    GridParams g;
+    if (bad || !isfinite(mnx) || !isfinite(mxx) || !isfinite(mny) || !isfinite(mxy)) {
+        // non-finite stage state: one cell (the stage check has already recorded the failure)
+        g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.nx = 1; g.ny = 1;
+    } else {
+        double h = cutoff;
+        for (;;) {
+            const double fx = floor((mxx - mnx) / h) + 1.0, fy = floor((mxy - mny) / h) + 1.0;
+            if (fx * fy <= (double)cap) {
+                g.nx = (int)fx; g.ny = (int)fy;
+                break;
+            }
+            h *= 1.25;
+        }
+        g.x0 = mnx; g.y0 = mny; g.inv_h = 1.0 / h;
+    }
+    g.ncells = g.nx * g.ny;
+    *gp = g;
+}
+
+__device__ __forceinline__ int cell_coord(double v, double v0, double inv_h, int nmax) {
+    int c = (int)floor((v - v0) * inv_h);
+    return min(max(c, 0), nmax - 1);
+}
+
+__global__ void k_cell_keys(const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
+                            unsigned* keys, unsigned* vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const GridParams g = *gp;
+    const double4 v = S[i];
+    const int cx = cell_coord(v.x, g.x0, g.inv_h, g.nx), cy = cell_coord(v.y, g.y0, g.inv_h, g.ny);
+    keys[i] = (unsigned)(cy * g.nx + cx);
+    vals[i] = (unsigned)i;
+}
+
+// start[c] = first sorted position whose key >= c, for c in [0, ncells]; permuted records
+__global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, const unsigned* __restrict__ perm,
+                                     const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
+                                     int* start, double4* Ss) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > n) return;
+    const int ncells = gp->ncells;
+    const long long prev = (k == 0) ? -1 : (long long)keys_sorted[k - 1];
+    const long long cur = (k == n) ? (long long)ncells : (long long)keys_sorted[k];
+    for (long long c = prev + 1; c <= cur; ++c) start[c] = (int)k;
+    if (k < n) Ss[k] = S[perm[k]];
+}
+
+// TPL lanes share one target (small N: fills the GPU); each lane takes every TPL-th
+// candidate of the stencil rows and the lanes' sums are xor-butterfly reduced, so every
+// target's summation order is fixed.
+template <int FAM, int TPL>
+__global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ Ss, const unsigned* __restrict__ perm,
+                                                   const unsigned* __restrict__ keys_sorted,
+                                                   const int* __restrict__ start, const GridParams* __restrict__ gp,
+                                                   int64_t n, int64_t row0, int64_t row1, double k1, double rc2,
+                                                   double4* __restrict__ part, DevStatus* st, unsigned long long event,
+                                                   const double* __restrict__ tbl_g, unsigned long long* accepted) {
+    __shared__ double s_tbl[kTbl];
+    __shared__ int s_list[kCL][kCB];
+    if (*((volatile unsigned long long*)&st->first_event) < event) return;
+    for (int t = threadIdx.x; t < kTbl; t += kCB) s_tbl[t] = tbl_g[t];
+    __syncthreads();
+
+    const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
+    const int64_t k = (int64_t)blockIdx.x * (kCB / TPL) + threadIdx.x / TPL;
+    const bool valid = k < n;
+    const int64_t kk = valid ? k : 0;
+    const int64_t i = (int64_t)perm[kk];
+    const bool active = valid && i >= row0 && i < row1;
+    const GridParams g = *gp;
+    const double4 me = Ss[kk];
+    const int key = (int)keys_sorted[kk];
+    const int cy = key / g.nx, cx = key - cy * g.nx;
+    const int xa = max(cx - 1, 0), xb = min(cx + 1, g.nx - 1);
+
+    double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
+    unsigned long long nacc = 0;
+    if (active) {
+        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.ny - 1); ++yy) {
+            const int a = start[yy * g.nx + xa], b = start[yy * g.nx + xb + 1];
+            for (int base = a + sub; base < b; base += TPL * kCL) {
+                const int m = min(kCL, (b - base + TPL - 1) / TPL);
+                int cnt = 0;
+                for (int t = 0; t < m; ++t) {  // filter: d^2 < cutoff^2
+                    const int j = base + TPL * t;
+                    const double2 xy = *reinterpret_cast<const double2*>(&Ss[j]);
+                    const double dx = me.x - xy.x, dy = me.y - xy.y;
+                    if (fma(dx, dx, dy * dy) < rc2) s_list[cnt++][threadIdx.x] = j;
+                }
+                nacc += cnt;
+                for (int u = 0; u < cnt; ++u) {
+                    const int j = s_list[u][threadIdx.x];
+                    const double4 s = Ss[j];
+                    double pdot;
+                    if (pair_accum<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, s_tbl, k1, aqx, aqy, apx, apy,
+                                        pdot)) {
+                        const int64_t jo = (int64_t)perm[j];
+                        if (jo != i && pdot != 0.0) record_event(st, event, (unsigned long long)(i * n + jo));
+                    }
+                }
+            }
+        }
+    }
+    for (int off = TPL >> 1; off; off >>= 1) {
+        aqx += __shfl_xor_sync(0xffffffffu, aqx, off);
+        aqy += __shfl_xor_sync(0xffffffffu, aqy, off);
+        apx += __shfl_xor_sync(0xffffffffu, apx, off);
+        apy += __shfl_xor_sync(0xffffffffu, apy, off);
+    }
+    if (active && sub == 0) part[i - row0] = make_double4(aqx, aqy, apx, apy);
+    if (accepted) {
+        // pair count for the throughput metric (accepted pairs incl. self), one atomic per warp
+        for (int off = 16; off; off >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, off);
+        if ((threadIdx.x & 31) == 0 && nacc) atomicAdd(accepted, nacc);
+    }
+}
+
+}  // namespace
+
+size_t cell_cub_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                    (const unsigned*)nullptr, (unsigned*)nullptr, (int)n, 0, 32);
+    return bytes;
+}
+
+int64_t cell_cap(int64_t n) {
+    int64_t cap = 4096;
+    while (cap < 4 * n) cap <<= 1;
+    return cap;
+}
+
+int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream) {
+    const int nb = (int)std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB);
+    k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, w.bbox_red);
+    const int64_t cap = cell_cap(n);
+    k_grid_params<<<1, 32, 0, stream>>>(w.bbox_red, nb, cutoff, cap, w.gp);
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
+    int end_bit = 1;
+    while ((1ll << end_bit) < cap) ++end_bit;
+    size_t bytes = w.cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(w.cub_temp, bytes, w.keys, w.keys_sorted, w.vals, w.perm,
+                                                    (int)n, 0, end_bit, stream);
+    if (e != cudaSuccess) return (int)e;
+    k_cell_start_permute<<<(unsigned)((n + 1 + 255) / 256), 256, 0, stream>>>(w.keys_sorted, w.perm, S, n, w.gp,
+                                                                            w.start, w.Ss);
+    return 0;
+}
+
+void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t row0, int64_t row1, double4* part,
+                      DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                      cudaStream_t stream) {
+    const double rc2 = sc.cutoff * sc.cutoff;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int tpl = 1;  // lanes per target: enough threads to cover every SM ~8 warps deep
+    while (tpl < 16 && n * tpl < (int64_t)sms * 1024) tpl *= 2;
+    const unsigned blocks = (unsigned)((n * tpl + kCB - 1) / kCB);
+#define GS_CELL_LAUNCH(F, T)                                                                                   \
+    k_cell_pair<F, T><<<blocks, kCB, 0, stream>>>(w.Ss, w.perm, w.keys_sorted, w.start, w.gp, n, row0, row1,  \
+                                                  sc.k1, rc2, part, st, event, tbl_dev, accepted)
+#define GS_CELL_FAM(F)                                    \
+    switch (tpl) {                                        \
+        case 1: GS_CELL_LAUNCH(F, 1); break;              \
+        case 2: GS_CELL_LAUNCH(F, 2); break;              \
+        case 4: GS_CELL_LAUNCH(F, 4); break;              \
+        case 8: GS_CELL_LAUNCH(F, 8); break;              \
+        default: GS_CELL_LAUNCH(F, 16); break;            \
+    }
+    if (sc.fam == kFamConical) { GS_CELL_FAM(kFamConical) }
+    else { GS_CELL_FAM(kFamGaussian) }
+#undef GS_CELL_FAM
+#undef GS_CELL_LAUNCH
+}
+
+}  // namespace gsb

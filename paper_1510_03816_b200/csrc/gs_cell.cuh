@@ -1,0 +1,42 @@
+// gs_cell.cuh — cell-list workspace and launchers (gs_cell.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gs_kernels.cuh"
+
+namespace gsb {
+
+struct GridParams {
+    double x0, y0, inv_h;
+    int nx, ny, ncells, pad;
+};
+
+constexpr int kCellBboxBlocks = 296;
+
+// Device buffers owned by the context (sizes for n particles, cell_cap(n) cells).
+struct CellWs {
+    unsigned* keys;         // n
+    unsigned* keys_sorted;  // n
+    unsigned* vals;         // n
+    unsigned* perm;         // n: sorted position -> original index
+    int* start;             // cell_cap(n) + 1
+    double4* Ss;            // n: records in sorted order
+    double* bbox_red;       // 4 * kCellBboxBlocks
+    GridParams* gp;         // 1
+    void* cub_temp;
+    size_t cub_bytes;
+};
+
+size_t cell_cub_bytes(int64_t n);
+int64_t cell_cap(int64_t n);
+// Builds the grid for the n records of S (positions of the current stage).  Returns a
+// cudaError_t value (0 on success).
+int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream);
+// Raw pair sums of the targets with original index in [row0, row1) -> part[i - row0].
+// `accepted` (nullable) accumulates the number of evaluated pairs (d < cutoff, self included).
+void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t row0, int64_t row1, double4* part,
+                      DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                      cudaStream_t stream);
+
+}  // namespace gsb

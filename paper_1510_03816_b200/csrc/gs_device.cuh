@@ -59,18 +59,24 @@ __device__ __forceinline__ double rsqrt_refined(double x) {
 }
 
 // 2^(y / kTbl) for y <= 0 (y = -r/alpha * kTbl/ln2); 0 below 2^-1020.
+// Rounding trick with a biased magic 1.5*2^52 + 2^30: for y in [-2^30, 0] the high word of
+// s = y + magic is exactly kMagicHi and its low word is rint(y) + 2^30, so one integer
+// compare on each word rejects both the underflow range and far-away pairs (|y| > 2^30,
+// where the low word would wrap) without an extra FP64 instruction.
+constexpr double kRoundMagicK = 6755399441055744.0 + 1073741824.0;
+constexpr int kMagicHi = 0x43380000;
 __device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ tbl) {
-    double s = y + kRoundMagic;
-    double kd = s - kRoundMagic;
+    double s = y + kRoundMagicK;
+    double kd = s - kRoundMagicK;
     double u = y - kd;
-    int k = __double2loint(s);
-    int kc = max(k, kKMin);
-    double t = tbl[kc & (kTbl - 1)];
-    int n = kc >> kTblBits;
+    const int k = __double2loint(s) - (1 << 30);
+    const bool ok = (__double2hiint(s) == kMagicHi) & (k >= kKMin);
+    double t = tbl[k & (kTbl - 1)];
+    int n = k >> kTblBits;
     double tn = __hiloint2double(__double2hiint(t) + (n << 20), __double2loint(t));
     double e1 = u * fma(fma(fma(kC4, u, kC3), u, kC2), u, kC1);
     double g = fma(tn, e1, tn);
-    return (k < kKMin) ? 0.0 : g;
+    return ok ? g : 0.0;
 }
 
 // Accumulates one ordered pair.  k1 = -kTbl/(alpha ln2) (conical, multiplies r) or

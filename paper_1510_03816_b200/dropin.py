@@ -1,0 +1,95 @@
+"""Drop-in registration: rebind the reference package ``geoshoot`` onto the B200 path.
+
+The reference has no plugin registry: its modules import their
+callees by name, so every alias must be rebound (SURVEY.md §8(b) "Rebinding points"):
+
+    rhs          geoshoot.particles.rhs, geoshoot.integrator.rhs (integrator.py:17, used :89), geoshoot.rhs
+    evolve       geoshoot.integrator.evolve, geoshoot.shooting.evolve (shooting.py:28), geoshoot.analysis.evolve
+                 (analysis.py:19), geoshoot.cli.evolve (cli.py:34), geoshoot.evolve
+    match        geoshoot.shooting.match, geoshoot.analysis.match (analysis.py:23), geoshoot.cli.match
+                 (cli.py:58), geoshoot.match
+    hamiltonian  geoshoot.particles.hamiltonian, geoshoot.shooting.hamiltonian (shooting.py:30), geoshoot.hamiltonian
+
+After ``install()`` the reference's own callers (analysis, cli, newton_match, the velocity-
+space feedback loop) run their shoots on the device, with the reference's exception classes
+and result types.  ``match`` with the momentum update runs entirely on the device; the
+velocity update keeps the reference's own host Gram solve around device shoots.  Kernel
+families the device does not provide (bessel) raise ConfigurationError — there is no CPU
+fallback.  Use ``pytest -p paper_1510_03816_b200.pytest_dropin`` to run a geoshoot-based
+test suite against the device path.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import errors as _errors
+from . import integrator as _integrator
+from . import particles as _particles
+from . import shooting as _shooting
+from . import types as _types
+
+_saved: list = []
+_ALIASES = {
+    "rhs": ("particles", "integrator", ""),
+    "evolve": ("integrator", "shooting", "analysis", "cli", ""),
+    "match": ("shooting", "analysis", "cli", ""),
+    "hamiltonian": ("particles", "shooting", ""),
+}
+
+
+def _module(pkg, sub: str):
+    if not sub:
+        return pkg
+    try:
+        return importlib.import_module(f"{pkg.__name__}.{sub}")
+    except ImportError:
+        return None
+
+
+def install(pkg=None):
+    """Rebind ``geoshoot`` (or the given package object) onto this package.  Idempotent."""
+    if _saved:
+        return pkg or importlib.import_module("geoshoot")
+    pkg = pkg or importlib.import_module("geoshoot")
+    ref_shooting = _module(pkg, "shooting")
+    original_match = ref_shooting.match
+
+    for name in ("GeoshootError", "ConfigurationError", "DegenerateConfigurationError", "DivergenceError"):
+        _saved.append((_errors, name, getattr(_errors, name)))
+        setattr(_errors, name, getattr(pkg, name))
+    _types.use(ParticleState=pkg.ParticleState, EvolveResult=pkg.EvolveResult, EvolveConfig=pkg.EvolveConfig,
+               MatchResult=pkg.MatchResult, LandmarkTemplate=pkg.LandmarkTemplate)
+
+    def match(reference, target, cfg):
+        """shooting.match: momentum update on the device; velocity update = the reference's
+        own loop (shooting.py:259-301) whose shoots call the rebound device ``evolve``."""
+        if str(getattr(cfg.update_space, "value", cfg.update_space)) == "momentum":
+            return _shooting.match(reference, target, cfg)
+        return original_match(reference, target, cfg)
+
+    impl = {"rhs": _particles.rhs, "evolve": _integrator.evolve, "match": match,
+            "hamiltonian": _particles.hamiltonian}
+    for fname, subs in _ALIASES.items():
+        for sub in subs:
+            mod = _module(pkg, sub)
+            if mod is not None and hasattr(mod, fname):
+                _saved.append((mod, fname, getattr(mod, fname)))
+                setattr(mod, fname, impl[fname])
+    return pkg
+
+
+def uninstall() -> None:
+    """Restore every attribute ``install`` rebound."""
+    while _saved:
+        mod, name, val = _saved.pop()
+        setattr(mod, name, val)
+    from . import integrator, particles, shapes, shooting  # noqa: F401  (re-register own types)
+
+    _types.use(ParticleState=particles.ParticleState, EvolveResult=integrator.EvolveResult,
+               EvolveConfig=integrator.EvolveConfig, MatchResult=shooting.MatchResult,
+               LandmarkTemplate=shapes.LandmarkTemplate)
+
+
+def installed() -> bool:
+    return bool(_saved)
