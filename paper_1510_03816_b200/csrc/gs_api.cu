@@ -95,6 +95,7 @@ struct gs_context {
     std::vector<cudaEvent_t>* capture_events = nullptr;  // non-null while capturing
     cudaStream_t cap_stream = nullptr;
     int graphs_on = 1;
+    int sym_on = 1;                     // symmetric dense kernel for full-row RHS
     double prof_ms_acc = 0.0;           // pair-kernel time already harvested (graph replays)
 };
 
@@ -256,7 +257,12 @@ int ensure_session(gs_context* ctx, int64_t n, int64_t nrows) {
     GS_CUDA(ctx->S.ensure(n + kStatePad));
     GS_CUDA(ctx->B.ensure(nrows));
     GS_CUDA(ctx->A.ensure(nrows));
-    GS_CUDA(ctx->part.ensure((size_t)plan.nchunks * nrows));
+    size_t part = (size_t)plan.nchunks * nrows;
+    if (nrows == n) {  // symmetric path: nb slots of nb * kDB rows
+        const size_t nb = (size_t)((n + kDB - 1) / kDB);
+        part = std::max(part, nb * nb * kDB);
+    }
+    GS_CUDA(ctx->part.ensure(part));
     return GS_OK;
 }
 
@@ -298,6 +304,14 @@ cudaEvent_t prof_event(gs_context* ctx) {
         ctx->prof_events.push_back(e);
     }
     return ctx->prof_events[ctx->prof_used++];
+}
+
+// Inside a stream capture the record must be "external" to stay a real, timeable event
+// on every graph replay; otherwise it would only be an intra-graph dependency.
+void prof_mark(gs_context* ctx, cudaStream_t stream) {
+    cudaEvent_t e = prof_event(ctx);
+    if (ctx->capture_events) cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal);
+    else cudaEventRecord(e, stream);
 }
 
 CellWs cell_ws(gs_context* ctx) {
@@ -348,39 +362,60 @@ int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64
     return GS_OK;
 }
 
+constexpr int64_t kSymMinN = 1024;
+
+bool use_sym(const gs_context* ctx, int64_t n, int64_t row0, int64_t nrows) {
+    return ctx->sym_on && !ctx->cell_on && row0 == 0 && nrows == n && n >= kSymMinN;
+}
+
+struct PairOut {
+    int nchunks;
+    int64_t pstride;
+};
+
 // The pair kernel (the hot spot) of every RHS goes through here: timed when profiling is on.
-// Dense: part holds plan.nchunks chunk partials; cell list: one record per row.
-void pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
-                 const DensePlan& plan, double4* part, unsigned long long ev, cudaStream_t stream) {
-    if (ctx->cell_on) {
+// Returns how the partials are laid out for k_finish: asymmetric dense = plan.nchunks chunk
+// partials per row; symmetric dense = nb slot partials per row; cell list = one per row.
+PairOut pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
+                    const DensePlan& plan, double4* part, unsigned long long ev, cudaStream_t stream) {
+    PairOut out{plan.nchunks, 0};
+    if (use_sym(ctx, n, row0, nrows)) {
+        const int64_t nb = (n + kDB - 1) / kDB;
+        out = PairOut{(int)nb, nb * kDB};
+        if (ctx->prof_on) prof_mark(ctx, stream);
+        launch_dense_sym(sc, S, n, part, nb * kDB, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
+        if (ctx->prof_on) prof_mark(ctx, stream);
+        ctx->host_pairs += nrows * n;
+    } else if (ctx->cell_on) {
+        out = PairOut{1, 0};
         CellWs w = cell_ws(ctx);
         cell_build(w, S, n, sc.cutoff, stream);
         ctx->launches += 6;  // bbox, params, keys, 2x radix passes (approx.), start/permute
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        if (ctx->prof_on) prof_mark(ctx, stream);
         launch_cell_pair(sc, w, n, row0, row0 + nrows, part, ctx->st.ptr, ev, ctx->tbl.ptr,
                          ctx->prof_on ? ctx->c_acc.ptr : nullptr, stream);
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        if (ctx->prof_on) prof_mark(ctx, stream);
     } else {
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        if (ctx->prof_on) prof_mark(ctx, stream);
         launch_dense_partial(sc, S, n, row0, nrows, plan, part, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), stream);
+        if (ctx->prof_on) prof_mark(ctx, stream);
         ctx->host_pairs += nrows * n;
     }
     ctx->launches++;
     ctx->pair_launches++;
+    return out;
 }
-
-inline int pair_chunks(gs_context* ctx, const DensePlan& plan) { return ctx->cell_on ? 1 : plan.nchunks; }
 
 // One RK4 stage for the session's rows (pair kernel + finish epilogue).
 void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cudaStream_t stream) {
     const int64_t n = ctx->n, nrows = ctx->row1 - ctx->row0;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)s;
-    pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
+    const PairOut po = pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
     ctx->launches++;  // finish
     FinishArgs fa{};
-    fa.part = ctx->part.ptr; fa.nchunks = pair_chunks(ctx, plan); fa.nrows = nrows; fa.row0 = ctx->row0;
+    fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = nrows;
+    fa.row0 = ctx->row0;
     fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr;
     fa.stage = s; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
     launch_finish(kFinStage, sc, fa, stream);
@@ -498,6 +533,7 @@ int gs_create(gs_context** out, int device) {
     gs_context* ctx = new gs_context();
     ctx->device = device;
     if (const char* g = std::getenv("GS_B200_GRAPHS")) ctx->graphs_on = std::atoi(g) != 0;
+    if (const char* g = std::getenv("GS_B200_SYM")) ctx->sym_on = std::atoi(g) != 0;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
     std::vector<double> t(kTbl);
@@ -564,10 +600,11 @@ static int rhs_impl(gs_context* ctx, const gs_system_t* sys, int64_t n, const do
     k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 1);
     if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
-    pair_kernel(ctx, sc, ctx->S.ptr, n, row0, nrows, plan, ctx->part.ptr, 2ull, s);
+    const PairOut po = pair_kernel(ctx, sc, ctx->S.ptr, n, row0, nrows, plan, ctx->part.ptr, 2ull, s);
     ctx->launches += 3;  // reset, pack, finish
     FinishArgs fa{};
-    fa.part = ctx->part.ptr; fa.nchunks = pair_chunks(ctx, plan); fa.nrows = nrows; fa.row0 = row0; fa.S = ctx->S.ptr;
+    fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = nrows; fa.row0 = row0;
+    fa.S = ctx->S.ptr;
     fa.dq = dq; fa.dp = dp; fa.st = ctx->st.ptr; fa.event = 3ull;
     launch_finish(kFinRhs, sc, fa, s);
     GS_CUDA(cudaGetLastError());
@@ -609,10 +646,11 @@ int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const dou
     const DensePlan plan = dense_plan(n, ctx->sm_count);
     // coincident pairs are irrelevant to H (particles.py:127-128 has no check): use an event id
     // that is never reported
-    pair_kernel(ctx, sc, ctx->S.ptr, n, 0, n, plan, ctx->part.ptr, 2ull, s);
+    const PairOut po = pair_kernel(ctx, sc, ctx->S.ptr, n, 0, n, plan, ctx->part.ptr, 2ull, s);
     ctx->launches += 5;  // reset, pack, finish, 2 reductions
     FinishArgs fa{};
-    fa.part = ctx->part.ptr; fa.nchunks = pair_chunks(ctx, plan); fa.nrows = n; fa.row0 = 0; fa.S = ctx->S.ptr;
+    fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = n; fa.row0 = 0;
+    fa.S = ctx->S.ptr;
     fa.ham = ctx->ham.ptr; fa.st = ctx->st.ptr; fa.event = 0ull;  // never skipped
     launch_finish(kFinHam, sc, fa, s);
     const int nb = (int)std::min<int64_t>(kRedBlocks, (n + 255) / 256);

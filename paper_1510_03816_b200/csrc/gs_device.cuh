@@ -114,6 +114,43 @@ __device__ __forceinline__ bool pair_accum(double xi, double yi, double pxi, dou
     return z;
 }
 
+// Symmetric variant: one evaluation of G and c serves both ordered pairs (i <- j) and
+// (j <- i) (G, c symmetric; q_j - q_i = -(q_i - q_j)).  Same exp/rsqrt path as pair_accum.
+template <int FAM>
+__device__ __forceinline__ bool pair_sym(double xi, double yi, double pxi, double pyi, double xj, double yj,
+                                         double pxj, double pyj, const double* __restrict__ tbl, double k1,
+                                         double& aqx, double& aqy, double& apx, double& apy, double& jqx,
+                                         double& jqy, double& jpx, double& jpy, double& pdot_out) {
+    double dx = xi - xj;
+    double dy = yi - yj;
+    double r2 = fma(dx, dx, dy * dy);
+    double pdot = fma(pxi, pxj, pyi * pyj);
+    bool z = (r2 == 0.0);
+    double g, c;
+    if (FAM == kFamConical) {
+        double r2s = z ? 1.0 : r2;
+        double rs = rsqrt_refined(r2s);
+        double r = r2s * rs;
+        g = exp2_tbl(r * k1, tbl);
+        g = z ? 1.0 : g;
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl(r2 * k1, tbl);
+        c = pdot * g;
+    }
+    c = z ? 0.0 : c;
+    aqx = fma(g, pxj, aqx);
+    aqy = fma(g, pyj, aqy);
+    apx = fma(c, dx, apx);
+    apy = fma(c, dy, apy);
+    jqx = fma(g, pxi, jqx);
+    jqy = fma(g, pyi, jqy);
+    jpx = fma(-c, dx, jpx);
+    jpy = fma(-c, dy, jpy);
+    pdot_out = pdot;
+    return z;
+}
+
 __device__ __forceinline__ bool finite4(double a, double b, double c, double d) {
     return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d);
 }

@@ -33,6 +33,11 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
                           const DensePlan& plan, double4* part, DevStatus* st, unsigned long long event,
                           const double* tbl_dev, cudaStream_t stream);
 
+// Symmetric all-pairs RHS of all n rows (single rank): each unordered pair once; row i gets
+// nb = ceil(n/kDB) partials part[slot * pstride + i], pstride >= nb * kDB.
+void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
+                      unsigned long long event, const double* tbl_dev, cudaStream_t stream);
+
 // Finish modes
 constexpr int kFinRhs = 0;    // write dq, dp rows ((nrows, 2) AoS)
 constexpr int kFinStage = 1;  // RK4 stage epilogue (integrator.py:98-114)
@@ -41,6 +46,7 @@ constexpr int kFinHam = 2;    // ham[li] = p_i . dq_i (sigma2 excluded)
 struct FinishArgs {
     const double4* part;
     int nchunks;
+    int64_t pstride;   // distance between chunk partials of one row (0: nrows)
     int64_t nrows, row0;
     double4* S;        // stage state (all n rows)
     double4* B;        // base rows (nrows)

@@ -343,17 +343,18 @@ def test_cell_path_detects_coincident_pairs(cuda):
 
 
 def test_cell_match_matches_dense_match(cuda):
-    """Config-4-like clustered match at N = 4096 through the cell list and the dense path."""
+    """A converging match (circle -> ellipse, N = 1024, sigma = 0.02: 36 iterations in the
+    C oracle) through the cell list and through the dense path."""
     import paper_1510_03816_b200 as gs
-    from paper_1510_03816_b200 import configs
 
-    w = configs.c4(4096)
-    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
-    cfg = gs.ShootingConfig(h=0.1, epsilon=1e-6, max_iter=100, update_space="momentum",
-                            evolve=gs.EvolveConfig(steps=w.steps), system=spec)
-    ref, tgt = gs.LandmarkTemplate(w.q, "X"), gs.LandmarkTemplate(w.target, "Y")
+    n = 1024
+    ref, tgt = gs.circle(1.0, n=n), gs.ellipse_rot_shift(1.3, 0.7, 0.0, n=n)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.02 / gs.LAMBDA))
+    cfg = gs.ShootingConfig(h=0.3, epsilon=1e-6, max_iter=100, update_space="momentum",
+                            evolve=gs.EvolveConfig(steps=20), system=spec)
     with _cell(gs):
         rc = gs.match(ref, tgt, cfg)
+    assert rc.converged and rc.iterations == 36
     gs.set_path("dense")
     try:
         rd = gs.match(ref, tgt, cfg)

@@ -1,0 +1,172 @@
+"""Host-side logic of the drop-in (no GPU): validation, error messages, templates, configs, rebinding."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+import paper_1510_03816_b200 as gs
+from paper_1510_03816_b200 import _native as N
+from paper_1510_03816_b200 import configs, device, shapes
+from paper_1510_03816_b200.integrator import frame_times
+
+REF_SRC = "/root/reference/pkg/src"
+have_reference = os.path.isdir(REF_SRC)
+
+
+def _reference():
+    import sys
+
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import geoshoot
+
+    return geoshoot
+
+
+def test_status_messages_match_reference_wording():
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msgs = json.load(f)
+    e = device.status_exception(N.Status(N.GS_ERR_COINCIDENT, 0, 0, 1, 0, 2))
+    assert isinstance(e, gs.DegenerateConfigurationError) and str(e) == msgs["rhs_coincident"]
+    e = device.status_exception(N.Status(N.GS_ERR_COINCIDENT, 1, 0, 1, 0, 0), 1.0, 10)
+    assert str(e) == msgs["evolve_coincident"]
+    e = device.status_exception(N.Status(N.GS_ERR_NONFINITE_STAGE, 1, -1, -1, 0, 1), 1.0, 4)
+    assert isinstance(e, gs.DivergenceError) and str(e) == msgs["evolve_divergence"]
+    e = device.status_exception(N.Status(N.GS_ERR_NONFINITE_STATE, 3, -1, -1, 0, 7), 1.0, 60)
+    assert str(e) == ("non-finite state at step 3 (t = 0.05); the step size is too large for this configuration")
+    assert device.status_exception(N.Status(N.GS_OK, 0, -1, -1, 0, 0)) is None
+
+
+def test_frame_times_follow_the_reference_grid():
+    from conftest import cases
+
+    c = cases("evolve_cases.npz")["capture_10_3"]
+    tf, steps, cap = c["cfg"]
+    np.testing.assert_array_equal(frame_times(tf, int(steps), int(cap)), c["times"])
+    assert device.n_frames(100, 7) == 2 + 100 // 7
+    assert device.n_frames(10, 1) == 11 and device.n_frames(10, 0) == 0
+
+
+def test_first_coincident_pair_is_row_major_first():
+    rng = np.random.default_rng(0)
+    for trial in range(200):
+        n = int(rng.integers(2, 40))
+        pts = rng.integers(0, 6, (n, 2)).astype(float)  # many duplicates
+        d = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1))
+        np.fill_diagonal(d, np.inf)
+        want = tuple(int(v) for v in np.argwhere(d == 0.0)[0]) if np.any(d == 0.0) else None
+        assert shapes.first_coincident_pair(pts) == want
+    pts = np.array([[0.0, 0.0], [1.0, 2.0], [3.0, 3.0], [1.0, 2.0]])
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msgs = json.load(f)
+    with pytest.raises(gs.DegenerateConfigurationError) as e:
+        gs.LandmarkTemplate(pts, "dup")
+    assert str(e.value) == msgs["template_dup"]
+    pts = np.array([[0.0, 0.0], [-0.0, 0.0]])  # signed zeros coincide
+    assert shapes.first_coincident_pair(pts) == (0, 1)
+
+
+def test_large_template_check_is_fast():
+    import time
+
+    w = configs.c5()
+    t0 = time.perf_counter()
+    gs.LandmarkTemplate(w.q, "X")
+    assert time.perf_counter() - t0 < 10.0
+
+
+def test_config_validation_matches_reference():
+    with pytest.raises(gs.ConfigurationError, match="MomentumDelta"):
+        gs.ShootingConfig(h=0.3, system=gs.SystemSpec(sigma2=0.1))
+    for bad in (dict(h=0.0), dict(h=-1.0), dict(h=float("inf"))):
+        with pytest.raises(gs.ConfigurationError):
+            gs.ShootingConfig(**bad)
+    with pytest.raises(gs.ConfigurationError):
+        gs.ShootingConfig(h=0.5, epsilon=0.0)
+    with pytest.raises(gs.ConfigurationError):
+        gs.ShootingConfig(h=0.5, max_iter=0)
+    cfg = gs.ShootingConfig(h=0.5, update_space="momentum", stop_rule="momentum-delta", norm="l2")
+    assert cfg.update_space is gs.UpdateSpace.MOMENTUM and cfg.norm is gs.ResidualNorm.L2
+    for bad in (dict(t_final=0.0), dict(steps=0), dict(capture_every=-1)):
+        with pytest.raises(gs.ConfigurationError):
+            gs.EvolveConfig(**bad)
+    with pytest.raises(gs.ConfigurationError):
+        gs.SystemSpec(sigma2=-0.1)
+    with pytest.raises(ValueError):
+        gs.ParticleState(np.zeros((3, 3)), np.zeros((3, 2)))
+    bad = np.zeros((3, 2))
+    bad[0, 0] = np.nan
+    with pytest.raises(ValueError):
+        gs.ParticleState(bad, np.zeros((3, 2)))
+
+
+def test_system_struct_and_kd1_support_radius():
+    s = device.system_struct(gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.05 / gs.LAMBDA), sigma2=0.1))
+    assert s.family == N.GS_FAMILY_CONICAL and s.normalized == 1 and s.cutoff == pytest.approx(0.05)
+    assert np.exp(-s.cutoff / s.alpha) == pytest.approx(2.0**-53, rel=1e-12)
+    g = device.system_struct(gs.SystemSpec(kernel=gs.KernelSpec(family="gaussian", alpha=0.1, normalized=False)))
+    assert g.family == N.GS_FAMILY_GAUSSIAN and g.normalized == 0
+    assert np.exp(-0.5 * (g.cutoff / 0.1) ** 2) == pytest.approx(2.0**-53, rel=1e-12)
+    with pytest.raises(gs.ConfigurationError, match="not available"):
+        device.system_struct(gs.SystemSpec(kernel=gs.KernelSpec(family="bessel", nu=2.0)))
+
+
+def test_configs_are_deterministic_and_follow_the_recipes():
+    a, b = configs.c4(1000), configs.c4(1000)
+    np.testing.assert_array_equal(a.q, b.q)
+    np.testing.assert_array_equal(a.target, b.target)
+    w = configs.c5(4096)
+    assert w.sigma2 == 0.1 and w.h == 0.4 and w.max_iter == 20 and w.epsilon == 1e-300
+    assert np.abs(w.target - w.q).max() < 0.5
+
+
+@pytest.mark.skipif(not have_reference, reason="reference package not mounted")
+def test_config1_templates_equal_the_reference_generators():
+    ref = _reference()
+    w = configs.c1()
+    np.testing.assert_array_equal(w.q, ref.circle(1.0, n=64).points)
+    np.testing.assert_array_equal(w.target, ref.ellipse_rot_shift(1.3, 0.7, 0.0, (0.0, 0.0), 64).points)
+    np.testing.assert_array_equal(gs.circle(1.0, n=8).points, ref.circle(1.0, n=8).points)
+    np.testing.assert_array_equal(gs.ellipse_rot_shift(1.3, 0.9, 0.4, (0.1, 0.0), n=8).points,
+                                  ref.ellipse_rot_shift(1.3, 0.9, 0.4, (0.1, 0.0), n=8).points)
+
+
+@pytest.mark.skipif(not have_reference, reason="reference package not mounted")
+def test_dropin_rebinds_every_alias_and_restores():
+    import torch
+
+    from paper_1510_03816_b200 import dropin, integrator, particles, types
+
+    import importlib
+
+    ref = _reference()
+    importlib.import_module("geoshoot.cli")
+    originals = {(m, f): getattr(getattr(ref, m), f) for m, f in [
+        ("particles", "rhs"), ("integrator", "rhs"), ("integrator", "evolve"), ("shooting", "evolve"),
+        ("analysis", "evolve"), ("cli", "evolve"), ("shooting", "match"), ("analysis", "match"), ("cli", "match"),
+        ("particles", "hamiltonian"), ("shooting", "hamiltonian")]}
+    dropin.install(ref)
+    try:
+        assert ref.integrator.rhs is particles.rhs and ref.particles.rhs is particles.rhs and ref.rhs is particles.rhs
+        for m in ("integrator", "shooting", "analysis", "cli"):
+            assert getattr(ref, m).evolve is integrator.evolve
+        assert ref.shooting.match is ref.analysis.match is ref.cli.match is ref.match
+        assert ref.shooting.hamiltonian is particles.hamiltonian
+        assert gs.errors.DivergenceError is ref.DivergenceError
+        assert types.get("EvolveResult") is ref.EvolveResult
+        if not torch.cuda.is_available():
+            st = ref.ParticleState(np.zeros((3, 2)), np.zeros((3, 2)))
+            with pytest.raises(N.NativeUnavailable):
+                ref.rhs(ref.SystemSpec(), st)  # no CPU fallback behind the drop-in
+            with pytest.raises(N.NativeUnavailable):
+                ref.integrator.evolve(ref.SystemSpec(), st)
+    finally:
+        dropin.uninstall()
+    for (m, f), fn in originals.items():
+        assert getattr(getattr(ref, m), f) is fn
+    assert gs.errors.DivergenceError is not ref.DivergenceError
+    assert types.get("EvolveResult") is integrator.EvolveResult
