@@ -257,12 +257,7 @@ int ensure_session(gs_context* ctx, int64_t n, int64_t nrows) {
     GS_CUDA(ctx->S.ensure(n + kStatePad));
     GS_CUDA(ctx->B.ensure(nrows));
     GS_CUDA(ctx->A.ensure(nrows));
-    size_t part = (size_t)plan.nchunks * nrows;
-    if (nrows == n) {  // symmetric path: nb slots of nb * kDB rows
-        const size_t nb = (size_t)((n + kDB - 1) / kDB);
-        part = std::max(part, nb * nb * kDB);
-    }
-    GS_CUDA(ctx->part.ensure(part));
+    GS_CUDA(ctx->part.ensure((size_t)plan.nchunks * nrows));
     return GS_OK;
 }
 
@@ -340,7 +335,7 @@ int ensure_cell(gs_context* ctx, int64_t n) {
 constexpr int64_t kCellMinN = 2048;
 constexpr int kCellMinCells = 25;
 
-int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s) {
+int choose_path_impl(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s) {
     ctx->cell_on = 0;
     if (sys->path == GS_PATH_DENSE) return GS_OK;
     if (sys->path == GS_PATH_CELL && !(sys->cutoff > 0.0))
@@ -365,7 +360,18 @@ int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64
 constexpr int64_t kSymMinN = 1024;
 
 bool use_sym(const gs_context* ctx, int64_t n, int64_t row0, int64_t nrows) {
-    return ctx->sym_on && !ctx->cell_on && row0 == 0 && nrows == n && n >= kSymMinN;
+    return ctx->sym_on && !ctx->cell_on && row0 == 0 && nrows == n && n >= kSymMinN && sym_plan(n).ok;
+}
+
+// Path of this call + the partial buffer it needs (allocated here, never inside a capture).
+int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s) {
+    int rc = choose_path_impl(ctx, sys, S, n, s);
+    if (rc) return rc;
+    if (use_sym(ctx, n, ctx->row0, ctx->row1 - ctx->row0)) {
+        const SymPlan sp = sym_plan(n);
+        GS_CUDA(ctx->part.ensure((size_t)sp.nsb * (size_t)sp.pstride));
+    }
+    return GS_OK;
 }
 
 struct PairOut {
@@ -379,11 +385,11 @@ struct PairOut {
 PairOut pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
                     const DensePlan& plan, double4* part, unsigned long long ev, cudaStream_t stream) {
     PairOut out{plan.nchunks, 0};
-    if (use_sym(ctx, n, row0, nrows)) {
-        const int64_t nb = (n + kDB - 1) / kDB;
-        out = PairOut{(int)nb, nb * kDB};
+    const SymPlan sp = sym_plan(n);
+    if (use_sym(ctx, n, row0, nrows) && ctx->part.cap >= (size_t)sp.nsb * (size_t)sp.pstride) {
+        out = PairOut{sp.nsb, sp.pstride};
         if (ctx->prof_on) prof_mark(ctx, stream);
-        launch_dense_sym(sc, S, n, part, nb * kDB, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
+        launch_dense_sym(sc, S, n, part, sp.pstride, ctx->st.ptr, ev, ctx->tbl.ptr, stream);
         if (ctx->prof_on) prof_mark(ctx, stream);
         ctx->host_pairs += nrows * n;
     } else if (ctx->cell_on) {

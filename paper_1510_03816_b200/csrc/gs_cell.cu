@@ -61,14 +61,30 @@ __global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double*
 }
 
 __global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, GridParams* gp) {
-    if (threadIdx.x != 0) return;
+    __shared__ double s[4][kBB];
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
     double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
-    bool bad = false;
-    for (int b = 0; b < nb; ++b) {
-        bad |= red[4 * b] != red[4 * b];
+    bool badl = false;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        badl |= red[4 * b] != red[4 * b];
         mnx = fmin(mnx, red[4 * b]); mny = fmin(mny, red[4 * b + 1]);
         mxx = fmax(mxx, red[4 * b + 2]); mxy = fmax(mxy, red[4 * b + 3]);
     }
+    s[0][threadIdx.x] = mnx; s[1][threadIdx.x] = mny; s[2][threadIdx.x] = mxx; s[3][threadIdx.x] = mxy;
+    __syncthreads();
+    if (badl) s_bad = 1;
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            s[0][threadIdx.x] = fmin(s[0][threadIdx.x], s[0][o]); s[1][threadIdx.x] = fmin(s[1][threadIdx.x], s[1][o]);
+            s[2][threadIdx.x] = fmax(s[2][threadIdx.x], s[2][o]); s[3][threadIdx.x] = fmax(s[3][threadIdx.x], s[3][o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const bool bad = s_bad != 0;
+    mnx = s[0][0]; mny = s[1][0]; mxx = s[2][0]; mxy = s[3][0];
     GridParams g;
     if (bad || !isfinite(mnx) || !isfinite(mxx) || !isfinite(mny) || !isfinite(mxy)) {
         // non-finite stage state: one cell (the stage check has already recorded the failure)
@@ -130,8 +146,10 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
                                                    const double* __restrict__ tbl_g, unsigned long long* accepted) {
     __shared__ double s_tbl[kTbl];
     __shared__ int s_list[kCL][kCB];
+    __shared__ unsigned long long s_acc_count;
     if (*((volatile unsigned long long*)&st->first_event) < event) return;
     for (int t = threadIdx.x; t < kTbl; t += kCB) s_tbl[t] = tbl_g[t];
+    if (threadIdx.x == 0) s_acc_count = 0;
     __syncthreads();
 
     const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
@@ -184,7 +202,9 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
     if (accepted) {
         // pair count for the throughput metric (accepted pairs incl. self), one atomic per warp
         for (int off = 16; off; off >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, off);
-        if ((threadIdx.x & 31) == 0 && nacc) atomicAdd(accepted, nacc);
+        if ((threadIdx.x & 31) == 0 && nacc) atomicAdd(&s_acc_count, nacc);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_acc_count) atomicAdd(accepted, s_acc_count);
     }
 }
 
@@ -207,7 +227,7 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
     const int nb = (int)std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB);
     k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, w.bbox_red);
     const int64_t cap = cell_cap(n);
-    k_grid_params<<<1, 32, 0, stream>>>(w.bbox_red, nb, cutoff, cap, w.gp);
+    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, w.gp);
     const unsigned blocks = (unsigned)((n + 255) / 256);
     k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
     int end_bit = 1;

@@ -90,102 +90,6 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
 }
 
 // ---------------------------------------------------------------------------------------
-// Symmetric all-pairs RHS (single rank, all rows).  The pair term is symmetric in (i, j)
-// (G_ij = G_ji, c_ij = c_ji, q_j - q_i = -(q_i - q_j)), so each unordered pair is evaluated
-// once and feeds both rows: ~16 DP-pipe slots per ordered pair instead of ~28.
-//
-// Tiles of 128 x 128 over the upper block triangle (I <= J), one CTA (4 warps) per tile.
-// Warp w owns target sub-block w of I (32 targets, accumulators in registers) and visits the
-// 4 source sub-blocks of J in phases k = 0..3 (sub-block (w + k) & 3, so the warps of a
-// phase never share a source sub-block).  Inside a phase, lane l pairs its target with
-// source (l + t) & 31 at step t; the source's accumulator travels with it around the warp
-// (one shuffle from lane l+1 per step), so after 32 steps lane l holds the complete
-// contribution of this warp's 32 targets to source l and adds it to the CTA's shared J-side
-// accumulator.  Diagonal tiles (I == J) are evaluated one-sided.  Partials land in
-// part[slot * pstride + row]: the I-side of tile (I, J) in slot J, the J-side in slot I, so
-// every row receives exactly nb partials, summed in slot order by k_finish (deterministic).
-template <int FAM>
-__global__ void __launch_bounds__(kDB) k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, double k1,
-                                                   double4* __restrict__ part, int64_t pstride, DevStatus* st,
-                                                   unsigned long long event, const double* __restrict__ tbl_g) {
-    __shared__ double s_tbl[kTbl];
-    __shared__ double4 s_src[kDB];
-    __shared__ double4 s_jacc[kDB];
-    if (*((volatile unsigned long long*)&st->first_event) < event) return;
-    for (int t = threadIdx.x; t < kTbl; t += kDB) s_tbl[t] = tbl_g[t];
-
-    // tile t -> (I, J), I <= J, row-major over the upper triangle
-    const long long t = blockIdx.x;
-    const double b2 = 2.0 * nb + 1.0;
-    long long I = (long long)floor((b2 - sqrt(b2 * b2 - 8.0 * (double)t)) * 0.5);
-    auto row_start = [nb](long long r) { return r * nb - r * (r - 1) / 2; };
-    while (I > 0 && row_start(I) > t) --I;
-    while (row_start(I + 1) <= t) ++I;
-    const long long J = I + (t - row_start(I));
-
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t i = I * kDB + threadIdx.x;
-    const double4 zero = make_double4(0.0, 0.0, 0.0, 0.0);
-    const double4 me = (i < n) ? S[i] : zero;
-    const int64_t js = J * kDB + threadIdx.x;
-    s_src[threadIdx.x] = (js < n) ? S[js] : zero;
-    s_jacc[threadIdx.x] = zero;
-    __syncthreads();
-
-    double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
-    if (I == J) {
-#pragma unroll 4
-        for (int jj = 0; jj < kDB; ++jj) {
-            const double4 s = s_src[jj];
-            double pdot;
-            if (pair_accum<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, s_tbl, k1, aqx, aqy, apx, apy, pdot)) {
-                const int64_t j = J * kDB + jj;
-                if (i < n && j != i && j < n && pdot != 0.0)
-                    record_event(st, event, (unsigned long long)(i * n + j));
-            }
-        }
-        if (i < n) part[J * pstride + i] = make_double4(aqx, aqy, apx, apy);
-        return;
-    }
-    for (int k = 0; k < 4; ++k) {
-        const int sb = ((w + k) & 3) * 32;
-        double jqx = 0.0, jqy = 0.0, jpx = 0.0, jpy = 0.0;
-#pragma unroll 2
-        for (int st_ = 0; st_ < 32; ++st_) {
-            const int jl = sb + ((lane + st_) & 31);
-            const double4 s = s_src[jl];
-            double pdot;
-            if (pair_sym<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, s_tbl, k1, aqx, aqy, apx, apy, jqx, jqy,
-                              jpx, jpy, pdot)) {
-                const int64_t j = J * kDB + jl;
-                if (i < n && j < n && pdot != 0.0) record_event(st, event, (unsigned long long)(i * n + j));
-            }
-            const int src = (lane + 1) & 31;
-            jqx = __shfl_sync(0xffffffffu, jqx, src);
-            jqy = __shfl_sync(0xffffffffu, jqy, src);
-            jpx = __shfl_sync(0xffffffffu, jpx, src);
-            jpy = __shfl_sync(0xffffffffu, jpy, src);
-        }
-        double4 a = s_jacc[sb + lane];
-        a.x += jqx; a.y += jqy; a.z += jpx; a.w += jpy;
-        s_jacc[sb + lane] = a;
-        __syncthreads();
-    }
-    if (i < n) part[J * pstride + i] = make_double4(aqx, aqy, apx, apy);
-    if (js < n) part[I * pstride + js] = s_jacc[threadIdx.x];
-}
-
-void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
-                      unsigned long long event, const double* tbl_dev, cudaStream_t stream) {
-    const int nb = (int)((n + kDB - 1) / kDB);
-    const unsigned tiles = (unsigned)((long long)nb * (nb + 1) / 2);
-    if (sc.fam == kFamConical)
-        k_dense_sym<kFamConical><<<tiles, kDB, 0, stream>>>(S, n, nb, sc.k1, part, pstride, st, event, tbl_dev);
-    else
-        k_dense_sym<kFamGaussian><<<tiles, kDB, 0, stream>>>(S, n, nb, sc.k1, part, pstride, st, event, tbl_dev);
-}
-
-// ---------------------------------------------------------------------------------------
 // Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_finish(SysConst sc, FinishArgs a) {

@@ -33,8 +33,17 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
                           const DensePlan& plan, double4* part, DevStatus* st, unsigned long long event,
                           const double* tbl_dev, cudaStream_t stream);
 
-// Symmetric all-pairs RHS of all n rows (single rank): each unordered pair once; row i gets
-// nb = ceil(n/kDB) partials part[slot * pstride + i], pstride >= nb * kDB.
+// Symmetric all-pairs RHS of all n rows (single rank, gs_sym.cu): each unordered pair once;
+// row i gets nsb partials part[slot * pstride + i], pstride = nb * kDB.
+constexpr int kSymMaxG = 8;
+struct SymPlan {
+    int nb;           // 128-row blocks
+    int G;            // blocks per superblock
+    int nsb;          // superblocks = partial slots per row
+    int64_t pstride;  // nb * kDB
+    bool ok;          // partial buffer stays bounded (nsb <= 256)
+};
+SymPlan sym_plan(int64_t n);
 void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
                       unsigned long long event, const double* tbl_dev, cudaStream_t stream);
 
