@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
 
     double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
     unsigned long long nacc = 0;
+    int nz = 0;
     if (active) {
         for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.ny - 1); ++yy) {
             const int a = start[yy * g.nx + xa], b = start[yy * g.nx + xb + 1];
@@ -182,23 +183,43 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
                 for (int u = 0; u < cnt; ++u) {
                     const int j = s_list[u][threadIdx.x];
                     const double4 s = Ss[j];
-                    double pdot;
-                    if (pair_accum<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, s_tbl, k1, aqx, aqy, apx, apy,
-                                        pdot)) {
-                        const int64_t jo = (int64_t)perm[j];
-                        if (jo != i && pdot != 0.0) record_event(st, event, (unsigned long long)(i * n + jo));
-                    }
+                    const double dx = me.x - s.x, dy = me.y - s.y;
+                    const double pdot = fma(me.z, s.z, me.w * s.w);
+                    double gk, c;
+                    int z;
+                    pair_core<FAM>(dx, dy, pdot, s_tbl, k1, gk, c, z);
+                    aqx = fma(gk, s.z, aqx);
+                    aqy = fma(gk, s.w, aqy);
+                    apx = fma(c, dx, apx);
+                    apy = fma(c, dy, apy);
+                    nz += z;
                 }
             }
         }
     }
+    for (int off = TPL >> 1; off; off >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, off);
     for (int off = TPL >> 1; off; off >>= 1) {
         aqx += __shfl_xor_sync(0xffffffffu, aqx, off);
         aqy += __shfl_xor_sync(0xffffffffu, aqy, off);
         apx += __shfl_xor_sync(0xffffffffu, apx, off);
         apy += __shfl_xor_sync(0xffffffffu, apy, off);
     }
-    if (active && sub == 0) part[i - row0] = make_double4(aqx, aqy, apx, apy);
+    if (active && sub == 0) {
+        if (nz > 1) {  // rare: a coincident particle among the candidates
+            for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.ny - 1); ++yy) {
+                const int a = start[yy * g.nx + xa], b = start[yy * g.nx + xb + 1];
+                for (int j = a; j < b; ++j) {
+                    const int64_t jo = (int64_t)perm[j];
+                    if (jo == i) continue;
+                    const double4 s = Ss[j];
+                    const double dx = me.x - s.x, dy = me.y - s.y;
+                    if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) != 0.0) continue;
+                    if (fma(me.z, s.z, me.w * s.w) != 0.0) record_event(st, event, (unsigned long long)(i * n + jo));
+                }
+            }
+        }
+        part[i - row0] = make_double4(aqx, aqy, apx, apy);
+    }
     if (accepted) {
         // pair count for the throughput metric (accepted pairs incl. self), one atomic per warp
         for (int off = 16; off; off >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, off);

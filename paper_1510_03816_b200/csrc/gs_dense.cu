@@ -53,11 +53,12 @@ __global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict
     const int64_t j1 = min(n, j0 + chunk);
 
     double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
+    int nz = 0;
     for (int64_t t0 = j0; t0 < j1; t0 += kDT) {
         __syncthreads();
         for (int t = threadIdx.x; t < kDT; t += kDB) {
             const int64_t j = t0 + t;
-            s_src[t] = (j < j1) ? S[j] : make_double4(0.0, 0.0, 0.0, 0.0);  // zero records add exactly 0
+            s_src[t] = (j < j1) ? S[j] : far_record(t);  // far, p = 0: contributes exactly 0
         }
         __syncthreads();
         const int m = (int)((j1 - t0) < kDT ? (j1 - t0) : kDT);
@@ -65,14 +66,20 @@ __global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict
 #pragma unroll 4
         for (int jj = 0; jj < mr; ++jj) {
             const double4 s = s_src[jj];
-            double pdot;
-            if (pair_accum<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, s_tbl, k1, aqx, aqy, apx, apy, pdot)) {
-                const int64_t j = t0 + jj;
-                if (valid && j != i && j < n && pdot != 0.0)
-                    record_event(st, event, (unsigned long long)(i * n + j));
-            }
+            const double dx = me.x - s.x, dy = me.y - s.y;
+            const double pdot = fma(me.z, s.z, me.w * s.w);
+            double g, c;
+            int z;
+            pair_core<FAM>(dx, dy, pdot, s_tbl, k1, g, c, z);
+            aqx = fma(g, s.z, aqx);
+            aqy = fma(g, s.w, aqy);
+            apx = fma(c, dx, apx);
+            apy = fma(c, dy, apy);
+            nz += z;
         }
     }
+    const int self_in = (i >= j0 && i < j1) ? 1 : 0;
+    if (nz > self_in && valid) record_coincident(S, n, i, me, j0, j1, st, event);  // rare
     if (valid) part[(int64_t)blockIdx.y * nrows + li] = make_double4(aqx, aqy, apx, apy);
 }
 

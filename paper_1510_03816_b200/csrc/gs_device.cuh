@@ -70,13 +70,38 @@ __device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ 
     double kd = s - kRoundMagicK;
     double u = y - kd;
     const int k = __double2loint(s) - (1 << 30);
-    const bool ok = (__double2hiint(s) == kMagicHi) & (k >= kKMin);
+    const bool ok = ((__double2hiint(s) ^ kMagicHi) | ((k - kKMin) >> 31)) == 0;  // one predicate
     double t = tbl[k & (kTbl - 1)];
     int n = k >> kTblBits;
     double tn = __hiloint2double(__double2hiint(t) + (n << 20), __double2loint(t));
     double e1 = u * fma(fma(fma(kC4, u, kC3), u, kC2), u, kC1);
     double g = fma(tn, e1, tn);
     return ok ? g : 0.0;
+}
+
+// ---- lean pair core for the hot loops -------------------------------------------------------
+// G and c for one pair with d^2 computed as dx^2 + dy^2 + 1e-200.  The offset changes nothing
+// for d > 1e-92 and makes the d == 0 pairs (self, coincident particles) come out exactly right
+// without a select: 1/d = 1e100 is finite, G(1e-100) rounds to exactly 1 = G(0), and c * dx =
+// c * 0 = 0, as the reference's zeroed diagonal (particles.py:100-105).  `z` flags
+// d^2 == 1e-200 (d == 0, or d < 1e-208) on the integer pipe; callers re-scan only when a
+// non-self pair was flagged (the reference raises for interacting coincident particles,
+// particles.py:92-98), see record_coincident().
+constexpr double kTinyR2 = 1e-200;
+
+template <int FAM>
+__device__ __forceinline__ void pair_core(double dx, double dy, double pdot, const double* __restrict__ tbl, double k1,
+                                          double& g, double& c, int& z) {
+    const double r2 = fma(dx, dx, fma(dy, dy, kTinyR2));
+    z = ((__double2hiint(r2) ^ __double2hiint(kTinyR2)) | (__double2loint(r2) ^ __double2loint(kTinyR2))) == 0;
+    if (FAM == kFamConical) {
+        const double rs = rsqrt_refined(r2);
+        g = exp2_tbl((r2 * rs) * k1, tbl);
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl(r2 * k1, tbl);
+        c = pdot * g;
+    }
 }
 
 // Accumulates one ordered pair.  k1 = -kTbl/(alpha ln2) (conical, multiplies r) or
@@ -149,6 +174,29 @@ __device__ __forceinline__ bool pair_sym(double xi, double yi, double pxi, doubl
     jpy = fma(-c, dy, jpy);
     pdot_out = pdot;
     return z;
+}
+
+__device__ __forceinline__ void record_event(DevStatus* st, unsigned long long event, unsigned long long key);
+
+// Padding record for partial tiles: far away (pairwise distinct, d^2 <= ~1e304) with p = 0, so
+// it contributes exactly 0 to every real row and never has d == 0 with anything.
+__device__ __forceinline__ double4 far_record(int k) {
+    return make_double4(1e150 * (double)(k + 1), 1e150, 0.0, 0.0);
+}
+
+// Rare path of the lean loops: row i had a flagged pair other than itself among sources
+// [j0, j1) of S.  Records the reference's error for each exactly coincident interacting pair
+// (d == 0 and p_i.p_j != 0, particles.py:92-98); the row-major-first pair is kept.
+__device__ __noinline__ inline void record_coincident(const double4* __restrict__ S, int64_t n, int64_t i, double4 me,
+                                                      int64_t j0, int64_t j1, DevStatus* st,
+                                                      unsigned long long event) {
+    for (int64_t j = j0; j < j1 && j < n; ++j) {
+        if (j == i) continue;
+        const double4 s = S[j];
+        const double dx = me.x - s.x, dy = me.y - s.y;
+        if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) != 0.0) continue;  // the reference's dist == 0
+        if (fma(me.z, s.z, me.w * s.w) != 0.0) record_event(st, event, (unsigned long long)(i * n + j));
+    }
 }
 
 __device__ __forceinline__ bool finite4(double a, double b, double c, double d) {
