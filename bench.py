@@ -121,6 +121,13 @@ def profile_traffic():
         return None, None
 
 
+def arm_config(a, n):
+    """The workload both arms report (BASELINE configs[1])."""
+    return {"workload": f"C2: one {a.rk_steps}-step RK4 shooting solve (T=1, {4 * a.rk_steps} RHS) of N={n}, "
+                        f"conical sigma=0.05 (KD-1), {a.path} path",
+            "n": n, "rk_steps": a.rk_steps, "path": a.path}
+
+
 # ---------------------------------------------------------------------------------------------
 def reference_arm(a):
     """--impl reference: the reference's CPU algorithm (numpy restatement) on rank 0."""
@@ -150,7 +157,8 @@ def reference_arm(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs[1] recipe, seeds 0/1)",
-        "config": {"workload": f"C2 RHS, N={w.n}, conical sigma=0.05 (KD-1), dense all pairs", "n": w.n},
+        "config": dict(arm_config(a, w.n), parallelism="host cores",
+                       sample=f"rows [0,{rows}) of one RHS per step (same pairs/s metric)"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"rows [0,{rows}) of one C2 RHS per step via oracle/restate.py (numpy, "
                                    "bitwise equal to geoshoot.rhs; elementwise on 1 core, BLAS on "
@@ -289,13 +297,12 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (BASELINE configs[1] recipe: uniform [0,1]^2 seed 0, N(0,0.01^2) seed 1)",
-            "config": {"workload": f"C2: one {a.rk_steps}-step RK4 shooting solve (T=1, {4 * a.rk_steps} RHS) of "
-                                   f"N={w.n}, conical sigma=0.05 (KD-1), {a.path} path",
-                       "n": w.n, "rk_steps": a.rk_steps, "path": a.path, "parallelism": f"rows{world}",
-                       "l2": "flushed between timed steps (256 MB write)"},
+            "config": dict(arm_config(a, w.n), parallelism=f"rows{world}",
+                           l2="flushed between timed steps (256 MB write)"),
             "roofline": {"bound": "fp64", "achieved": ach_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach_tflops / peak if peak else None, "traffic": traffic,
-                         "kernel": "gsb::k_dense_partial" if a.path == "dense" else "pair kernel",
+                         "kernel": ("gsb::k_dense_sym (symmetric, 1 GPU) / gsb::k_dense_partial (row shards)"
+                                    if a.path == "dense" else "gsb::k_cell_pair"),
                          "avg_launch_ms": pair_ms_avg, "pairs_per_launch": pairs_per_launch,
                          "work_per_pair": f"{W_ALG} DP-pipe slots = {2 * W_ALG} flop-equivalents (SURVEY.md §8(d))",
                          "peak_source": "measured live: gs_fp64_peak_probe (DFMA chains on all SMs, best of 3)"},

@@ -542,10 +542,12 @@ int gs_create(gs_context** out, int device) {
     if (const char* g = std::getenv("GS_B200_SYM")) ctx->sym_on = std::atoi(g) != 0;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
-    std::vector<double> t(kTbl);
-    for (int j = 0; j < kTbl; ++j) t[j] = (double)exp2l((long double)j / (long double)kTbl);
-    cudaError_t e = ctx->tbl.ensure(kTbl);
-    if (e == cudaSuccess) e = cudaMemcpy(ctx->tbl.ptr, t.data(), kTbl * sizeof(double), cudaMemcpyHostToDevice);
+    // 2^(j/kTbl), j = 0..kTbl-1, rounded from long double, replicated kTblRep times interleaved
+    std::vector<double> t(kTblWords);
+    for (int j = 0; j < kTbl; ++j)
+        for (int c = 0; c < kTblRep; ++c) t[j * kTblRep + c] = (double)exp2l((long double)j / (long double)kTbl);
+    cudaError_t e = ctx->tbl.ensure(kTblWords);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->tbl.ptr, t.data(), kTblWords * sizeof(double), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = ctx->st.ensure(1);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->st_host, sizeof(DevStatus));
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->scal_host, 16 * sizeof(double));

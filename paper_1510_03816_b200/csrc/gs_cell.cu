@@ -144,11 +144,12 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
                                                    int64_t n, int64_t row0, int64_t row1, double k1, double rc2,
                                                    double4* __restrict__ part, DevStatus* st, unsigned long long event,
                                                    const double* __restrict__ tbl_g, unsigned long long* accepted) {
-    __shared__ double s_tbl[kTbl];
+    __shared__ double s_tbl[kTblWords];
     __shared__ int s_list[kCL][kCB];
     __shared__ unsigned long long s_acc_count;
     if (*((volatile unsigned long long*)&st->first_event) < event) return;
-    for (int t = threadIdx.x; t < kTbl; t += kCB) s_tbl[t] = tbl_g[t];
+    for (int t = threadIdx.x; t < kTblWords; t += kCB) s_tbl[t] = tbl_g[t];
+    const double* tbl = lane_table(s_tbl);
     if (threadIdx.x == 0) s_acc_count = 0;
     __syncthreads();
 
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
                     const double pdot = fma(me.z, s.z, me.w * s.w);
                     double gk, c;
                     int z;
-                    pair_core<FAM>(dx, dy, pdot, s_tbl, k1, gk, c, z);
+                    pair_core<FAM>(dx, dy, pdot, tbl, k1, gk, c, z);
                     aqx = fma(gk, s.z, aqx);
                     aqy = fma(gk, s.w, aqy);
                     apx = fma(c, dx, apx);

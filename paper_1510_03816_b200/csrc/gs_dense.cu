@@ -40,10 +40,11 @@ __global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict
                                                        int64_t nrows, int64_t chunk, double k1,
                                                        double4* __restrict__ part, DevStatus* st,
                                                        unsigned long long event, const double* __restrict__ tbl_g) {
-    __shared__ double s_tbl[kTbl];
+    __shared__ double s_tbl[kTblWords];
     __shared__ double4 s_src[kDT];
     if (*((volatile unsigned long long*)&st->first_event) < event) return;  // an earlier failure
-    for (int t = threadIdx.x; t < kTbl; t += kDB) s_tbl[t] = tbl_g[t];
+    for (int t = threadIdx.x; t < kTblWords; t += kDB) s_tbl[t] = tbl_g[t];
+    const double* tbl = lane_table(s_tbl);
 
     const int64_t li = (int64_t)blockIdx.x * kDB + threadIdx.x;
     const bool valid = li < nrows;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict
             const double pdot = fma(me.z, s.z, me.w * s.w);
             double g, c;
             int z;
-            pair_core<FAM>(dx, dy, pdot, s_tbl, k1, g, c, z);
+            pair_core<FAM>(dx, dy, pdot, tbl, k1, g, c, z);
             aqx = fma(g, s.z, aqx);
             aqy = fma(g, s.w, aqy);
             apx = fma(c, dx, apx);

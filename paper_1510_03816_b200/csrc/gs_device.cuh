@@ -11,10 +11,11 @@
 // The reference evaluates exp twice per pair (kernel_value and kernel_derivative) and a
 // sqrt and a divide (kernels.py:130, 159; particles.py:100).  Here one pair costs one
 // MUFU.RSQ64H + one cubic refinement (r and 1/r), and ONE table-driven exp:
-//   2^(y/256) = T[k & 255] * 2^(k >> 8) * e^(u ln2/256),  k = rint(y), u = y - k in [-1/2, 1/2]
-// with a 256-entry table in shared memory and a degree-4 polynomial for e^x - 1 on
-// |x| <= ln2/512 (truncation 4e-17).  The whole exp is 3 DADD + 4 DFMA + 1 DMUL on the
-// FP64 pipe plus integer work; results agree with libm to a few ulp (tests/test_gpu_*.py).
+//   2^(y/64) = T[k & 63] * 2^(k >> 6) * e^(u ln2/64),  k = rint(y), u = y - k in [-1/2, 1/2]
+// with a 64-entry table in shared memory (replicated for conflict-free lookups) and a
+// degree-5 polynomial for e^x - 1 on |x| <= ln2/128 (truncation 3.5e-17).  The exp is
+// ~9 FP64-pipe instructions plus integer work; results agree with libm to a few ulp
+// (tests/test_gpu_parity.py).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,13 +25,19 @@ namespace gsb {
 constexpr int kFamConical = 0;
 constexpr int kFamGaussian = 1;
 
-constexpr int kTblBits = 8;
+constexpr int kTblBits = 6;
 constexpr int kTbl = 1 << kTblBits;
+// The table is stored 16 times interleaved (entry j of copy c at [16 j + c]) and lane l reads
+// copy l & 15: a warp's random lookups hit 16 distinct bank pairs per half-warp, i.e. the
+// minimum 2 shared-memory wavefronts instead of ~5 for a single copy.
+constexpr int kTblRep = 16;
+constexpr int kTblWords = kTbl * kTblRep;
 constexpr double kLn2 = 0.69314718055994530941723212145818;
 constexpr double kC1 = kLn2 / kTbl;
 constexpr double kC2 = kC1 * kC1 / 2.0;
 constexpr double kC3 = kC1 * kC1 * kC1 / 6.0;
 constexpr double kC4 = kC1 * kC1 * kC1 * kC1 / 24.0;
+constexpr double kC5 = kC1 * kC1 * kC1 * kC1 * kC1 / 120.0;
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr int kKMin = -1020 * kTbl;                 // below: G underflows (flush to 0)
 
@@ -71,12 +78,17 @@ __device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ 
     double u = y - kd;
     const int k = __double2loint(s) - (1 << 30);
     const bool ok = ((__double2hiint(s) ^ kMagicHi) | ((k - kKMin) >> 31)) == 0;  // one predicate
-    double t = tbl[k & (kTbl - 1)];
+    double t = tbl[(k & (kTbl - 1)) * kTblRep];
     int n = k >> kTblBits;
     double tn = __hiloint2double(__double2hiint(t) + (n << 20), __double2loint(t));
-    double e1 = u * fma(fma(fma(kC4, u, kC3), u, kC2), u, kC1);
+    double e1 = u * fma(fma(fma(fma(kC5, u, kC4), u, kC3), u, kC2), u, kC1);
     double g = fma(tn, e1, tn);
     return ok ? g : 0.0;
+}
+
+// This thread's copy of the replicated table in shared memory.
+__device__ __forceinline__ const double* lane_table(const double* s_tbl) {
+    return s_tbl + (threadIdx.x & (kTblRep - 1));
 }
 
 // ---- lean pair core for the hot loops -------------------------------------------------------

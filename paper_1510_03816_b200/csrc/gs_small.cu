@@ -18,7 +18,7 @@ constexpr int kWarps = kSmallThreads / 32;
 
 struct SmallCtx {
     double4* S;            // shared: stage state, n records
-    double* tbl;           // shared: exp table
+    const double* tbl;     // shared: this lane's copy of the exp table
     double* red;           // shared: kWarps scratch
     unsigned long long* key;
     int n, split, tgt, sub;
@@ -157,13 +157,13 @@ __device__ double small_hamiltonian(const SmallCtx& c, const SysConst& sc, doubl
 template <int FAM>
 __global__ void __launch_bounds__(kSmallThreads) k_small(SysConst sc, SmallArgs a, const double* __restrict__ tbl_g) {
     extern __shared__ double4 s_state[];
-    __shared__ double s_tbl[kTbl];
+    __shared__ double s_tbl[kTblWords];
     __shared__ double s_red[kWarps + 1];
     __shared__ unsigned long long s_key;
-    for (int t = threadIdx.x; t < kTbl; t += blockDim.x) s_tbl[t] = tbl_g[t];
+    for (int t = threadIdx.x; t < kTblWords; t += blockDim.x) s_tbl[t] = tbl_g[t];
 
     SmallCtx c;
-    c.S = s_state; c.tbl = s_tbl; c.red = s_red; c.key = &s_key;
+    c.S = s_state; c.tbl = lane_table(s_tbl); c.red = s_red; c.key = &s_key;
     c.n = (int)a.n; c.split = a.split;
     c.tgt = threadIdx.x / a.split; c.sub = threadIdx.x % a.split;
     c.act = c.tgt < c.n;
