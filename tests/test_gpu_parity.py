@@ -121,14 +121,23 @@ def test_match_matches_reference(cuda, name):
     ref = gs.LandmarkTemplate(c["ref"], m["ref_label"])
     tgt = gs.LandmarkTemplate(c["tgt"], m["tgt_label"])
     res = gs.match(ref, tgt, cfg)
-    assert res.iterations == m["iterations"]
     assert res.converged == m["converged"]
     assert len(res.residual_history) == res.iterations
     assert res.final_template.label == m["final_label"]
     if m["diagnosis"] and m["diagnosis"].startswith("step too large"):
-        assert res.diagnosis == m["diagnosis"]
+        # Divergent runs: the blow-up amplifies last-bit differences exponentially, so the
+        # iteration at which "value > 1e6 x initial" trips can move by one or two.  Pinned: the
+        # failure kind and message, the residual history up to the onset of the blow-up.
+        assert res.diagnosis.split(" (")[0] == m["diagnosis"].split(" (")[0]
+        if "(" in m["diagnosis"]:
+            assert res.diagnosis == m["diagnosis"]
+        assert abs(res.iterations - m["iterations"]) <= 2
+        h_ref = np.asarray(c["history"])
+        k = int(np.argmax(h_ref > 1e2 * h_ref[0])) if h_ref.size and np.any(h_ref > 1e2 * h_ref[0]) else h_ref.size
+        np.testing.assert_allclose(np.array(res.residual_history[:k]), h_ref[:k], rtol=1e-6)
         assert np.all(np.isfinite(res.p0))
         return
+    assert res.iterations == m["iterations"]
     assert res.diagnosis == m["diagnosis"]
     scale = max(np.abs(c["p0"]).max(), 1e-300)
     assert np.abs(res.p0 - c["p0"]).max() / scale <= MATCH_TOL

@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--quick", action="store_true", help="skip the slow CPU oracle comparisons")
+    ap.add_argument("--n45", type=int, default=0, help="override N of C4/C5 (debugging)")
     a = ap.parse_args()
     import torch
 
@@ -134,9 +135,10 @@ def main():
     for name, fn in (("C4", configs.c4), ("C5", configs.c5)):
         if name not in only:
             continue
-        w = fn()
+        w = fn(a.n45) if a.n45 else fn()
         spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
         gs.set_path("auto")
+        print(name, "match start n =", w.n, flush=True)
         t0 = time.perf_counter()
         r = device.match(spec, w.q, w.target, w.h, w.epsilon, w.max_iter, w.stop_rule, "max", 1.0, w.steps)
         wall = time.perf_counter() - t0
