@@ -83,9 +83,11 @@ static int grid_build(go_grid* g, const double* q, long n, double cutoff) {
         ymin = fmin(ymin, q[2 * i + 1]); ymax = fmax(ymax, q[2 * i + 1]);
     }
     g->x0 = xmin; g->y0 = ymin; g->inv = 1.0 / cutoff;
-    g->nx = (long)floor((xmax - xmin) * g->inv) + 1;
-    g->ny = (long)floor((ymax - ymin) * g->inv) + 1;
-    if (g->nx * g->ny > 64L * n + 1024) return -1;   /* caller falls back to dense */
+    /* decide in floating point: a blown-up state spreads the points far beyond any grid */
+    double fx = floor((xmax - xmin) * g->inv) + 1.0, fy = floor((ymax - ymin) * g->inv) + 1.0;
+    if (!(fx * fy <= 64.0 * (double)n + 1024.0)) return -1;   /* caller falls back to the pair loop */
+    g->nx = (long)fx;
+    g->ny = (long)fy;
     long nc = g->nx * g->ny;
     g->start = (long*)calloc(nc + 1, sizeof(long));
     g->idx = (long*)malloc(n * sizeof(long));

@@ -79,6 +79,7 @@ struct gs_context {
     DevBuf<unsigned> c_keys, c_keys_sorted, c_vals, c_perm;
     DevBuf<int> c_start;
     DevBuf<double4> c_Ss;
+    DevBuf<float2> c_Sf;
     DevBuf<double> c_bbox;
     DevBuf<GridParams> c_gp;
     DevBuf<unsigned char> c_cub;
@@ -312,14 +313,14 @@ void prof_mark(gs_context* ctx, cudaStream_t stream) {
 CellWs cell_ws(gs_context* ctx) {
     CellWs w;
     w.keys = ctx->c_keys.ptr; w.keys_sorted = ctx->c_keys_sorted.ptr; w.vals = ctx->c_vals.ptr;
-    w.perm = ctx->c_perm.ptr; w.start = ctx->c_start.ptr; w.Ss = ctx->c_Ss.ptr; w.bbox_red = ctx->c_bbox.ptr;
+    w.perm = ctx->c_perm.ptr; w.start = ctx->c_start.ptr; w.Ss = ctx->c_Ss.ptr; w.Sf = ctx->c_Sf.ptr; w.bbox_red = ctx->c_bbox.ptr;
     w.gp = ctx->c_gp.ptr; w.cub_temp = ctx->c_cub.ptr; w.cub_bytes = ctx->c_cub_bytes;
     return w;
 }
 
 int ensure_cell(gs_context* ctx, int64_t n) {
     GS_CUDA(ctx->c_keys.ensure(n)); GS_CUDA(ctx->c_keys_sorted.ensure(n)); GS_CUDA(ctx->c_vals.ensure(n));
-    GS_CUDA(ctx->c_perm.ensure(n)); GS_CUDA(ctx->c_Ss.ensure(n));
+    GS_CUDA(ctx->c_perm.ensure(n)); GS_CUDA(ctx->c_Ss.ensure(n)); GS_CUDA(ctx->c_Sf.ensure(n));
     GS_CUDA(ctx->c_start.ensure(cell_cap(n) + 1));
     GS_CUDA(ctx->c_bbox.ensure(4 * kCellBboxBlocks));
     GS_CUDA(ctx->c_gp.ensure(1));
@@ -438,7 +439,7 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
     auto P = [](const void* p) { return (double)(uintptr_t)p; };
     return {(double)ctx->n, (double)ctx->row0, (double)ctx->row1, (double)steps, dt, (double)ctx->cell_on,
             (double)ctx->prof_on, (double)sc.fam, sc.k1, sc.scale_q, sc.scale_p, sc.sigma2, sc.cutoff,
-            P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr),
+            P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr), P(ctx->c_Sf.ptr),
             P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr)};
 }
 
@@ -573,7 +574,7 @@ int gs_destroy(gs_context* ctx) {
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
-    ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
+    ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     ctx->c_acc.release();
     delete ctx;
     return GS_OK;

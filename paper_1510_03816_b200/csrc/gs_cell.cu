@@ -12,8 +12,10 @@
 //      offsets (start[c] = first sorted position with key >= c), permuted copy of the
 //      32-byte (x, y, px, py) records so that a cell's particles are contiguous;
 //   3. the pair kernel: one thread per target in sorted order; the 3 stencil rows of its
-//      cell are 3 contiguous sorted ranges.  Candidates are filtered (4 FP64 ops) into a
-//      per-lane list in shared memory, then the accepted pairs run the full pair body of
+//      cell are 3 contiguous sorted ranges.  Candidates are filtered in fp32 on the FMA pipe
+//      (8-byte float positions relative to the grid origin, radius grown by the fp32 error
+//      bound so no pair within the cutoff is lost) into a per-lane list in shared memory,
+//      then the accepted pairs run the full fp64 pair body of
 //      gs_device.cuh — lanes do not idle on rejected candidates.  Each target's sum runs
 //      over its candidates in a fixed order (row, then sorted position), so results are
 //      deterministic.  Raw sums are written at the target's original index; the shared
@@ -31,7 +33,7 @@ namespace {
 
 constexpr int kBB = 256;        // bbox block
 constexpr int kCB = 128;        // pair-kernel threads per CTA
-constexpr int kCL = 64;         // candidate chunk (per-lane list capacity)
+constexpr int kCL = 32;         // candidate chunk (per-lane list capacity)
 
 __global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double* red) {
     __shared__ double s[4][kBB];
@@ -86,9 +88,16 @@ __global__ void k_grid_params(const double* __restrict__ red, int nb, double cut
     const bool bad = s_bad != 0;
     mnx = s[0][0]; mny = s[1][0]; mxx = s[2][0]; mxy = s[3][0];
     GridParams g;
+    // fp32 filter radius: positions are stored as float(x - x0); each carries an error of at
+    // most 2^-24 * extent, so a pair's distance in fp32 is off by <= 4 * 2^-24 * extent.
+    // Pairs admitted only by this margin have G < 2^-53 (they add < 1e-16 relative).
+    const double extent = fmax(fmax(mxx - mnx, mxy - mny), 0.0);
+    const double rcf = cutoff * (1.0 + 1e-6) + 4.0 * extent * 5.9604644775390625e-08 + 1e-30;
+    g.rc2f = __double2float_ru(rcf * rcf);
     if (bad || !isfinite(mnx) || !isfinite(mxx) || !isfinite(mny) || !isfinite(mxy)) {
         // non-finite stage state: one cell (the stage check has already recorded the failure)
         g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.nx = 1; g.ny = 1;
+        g.rc2f = __int_as_float(0x7f800000);  // accept everything
     } else {
         double h = cutoff;
         for (;;) {
@@ -124,26 +133,32 @@ __global__ void k_cell_keys(const double4* __restrict__ S, int64_t n, const Grid
 // start[c] = first sorted position whose key >= c, for c in [0, ncells]; permuted records
 __global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, const unsigned* __restrict__ perm,
                                      const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
-                                     int* start, double4* Ss) {
+                                     int* start, double4* Ss, float2* Sf) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k > n) return;
-    const int ncells = gp->ncells;
+    const GridParams g = *gp;
     const long long prev = (k == 0) ? -1 : (long long)keys_sorted[k - 1];
-    const long long cur = (k == n) ? (long long)ncells : (long long)keys_sorted[k];
+    const long long cur = (k == n) ? (long long)g.ncells : (long long)keys_sorted[k];
     for (long long c = prev + 1; c <= cur; ++c) start[c] = (int)k;
-    if (k < n) Ss[k] = S[perm[k]];
+    if (k < n) {
+        const double4 v = S[perm[k]];
+        Ss[k] = v;
+        Sf[k] = make_float2((float)(v.x - g.x0), (float)(v.y - g.y0));
+    }
 }
 
 // TPL lanes share one target (small N: fills the GPU); each lane takes every TPL-th
 // candidate of the stencil rows and the lanes' sums are xor-butterfly reduced, so every
 // target's summation order is fixed.
 template <int FAM, int TPL>
-__global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ Ss, const unsigned* __restrict__ perm,
-                                                   const unsigned* __restrict__ keys_sorted,
-                                                   const int* __restrict__ start, const GridParams* __restrict__ gp,
-                                                   int64_t n, int64_t row0, int64_t row1, double k1, double rc2,
-                                                   double4* __restrict__ part, DevStatus* st, unsigned long long event,
-                                                   const double* __restrict__ tbl_g, unsigned long long* accepted) {
+__global__ void __launch_bounds__(kCB, 8) k_cell_pair(const double4* __restrict__ Ss, const float2* __restrict__ Sf,
+                                                      const unsigned* __restrict__ perm,
+                                                      const unsigned* __restrict__ keys_sorted,
+                                                      const int* __restrict__ start, const GridParams* __restrict__ gp,
+                                                      int64_t n, int64_t row0, int64_t row1, double k1,
+                                                      double4* __restrict__ part, DevStatus* st,
+                                                      unsigned long long event, const double* __restrict__ tbl_g,
+                                                      unsigned long long* accepted) {
     __shared__ double s_tbl[kTblWords];
     __shared__ int s_list[kCL][kCB];
     __shared__ unsigned long long s_acc_count;
@@ -161,6 +176,7 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
     const bool active = valid && i >= row0 && i < row1;
     const GridParams g = *gp;
     const double4 me = Ss[kk];
+    const float2 mef = Sf[kk];
     const int key = (int)keys_sorted[kk];
     const int cy = key / g.nx, cx = key - cy * g.nx;
     const int xa = max(cx - 1, 0), xb = min(cx + 1, g.nx - 1);
@@ -174,11 +190,11 @@ __global__ void __launch_bounds__(kCB) k_cell_pair(const double4* __restrict__ S
             for (int base = a + sub; base < b; base += TPL * kCL) {
                 const int m = min(kCL, (b - base + TPL - 1) / TPL);
                 int cnt = 0;
-                for (int t = 0; t < m; ++t) {  // filter: d^2 < cutoff^2
+                for (int t = 0; t < m; ++t) {  // fp32 filter (FMA pipe): d < cutoff (+ fp32 margin)
                     const int j = base + TPL * t;
-                    const double2 xy = *reinterpret_cast<const double2*>(&Ss[j]);
-                    const double dx = me.x - xy.x, dy = me.y - xy.y;
-                    if (fma(dx, dx, dy * dy) < rc2) s_list[cnt++][threadIdx.x] = j;
+                    const float2 xy = Sf[j];
+                    const float dx = mef.x - xy.x, dy = mef.y - xy.y;
+                    if (fmaf(dx, dx, dy * dy) < g.rc2f) s_list[cnt++][threadIdx.x] = j;
                 }
                 nacc += cnt;
                 for (int u = 0; u < cnt; ++u) {
@@ -240,8 +256,10 @@ size_t cell_cub_bytes(int64_t n) {
 }
 
 int64_t cell_cap(int64_t n) {
+    // >= 16 particles per cell on average (coarser grids only cost candidates): 16-bit keys,
+    // i.e. two radix passes, up to n = 2^20
     int64_t cap = 4096;
-    while (cap < 4 * n) cap <<= 1;
+    while (cap < n / 16) cap <<= 1;
     return cap;
 }
 
@@ -259,14 +277,13 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
                                                     (int)n, 0, end_bit, stream);
     if (e != cudaSuccess) return (int)e;
     k_cell_start_permute<<<(unsigned)((n + 1 + 255) / 256), 256, 0, stream>>>(w.keys_sorted, w.perm, S, n, w.gp,
-                                                                            w.start, w.Ss);
+                                                                            w.start, w.Ss, w.Sf);
     return 0;
 }
 
 void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t row0, int64_t row1, double4* part,
                       DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
                       cudaStream_t stream) {
-    const double rc2 = sc.cutoff * sc.cutoff;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -274,8 +291,8 @@ void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t ro
     while (tpl < 16 && n * tpl < (int64_t)sms * 1024) tpl *= 2;
     const unsigned blocks = (unsigned)((n * tpl + kCB - 1) / kCB);
 #define GS_CELL_LAUNCH(F, T)                                                                                   \
-    k_cell_pair<F, T><<<blocks, kCB, 0, stream>>>(w.Ss, w.perm, w.keys_sorted, w.start, w.gp, n, row0, row1,  \
-                                                  sc.k1, rc2, part, st, event, tbl_dev, accepted)
+    k_cell_pair<F, T><<<blocks, kCB, 0, stream>>>(w.Ss, w.Sf, w.perm, w.keys_sorted, w.start, w.gp, n, row0,  \
+                                                  row1, sc.k1, part, st, event, tbl_dev, accepted)
 #define GS_CELL_FAM(F)                                    \
     switch (tpl) {                                        \
         case 1: GS_CELL_LAUNCH(F, 1); break;              \

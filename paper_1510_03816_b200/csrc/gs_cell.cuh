@@ -9,7 +9,8 @@ namespace gsb {
 
 struct GridParams {
     double x0, y0, inv_h;
-    int nx, ny, ncells, pad;
+    int nx, ny, ncells;
+    float rc2f;  // fp32 candidate-filter radius^2: cutoff^2 grown by the fp32 position error
 };
 
 constexpr int kCellBboxBlocks = 296;
@@ -22,6 +23,7 @@ struct CellWs {
     unsigned* perm;         // n: sorted position -> original index
     int* start;             // cell_cap(n) + 1
     double4* Ss;            // n: records in sorted order
+    float2* Sf;             // n: fp32 positions relative to the grid origin, sorted order
     double* bbox_red;       // 4 * kCellBboxBlocks
     GridParams* gp;         // 1
     void* cub_temp;
