@@ -176,6 +176,22 @@ int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
 double* gs_stage_state(gs_context* ctx);
 int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream);
 
+/* Symmetric multi-GPU split of the dense RHS (each unordered pair once, gs_sym.cu):
+ *   gs_sym_parts       : number of work items (superblock pairs) of one RHS at this n (0 if the
+ *                        symmetric kernel is not available for n)
+ *   gs_stage_pairs_sym : evaluates items [part_begin, part_end) on the session state S and writes
+ *                        this rank's raw partial sums for ALL n rows into R (device, n x 4 doubles:
+ *                        sum G p_j, sum c (q_i - q_j)); the ranks' R are summed by a
+ *                        reduce-scatter over rows
+ *   gs_stage_finish    : RK4 stage epilogue of the session rows from their reduced raw sums
+ *                        (device, (row1-row0) x 4), as gs_stage_run's second half */
+int gs_stage_path(gs_context* ctx, const gs_system_t* sys, void* stream); /* GS_PATH_DENSE/CELL, <0: -GS_ERR_* */
+int64_t gs_sym_parts(int64_t n);
+int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, int64_t part_begin,
+                       int64_t part_end, double* R, void* stream);
+int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt,
+                    const double* R_rows, void* stream);
+
 /* Profiling: with profiling enabled, every launch of the pair kernel (the dense or cell-list
  * RHS sweep, or the persistent small-N kernel) is bracketed by CUDA events on its stream;
  * gs_profile_read returns their summed device time (ms), the number of pair-kernel launches,

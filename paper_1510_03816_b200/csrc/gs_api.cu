@@ -886,6 +886,66 @@ int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream) 
     return GS_OK;
 }
 
+int gs_stage_path(gs_context* ctx, const gs_system_t* sys, void* stream) {
+    if (!ctx || ctx->n < 1) return -fail(GS_ERR_INVALID, "no stage session");
+    int rc = check_system(sys);
+    if (rc) return -rc;
+    if ((rc = choose_path(ctx, sys, ctx->S.ptr, ctx->n, (cudaStream_t)stream))) return -rc;
+    return ctx->cell_on ? GS_PATH_CELL : GS_PATH_DENSE;
+}
+
+int64_t gs_sym_parts(int64_t n) {
+    const SymPlan p = sym_plan(n);
+    return (p.ok && n >= kSymMinN) ? (int64_t)sym_ctas(n) : 0;
+}
+
+int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
+                       int64_t part_end, double* R, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || ctx->n < 1 || !R) return fail(GS_ERR_INVALID, "no stage session");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    const int64_t n = ctx->n, total = gs_sym_parts(n);
+    if (total == 0) return fail(GS_ERR_UNSUPPORTED, "symmetric split not available for this n");
+    if (stg < 0 || stg > 3 || step < 1 || part_begin < 0 || part_end > total || part_begin > part_end)
+        return fail(GS_ERR_INVALID, "bad stage / part range");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const SymPlan sp = sym_plan(n);
+    GS_CUDA(ctx->part.ensure((size_t)sp.nsb * (size_t)sp.pstride));
+    GS_CUDA(cudaMemsetAsync(ctx->part.ptr, 0, (size_t)sp.nsb * (size_t)sp.pstride * sizeof(double4), s));
+    const SysConst sc = make_const(sys);
+    const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg;
+    if (ctx->prof_on) prof_mark(ctx, s);
+    launch_dense_sym(sc, ctx->S.ptr, n, ctx->part.ptr, sp.pstride, ctx->st.ptr, ev, ctx->tbl.ptr, s, part_begin,
+                     part_end);
+    if (ctx->prof_on) prof_mark(ctx, s);
+    launch_slot_reduce(ctx->part.ptr, sp.nsb, sp.pstride, n, reinterpret_cast<double4*>(R), s);
+    ctx->launches += 2;
+    ctx->pair_launches++;
+    ctx->host_pairs += (long long)((double)n * (double)n * (double)(part_end - part_begin) / (double)total);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt,
+                    const double* R_rows, void* stream) {
+    if (!ctx || ctx->n < 1) return fail(GS_ERR_INVALID, "no stage session");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (stg < 0 || stg > 3 || step < 1) return fail(GS_ERR_INVALID, "bad stage index");
+    const int64_t nrows = ctx->row1 - ctx->row0;
+    if (nrows > 0 && !R_rows) return fail(GS_ERR_INVALID, "R_rows is NULL");
+    FinishArgs fa{};
+    fa.part = reinterpret_cast<const double4*>(R_rows); fa.nchunks = 1; fa.pstride = 0; fa.nrows = nrows;
+    fa.row0 = ctx->row0; fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr; fa.stage = stg; fa.dt = dt;
+    fa.st = ctx->st.ptr;
+    fa.event = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg + 1ull;
+    launch_finish(kFinStage, make_const(sys), fa, (cudaStream_t)stream);
+    ctx->launches++;
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
 int gs_profile_enable(gs_context* ctx, int32_t on) {
     if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
     ctx->prof_on = on ? 1 : 0;

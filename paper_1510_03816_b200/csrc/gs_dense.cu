@@ -35,31 +35,54 @@ DensePlan dense_plan(int64_t n, int sm_count) {
     return p;
 }
 
+// Two target rows per thread (64 threads x 2 = the kDB rows of a CTA): every shared-memory
+// source broadcast and the loop overhead serve two pair evaluations.
+constexpr int kDPT = kDB / 2;
+
+struct Row {
+    double qx, qy, px, py;
+    int nz;
+};
+
 template <int FAM>
-__global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict__ S, int64_t n, int64_t row0,
-                                                       int64_t nrows, int64_t chunk, double k1,
-                                                       double4* __restrict__ part, DevStatus* st,
-                                                       unsigned long long event, const double* __restrict__ tbl_g) {
+__device__ __forceinline__ void row_pair(const double4& me, const double4& s, const double* tbl, double k1, Row& a) {
+    const double dx = me.x - s.x, dy = me.y - s.y;
+    const double pdot = fma(me.z, s.z, me.w * s.w);
+    double g, c;
+    int z;
+    pair_core<FAM>(dx, dy, pdot, tbl, k1, g, c, z);
+    a.qx = fma(g, s.z, a.qx);
+    a.qy = fma(g, s.w, a.qy);
+    a.px = fma(c, dx, a.px);
+    a.py = fma(c, dy, a.py);
+    a.nz += z;
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(kDPT, 12) k_dense_partial(const double4* __restrict__ S, int64_t n, int64_t row0,
+                                                            int64_t nrows, int64_t chunk, double k1,
+                                                            double4* __restrict__ part, DevStatus* st,
+                                                            unsigned long long event, const double* __restrict__ tbl_g) {
     __shared__ double s_tbl[kTblWords];
     __shared__ double4 s_src[kDT];
     if (*((volatile unsigned long long*)&st->first_event) < event) return;  // an earlier failure
-    for (int t = threadIdx.x; t < kTblWords; t += kDB) s_tbl[t] = tbl_g[t];
+    for (int t = threadIdx.x; t < kTblWords; t += kDPT) s_tbl[t] = tbl_g[t];
     const double* tbl = lane_table(s_tbl);
 
-    const int64_t li = (int64_t)blockIdx.x * kDB + threadIdx.x;
-    const bool valid = li < nrows;
-    const int64_t i = row0 + (valid ? li : 0);
-    const double4 me = S[i];
+    const int64_t li0 = (int64_t)blockIdx.x * kDB + threadIdx.x, li1 = li0 + kDPT;
+    const bool v0 = li0 < nrows, v1 = li1 < nrows;
+    const int64_t i0 = row0 + li0, i1 = row0 + li1;
+    const double4 me0 = v0 ? S[i0] : far_record(threadIdx.x);
+    const double4 me1 = v1 ? S[i1] : far_record(threadIdx.x + kDPT);
     const int64_t j0 = (int64_t)blockIdx.y * chunk;
     const int64_t j1 = min(n, j0 + chunk);
 
-    double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
-    int nz = 0;
+    Row a0{0.0, 0.0, 0.0, 0.0, 0}, a1{0.0, 0.0, 0.0, 0.0, 0};
     for (int64_t t0 = j0; t0 < j1; t0 += kDT) {
         __syncthreads();
-        for (int t = threadIdx.x; t < kDT; t += kDB) {
+        for (int t = threadIdx.x; t < kDT; t += kDPT) {
             const int64_t j = t0 + t;
-            s_src[t] = (j < j1) ? S[j] : far_record(t);  // far, p = 0: contributes exactly 0
+            s_src[t] = (j < j1) ? S[j] : far_record(kDB + t);  // far, p = 0: contributes exactly 0
         }
         __syncthreads();
         const int m = (int)((j1 - t0) < kDT ? (j1 - t0) : kDT);
@@ -67,21 +90,15 @@ __global__ void __launch_bounds__(kDB) k_dense_partial(const double4* __restrict
 #pragma unroll 4
         for (int jj = 0; jj < mr; ++jj) {
             const double4 s = s_src[jj];
-            const double dx = me.x - s.x, dy = me.y - s.y;
-            const double pdot = fma(me.z, s.z, me.w * s.w);
-            double g, c;
-            int z;
-            pair_core<FAM>(dx, dy, pdot, tbl, k1, g, c, z);
-            aqx = fma(g, s.z, aqx);
-            aqy = fma(g, s.w, aqy);
-            apx = fma(c, dx, apx);
-            apy = fma(c, dy, apy);
-            nz += z;
+            row_pair<FAM>(me0, s, tbl, k1, a0);
+            row_pair<FAM>(me1, s, tbl, k1, a1);
         }
     }
-    const int self_in = (i >= j0 && i < j1) ? 1 : 0;
-    if (nz > self_in && valid) record_coincident(S, n, i, me, j0, j1, st, event);  // rare
-    if (valid) part[(int64_t)blockIdx.y * nrows + li] = make_double4(aqx, aqy, apx, apy);
+    // rare: a flagged pair other than the row itself (coincident particles)
+    if (v0 && a0.nz > ((i0 >= j0 && i0 < j1) ? 1 : 0)) record_coincident(S, n, i0, me0, j0, j1, st, event);
+    if (v1 && a1.nz > ((i1 >= j0 && i1 < j1) ? 1 : 0)) record_coincident(S, n, i1, me1, j0, j1, st, event);
+    if (v0) part[(int64_t)blockIdx.y * nrows + li0] = make_double4(a0.qx, a0.qy, a0.px, a0.py);
+    if (v1) part[(int64_t)blockIdx.y * nrows + li1] = make_double4(a1.qx, a1.qy, a1.px, a1.py);
 }
 
 void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64_t row0, int64_t nrows,
@@ -90,11 +107,11 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
     if (nrows <= 0) return;
     dim3 grid((unsigned)((nrows + kDB - 1) / kDB), (unsigned)plan.nchunks);
     if (sc.fam == kFamConical)
-        k_dense_partial<kFamConical><<<grid, kDB, 0, stream>>>(S, n, row0, nrows, plan.chunk, sc.k1, part, st,
-                                                                event, tbl_dev);
-    else
-        k_dense_partial<kFamGaussian><<<grid, kDB, 0, stream>>>(S, n, row0, nrows, plan.chunk, sc.k1, part, st,
+        k_dense_partial<kFamConical><<<grid, kDPT, 0, stream>>>(S, n, row0, nrows, plan.chunk, sc.k1, part, st,
                                                                  event, tbl_dev);
+    else
+        k_dense_partial<kFamGaussian><<<grid, kDPT, 0, stream>>>(S, n, row0, nrows, plan.chunk, sc.k1, part, st,
+                                                                  event, tbl_dev);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -44,8 +44,14 @@ struct SymPlan {
     bool ok;          // partial buffer stays bounded (nsb <= 256)
 };
 SymPlan sym_plan(int64_t n);
+long long sym_ctas(int64_t n);  // work items (superblock pairs) of one symmetric RHS
+// CTAs [cta0, cta1) of the superblock-pair list (cta1 < 0: all).  A multi-GPU rank runs its
+// share of the list; the slots of the other ranks' items must be zero in `part`.
 void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
-                      unsigned long long event, const double* tbl_dev, cudaStream_t stream);
+                      unsigned long long event, const double* tbl_dev, cudaStream_t stream, long long cta0 = 0,
+                      long long cta1 = -1);
+// R[i] = sum over slots of part[slot * pstride + i] (fixed order), i < n.
+void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream);
 
 // Finish modes
 constexpr int kFinRhs = 0;    // write dq, dp rows ((nrows, 2) AoS)

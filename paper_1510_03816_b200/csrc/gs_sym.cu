@@ -83,8 +83,8 @@ __device__ __forceinline__ void add_to(double4* dst, const Acc& a) {
 
 template <int FAM>
 __global__ void __launch_bounds__(kST, 10) k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, int G,
-                                                       int nsb, double k1, double4* __restrict__ part, int64_t pstride,
-                                                       DevStatus* st, unsigned long long event,
+                                                       int nsb, long long cta0, double k1, double4* __restrict__ part,
+                                                       int64_t pstride, DevStatus* st, unsigned long long event,
                                                        const double* __restrict__ tbl_g) {
     __shared__ double s_tbl[kTblWords];
     __shared__ double4 s_rot[4][64];     // sub-block b of J twice: s_rot[b][k] = record 32 b + (k & 31)
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kST, 10) k_dense_sym(const double4* __restrict
     const double* tbl = lane_table(s_tbl);
 
     // CTA -> superblock pair (SI, SJ), SI <= SJ, row-major over the upper triangle
-    const long long t = blockIdx.x;
+    const long long t = cta0 + blockIdx.x;
     const double b2 = 2.0 * nsb + 1.0;
     long long SI = (long long)floor((b2 - sqrt(b2 * b2 - 8.0 * (double)t)) * 0.5);
     auto row_start = [nsb](long long r) { return r * nsb - r * (r - 1) / 2; };
@@ -195,17 +195,42 @@ SymPlan sym_plan(int64_t n) {
     return p;
 }
 
-void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
-                      unsigned long long event, const double* tbl_dev, cudaStream_t stream) {
+long long sym_ctas(int64_t n) {
     const SymPlan p = sym_plan(n);
-    const unsigned ctas = (unsigned)((long long)p.nsb * (p.nsb + 1) / 2);
+    return (long long)p.nsb * (p.nsb + 1) / 2;
+}
+
+void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
+                      unsigned long long event, const double* tbl_dev, cudaStream_t stream, long long cta0,
+                      long long cta1) {
+    const SymPlan p = sym_plan(n);
+    if (cta1 < 0) cta1 = sym_ctas(n);
+    if (cta1 <= cta0) return;
+    const unsigned ctas = (unsigned)(cta1 - cta0);
     const size_t smem = (size_t)p.G * kDB * sizeof(double4);
     if (sc.fam == kFamConical)
-        k_dense_sym<kFamConical><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, sc.k1, part, pstride, st, event,
-                                                              tbl_dev);
+        k_dense_sym<kFamConical><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, cta0, sc.k1, part, pstride, st,
+                                                              event, tbl_dev);
     else
-        k_dense_sym<kFamGaussian><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, sc.k1, part, pstride, st,
-                                                               event, tbl_dev);
+        k_dense_sym<kFamGaussian><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, cta0, sc.k1, part, pstride,
+                                                               st, event, tbl_dev);
+}
+
+namespace {
+__global__ void k_slot_reduce(const double4* __restrict__ part, int nslots, int64_t pstride, int64_t n, double4* R) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double4 s = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int c = 0; c < nslots; ++c) {
+        const double4 v = part[(int64_t)c * pstride + i];
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    R[i] = s;
+}
+}  // namespace
+
+void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream) {
+    if (n > 0) k_slot_reduce<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(part, nslots, pstride, n, R);
 }
 
 }  // namespace gsb

@@ -93,6 +93,29 @@ class DeviceStageBackend:
         N.check(self.ctx.lib.gs_stage_run(self.ctx.handle, ctypes.byref(self.sysc), step, stage, dt, self._s()),
                 "gs_stage_run")
 
+    # -- symmetric split (dense path, world > 1) -------------------------------------------
+    supports_sym = True
+
+    def path(self) -> str:
+        rc = self.ctx.lib.gs_stage_path(self.ctx.handle, ctypes.byref(self.sysc), self._s())
+        if rc < 0:
+            N.check(-rc, "gs_stage_path")
+        return "cell" if rc == N.GS_PATH_CELL else "dense"
+
+    def sym_parts(self) -> int:
+        return int(self.ctx.lib.gs_sym_parts(self.n))
+
+    def new_partials(self, rows: int):
+        return self.torch.zeros((rows, 4), dtype=self.torch.float64, device="cuda")
+
+    def pairs_sym(self, step: int, stage: int, b: int, e: int, R):
+        N.check(self.ctx.lib.gs_stage_pairs_sym(self.ctx.handle, ctypes.byref(self.sysc), step, stage, b, e,
+                                                R.data_ptr(), self._s()), "gs_stage_pairs_sym")
+
+    def finish(self, step: int, stage: int, dt: float, R_rows):
+        N.check(self.ctx.lib.gs_stage_finish(self.ctx.handle, ctypes.byref(self.sysc), step, stage, dt,
+                                             R_rows.data_ptr(), self._s()), "gs_stage_finish")
+
     def status(self) -> N.Status:
         st = N.Status()
         N.check(self.ctx.lib.gs_status_fetch(self.ctx.handle, ctypes.byref(st), self._s()), "gs_status_fetch")
@@ -134,6 +157,15 @@ class ShardedSolver:
         if self.world > 1:
             self.dist.all_gather_into_tensor(S[: c * self.world], S[r0:r0 + c].clone(), group=self.group)
 
+    def _reduce_scatter_rows(self, R_rows, R, c: int):
+        """R_rows = (sum over ranks of R)[rank*c:(rank+1)*c]  (NCCL reduce-scatter; gloo, used by
+        the CPU tests, has no reduce-scatter and takes an all-reduce)."""
+        if self.dist.get_backend(self.group) == "gloo":
+            self.dist.all_reduce(R, group=self.group)
+            R_rows.copy_(R[self.rank * c:(self.rank + 1) * c])
+        else:
+            self.dist.reduce_scatter_tensor(R_rows, R, group=self.group)
+
     def _allreduce(self, t, op):
         if self.world > 1:
             self.dist.all_reduce(t, op=op, group=self.group)
@@ -159,15 +191,35 @@ class ShardedSolver:
 
     # -- integrator.evolve ------------------------------------------------------------------
     def evolve(self, q, p, t_final: float, steps: int):
-        """Full (q, p) at t_final on every rank (integrator.py:66-121)."""
+        """Full (q, p) at t_final on every rank (integrator.py:66-121).
+
+        Dense path with world > 1: the symmetric split — rank r evaluates its share of the
+        unordered pairs (each pair once, both rows fed), the raw row sums are reduce-scattered
+        to the row owners (NCCL), the owners run the stage epilogue and the stage records are
+        all-gathered.  Otherwise every rank evaluates its own rows one-sided (cell list or
+        dense) and only the all-gather is needed."""
         n = q.shape[0]
-        r0, r1, c = row_split(n, self.world, self.rank)
+        W = self.world
+        r0, r1, c = row_split(n, W, self.rank)
         self.backend.begin(q, p, r0, r1)
-        S = self.backend.state(c * self.world)
+        S = self.backend.state(c * W)
         dt = t_final / steps
+        sym = False
+        if W > 1 and getattr(self.backend, "supports_sym", False) and self.backend.path() == "dense":
+            total = self.backend.sym_parts()
+            sym = total > 0
+        if sym:
+            b, e = self.rank * total // W, (self.rank + 1) * total // W
+            R = self.backend.new_partials(c * W)
+            R_rows = self.backend.new_partials(c)
         for step in range(1, steps + 1):
             for s in range(4):
-                self.backend.run(step, s, dt)
+                if sym:
+                    self.backend.pairs_sym(step, s, b, e, R)
+                    self._reduce_scatter_rows(R_rows, R, c)
+                    self.backend.finish(step, s, dt, R_rows)
+                else:
+                    self.backend.run(step, s, dt)
                 self._allgather_rows(S, r0, c)
         self._raise_first_failure(t_final, steps)
         return S[:n, 0:2].clone(), S[:n, 2:4].clone()

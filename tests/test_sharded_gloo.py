@@ -25,11 +25,12 @@ class NumpyStageBackend:
 
     device = "cpu"
 
-    def __init__(self, spec):
+    def __init__(self, spec, sym=False):
         from oracle.restate import Kernel
 
         self.k = Kernel(0 if spec.kernel.family.value == "conical" else 1, spec.kernel.alpha, spec.kernel.normalized)
         self.sigma2 = spec.sigma2
+        self.supports_sym = sym
 
     def begin(self, q, p, r0, r1):
         q = np.asarray(q, dtype=np.float64)
@@ -59,6 +60,66 @@ class NumpyStageBackend:
             self.fail = (step * 8 + 2 * s, N.GS_ERR_COINCIDENT, step, 2 * s, i, j)
             return
         k = np.concatenate([dq, dp], axis=1)
+        if s == 0:
+            self.A = k.copy()
+        else:
+            self.A = self.A + (1.0 if s == 3 else 2.0) * k
+        if s < 3:
+            nxt = self.B + ((dt if s == 2 else 0.5 * dt) * k)
+        else:
+            nxt = self.B + (dt / 6.0) * self.A
+            self.B = nxt
+        self.S[self.r0:self.r1] = torch.from_numpy(nxt)
+        if not np.all(np.isfinite(nxt)):
+            code = N.GS_ERR_NONFINITE_STATE if s == 3 else N.GS_ERR_NONFINITE_STAGE
+            self.fail = (step * 8 + 2 * s + 1, code, step, 2 * s + 1, -1, -1)
+
+    # -- symmetric split emulation: rank b..e owns source blocks of 32 columns ------------------
+    def path(self):
+        return "dense"
+
+    def sym_parts(self):
+        return (self.n + 31) // 32
+
+    def new_partials(self, rows):
+        return torch.zeros((rows, 4), dtype=torch.float64)
+
+    def pairs_sym(self, step, s, b, e, R):
+        """Raw sums (sum_j G p_j, sum_j c (q_i - q_j)) of all rows over sources [32b, 32e)."""
+        R.zero_()
+        if self.fail is not None:
+            return
+        S = self.S[: self.n].numpy()
+        q, p = S[:, 0:2], S[:, 2:4]
+        J = np.arange(32 * b, min(self.n, 32 * e))
+        if J.size == 0:
+            return
+        d = q[:, None, :] - q[None, J, :]
+        r = np.sqrt(np.sum(d * d, axis=-1))
+        pdot = p @ p[J].T
+        bad = (r == 0.0) & (np.arange(self.n)[:, None] != J[None, :]) & (pdot != 0.0)
+        if np.any(bad):
+            i, jj = np.argwhere(bad)[0]
+            self.fail = (step * 8 + 2 * s, N.GS_ERR_COINCIDENT, step, 2 * s, int(i), int(J[jj]))
+            return
+        G = np.exp(-r / self.k.alpha) if self.k.family == 0 else np.exp(-0.5 * (r / self.k.alpha) ** 2)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            c = np.where(r > 0, pdot * G / (r if self.k.family == 0 else 1.0), 0.0)
+        R[: self.n, 0:2] = torch.from_numpy(G @ p[J])
+        R[: self.n, 2:4] = torch.from_numpy(np.sum(c[..., None] * d, axis=1))
+
+    def finish(self, step, s, dt, R_rows):
+        if self.fail is not None or self.r1 <= self.r0:
+            return
+        raw = R_rows[: self.r1 - self.r0].numpy()
+        sq = 1.0 if self.k.normalized else 1.0 / (2 * np.pi * self.k.alpha ** 2)
+        sp = sq / (self.k.alpha if self.k.family == 0 else self.k.alpha ** 2)
+        pin = self.S[self.r0:self.r1, 2:4].numpy()
+        dq = raw[:, 0:2] * sq + (self.sigma2 * pin if self.sigma2 != 0.0 else 0.0)
+        k = np.concatenate([dq, raw[:, 2:4] * sp], axis=1)
+        self._epilogue(step, s, dt, k)
+
+    def _epilogue(self, step, s, dt, k):
         if s == 0:
             self.A = k.copy()
         else:
@@ -116,6 +177,11 @@ def _worker(rank, world, port, outdir):
         qT, pT = solver.evolve(q, p, 1.0, 5)
         np.save(os.path.join(outdir, f"evolve_q_{rank}.npy"), qT.numpy())
         np.save(os.path.join(outdir, f"evolve_p_{rank}.npy"), pT.numpy())
+        # 1b) the symmetric split: pair subsets per rank + reduce-scatter of raw row sums
+        sym = sharded.ShardedSolver(spec, backend=NumpyStageBackend(spec, sym=True))
+        qS, pS = sym.evolve(q, p, 1.0, 5)
+        np.save(os.path.join(outdir, f"sym_q_{rank}.npy"), qS.numpy())
+        np.save(os.path.join(outdir, f"sym_p_{rank}.npy"), pS.numpy())
 
         # 2) the C1 match (momentum update) across ranks
         w = configs.c1()
@@ -161,6 +227,10 @@ def test_two_rank_sharded_solver_matches_single_process_oracle():
         for r in range(2):
             np.testing.assert_array_equal(np.load(os.path.join(d, f"evolve_q_{r}.npy")), oq)
             np.testing.assert_array_equal(np.load(os.path.join(d, f"evolve_p_{r}.npy")), op)
+            sq, sp = np.load(os.path.join(d, f"sym_q_{r}.npy")), np.load(os.path.join(d, f"sym_p_{r}.npy"))
+            assert np.abs(sq - oq).max() / np.abs(oq).max() <= 1e-13
+            assert np.abs(sp - op).max() / np.abs(op).max() <= 1e-11
+        np.testing.assert_array_equal(np.load(os.path.join(d, "sym_q_0.npy")), np.load(os.path.join(d, "sym_q_1.npy")))
 
         w = configs.c1()
         o = restate.match_momentum(Kernel(0, w.alpha, True), 0.0, w.q, w.target, w.h, w.epsilon, w.max_iter,
