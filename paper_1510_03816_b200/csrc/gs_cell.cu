@@ -96,21 +96,18 @@ __global__ void k_grid_params(const double* __restrict__ red, int nb, double cut
     g.rc2f = __double2float_ru(rcf * rcf);
     if (bad || !isfinite(mnx) || !isfinite(mxx) || !isfinite(mny) || !isfinite(mxy)) {
         // non-finite stage state: one cell (the stage check has already recorded the failure)
-        g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.nx = 1; g.ny = 1;
+        g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.nx = 1; g.ny = 1; g.ncells = 1; g.hashed = 0;
         g.rc2f = __int_as_float(0x7f800000);  // accept everything
     } else {
-        double h = cutoff;
-        for (;;) {
-            const double fx = floor((mxx - mnx) / h) + 1.0, fy = floor((mxy - mny) / h) + 1.0;
-            if (fx * fy <= (double)cap) {
-                g.nx = (int)fx; g.ny = (int)fy;
-                break;
-            }
-            h *= 1.25;
+        const double fx = floor((mxx - mnx) / cutoff) + 1.0, fy = floor((mxy - mny) / cutoff) + 1.0;
+        g.x0 = mnx; g.y0 = mny; g.inv_h = 1.0 / cutoff;
+        if (fx * fy <= (double)cap) {
+            g.nx = (int)fx; g.ny = (int)fy; g.ncells = g.nx * g.ny; g.hashed = 0;
+        } else {
+            g.nx = 0; g.ny = 0; g.ncells = (int)cap; g.hashed = 1;
         }
-        g.x0 = mnx; g.y0 = mny; g.inv_h = 1.0 / h;
     }
-    g.ncells = g.nx * g.ny;
+    g.pad = 0;
     *gp = g;
 }
 
@@ -119,14 +116,64 @@ __device__ __forceinline__ int cell_coord(double v, double v0, double inv_h, int
     return min(max(c, 0), nmax - 1);
 }
 
+__device__ __forceinline__ long long cell_coord64(double v, double v0, double inv_h) {
+    return (long long)floor(fmin(fmax((v - v0) * inv_h, -4e18), 4e18));
+}
+
+__device__ __forceinline__ unsigned cell_hash(long long cx, long long cy, int ncells) {
+    unsigned long long h = (unsigned long long)cx * 0x9E3779B97F4A7C15ull ^ (unsigned long long)cy * 0xC2B2AE3D27D4EB4Full;
+    h ^= h >> 31;
+    return (unsigned)h & (unsigned)(ncells - 1);
+}
+
+__device__ __forceinline__ unsigned cell_key(const GridParams& g, double x, double y) {
+    if (g.hashed) return cell_hash(cell_coord64(x, g.x0, g.inv_h), cell_coord64(y, g.y0, g.inv_h), g.ncells);
+    const int cx = cell_coord(x, g.x0, g.inv_h, g.nx), cy = cell_coord(y, g.y0, g.inv_h, g.ny);
+    return (unsigned)(cy * g.nx + cx);
+}
+
+// The candidate ranges of a target at (x, y): 3 contiguous stencil rows of the row-major grid,
+// or the (deduplicated) buckets of the 9 stencil cells of the hashed grid.
+struct Ranges {
+    int a[9], b[9];
+    int cnt;
+};
+
+__device__ __forceinline__ void stencil_ranges(const GridParams& g, const int* __restrict__ start, double x, double y,
+                                               Ranges& r) {
+    r.cnt = 0;
+    if (!g.hashed) {
+        const int cx = cell_coord(x, g.x0, g.inv_h, g.nx), cy = cell_coord(y, g.y0, g.inv_h, g.ny);
+        const int xa = max(cx - 1, 0), xb = min(cx + 1, g.nx - 1);
+        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.ny - 1); ++yy) {
+            r.a[r.cnt] = start[yy * g.nx + xa];
+            r.b[r.cnt] = start[yy * g.nx + xb + 1];
+            ++r.cnt;
+        }
+        return;
+    }
+    const long long cx = cell_coord64(x, g.x0, g.inv_h), cy = cell_coord64(y, g.y0, g.inv_h);
+    unsigned seen[9];
+    for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+            const unsigned key = cell_hash(cx + dx, cy + dy, g.ncells);
+            bool dup = false;
+            for (int t = 0; t < r.cnt; ++t) dup |= seen[t] == key;
+            if (dup) continue;  // two stencil cells in one bucket: visit it once
+            seen[r.cnt] = key;
+            r.a[r.cnt] = start[key];
+            r.b[r.cnt] = start[key + 1];
+            ++r.cnt;
+        }
+}
+
 __global__ void k_cell_keys(const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
                             unsigned* keys, unsigned* vals) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const GridParams g = *gp;
     const double4 v = S[i];
-    const int cx = cell_coord(v.x, g.x0, g.inv_h, g.nx), cy = cell_coord(v.y, g.y0, g.inv_h, g.ny);
-    keys[i] = (unsigned)(cy * g.nx + cx);
+    keys[i] = cell_key(g, v.x, v.y);
     vals[i] = (unsigned)i;
 }
 
@@ -177,16 +224,15 @@ __global__ void __launch_bounds__(kCB, 8) k_cell_pair(const double4* __restrict_
     const GridParams g = *gp;
     const double4 me = Ss[kk];
     const float2 mef = Sf[kk];
-    const int key = (int)keys_sorted[kk];
-    const int cy = key / g.nx, cx = key - cy * g.nx;
-    const int xa = max(cx - 1, 0), xb = min(cx + 1, g.nx - 1);
+    Ranges rg;
+    stencil_ranges(g, start, me.x, me.y, rg);
 
     double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
     unsigned long long nacc = 0;
     int nz = 0;
     if (active) {
-        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.ny - 1); ++yy) {
-            const int a = start[yy * g.nx + xa], b = start[yy * g.nx + xb + 1];
+        for (int rr = 0; rr < rg.cnt; ++rr) {
+            const int a = rg.a[rr], b = rg.b[rr];
             for (int base = a + sub; base < b; base += TPL * kCL) {
                 const int m = min(kCL, (b - base + TPL - 1) / TPL);
                 int cnt = 0;
@@ -223,8 +269,8 @@ __global__ void __launch_bounds__(kCB, 8) k_cell_pair(const double4* __restrict_
     }
     if (active && sub == 0) {
         if (nz > 1) {  // rare: a coincident particle among the candidates
-            for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.ny - 1); ++yy) {
-                const int a = start[yy * g.nx + xa], b = start[yy * g.nx + xb + 1];
+            for (int rr = 0; rr < rg.cnt; ++rr) {
+                const int a = rg.a[rr], b = rg.b[rr];
                 for (int j = a; j < b; ++j) {
                     const int64_t jo = (int64_t)perm[j];
                     if (jo == i) continue;

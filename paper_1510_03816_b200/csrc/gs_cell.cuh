@@ -7,10 +7,16 @@
 
 namespace gsb {
 
+// Cells have edge = cutoff.  When the point cloud fits in cell_cap(n) such cells the grid is a
+// dense row-major array (a stencil row = one contiguous sorted range); otherwise (e.g. a
+// diverging flow flinging particles far apart) cells are hashed into cell_cap(n) buckets and
+// the 9 stencil cells are looked up separately — the work stays ~O(N x neighbours).
 struct GridParams {
     double x0, y0, inv_h;
-    int nx, ny, ncells;
-    float rc2f;  // fp32 candidate-filter radius^2: cutoff^2 grown by the fp32 position error
+    int nx, ny, ncells;  // row-major: nx * ny cells; hashed: ncells buckets (a power of two)
+    float rc2f;          // fp32 candidate-filter radius^2: cutoff^2 grown by the fp32 position error
+    int hashed;
+    int pad;
 };
 
 constexpr int kCellBboxBlocks = 296;

@@ -337,6 +337,29 @@ def test_cell_paths_match_oracle_clustered_and_gaussian(cuda):
         assert rel(out.final.q, eq) <= RHS_TOL and rel(out.final.p, ep) <= RHS_TOL
 
 
+def test_cell_path_hashed_grid_for_spread_clouds(cuda):
+    """A few particles flung far away (as in a diverging flow) switch the cell list to hashed
+    buckets; results still equal the oracle's truncated sum, including a coincidence check."""
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+
+    rng = np.random.default_rng(12)
+    n = 6000
+    q = rng.uniform(0, 1, (n, 2))
+    q[:7] = rng.uniform(-1e7, 1e7, (7, 2))   # the bounding box is now ~1e7 wide
+    q[7] = q[0] + 1e-3                          # a neighbour of a far particle
+    p = rng.normal(0, 0.01, (n, 2))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.03 / gs.LAMBDA), sigma2=0.1)
+    with _cell(gs):
+        dq, dp = gs.rhs(spec, gs.ParticleState(q, p))
+    oq, op = native.rhs(_kern(spec), spec.sigma2, q, p, cutoff=0.03)
+    assert rel(dq, oq) <= RHS_TOL and rel(dp, op) <= RHS_TOL
+    q[4444] = q[3]  # coincident with a far particle
+    with _cell(gs):
+        with pytest.raises(gs.DegenerateConfigurationError, match="particles 3 and 4444 coincide"):
+            gs.rhs(spec, gs.ParticleState(q, p))
+
+
 def test_cell_path_detects_coincident_pairs(cuda):
     import paper_1510_03816_b200 as gs
 

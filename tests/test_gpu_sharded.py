@@ -1,0 +1,113 @@
+"""The multi-GPU building blocks on one GPU: stage API, symmetric pair split, ShardedSolver (world 1).
+
+Nothing here runs ranks that wait on each other; the decomposition is checked by evaluating
+the ranks' work items one after another on the single device.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _setup(n=6000, seed=7):
+    import paper_1510_03816_b200 as gs
+
+    rng = np.random.default_rng(seed)
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 0.01, (n, 2))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.4 / gs.LAMBDA), sigma2=0.05)
+    return gs, q, p, spec
+
+
+def test_symmetric_split_sums_to_the_full_pair_sum(cuda):
+    import torch
+
+    from paper_1510_03816_b200 import _native as N
+    from paper_1510_03816_b200 import device, sharded
+
+    gs, q, p, spec = _setup()
+    n = q.shape[0]
+    be = sharded.DeviceStageBackend(spec)
+    lib, h = be.ctx.lib, be.ctx.handle
+    total = int(lib.gs_sym_parts(n))
+    assert total > 0
+    be.begin(q, p, 0, n)
+    assert be.path() == "dense"
+    full = be.new_partials(n)
+    be.pairs_sym(1, 0, 0, total, full)
+    parts = []
+    for b, e in ((0, total // 3), (total // 3, 2 * total // 3), (2 * total // 3, total)):
+        R = be.new_partials(n)
+        be.pairs_sym(1, 0, b, e, R)
+        parts.append(R)
+    split = parts[0] + parts[1] + parts[2]
+    torch.cuda.synchronize()
+    assert rel(split.cpu().numpy(), full.cpu().numpy()) <= 1e-13
+    # the raw sums reproduce particles.rhs after the kernel scales
+    sysc = device.system_struct(spec)
+    dq, dp = device.rhs(spec, q, p)
+    alpha = spec.kernel.alpha
+    want_dq = full[:, 0:2].cpu().numpy() + spec.sigma2 * p
+    want_dp = full[:, 2:4].cpu().numpy() / alpha
+    assert rel(want_dq, dq.cpu().numpy()) <= 1e-13 and rel(want_dp, dp.cpu().numpy()) <= 1e-12
+    st = N.Status()
+    N.check(lib.gs_status_fetch(h, ctypes.byref(st), None), "status")
+    assert st.code == N.GS_OK
+
+
+def test_stage_finish_matches_stage_run(cuda):
+    """rows [r0, r1): (symmetric raw sums -> gs_stage_finish) == gs_stage_run on the same rows."""
+    import torch
+
+    from paper_1510_03816_b200 import sharded
+
+    gs, q, p, spec = _setup(n=5000)
+    n = q.shape[0]
+    r0, r1 = 1200, 3700
+    a = sharded.DeviceStageBackend(spec)
+    a.begin(q, p, 0, n)
+    R = a.new_partials(n)
+    a.pairs_sym(1, 0, 0, a.sym_parts(), R)
+    a.begin(q, p, r0, r1)
+    a.finish(1, 0, 0.1, R[r0:r1].contiguous())
+    Sa = a.state(n).clone()
+    b = sharded.DeviceStageBackend(spec)
+    b.ctx = sharded.N.Context(torch.cuda.current_device())  # separate workspaces
+    b.begin(q, p, r0, r1)
+    b.run(1, 0, 0.1)
+    Sb = b.state(n).clone()
+    torch.cuda.synchronize()
+    assert rel(Sa[r0:r1].cpu().numpy(), Sb[r0:r1].cpu().numpy()) <= 1e-13
+    np.testing.assert_array_equal(Sa[:r0].cpu().numpy(), Sb[:r0].cpu().numpy())  # other rows untouched
+
+
+def test_sharded_solver_world1_equals_evolve(cuda):
+    from paper_1510_03816_b200 import device, sharded
+
+    gs, q, p, spec = _setup(n=3000)
+    solver = sharded.ShardedSolver(spec)
+    qT, pT = solver.evolve(q, p, 1.0, 4)
+    q2, p2, _ = device.evolve(spec, q, p, 1.0, 4)
+    np.testing.assert_array_equal(qT.cpu().numpy(), q2.cpu().numpy())
+    np.testing.assert_array_equal(pT.cpu().numpy(), p2.cpu().numpy())
+
+
+def test_sharded_match_world1_matches_device_match(cuda):
+    from paper_1510_03816_b200 import configs, device, sharded
+
+    import paper_1510_03816_b200 as gs
+
+    w = configs.c1()
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
+    r = sharded.ShardedSolver(spec).match(w.q, w.target, w.h, w.epsilon, w.max_iter, "residual", "max", 1.0, w.steps)
+    d = device.match(spec, w.q, w.target, w.h, w.epsilon, w.max_iter, "residual", "max", 1.0, w.steps)
+    assert r["iterations"] == d["iterations"] == 36 and r["converged"]
+    assert rel(r["p0"].cpu().numpy(), d["p0"].cpu().numpy()) <= 1e-10
+    assert r["hamiltonian"] == pytest.approx(d["hamiltonian"], rel=1e-10)
