@@ -91,13 +91,16 @@ __global__ void k_grid_params(const double* __restrict__ red, int nb, double cut
     // fp32 filter radius: positions are stored as float(x - x0); each carries an error of at
     // most 2^-24 * extent, so a pair's distance in fp32 is off by <= 4 * 2^-24 * extent.
     // Pairs admitted only by this margin have G < 2^-53 (they add < 1e-16 relative).
+    // Once the margin dwarfs the cutoff (a flung-apart cloud) the fp32 test is useless and is
+    // switched off with a NaN radius: the filter `!(r2 >= rc2f)` then admits every candidate.
     const double extent = fmax(fmax(mxx - mnx, mxy - mny), 0.0);
-    const double rcf = cutoff * (1.0 + 1e-6) + 4.0 * extent * 5.9604644775390625e-08 + 1e-30;
-    g.rc2f = __double2float_ru(rcf * rcf);
+    const double margin = 4.0 * extent * 5.9604644775390625e-08;
+    const double rcf = cutoff * (1.0 + 1e-6) + margin + 1e-30;
+    g.rc2f = (margin < 64.0 * cutoff && extent < 1e30) ? __double2float_ru(rcf * rcf) : __int_as_float(0x7fc00000);
     if (bad || !isfinite(mnx) || !isfinite(mxx) || !isfinite(mny) || !isfinite(mxy)) {
         // non-finite stage state: one cell (the stage check has already recorded the failure)
         g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.nx = 1; g.ny = 1; g.ncells = 1; g.hashed = 0;
-        g.rc2f = __int_as_float(0x7f800000);  // accept everything
+        g.rc2f = __int_as_float(0x7fc00000);  // NaN: accept everything
     } else {
         const double fx = floor((mxx - mnx) / cutoff) + 1.0, fy = floor((mxy - mny) / cutoff) + 1.0;
         g.x0 = mnx; g.y0 = mny; g.inv_h = 1.0 / cutoff;
@@ -116,18 +119,20 @@ __device__ __forceinline__ int cell_coord(double v, double v0, double inv_h, int
     return min(max(c, 0), nmax - 1);
 }
 
-__device__ __forceinline__ long long cell_coord64(double v, double v0, double inv_h) {
-    return (long long)floor(fmin(fmax((v - v0) * inv_h, -4e18), 4e18));
-}
+// Hashed cells are identified by the bits of the double floor((x - x0) / cutoff): exact below
+// 2^53 and, beyond, particles within the cutoff of each other still share the value — so no
+// clamping can pile far-flung particles into one cell.
+__device__ __forceinline__ double cell_coordf(double v, double v0, double inv_h) { return floor((v - v0) * inv_h); }
 
-__device__ __forceinline__ unsigned cell_hash(long long cx, long long cy, int ncells) {
-    unsigned long long h = (unsigned long long)cx * 0x9E3779B97F4A7C15ull ^ (unsigned long long)cy * 0xC2B2AE3D27D4EB4Full;
+__device__ __forceinline__ unsigned cell_hash(double cx, double cy, int ncells) {
+    unsigned long long h = (unsigned long long)__double_as_longlong(cx + 0.0) * 0x9E3779B97F4A7C15ull ^
+                           (unsigned long long)__double_as_longlong(cy + 0.0) * 0xC2B2AE3D27D4EB4Full;
     h ^= h >> 31;
     return (unsigned)h & (unsigned)(ncells - 1);
 }
 
 __device__ __forceinline__ unsigned cell_key(const GridParams& g, double x, double y) {
-    if (g.hashed) return cell_hash(cell_coord64(x, g.x0, g.inv_h), cell_coord64(y, g.y0, g.inv_h), g.ncells);
+    if (g.hashed) return cell_hash(cell_coordf(x, g.x0, g.inv_h), cell_coordf(y, g.y0, g.inv_h), g.ncells);
     const int cx = cell_coord(x, g.x0, g.inv_h, g.nx), cy = cell_coord(y, g.y0, g.inv_h, g.ny);
     return (unsigned)(cy * g.nx + cx);
 }
@@ -152,7 +157,7 @@ __device__ __forceinline__ void stencil_ranges(const GridParams& g, const int* _
         }
         return;
     }
-    const long long cx = cell_coord64(x, g.x0, g.inv_h), cy = cell_coord64(y, g.y0, g.inv_h);
+    const double cx = cell_coordf(x, g.x0, g.inv_h), cy = cell_coordf(y, g.y0, g.inv_h);
     unsigned seen[9];
     for (int dy = -1; dy <= 1; ++dy)
         for (int dx = -1; dx <= 1; ++dx) {
@@ -240,7 +245,7 @@ __global__ void __launch_bounds__(kCB, 8) k_cell_pair(const double4* __restrict_
                     const int j = base + TPL * t;
                     const float2 xy = Sf[j];
                     const float dx = mef.x - xy.x, dy = mef.y - xy.y;
-                    if (fmaf(dx, dx, dy * dy) < g.rc2f) s_list[cnt++][threadIdx.x] = j;
+                    if (!(fmaf(dx, dx, dy * dy) >= g.rc2f)) s_list[cnt++][threadIdx.x] = j;  // NaN: keep
                 }
                 nacc += cnt;
                 for (int u = 0; u < cnt; ++u) {
@@ -304,7 +309,7 @@ size_t cell_cub_bytes(int64_t n) {
 int64_t cell_cap(int64_t n) {
     // >= 16 particles per cell on average (coarser grids only cost candidates): 16-bit keys,
     // i.e. two radix passes, up to n = 2^20
-    int64_t cap = 4096;
+    int64_t cap = 16384;
     while (cap < n / 16) cap <<= 1;
     return cap;
 }
