@@ -176,6 +176,13 @@ int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
 double* gs_stage_state(gs_context* ctx);
 int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream);
 
+/* kernels.gram_matrix (kernels.py:181-197) on the device: K (device, n x n row-major) =
+ * G(|q_i - q_j|) for the velocity-space feedback update (shooting.py:138-175, 263-265).
+ * Returns GS_ERR_COINCIDENT with the row-major first coincident pair in *bad_i, *bad_j
+ * ("points i and j coincide; Gram matrix would be singular").  Synchronises. */
+int gs_gram(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, double* K, int64_t* bad_i,
+            int64_t* bad_j, void* stream);
+
 /* Symmetric multi-GPU split of the dense RHS (each unordered pair once, gs_sym.cu):
  *   gs_sym_parts       : number of work items (superblock pairs) of one RHS at this n (0 if the
  *                        symmetric kernel is not available for n)

@@ -13,7 +13,7 @@ from .particles import (ParticleState, SystemSpec, conserved_quantities, hamilto
 from .integrator import EvolveConfig, EvolveResult, evolve
 from .shapes import LandmarkTemplate, circle, ellipse_rot_shift
 from .shooting import (MatchResult, ResidualNorm, ShootingConfig, StopRule, UpdateSpace, contraction_diagnostics,
-                       match)
+                       match, momenta_from_velocity)
 from .device import get_path, set_path
 
 __version__ = "0.1.0"
@@ -23,5 +23,5 @@ __all__ = [
     "KernelFamily", "KernelSpec", "support_radius", "ParticleState", "SystemSpec", "conserved_quantities",
     "hamiltonian", "inexactness_energy", "rhs", "EvolveConfig", "EvolveResult", "evolve", "LandmarkTemplate",
     "circle", "ellipse_rot_shift", "MatchResult", "ResidualNorm", "ShootingConfig", "StopRule", "UpdateSpace",
-    "contraction_diagnostics", "match", "get_path", "set_path",
+    "contraction_diagnostics", "match", "momenta_from_velocity", "get_path", "set_path",
 ]

@@ -33,7 +33,7 @@ EXPORTS = (
     "gs_version", "gs_abi_version", "gs_last_error", "gs_create", "gs_destroy", "gs_rhs", "gs_rhs_rows",
     "gs_status_fetch", "gs_status_reset", "gs_hamiltonian", "gs_evolve", "gs_match", "gs_stage_begin",
     "gs_stage_run", "gs_stage_state", "gs_stage_end", "gs_fp64_peak_probe", "gs_profile_enable",
-    "gs_profile_read", "gs_stage_path", "gs_sym_parts", "gs_stage_pairs_sym", "gs_stage_finish",
+    "gs_profile_read", "gs_stage_path", "gs_sym_parts", "gs_stage_pairs_sym", "gs_stage_finish", "gs_gram",
 )
 
 
@@ -110,6 +110,7 @@ def load(path: str = LIB_PATH):
             "gs_stage_end": ([_vp, _dp, _dp, _vp], ctypes.c_int),
             "gs_fp64_peak_probe": ([_vp, ctypes.c_int32, P(ctypes.c_double), P(ctypes.c_double), _vp], ctypes.c_int),
             "gs_stage_path": ([_vp, P(System), _vp], ctypes.c_int),
+            "gs_gram": ([_vp, P(System), _i64, _dp, _dp, P(_i64), P(_i64), _vp], ctypes.c_int),
             "gs_sym_parts": ([_i64], _i64),
             "gs_stage_pairs_sym": ([_vp, P(System), ctypes.c_int32, ctypes.c_int32, _i64, _i64, _dp, _vp],
                                    ctypes.c_int),

@@ -84,6 +84,7 @@ struct gs_context {
     DevBuf<GridParams> c_gp;
     DevBuf<unsigned char> c_cub;
     DevBuf<unsigned long long> c_acc;   // accepted pairs (profiling)
+    DevBuf<unsigned long long> gram_bad;  // gs_gram's first coincident pair
     size_t c_cub_bytes = 0;
     int cell_on = 0;                    // path of the current call
     // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds
@@ -575,7 +576,7 @@ int gs_destroy(gs_context* ctx) {
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
-    ctx->c_acc.release();
+    ctx->c_acc.release(); ctx->gram_bad.release();
     delete ctx;
     return GS_OK;
 }
@@ -884,6 +885,26 @@ int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream) 
     if (nrows > 0) k_unpack<<<nblk(nrows), 256, 0, (cudaStream_t)stream>>>(ctx->B.ptr, nrows, q_rows, p_rows);
     GS_CUDA(cudaGetLastError());
     return GS_OK;
+}
+
+int gs_gram(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, double* K, int64_t* bad_i,
+            int64_t* bad_j, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !q || !K || !bad_i || !bad_j || n < 1) return fail(GS_ERR_INVALID, "bad gram args");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    GS_CUDA(cudaSetDevice(ctx->device));
+    GS_CUDA(ctx->gram_bad.ensure(1));
+    unsigned long long key = kNoEvent;
+    GS_CUDA(cudaMemsetAsync(ctx->gram_bad.ptr, 0xff, sizeof(key), s));
+    launch_gram(make_const(sys), q, n, K, ctx->gram_bad.ptr, ctx->tbl.ptr, s);
+    ctx->launches++;
+    GS_CUDA(cudaGetLastError());
+    GS_CUDA(cudaMemcpyAsync(&key, ctx->gram_bad.ptr, sizeof(key), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    *bad_i = key == kNoEvent ? -1 : (int64_t)(key / (unsigned long long)n);
+    *bad_j = key == kNoEvent ? -1 : (int64_t)(key % (unsigned long long)n);
+    return key == kNoEvent ? GS_OK : GS_ERR_COINCIDENT;
 }
 
 int gs_stage_path(gs_context* ctx, const gs_system_t* sys, void* stream) {

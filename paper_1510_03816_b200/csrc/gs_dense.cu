@@ -115,6 +115,38 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
 }
 
 // ---------------------------------------------------------------------------------------
+// Gram matrix K[i][j] = G(|q_i - q_j|) (kernels.gram_matrix, kernels.py:181-197) for the
+// velocity-space feedback update (shooting.py:138-175): row-major n x n, and the row-major
+// first coincident pair (i != j, d == 0) recorded in *bad as i*n + j.
+template <int FAM>
+__global__ void k_gram(const double* __restrict__ q, int64_t n, double k1, double scale, double* K,
+                       unsigned long long* bad, const double* __restrict__ tbl_g) {
+    __shared__ double s_tbl[kTblWords];
+    for (int t = threadIdx.y * blockDim.x + threadIdx.x; t < kTblWords; t += blockDim.x * blockDim.y)
+        s_tbl[t] = tbl_g[t];
+    __syncthreads();
+    const double* tbl = s_tbl + ((threadIdx.y * blockDim.x + threadIdx.x) & (kTblRep - 1));
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const double dx = q[2 * i] - q[2 * j], dy = q[2 * i + 1] - q[2 * j + 1];
+    const double r2 = fma(dx, dx, fma(dy, dy, kTinyR2));
+    double g;
+    if (FAM == kFamConical) g = exp2_tbl((r2 * rsqrt_refined(r2)) * k1, tbl);
+    else g = exp2_tbl(r2 * k1, tbl);
+    K[i * n + j] = g * scale;
+    if (i != j && __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) == 0.0)
+        atomicMin(bad, (unsigned long long)(i * n + j));
+}
+
+void launch_gram(const SysConst& sc, const double* q, int64_t n, double* K, unsigned long long* bad,
+                 const double* tbl_dev, cudaStream_t stream) {
+    dim3 block(32, 8), grid((unsigned)((n + 31) / 32), (unsigned)((n + 7) / 8));
+    if (sc.fam == kFamConical) k_gram<kFamConical><<<grid, block, 0, stream>>>(q, n, sc.k1, sc.scale_q, K, bad, tbl_dev);
+    else k_gram<kFamGaussian><<<grid, block, 0, stream>>>(q, n, sc.k1, sc.scale_q, K, bad, tbl_dev);
+}
+
+// ---------------------------------------------------------------------------------------
 // Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_finish(SysConst sc, FinishArgs a) {

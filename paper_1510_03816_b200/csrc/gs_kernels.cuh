@@ -53,6 +53,10 @@ void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* 
 // R[i] = sum over slots of part[slot * pstride + i] (fixed order), i < n.
 void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream);
 
+// Gram matrix of the kernel over q (n x n row-major), first coincident pair -> *bad (i*n+j).
+void launch_gram(const SysConst& sc, const double* q, int64_t n, double* K, unsigned long long* bad,
+                 const double* tbl_dev, cudaStream_t stream);
+
 // Finish modes
 constexpr int kFinRhs = 0;    // write dq, dp rows ((nrows, 2) AoS)
 constexpr int kFinStage = 1;  // RK4 stage epilogue (integrator.py:98-114)

@@ -151,6 +151,24 @@ def hamiltonian(spec, q, p) -> float:
     return float(out.value)
 
 
+def gram(spec, q):
+    """kernels.gram_matrix (kernels.py:181-197) on the device: (N, N) cuda float64."""
+    torch = _torch()
+    ctx = N.Context.get()
+    q = as_device(q, torch)
+    n = q.shape[0]
+    K = torch.empty((n, n), dtype=torch.float64, device=q.device)
+    bi, bj = ctypes.c_int64(), ctypes.c_int64()
+    sysc = system_struct(spec)
+    rc = ctx.lib.gs_gram(ctx.handle, ctypes.byref(sysc), n, _ptr(q), _ptr(K), ctypes.byref(bi), ctypes.byref(bj),
+                         _stream_ptr(torch))
+    if rc == N.GS_ERR_COINCIDENT:
+        raise _errors.DegenerateConfigurationError(
+            f"points {bi.value} and {bj.value} coincide; Gram matrix would be singular")
+    N.check(rc, "gs_gram")
+    return K
+
+
 def n_frames(steps: int, capture_every: int) -> int:
     if capture_every <= 0:
         return 0

@@ -10,10 +10,10 @@ callees by name, so every alias must be rebound (SURVEY.md §8(b) "Rebinding poi
                  (cli.py:58), geoshoot.match
     hamiltonian  geoshoot.particles.hamiltonian, geoshoot.shooting.hamiltonian (shooting.py:30), geoshoot.hamiltonian
 
-After ``install()`` the reference's own callers (analysis, cli, newton_match, the velocity-
-space feedback loop) run their shoots on the device, with the reference's exception classes
-and result types.  ``match`` with the momentum update runs entirely on the device; the
-velocity update keeps the reference's own host Gram solve around device shoots.  Kernel
+After ``install()`` the reference's own callers (analysis, cli, newton_match) run their shoots
+on the device, with the reference's exception classes and result types.  ``match`` runs on the
+device in both update spaces (momentum: one device loop; velocity: device Gram matrix, cuSOLVER
+Cholesky via torch.linalg, device shoots), as does ``momenta_from_velocity``.  Kernel
 families the device does not provide (bessel) raise ConfigurationError — there is no CPU
 fallback.  Use ``pytest -p paper_1510_03816_b200.pytest_dropin`` to run a geoshoot-based
 test suite against the device path.
@@ -35,6 +35,7 @@ _ALIASES = {
     "evolve": ("integrator", "shooting", "analysis", "cli", ""),
     "match": ("shooting", "analysis", "cli", ""),
     "hamiltonian": ("particles", "shooting", ""),
+    "momenta_from_velocity": ("shooting", ""),
 }
 
 
@@ -62,14 +63,13 @@ def install(pkg=None):
                MatchResult=pkg.MatchResult, LandmarkTemplate=pkg.LandmarkTemplate)
 
     def match(reference, target, cfg):
-        """shooting.match: momentum update on the device; velocity update = the reference's
-        own loop (shooting.py:259-301) whose shoots call the rebound device ``evolve``."""
-        if str(getattr(cfg.update_space, "value", cfg.update_space)) == "momentum":
-            return _shooting.match(reference, target, cfg)
-        return original_match(reference, target, cfg)
+        """shooting.match on the device, both update spaces (momentum: one device loop;
+        velocity: device Gram + cuSOLVER factor + device shoots)."""
+        return _shooting.match(reference, target, cfg)
 
+    match.original = original_match
     impl = {"rhs": _particles.rhs, "evolve": _integrator.evolve, "match": match,
-            "hamiltonian": _particles.hamiltonian}
+            "hamiltonian": _particles.hamiltonian, "momenta_from_velocity": _shooting.momenta_from_velocity}
     for fname, subs in _ALIASES.items():
         for sub in subs:
             mod = _module(pkg, sub)

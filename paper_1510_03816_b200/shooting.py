@@ -4,9 +4,9 @@
 p0 <- p0 + h (Y - X(T)) (shooting.py:266-267) — runs entirely in libgs_b200.so: the
 initial shoot, every RK4 stage, the residual, its norm, the update and both stop rules,
 with one persistent kernel for N <= 512 and a device loop reading two scalars per
-iteration above that.  ``UpdateSpace.VELOCITY`` (the reference default) keeps the
-reference's host Gram/Cholesky solve between device shoots (SURVEY.md §8(f1) moves it
-to the device next).
+iteration above that.  ``UpdateSpace.VELOCITY`` (the reference default)
+builds the Gram matrix on the device (gs_gram), factors it once with cuSOLVER (torch.linalg)
+and runs each iteration as a triangular solve pair plus a device shoot.
 """
 
 from __future__ import annotations
@@ -21,11 +21,10 @@ from . import device
 from . import errors as _errors
 from . import types as _types
 from .integrator import EvolveConfig
-from .kernels import family_name
 from .particles import SystemSpec
 
 __all__ = ["UpdateSpace", "StopRule", "ResidualNorm", "ShootingConfig", "MatchResult", "match",
-           "contraction_diagnostics"]
+           "contraction_diagnostics", "momenta_from_velocity"]
 
 _BLOWUP_FACTOR = 1e6          # shooting.py:47
 _ILL_CONDITIONED = 1e12       # shooting.py:48
@@ -129,33 +128,28 @@ def match(reference, target, cfg):
                         r["diagnosis"], ())
 
 
-# --- velocity-space update: host Gram solve between device shoots ---------------------------
-def _gram(kernel, q0: np.ndarray) -> np.ndarray:
-    """kernels.gram_matrix (kernels.py:181-197) for conical/gaussian."""
-    diff = q0[:, None, :] - q0[None, :, :]
-    dist = np.sqrt(np.sum(diff * diff, axis=-1))
-    off = ~np.eye(len(q0), dtype=bool)
-    if np.any(dist[off] == 0.0):
-        i, j = np.argwhere((dist == 0.0) & off)[0]
-        raise _errors.DegenerateConfigurationError(f"points {i} and {j} coincide; Gram matrix would be singular")
-    fam = family_name(kernel)
-    k = np.exp(-dist / kernel.alpha) if fam == "conical" else np.exp(-0.5 * (dist / kernel.alpha) ** 2)
-    if not kernel.normalized:
-        k *= 1.0 / (2.0 * math.pi * kernel.alpha**2)
-    return k
-
-
+# --- velocity-space update: Gram solve on the device -----------------------
 def _match_velocity(reference, target, cfg):
-    from scipy.linalg import cho_factor, cho_solve
+    """shooting.py:218-301 with UpdateSpace.VELOCITY: u <- u + h r, p = K^-1 u (:263-265).
 
-    q0 = reference.points
-    n = reference.n
-    K = _gram(cfg.system.kernel, q0)
-    cond = float(np.linalg.cond(K))
-    try:
-        factor = cho_factor(K, lower=True)
-    except np.linalg.LinAlgError as exc:
-        raise _errors.DegenerateConfigurationError(f"kernel Gram matrix is not positive definite: {exc}") from exc
+    Everything stays on the device: the Gram matrix over q0 comes from libgs_b200 (`gs_gram`,
+    kernels.py:181-197), its Cholesky factor and condition number (2-norm, = the reference's
+    np.linalg.cond for an SPD K) from cuSOLVER through torch.linalg (a library factorisation,
+    once per match), every iteration is one triangular solve pair + one device shoot; the
+    host reads the residual norm.
+    """
+    torch = device._torch()
+    q0 = device.as_device(reference.points, torch)
+    tgt = device.as_device(target.points, torch)
+    K = device.gram(cfg.system, q0)
+    evals = torch.linalg.eigvalsh(K)
+    amin, amax = float(evals.abs().min()), float(evals.abs().max())
+    cond = amax / amin if amin > 0 else math.inf
+    L, info = torch.linalg.cholesky_ex(K)
+    if int(info) != 0:
+        raise _errors.DegenerateConfigurationError(
+            f"kernel Gram matrix is not positive definite: {int(info)}-th leading minor of the array is not "
+            "positive definite")
     warnings = ()
     if not (cond < _ILL_CONDITIONED):
         warnings = (f"Gram matrix condition number {cond:.3e} exceeds {_ILL_CONDITIONED:.0e}; "
@@ -164,35 +158,37 @@ def _match_velocity(reference, target, cfg):
     mdelta = _enum_value(cfg.stop_rule) == "momentum-delta"
     ev = cfg.evolve
 
-    def shoot(p):
-        q, _, _ = device.evolve(cfg.system, q0, p, ev.t_final, ev.steps, 0)
-        return q.cpu().numpy()
+    def dnorm(r) -> float:
+        if norm_kind == "max":
+            return float(torch.hypot(r[:, 0], r[:, 1]).max())
+        return float(torch.linalg.vector_norm(r.reshape(-1)))
 
     def result(p, history, converged, endpoint, diagnosis):
-        return _make_result(p, len(history), converged, history, device.hamiltonian(cfg.system, q0, p), endpoint,
-                            reference, target, _norm(norm_kind, target.points - endpoint), diagnosis, warnings)
+        return _make_result(p.cpu().numpy(), len(history), converged, history,
+                            device.hamiltonian(cfg.system, q0, p), endpoint.cpu().numpy(), reference, target,
+                            dnorm(tgt - endpoint), diagnosis, warnings)
 
-    u = np.zeros((n, 2))
-    p = np.zeros((n, 2))
-    endpoint = q0.copy()  # evolve(q0, 0) leaves q0 unchanged
-    residual = target.points - endpoint
+    u = torch.zeros_like(q0)
+    p = torch.zeros_like(q0)
+    endpoint = q0.clone()  # evolve(q0, 0) leaves q0 unchanged
+    residual = tgt - endpoint
     history: list = []
     initial = None
     if not mdelta:
-        initial = _norm(norm_kind, residual)
+        initial = dnorm(residual)
         if initial < cfg.epsilon:
             return result(p, history, True, endpoint, None)
     for _ in range(cfg.max_iter):
-        delta = cfg.h * _norm(norm_kind, residual)
+        delta = cfg.h * dnorm(residual)
         u = u + cfg.h * residual
-        p = cho_solve(factor, u)
+        p = torch.cholesky_solve(u, L)
         try:
-            endpoint_new = shoot(p)
+            endpoint_new, _, _ = device.evolve(cfg.system, q0, p, ev.t_final, ev.steps, 0)
         except (_errors.DivergenceError, _errors.DegenerateConfigurationError) as exc:
             return result(p, history, False, endpoint, f"step too large ({exc})")
         endpoint = endpoint_new
-        residual = target.points - endpoint
-        value = delta if mdelta else _norm(norm_kind, residual)
+        residual = tgt - endpoint
+        value = delta if mdelta else dnorm(residual)
         if initial is None:
             initial = value
         history.append(value)
@@ -201,6 +197,26 @@ def _match_velocity(reference, target, cfg):
         if value < cfg.epsilon:
             return result(p, history, True, endpoint, None)
     return result(p, history, False, endpoint, "iteration cap reached before the stopping rule")
+
+
+def momenta_from_velocity(kernel, q0, u0) -> np.ndarray:
+    """shooting.py:162-175: solve (K (x) I2) p = u on the device (Gram kernel + Cholesky)."""
+    q0 = np.asarray(q0, dtype=float)
+    u0 = np.asarray(u0, dtype=float)
+    if q0.shape != u0.shape or q0.ndim != 2 or q0.shape[1] != 2:
+        raise ValueError(f"q0 and u0 must both have shape (N, 2), got {q0.shape} and {u0.shape}")
+    torch = device._torch()
+
+    class _Spec:
+        pass
+
+    spec = _Spec()
+    spec.kernel, spec.sigma2 = kernel, 0.0
+    K = device.gram(spec, device.as_device(q0, torch))
+    L, info = torch.linalg.cholesky_ex(K)
+    if int(info) != 0:
+        raise _errors.DegenerateConfigurationError("kernel Gram matrix is not positive definite")
+    return torch.cholesky_solve(device.as_device(u0, torch), L).cpu().numpy()
 
 
 def contraction_diagnostics(result) -> list:

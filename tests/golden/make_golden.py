@@ -199,6 +199,18 @@ def match_cases():
         "blowup": (gs.circle(2.0, n=16), gs.heart4(n=16), quick(h=2.0, epsilon=1e-3)),
         "blowup_big": (gs.circle(2.0, n=16), gs.heart4(n=16), quick(h=60.0, epsilon=1e-3)),
         "blowup_inf": (gs.circle(2.0, n=16), gs.heart4(n=16), quick(h=1e160, epsilon=1e-3)),
+        # velocity-space update (the reference default, shooting.py:80, 263-265)
+        "vel_small": (REF, TGT, quick(epsilon=1e-8, update_space=gs.UpdateSpace.VELOCITY)),
+        "vel_c1": (gs.LandmarkTemplate(c1.q, "X"), gs.LandmarkTemplate(c1.target, "Y"),
+                   gs.ShootingConfig(h=c1.h, epsilon=c1.epsilon, max_iter=c1.max_iter, update_space="velocity",
+                                     evolve=gs.EvolveConfig(t_final=1.0, steps=c1.steps),
+                                     system=spec_of(alpha=c1.alpha))),
+        "vel_inexact": (REF, TGT, quick(h=0.4, stop_rule=gs.StopRule.MOMENTUM_DELTA, system=gs.SystemSpec(sigma2=0.3),
+                                        update_space=gs.UpdateSpace.VELOCITY)),
+        "vel_heart": (gs.circle(2.0, n=16), gs.heart4(16), gs.ShootingConfig(h=0.4, max_iter=2000)),
+        "vel_illcond": (gs.circle(1.0, n=8), gs.circle(1.1, n=8),
+                        quick(epsilon=1e-2, max_iter=5, update_space=gs.UpdateSpace.VELOCITY,
+                              system=spec_of(family="gaussian", alpha=20.0), evolve=gs.EvolveConfig(steps=20))),
         "circ256": (gs.circle(1.0, n=256), gs.ellipse_rot_shift(1.3, 0.7, 0.0, n=256),
                     gs.ShootingConfig(h=0.5, epsilon=1e-6, max_iter=300, update_space="momentum",
                                       evolve=gs.EvolveConfig(steps=20), system=spec_of(alpha=0.1 / LAM))),
@@ -225,7 +237,7 @@ def gen_match(out):
             t_final=cfg.evolve.t_final, steps=cfg.evolve.steps,
             iterations=res.iterations, converged=res.converged, hamiltonian=res.hamiltonian,
             final_residual=res.final_residual, diagnosis=res.diagnosis,
-            final_label=res.final_template.label, seconds=dt,
+            final_label=res.final_template.label, seconds=dt, warnings=list(res.warnings),
         )
         print(f"match {name}: it={res.iterations} conv={res.converged} H={res.hamiltonian:.10g} "
               f"diag={res.diagnosis!r} ({dt:.2f}s)")

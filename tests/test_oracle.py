@@ -96,7 +96,7 @@ def _kernel(meta):
     return Kernel(0 if meta["family"] == "conical" else 1, meta["alpha"], meta["normalized"])
 
 
-@pytest.mark.parametrize("name", sorted(MATCH_META))
+@pytest.mark.parametrize("name", sorted(n for n, m in MATCH_META.items() if m["update_space"] == "momentum"))
 def test_oracle_match_matches_reference(name):
     m, c = MATCH_META[name], MATCH[name]
     out = native.match_momentum(_kernel(m), m["sigma2"], c["ref"], c["tgt"], m["h"], m["epsilon"], m["max_iter"],
