@@ -68,45 +68,43 @@ static inline int pair_term(const go_params* k, long i, long j, const double* q,
     return 0;
 }
 
-/* uniform grid over the bounding box, cell edge >= cutoff */
+/* Cells of edge = cutoff, hashed into nb (power of two >= 2n) buckets by the bits of the double
+ * cell coordinate floor(x / cutoff): no bounding box, so a flung-apart (diverging) state costs
+ * the same as a compact one.  Pairs are still decided by the exact distance test. */
 typedef struct {
-    double x0, y0, inv;
-    long nx, ny;
-    long* start;   /* nx*ny + 1 */
-    long* idx;     /* n, particle indices sorted by cell (stable) */
+    double inv;
+    unsigned long nb;
+    long* start;   /* nb + 1 */
+    long* idx;     /* n, particle indices grouped by bucket (ascending within a bucket) */
 } go_grid;
 
-static int grid_build(go_grid* g, const double* q, long n, double cutoff) {
-    double xmin = q[0], xmax = q[0], ymin = q[1], ymax = q[1];
-    for (long i = 1; i < n; i++) {
-        xmin = fmin(xmin, q[2 * i]); xmax = fmax(xmax, q[2 * i]);
-        ymin = fmin(ymin, q[2 * i + 1]); ymax = fmax(ymax, q[2 * i + 1]);
-    }
-    g->x0 = xmin; g->y0 = ymin; g->inv = 1.0 / cutoff;
-    /* decide in floating point: a blown-up state spreads the points far beyond any grid */
-    double fx = floor((xmax - xmin) * g->inv) + 1.0, fy = floor((ymax - ymin) * g->inv) + 1.0;
-    if (!(fx * fy <= 64.0 * (double)n + 1024.0)) return -1;   /* caller falls back to the pair loop */
-    g->nx = (long)fx;
-    g->ny = (long)fy;
-    long nc = g->nx * g->ny;
-    g->start = (long*)calloc(nc + 1, sizeof(long));
+static unsigned long cell_bucket(double cx, double cy, unsigned long nb) {
+    double ax = cx + 0.0, ay = cy + 0.0;   /* -0.0 -> +0.0 */
+    unsigned long long bx, by;
+    memcpy(&bx, &ax, 8);
+    memcpy(&by, &ay, 8);
+    unsigned long long h = bx * 0x9E3779B97F4A7C15ull ^ by * 0xC2B2AE3D27D4EB4Full;
+    h ^= h >> 31;
+    return (unsigned long)(h & (nb - 1));
+}
+
+static void grid_build(go_grid* g, const double* q, long n, double cutoff) {
+    g->inv = 1.0 / cutoff;
+    g->nb = 1;
+    while (g->nb < 2ul * (unsigned long)n) g->nb <<= 1;
+    g->start = (long*)calloc(g->nb + 1, sizeof(long));
     g->idx = (long*)malloc(n * sizeof(long));
-    long* cell = (long*)malloc(n * sizeof(long));
+    unsigned long* cell = (unsigned long*)malloc(n * sizeof(unsigned long));
     for (long i = 0; i < n; i++) {
-        long cx = (long)floor((q[2 * i] - g->x0) * g->inv);
-        long cy = (long)floor((q[2 * i + 1] - g->y0) * g->inv);
-        if (cx >= g->nx) cx = g->nx - 1;
-        if (cy >= g->ny) cy = g->ny - 1;
-        cell[i] = cy * g->nx + cx;
+        cell[i] = cell_bucket(floor(q[2 * i] * g->inv), floor(q[2 * i + 1] * g->inv), g->nb);
         g->start[cell[i] + 1]++;
     }
-    for (long c = 0; c < nc; c++) g->start[c + 1] += g->start[c];
-    long* fill = (long*)malloc(nc * sizeof(long));
-    memcpy(fill, g->start, nc * sizeof(long));
+    for (unsigned long c = 0; c < g->nb; c++) g->start[c + 1] += g->start[c];
+    long* fill = (long*)malloc(g->nb * sizeof(long));
+    memcpy(fill, g->start, g->nb * sizeof(long));
     for (long i = 0; i < n; i++) g->idx[fill[cell[i]]++] = i;
     free(fill);
     free(cell);
-    return 0;
 }
 
 static void grid_free(go_grid* g) { free(g->start); free(g->idx); }
@@ -116,40 +114,40 @@ int go_rhs(const go_params* k, long n, const double* q, const double* p, double*
            long r0, long r1, long long* bad) {
     long long best = INT64_MAX;
     go_grid g;
-    int use_grid = (k->cutoff > 0.0) && grid_build(&g, q, n, k->cutoff) == 0;
+    const int use_grid = k->cutoff > 0.0;
+    if (use_grid) grid_build(&g, q, n, k->cutoff);
     double c2 = k->cutoff * k->cutoff;
 #pragma omp parallel for schedule(dynamic, 64) reduction(min : best)
     for (long i = r0; i < r1; i++) {
         double aq[2] = {0.0, 0.0}, ap[2] = {0.0, 0.0};
         if (!use_grid) {
             for (long j = 0; j < n; j++) {
-                if (k->cutoff > 0.0) {
-                    double dx = q[2 * i] - q[2 * j], dy = q[2 * i + 1] - q[2 * j + 1];
-                    if (!(dx * dx + dy * dy < c2)) continue;
-                }
                 if (pair_term(k, i, j, q, p, aq, ap)) {
                     long long key = (long long)i * n + j;
                     if (key < best) best = key;
                 }
             }
         } else {
-            long cx = (long)floor((q[2 * i] - g.x0) * g.inv);
-            long cy = (long)floor((q[2 * i + 1] - g.y0) * g.inv);
-            if (cx >= g.nx) cx = g.nx - 1;
-            if (cy >= g.ny) cy = g.ny - 1;
-            for (long yy = cy - 1; yy <= cy + 1; yy++) {
-                if (yy < 0 || yy >= g.ny) continue;
-                long xa = cx > 0 ? cx - 1 : 0, xb = cx + 1 < g.nx ? cx + 1 : g.nx - 1;
-                for (long s = g.start[yy * g.nx + xa]; s < g.start[yy * g.nx + xb + 1]; s++) {
-                    long j = g.idx[s];
-                    double dx = q[2 * i] - q[2 * j], dy = q[2 * i + 1] - q[2 * j + 1];
-                    if (!(dx * dx + dy * dy < c2)) continue;
-                    if (pair_term(k, i, j, q, p, aq, ap)) {
-                        long long key = (long long)i * n + j;
-                        if (key < best) best = key;
+            const double cx = floor(q[2 * i] * g.inv), cy = floor(q[2 * i + 1] * g.inv);
+            unsigned long seen[9];
+            int ns = 0;
+            for (int ddy = -1; ddy <= 1; ddy++)
+                for (int ddx = -1; ddx <= 1; ddx++) {
+                    const unsigned long b = cell_bucket(cx + ddx, cy + ddy, g.nb);
+                    int dup = 0;
+                    for (int t = 0; t < ns; t++) dup |= seen[t] == b;
+                    if (dup) continue;
+                    seen[ns++] = b;
+                    for (long s = g.start[b]; s < g.start[b + 1]; s++) {
+                        long j = g.idx[s];
+                        double dx = q[2 * i] - q[2 * j], dy = q[2 * i + 1] - q[2 * j + 1];
+                        if (!(dx * dx + dy * dy < c2)) continue;
+                        if (pair_term(k, i, j, q, p, aq, ap)) {
+                            long long key = (long long)i * n + j;
+                            if (key < best) best = key;
+                        }
                     }
                 }
-            }
         }
         if (k->sigma2 != 0.0) {
             aq[0] += k->sigma2 * p[2 * i];

@@ -41,18 +41,22 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), tag: str = "") -> str:
+    """Compile + link.  `defines`/`tag` build an A/B variant (libgs_b200_<tag>.so, objects in
+    build/<tag>) for experiments; the product library is the untagged one."""
+    build_dir = os.path.join(BUILD, tag) if tag else BUILD
+    lib = LIB.replace(".so", f"_{tag}.so") if tag else LIB
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS]
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     objs = []
     jobs = []
     for s in srcs:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(BUILD, s.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, s.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + headers + [__file__]):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
+            cmd = [nvcc(), *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -67,12 +71,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for out in ex.map(run, jobs):
             if verbose and out:
                 print(out, file=sys.stderr)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+    if force or jobs or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -11,7 +11,7 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgs_b200.so")
+LIB_PATH = os.environ.get("GS_B200_LIB") or os.path.join(_PKG, "libgs_b200.so")  # override: A/B variants
 
 GS_OK = 0
 GS_ERR_INVALID = 1

@@ -36,6 +36,9 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kST = 64;  // threads per CTA
+#ifndef GS_SYM_MINB      // resident CTAs per SM the register allocation is bounded for (A/B builds)
+#define GS_SYM_MINB 10
+#endif
 
 struct Acc {
     double qx, qy, px, py;
@@ -82,7 +85,7 @@ __device__ __forceinline__ void add_to(double4* dst, const Acc& a) {
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(kST, 10) k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, int G,
+__global__ void __launch_bounds__(kST, GS_SYM_MINB) k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, int G,
                                                        int nsb, long long cta0, double k1, double4* __restrict__ part,
                                                        int64_t pstride, DevStatus* st, unsigned long long event,
                                                        const double* __restrict__ tbl_g) {

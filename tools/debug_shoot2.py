@@ -36,7 +36,16 @@ def main():
     torch.cuda.synchronize()
     print(f"shoot 1: {time.perf_counter() - t0:.3f} s, max|q| {float(q1.abs().max()):.3e}", flush=True)
     p2 = p1 + w.h * (w.target - q1.cpu().numpy())
-    print(f"max|p2| {np.abs(p2).max():.3e}", flush=True)
+    big = np.abs(p2).max(axis=1)
+    print(f"max|p2| {big.max():.3e}; |p2| > 1: {(big > 1).sum()} of {len(big)}; median {np.median(big):.3e}",
+          flush=True)
+    for k in (1, 2, 4):
+        t0 = time.perf_counter()
+        qk, _, _ = device.evolve(spec, w.q, p2, 1.0 * k / steps, k)
+        torch.cuda.synchronize()
+        qa = qk.abs().max(dim=1).values
+        print(f"shoot 2, first {k} steps: {time.perf_counter() - t0:.3f} s, max|q| {float(qa.max()):.3e}, "
+              f"#|q|>10: {int((qa > 10).sum())}", flush=True)
     t0 = time.perf_counter()
     try:
         q2, pp2, _ = device.evolve(spec, w.q, p2, 1.0, steps)
