@@ -155,7 +155,13 @@ def main():
         out["first_shoot_s"] = t_ev
         out["first_shoot_max_abs_q"] = float(qT.abs().max())
         if not a.quick:
-            ck = 1 if name == "C5" else 2  # the diverging shoot makes later steps quadratic for the CPU grid
+            # per-RHS parity at full size on the first shoot's initial state (before any blow-up)
+            dq, dp = device.rhs(spec, w.q, p1)
+            oq, op = native.rhs(kern(w.alpha), w.sigma2, w.q, p1, cutoff=w.sigma)
+            out["rhs_rel_err_dq_vs_oracle"] = rel(dq.cpu().numpy(), oq)
+            out["rhs_rel_err_dp_vs_oracle"] = rel(dp.cpu().numpy(), op)
+            # the stiff flow amplifies rounding from the first step on: the 1-step shoot is info only
+            ck = 1
             tf = 1.0 * ck / w.steps
             (qk, pk, _), _ = timed(torch, lambda: device.evolve(spec, w.q, p1, tf, ck))
             t0 = time.perf_counter()
