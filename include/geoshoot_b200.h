@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 #define GS_OK 0
 #define GS_ERR_INVALID 1
@@ -152,10 +152,45 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
 /* shooting.match with UpdateSpace.MOMENTUM: q0, target (device, n x 2).  Outputs p0_out and
  * endpoint_out (device, n x 2), history_out (host, >= max_iter doubles) and *result (host).
  * The whole feedback loop runs on the device; the host reads two scalars per iteration
- * (one persistent kernel for n <= 1024).  Synchronises. */
+ * (one persistent kernel for n <= 512).  Synchronises. */
 int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* cfg, int64_t n,
              const double* q0, const double* target, double* p0_out, double* endpoint_out,
              double* history_out, gs_match_result_t* result, void* stream);
+
+/* ---- batched independent trajectories ---------------------------------
+ * Replace the reference's serial loops over independent matches / shoots:
+ *   convergence_sweep cells (analysis.py:254-283), cluster_test / shape_distance pairs
+ *   (analysis.py:109-126, 162-207), exact_vs_inexact rows (analysis.py:326-377): gs_match_batch;
+ *   newton_match Jacobian columns, 2N shoots per iteration (shooting.py:367-372): gs_evolve_batch.
+ * For n <= 512 on the dense path every item is one CTA of ONE persistent launch; otherwise the
+ * items run one after another through gs_match / gs_evolve. */
+typedef struct {
+    gs_system_t system;        /* per item (alpha, sigma2 may differ; the family may not) */
+    gs_match_config_t config;  /* per item (h, epsilon, max_iter, stop rule, norm, evolve config) */
+} gs_batch_item_t;
+
+/* batch matches over n landmarks.  Item b reads q0 + b*q0_stride and target + b*target_stride
+ * (device, n x 2; stride 0 = shared) and writes p0_out / endpoint_out + b*2n (device) and
+ * history_out + b*history_stride (DEVICE; history_stride >= every max_iter) and results[b]
+ * (host; seconds_device = the whole batch's device time).
+ * gram_factor != NULL selects the VELOCITY update space (shooting.py:263-265): the lower
+ * Cholesky factor L of the Gram matrix over item b's q0 at gram_factor + b*factor_stride
+ * (device, n x n row-major, K = L L^T; stride 0 = shared), and p = K^-1 u is solved on the
+ * device every iteration (velocity batches need n <= 512 and the dense path).
+ * Validation errors name the item.  Synchronises. */
+int gs_match_batch(gs_context* ctx, const gs_batch_item_t* items, int64_t batch, int64_t n,
+                   const double* q0, int64_t q0_stride, const double* target, int64_t target_stride,
+                   const double* gram_factor, int64_t factor_stride, double* p0_out,
+                   double* endpoint_out, double* history_out, int64_t history_stride,
+                   gs_match_result_t* results, void* stream);
+
+/* batch evolves of one system: item b starts from (q_in + b*q_stride, p_io + b*2n) (device;
+ * q_stride 0 = shared q0) and ends in (q_out + b*2n, p_io + b*2n).  status[b] (host) carries
+ * each item's failure as gs_evolve would report it; the call returns GS_OK unless the batch
+ * itself is invalid.  Synchronises. */
+int gs_evolve_batch(gs_context* ctx, const gs_system_t* sys, int64_t batch, int64_t n,
+                    double t_final, int32_t steps, const double* q_in, int64_t q_stride,
+                    double* q_out, double* p_io, gs_status_t* status, void* stream);
 
 /* ---- stage-level API (multi-GPU driver; one rank owns rows [row0, row1)) -----------------
  * The context keeps a packed stage state S (n x 4: x, y, px, py, device) that every rank

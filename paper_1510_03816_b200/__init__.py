@@ -13,7 +13,10 @@ from .particles import (ParticleState, SystemSpec, conserved_quantities, hamilto
 from .integrator import EvolveConfig, EvolveResult, evolve
 from .shapes import LandmarkTemplate, circle, ellipse_rot_shift
 from .shooting import (MatchResult, ResidualNorm, ShootingConfig, StopRule, UpdateSpace, contraction_diagnostics,
-                       match, momenta_from_velocity)
+                       match, momenta_from_velocity, newton_match)
+from .analysis import (DIVERGED, ClusterVerdict, DistanceRecord, ExactnessRow, SweepGrid, cluster_test,
+                       convergence_sweep, exact_vs_inexact, iso_invariance_check, predict, shape_distance,
+                       triangle_inequality_audit)
 from .device import get_path, set_path
 
 __version__ = "0.1.0"
@@ -23,5 +26,7 @@ __all__ = [
     "KernelFamily", "KernelSpec", "support_radius", "ParticleState", "SystemSpec", "conserved_quantities",
     "hamiltonian", "inexactness_energy", "rhs", "EvolveConfig", "EvolveResult", "evolve", "LandmarkTemplate",
     "circle", "ellipse_rot_shift", "MatchResult", "ResidualNorm", "ShootingConfig", "StopRule", "UpdateSpace",
-    "contraction_diagnostics", "match", "momenta_from_velocity", "get_path", "set_path",
+    "contraction_diagnostics", "match", "momenta_from_velocity", "newton_match", "get_path", "set_path",
+    "DIVERGED", "ClusterVerdict", "DistanceRecord", "ExactnessRow", "SweepGrid", "cluster_test", "convergence_sweep",
+    "exact_vs_inexact", "iso_invariance_check", "predict", "shape_distance", "triangle_inequality_audit",
 ]

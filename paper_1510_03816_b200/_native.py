@@ -34,6 +34,7 @@ EXPORTS = (
     "gs_status_fetch", "gs_status_reset", "gs_hamiltonian", "gs_evolve", "gs_match", "gs_stage_begin",
     "gs_stage_run", "gs_stage_state", "gs_stage_end", "gs_fp64_peak_probe", "gs_profile_enable",
     "gs_profile_read", "gs_stage_path", "gs_sym_parts", "gs_stage_pairs_sym", "gs_stage_finish", "gs_gram",
+    "gs_match_batch", "gs_evolve_batch",
 )
 
 
@@ -67,6 +68,10 @@ class MatchConfig(ctypes.Structure):
 class MatchResultC(ctypes.Structure):
     _fields_ = [("outcome", ctypes.c_int32), ("iterations", ctypes.c_int32), ("hamiltonian", ctypes.c_double),
                 ("final_residual", ctypes.c_double), ("status", Status), ("seconds_device", ctypes.c_double)]
+
+
+class BatchItem(ctypes.Structure):
+    _fields_ = [("system", System), ("config", MatchConfig)]
 
 
 _lib = None
@@ -116,6 +121,10 @@ def load(path: str = LIB_PATH):
                                    ctypes.c_int),
             "gs_stage_finish": ([_vp, P(System), ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _dp, _vp],
                                 ctypes.c_int),
+            "gs_match_batch": ([_vp, P(BatchItem), _i64, _i64, _dp, _i64, _dp, _i64, _dp, _i64, _dp, _dp, _dp, _i64,
+                                P(MatchResultC), _vp], ctypes.c_int),
+            "gs_evolve_batch": ([_vp, P(System), _i64, _i64, ctypes.c_double, ctypes.c_int32, _dp, _i64, _dp, _dp,
+                                 P(Status), _vp], ctypes.c_int),
             "gs_profile_enable": ([_vp, ctypes.c_int32], ctypes.c_int),
             "gs_profile_read": ([_vp, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64),
                                  ctypes.c_int32], ctypes.c_int),

@@ -68,6 +68,8 @@ struct gs_context {
     // match / reductions
     DevBuf<double> q0, tgt, p, resid, red, ham, hist, scal;
     DevBuf<SmallResult> small_res;
+    DevBuf<SmallItem> b_items;       // batched launches: per-item constants
+    DevBuf<DevStatus> b_st;          // batched evolve: per-item failure records
     // profiling: CUDA events around every pair-kernel launch, kernel launch counter
     int prof_on = 0;
     std::vector<cudaEvent_t> prof_events;
@@ -522,6 +524,48 @@ bool use_small(const gs_system_t* sys, int64_t n) {
     return n <= kSmallMax && sys->path != GS_PATH_CELL;
 }
 
+SmallItem small_item(const SysConst& sc, const gs_match_config_t* cfg) {
+    SmallItem it{};
+    it.sc = sc;
+    it.t_final = cfg->t_final; it.steps = cfg->steps;
+    it.h = cfg->h; it.epsilon = cfg->epsilon;
+    it.max_iter = cfg->max_iter; it.stop_rule = cfg->stop_rule; it.norm = cfg->norm;
+    return it;
+}
+
+// shooting.py:66-100 / integrator.py:35-43 validation of one (system, match config) item
+int check_match(const gs_system_t* sys, const gs_match_config_t* cfg) {
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (!cfg) return fail(GS_ERR_INVALID, "match config is NULL");
+    if (!(cfg->h > 0.0) || !std::isfinite(cfg->h)) return fail(GS_ERR_INVALID, "h must be positive");
+    if (!(cfg->epsilon > 0.0) || !std::isfinite(cfg->epsilon)) return fail(GS_ERR_INVALID, "epsilon must be positive");
+    if (cfg->max_iter < 1) return fail(GS_ERR_INVALID, "max_iter must be >= 1");
+    if (cfg->steps < 1 || !(cfg->t_final > 0.0) || !std::isfinite(cfg->t_final))
+        return fail(GS_ERR_INVALID, "bad evolve config");
+    if (cfg->stop_rule != GS_STOP_TARGET_RESIDUAL && cfg->stop_rule != GS_STOP_MOMENTUM_DELTA)
+        return fail(GS_ERR_INVALID, "unknown stop rule");
+    if (cfg->norm != GS_NORM_MAX && cfg->norm != GS_NORM_L2) return fail(GS_ERR_INVALID, "unknown norm");
+    if (sys->sigma2 > 0.0 && cfg->stop_rule != GS_STOP_MOMENTUM_DELTA)
+        return fail(GS_ERR_INVALID, "inexact matching (sigma2 > 0) cannot stop on the endpoint residual; "
+                                    "use stop_rule = MomentumDelta");
+    return GS_OK;
+}
+
+void small_to_result(const SmallResult& r, int64_t n, gs_match_result_t* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->status.i = out->status.j = -1;
+    out->outcome = r.outcome;
+    out->iterations = r.iterations;
+    out->hamiltonian = r.hamiltonian;
+    out->final_residual = r.final_residual;
+    if (r.outcome == GS_MATCH_EVOLVE_FAILED) {
+        DevStatus d{r.fail_event, r.pair_key};
+        decode_status(d, n, &out->status);
+        out->status.iteration = r.fail_iter;
+    }
+}
+
 }  // namespace
 
 // ======================================================================================
@@ -576,7 +620,7 @@ int gs_destroy(gs_context* ctx) {
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
-    ctx->c_acc.release(); ctx->gram_bad.release();
+    ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release();
     delete ctx;
     return GS_OK;
 }
@@ -687,16 +731,16 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
     ctx->n = n;
     if (use_small(sys, n)) {
         SmallArgs a{};
-        a.n = n; a.split = small_split(n); a.mode = 0; a.t_final = t_final; a.steps = steps;
+        a.n = n; a.batch = 1; a.split = small_split(n); a.mode = 0;
+        a.item.sc = sc; a.item.t_final = t_final; a.item.steps = steps;
         a.capture_every = capture_every; a.q_in = q; a.p_in = p; a.q_out = q; a.p_out = p; a.frames = frames;
         a.st = ctx->st.ptr;
         ctx->host_pairs += 4LL * steps * n * n;
         if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
-        launch_small(sc, a, ctx->tbl.ptr, s);
+        GS_CUDA((cudaError_t)launch_small(sc.fam, a, ctx->tbl.ptr, s));
         if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
         ctx->launches++;
         ctx->pair_launches++;
-        GS_CUDA(cudaGetLastError());
     } else {
         if ((rc = ensure_session(ctx, n, n))) return rc;
         ctx->row0 = 0; ctx->row1 = n;
@@ -724,17 +768,10 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
              gs_match_result_t* result, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !cfg || !result || !history_out) return fail(GS_ERR_INVALID, "NULL argument");
-    int rc = check_system(sys);
+    int rc = check_match(sys, cfg);
     if (rc) return rc;
     if (n < 1 || !q0 || !target || !p0_out || !endpoint_out)
         return fail(GS_ERR_INVALID, "templates must have shape (N, 2), N >= 1");
-    if (!(cfg->h > 0.0) || !std::isfinite(cfg->h)) return fail(GS_ERR_INVALID, "h must be positive");
-    if (!(cfg->epsilon > 0.0) || !std::isfinite(cfg->epsilon)) return fail(GS_ERR_INVALID, "epsilon must be positive");
-    if (cfg->max_iter < 1) return fail(GS_ERR_INVALID, "max_iter must be >= 1");
-    if (cfg->steps < 1 || !(cfg->t_final > 0.0)) return fail(GS_ERR_INVALID, "bad evolve config");
-    if (sys->sigma2 > 0.0 && cfg->stop_rule != GS_STOP_MOMENTUM_DELTA)
-        return fail(GS_ERR_INVALID, "inexact matching (sigma2 > 0) cannot stop on the endpoint residual; "
-                                    "use stop_rule = MomentumDelta");
     GS_CUDA(cudaSetDevice(ctx->device));
     const SysConst sc = make_const(sys);
     std::memset(result, 0, sizeof(*result));
@@ -748,16 +785,15 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
     if (use_small(sys, n)) {
         GS_CUDA(ctx->hist.ensure(cfg->max_iter));
         SmallArgs a{};
-        a.n = n; a.split = small_split(n); a.mode = 1; a.t_final = cfg->t_final; a.steps = cfg->steps;
+        a.n = n; a.batch = 1; a.split = small_split(n); a.mode = 1;
+        a.item = small_item(sc, cfg);
         a.q_in = q0; a.target = target; a.q_out = endpoint_out; a.p_out = p0_out;
-        a.h = cfg->h; a.epsilon = cfg->epsilon; a.max_iter = cfg->max_iter; a.stop_rule = cfg->stop_rule;
-        a.norm = cfg->norm; a.history = ctx->hist.ptr; a.result = ctx->small_res.ptr; a.st = ctx->st.ptr;
+        a.history = ctx->hist.ptr; a.result = ctx->small_res.ptr; a.st = ctx->st.ptr;
         if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
-        launch_small(sc, a, ctx->tbl.ptr, s);
+        GS_CUDA((cudaError_t)launch_small(sc.fam, a, ctx->tbl.ptr, s));
         if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
         ctx->launches++;
         ctx->pair_launches++;
-        GS_CUDA(cudaGetLastError());
         GS_CUDA(cudaEventRecord(e1, s));
         SmallResult r;
         GS_CUDA(cudaMemcpyAsync(&r, ctx->small_res.ptr, sizeof(r), cudaMemcpyDeviceToHost, s));
@@ -766,15 +802,7 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
             GS_CUDA(cudaMemcpy(history_out, ctx->hist.ptr, r.iterations * sizeof(double), cudaMemcpyDeviceToHost));
         ctx->host_pairs += (long long)(r.iterations + (r.outcome == GS_MATCH_EVOLVE_FAILED)) * 4LL * cfg->steps * n * n +
                            n * n;
-        result->outcome = r.outcome;
-        result->iterations = r.iterations;
-        result->hamiltonian = r.hamiltonian;
-        result->final_residual = r.final_residual;
-        if (r.outcome == GS_MATCH_EVOLVE_FAILED) {
-            DevStatus d{r.fail_event, r.pair_key};
-            decode_status(d, n, &result->status);
-            result->status.iteration = r.fail_iter;
-        }
+        small_to_result(r, n, result);
     } else {
         // host-driven loop, all state on the device, two scalars read back per iteration
         if ((rc = ensure_session(ctx, n, n))) return rc;
@@ -846,6 +874,148 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
     result->seconds_device = ms * 1e-3;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    return GS_OK;
+}
+
+// ---- batched trajectories --------------------------------------------
+// One CTA per item of a persistent small-N launch: convergence-sweep cells, cluster-test
+// pairs, exact-vs-inexact rows (gs_match_batch) and Newton Jacobian columns (gs_evolve_batch)
+// run side by side instead of one after another.  Above kSmallMax (or on the cell path) the
+// items run one after another through the general path.
+namespace {
+
+constexpr size_t kSmemBudget = 220 * 1024;  // dynamic shared memory one CTA may claim
+
+int upload_items(gs_context* ctx, const std::vector<SmallItem>& items, cudaStream_t s) {
+    GS_CUDA(ctx->b_items.ensure(items.size()));
+    GS_CUDA(cudaMemcpyAsync(ctx->b_items.ptr, items.data(), items.size() * sizeof(SmallItem), cudaMemcpyHostToDevice,
+                            s));
+    return GS_OK;
+}
+
+}  // namespace
+
+int gs_match_batch(gs_context* ctx, const gs_batch_item_t* items, int64_t batch, int64_t n, const double* q0,
+                   int64_t q0_stride, const double* target, int64_t target_stride, const double* gram_factor,
+                   int64_t factor_stride, double* p0_out, double* endpoint_out, double* history_out,
+                   int64_t history_stride, gs_match_result_t* results, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !items || !results || !history_out) return fail(GS_ERR_INVALID, "NULL argument");
+    if (batch < 1) return fail(GS_ERR_INVALID, "batch must be >= 1");
+    if (n < 1 || !q0 || !target || !p0_out || !endpoint_out)
+        return fail(GS_ERR_INVALID, "templates must have shape (N, 2), N >= 1");
+    if (q0_stride < 0 || target_stride < 0 || factor_stride < 0)
+        return fail(GS_ERR_INVALID, "strides must be >= 0");
+    bool small = n <= kSmallMax;
+    std::vector<SmallItem> host_items((size_t)batch);
+    for (int64_t b = 0; b < batch; ++b) {
+        int rc = check_match(&items[b].system, &items[b].config);
+        if (rc) return fail(rc, "item " + std::to_string(b) + ": " + g_last_error);
+        if (items[b].system.family != items[0].system.family)
+            return fail(GS_ERR_INVALID, "all items of a batch must use the same kernel family");
+        if (history_stride < items[b].config.max_iter)
+            return fail(GS_ERR_INVALID, "history_stride must be >= every item's max_iter");
+        small = small && use_small(&items[b].system, n);
+        host_items[b] = small_item(make_const(&items[b].system), &items[b].config);
+    }
+    GS_CUDA(cudaSetDevice(ctx->device));
+    cudaEvent_t e0, e1;
+    GS_CUDA(cudaEventCreate(&e0));
+    GS_CUDA(cudaEventCreate(&e1));
+    GS_CUDA(cudaEventRecord(e0, s));
+    if (small) {
+        int rc = upload_items(ctx, host_items, s);
+        if (rc) return rc;
+        GS_CUDA(ctx->small_res.ensure(batch));
+        SmallArgs a{};
+        a.n = n; a.batch = batch; a.split = small_split(n); a.mode = 1;
+        a.item = host_items[0]; a.items = ctx->b_items.ptr;
+        a.q_in = q0; a.q_stride = q0_stride; a.target = target; a.t_stride = target_stride;
+        a.q_out = endpoint_out; a.p_out = p0_out;
+        a.history = history_out; a.hist_stride = history_stride; a.result = ctx->small_res.ptr;
+        a.L = gram_factor; a.L_stride = factor_stride;
+        if (gram_factor) {
+            a.L_smem = 1;
+            if (small_smem_bytes(a) > kSmemBudget) a.L_smem = 0;
+        }
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        GS_CUDA((cudaError_t)launch_small(items[0].system.family, a, ctx->tbl.ptr, s));
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        ctx->launches++;
+        ctx->pair_launches++;
+        GS_CUDA(cudaEventRecord(e1, s));
+        std::vector<SmallResult> r((size_t)batch);
+        GS_CUDA(cudaMemcpyAsync(r.data(), ctx->small_res.ptr, batch * sizeof(SmallResult), cudaMemcpyDeviceToHost, s));
+        GS_CUDA(cudaStreamSynchronize(s));
+        for (int64_t b = 0; b < batch; ++b) {
+            small_to_result(r[b], n, &results[b]);
+            ctx->host_pairs += (long long)(r[b].iterations + (r[b].outcome == GS_MATCH_EVOLVE_FAILED)) * 4LL *
+                                   items[b].config.steps * n * n + n * n;
+        }
+    } else {
+        if (gram_factor)
+            return fail(GS_ERR_UNSUPPORTED, "velocity-space batches need N <= 512 on the dense path");
+        std::vector<double> hist((size_t)history_stride);
+        for (int64_t b = 0; b < batch; ++b) {
+            int rc = gs_match(ctx, &items[b].system, &items[b].config, n, q0 + b * q0_stride,
+                              target + b * target_stride, p0_out + b * 2 * n, endpoint_out + b * 2 * n, hist.data(),
+                              &results[b], stream);
+            if (rc) return fail(rc, "item " + std::to_string(b) + ": " + g_last_error);
+            if (results[b].iterations > 0)
+                GS_CUDA(cudaMemcpyAsync(history_out + b * history_stride, hist.data(),
+                                        results[b].iterations * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        GS_CUDA(cudaEventRecord(e1, s));
+    }
+    GS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    for (int64_t b = 0; b < batch; ++b) results[b].seconds_device = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return GS_OK;
+}
+
+int gs_evolve_batch(gs_context* ctx, const gs_system_t* sys, int64_t batch, int64_t n, double t_final, int32_t steps,
+                    const double* q_in, int64_t q_stride, double* q_out, double* p_io, gs_status_t* status,
+                    void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !status) return fail(GS_ERR_INVALID, "NULL argument");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (batch < 1) return fail(GS_ERR_INVALID, "batch must be >= 1");
+    if (n < 1 || !q_in || !q_out || !p_io) return fail(GS_ERR_INVALID, "q and p must have shape (N, 2), N >= 1");
+    if (q_stride < 0) return fail(GS_ERR_INVALID, "q_stride must be >= 0");
+    if (!(t_final > 0.0) || !std::isfinite(t_final)) return fail(GS_ERR_INVALID, "t_final must be positive");
+    if (steps < 1) return fail(GS_ERR_INVALID, "steps must be >= 1");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const SysConst sc = make_const(sys);
+    if (use_small(sys, n)) {
+        GS_CUDA(ctx->b_st.ensure(batch));
+        SmallArgs a{};
+        a.n = n; a.batch = batch; a.split = small_split(n); a.mode = 0;
+        a.item.sc = sc; a.item.t_final = t_final; a.item.steps = steps;
+        a.q_in = q_in; a.q_stride = q_stride; a.p_in = p_io; a.q_out = q_out; a.p_out = p_io;
+        a.st = ctx->b_st.ptr;
+        ctx->host_pairs += 4LL * steps * n * n * batch;
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        GS_CUDA((cudaError_t)launch_small(sc.fam, a, ctx->tbl.ptr, s));
+        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
+        ctx->launches++;
+        ctx->pair_launches++;
+        std::vector<DevStatus> d((size_t)batch);
+        GS_CUDA(cudaMemcpyAsync(d.data(), ctx->b_st.ptr, batch * sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+        GS_CUDA(cudaStreamSynchronize(s));
+        for (int64_t b = 0; b < batch; ++b) decode_status(d[b], n, &status[b]);
+        return GS_OK;
+    }
+    for (int64_t b = 0; b < batch; ++b) {
+        GS_CUDA(cudaMemcpyAsync(q_out + b * 2 * n, q_in + b * q_stride, 2 * n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+        rc = gs_evolve(ctx, sys, n, t_final, steps, 0, q_out + b * 2 * n, p_io + b * 2 * n, nullptr, &status[b],
+                       stream);
+        if (rc == GS_ERR_CUDA || rc == GS_ERR_INVALID || rc == GS_ERR_UNSUPPORTED) return rc;
+    }
     return GS_OK;
 }
 

@@ -95,27 +95,46 @@ struct SmallResult {
     int pad;
 };
 
+// Per-trajectory constants.  A batched launch runs one CTA per item (SURVEY.md §8(f2):
+// convergence-sweep cells, cluster-test pairs, Newton Jacobian columns); the family must be
+// uniform across a launch (it selects the template instance).
+struct SmallItem {
+    SysConst sc;
+    double t_final;
+    double h, epsilon;
+    int steps;
+    int max_iter, stop_rule, norm;
+};
+
 struct SmallArgs {
     int64_t n;
+    int64_t batch;         // CTAs = items
     int split;             // lanes per target (power of two <= 32)
     int mode;              // 0 evolve, 1 match
-    double t_final;
-    int steps;
-    int capture_every;
-    // evolve: q_in/p_in (n,2) in, q_out/p_out (n,2) out, frames (n x 4 per frame) or null
+    int capture_every;     // evolve, batch == 1 only
+    SmallItem item;        // used when items == null
+    const SmallItem* items;  // device, batch entries (or null)
+    // evolve: q_in (+ b*q_stride), p_in (+ b*2n) in; q_out/p_out (+ b*2n) out; frames or null
     const double* q_in;
+    int64_t q_stride;      // doubles between items' q0 / q_in (0: shared)
     const double* p_in;
     double* q_out;
     double* p_out;
     double* frames;
     // match
     const double* target;
-    double h, epsilon;
-    int max_iter, stop_rule, norm;
-    double* history;       // device, max_iter
-    SmallResult* result;   // device
-    DevStatus* st;         // evolve: failure record
+    int64_t t_stride;      // doubles between items' targets (0: shared)
+    double* history;       // device, + b*hist_stride
+    int64_t hist_stride;
+    SmallResult* result;   // device, + b
+    DevStatus* st;         // evolve: failure record, + b
+    // velocity update space (shooting.py:263-265): lower Cholesky factor of the Gram matrix
+    // over q0, row-major n x n (+ b*L_stride; 0: shared), or null for the momentum update
+    const double* L;
+    int64_t L_stride;
+    int L_smem;            // stage L in shared memory (row stride n + 1)
 };
-void launch_small(const SysConst& sc, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream);
+size_t small_smem_bytes(const SmallArgs& a);
+int launch_small(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream);
 
 }  // namespace gsb

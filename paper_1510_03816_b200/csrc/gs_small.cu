@@ -154,93 +154,178 @@ __device__ double small_hamiltonian(const SmallCtx& c, const SysConst& sc, doubl
     return block_reduce(c, (c.act && c.sub == 0) ? v : 0.0, false);
 }
 
+// p = K^-1 u with K = L L^T (shooting.py:157-159, cho_solve): forward substitution L y = u
+// (column-oriented: y_j = v_j / L_jj, then v_i -= L_ij y_j for i > j) into w, backward
+// L^T x = y into w.  One barrier per column; every thread updates rows of the column.
+__device__ void small_chol_solve(const SmallCtx& c, const double* L, int ld, double2* v, double2* w) {
+    const int n = c.n;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) w[t] = v[t];
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        const double2 bj = w[j];
+        const double d = L[(int64_t)j * ld + j];
+        const double yx = __ddiv_rn(bj.x, d), yy = __ddiv_rn(bj.y, d);
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+            const double l = L[(int64_t)i * ld + j];
+            double2 r = w[i];
+            r.x = __dsub_rn(r.x, __dmul_rn(l, yx));
+            r.y = __dsub_rn(r.y, __dmul_rn(l, yy));
+            w[i] = r;
+        }
+        if (threadIdx.x == 0) v[j] = make_double2(yx, yy);
+        __syncthreads();
+    }
+    // v = y; backward: x_j = v_j / L_jj, v_i -= L_ji x_j for i < j
+    for (int j = n - 1; j >= 0; --j) {
+        const double2 bj = v[j];
+        const double d = L[(int64_t)j * ld + j];
+        const double xx = __ddiv_rn(bj.x, d), xy = __ddiv_rn(bj.y, d);
+        for (int i = threadIdx.x; i < j; i += blockDim.x) {
+            const double l = L[(int64_t)j * ld + i];
+            double2 r = v[i];
+            r.x = __dsub_rn(r.x, __dmul_rn(l, xx));
+            r.y = __dsub_rn(r.y, __dmul_rn(l, xy));
+            v[i] = r;
+        }
+        if (threadIdx.x == 0) w[j] = make_double2(xx, xy);
+        __syncthreads();
+    }
+}
+
 template <int FAM>
-__global__ void __launch_bounds__(kSmallThreads) k_small(SysConst sc, SmallArgs a, const double* __restrict__ tbl_g) {
+__global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const double* __restrict__ tbl_g) {
     extern __shared__ double4 s_state[];
     __shared__ double s_tbl[kTblWords];
     __shared__ double s_red[kWarps + 1];
     __shared__ unsigned long long s_key;
     for (int t = threadIdx.x; t < kTblWords; t += blockDim.x) s_tbl[t] = tbl_g[t];
 
+    const int64_t b = blockIdx.x;
+    const SmallItem item = a.items ? a.items[b] : a.item;
+    const SysConst& sc = item.sc;
     SmallCtx c;
     c.S = s_state; c.tbl = lane_table(s_tbl); c.red = s_red; c.key = &s_key;
     c.n = (int)a.n; c.split = a.split;
     c.tgt = threadIdx.x / a.split; c.sub = threadIdx.x % a.split;
     c.act = c.tgt < c.n;
     const int t = c.act ? c.tgt : 0;
-    const double dt = a.t_final / a.steps;
+    const double dt = item.t_final / item.steps;
+    const int64_t own = b * 2 * a.n;  // this item's (n, 2) slice of the per-item outputs
+    const double* q_in = a.q_in + b * a.q_stride;
     __syncthreads();
 
     if (a.mode == 0) {  // ------------------------------------------------ evolve
-        double4 b = make_double4(a.q_in[2 * t], a.q_in[2 * t + 1], a.p_in[2 * t], a.p_in[2 * t + 1]);
-        const unsigned long long ev = small_evolve<FAM>(c, sc, b, a.steps, dt, a.capture_every, a.frames);
+        const double* p_in = a.p_in + own;
+        double4 bs = make_double4(q_in[2 * t], q_in[2 * t + 1], p_in[2 * t], p_in[2 * t + 1]);
+        const unsigned long long ev = small_evolve<FAM>(c, sc, bs, item.steps, dt, a.capture_every, a.frames);
         if (c.act && c.sub == 0) {
-            a.q_out[2 * t] = b.x; a.q_out[2 * t + 1] = b.y;
-            a.p_out[2 * t] = b.z; a.p_out[2 * t + 1] = b.w;
+            a.q_out[own + 2 * t] = bs.x; a.q_out[own + 2 * t + 1] = bs.y;
+            a.p_out[own + 2 * t] = bs.z; a.p_out[own + 2 * t + 1] = bs.w;
         }
         if (threadIdx.x == 0) {
-            a.st->first_event = ev;
-            a.st->pair_key = (ev != kNoEvent && (ev & 1ull) == 0) ? s_key : kNoEvent;
+            a.st[b].first_event = ev;
+            a.st[b].pair_key = (ev != kNoEvent && (ev & 1ull) == 0) ? s_key : kNoEvent;
         }
         return;
     }
 
     // ------------------------------------------------------------------ match
-    const double qx0 = a.q_in[2 * t], qy0 = a.q_in[2 * t + 1];
-    const double yx = a.target[2 * t], yy = a.target[2 * t + 1];
-    double px = 0.0, py = 0.0;
+    // velocity workspace after the state records: v, w (n double2 each), then L (smem copy)
+    double2* v = reinterpret_cast<double2*>(s_state + a.n);
+    double2* w = v + a.n;
+    const double* L = nullptr;
+    int ld = (int)a.n;
+    if (a.L) {
+        L = a.L + b * a.L_stride;
+        if (a.L_smem) {
+            double* Ls = reinterpret_cast<double*>(w + a.n);
+            for (int64_t k = threadIdx.x; k < a.n * a.n; k += blockDim.x)
+                Ls[(k / a.n) * (a.n + 1) + k % a.n] = L[k];
+            L = Ls;
+            ld = (int)a.n + 1;
+        }
+    }
+    const double* target = a.target + b * a.t_stride;
+    double* history = a.history + b * a.hist_stride;
+    const double qx0 = q_in[2 * t], qy0 = q_in[2 * t + 1];
+    const double yx = target[2 * t], yy = target[2 * t + 1];
+    double px = 0.0, py = 0.0, ux = 0.0, uy = 0.0;
     double ex = qx0, ey = qy0;  // evolve(q0, 0) is exactly q0 (zero momenta: dq = dp = 0)
     double rx = __dsub_rn(yx, ex), ry = __dsub_rn(yy, ey);
-    double nrm = block_norm(c, rx, ry, a.norm);
+    double nrm = block_norm(c, rx, ry, item.norm);
     double initial = nrm;
-    bool have_initial = (a.stop_rule == 0);
+    bool have_initial = (item.stop_rule == 0);
     int outcome = 1, iters = 0, fail_iter = -1;
     unsigned long long fail_event = kNoEvent, fail_key = kNoEvent;
-    if (a.stop_rule == 0 && nrm < a.epsilon) {
+    if (item.stop_rule == 0 && nrm < item.epsilon) {
         outcome = 0;
     } else {
-        for (int it = 0; it < a.max_iter; ++it) {
-            const double delta = a.h * nrm;
-            px = __dadd_rn(px, __dmul_rn(a.h, rx));
-            py = __dadd_rn(py, __dmul_rn(a.h, ry));
-            double4 b = make_double4(qx0, qy0, px, py);
-            const unsigned long long ev = small_evolve<FAM>(c, sc, b, a.steps, dt, 0, nullptr);
+        for (int it = 0; it < item.max_iter; ++it) {
+            const double delta = item.h * nrm;
+            if (L) {  // u <- u + h r; p = K^-1 u (shooting.py:263-265)
+                ux = __dadd_rn(ux, __dmul_rn(item.h, rx));
+                uy = __dadd_rn(uy, __dmul_rn(item.h, ry));
+                if (c.act && c.sub == 0) v[c.tgt] = make_double2(ux, uy);
+                small_chol_solve(c, L, ld, v, w);
+                const double2 pv = w[t];
+                px = pv.x; py = pv.y;
+            } else {  // p <- p + h r (shooting.py:266-267)
+                px = __dadd_rn(px, __dmul_rn(item.h, rx));
+                py = __dadd_rn(py, __dmul_rn(item.h, ry));
+            }
+            double4 bs = make_double4(qx0, qy0, px, py);
+            const unsigned long long ev = small_evolve<FAM>(c, sc, bs, item.steps, dt, 0, nullptr);
             if (ev != kNoEvent) {
                 outcome = 3; fail_event = ev; fail_iter = it + 1;
                 fail_key = ((ev & 1ull) == 0) ? s_key : kNoEvent;
                 break;
             }
-            ex = b.x; ey = b.y;
+            ex = bs.x; ey = bs.y;
             rx = __dsub_rn(yx, ex); ry = __dsub_rn(yy, ey);
-            nrm = block_norm(c, rx, ry, a.norm);
-            double value = (a.stop_rule == 0) ? nrm : delta;
+            nrm = block_norm(c, rx, ry, item.norm);
+            double value = (item.stop_rule == 0) ? nrm : delta;
             if (!have_initial) { initial = value; have_initial = true; }
-            if (threadIdx.x == 0) a.history[it] = value;
+            if (threadIdx.x == 0) history[it] = value;
             iters = it + 1;
             if (!isfinite(value) || (initial > 0.0 && value > 1e6 * initial)) { outcome = 2; break; }
-            if (value < a.epsilon) { outcome = 0; break; }
+            if (value < item.epsilon) { outcome = 0; break; }
         }
     }
     const double H = small_hamiltonian<FAM>(c, sc, make_double4(qx0, qy0, px, py));
     if (c.act && c.sub == 0) {
-        a.p_out[2 * t] = px; a.p_out[2 * t + 1] = py;
-        a.q_out[2 * t] = ex; a.q_out[2 * t + 1] = ey;
+        a.p_out[own + 2 * t] = px; a.p_out[own + 2 * t + 1] = py;
+        a.q_out[own + 2 * t] = ex; a.q_out[own + 2 * t + 1] = ey;
     }
     if (threadIdx.x == 0) {
         SmallResult r;
         r.hamiltonian = H; r.final_residual = nrm; r.fail_event = fail_event; r.pair_key = fail_key;
         r.outcome = outcome; r.iterations = iters; r.fail_iter = fail_iter; r.pad = 0;
-        *a.result = r;
+        a.result[b] = r;
     }
 }
 
 }  // namespace
 
-void launch_small(const SysConst& sc, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream) {
+size_t small_smem_bytes(const SmallArgs& a) {
+    size_t bytes = (size_t)a.n * sizeof(double4);
+    if (a.mode == 1 && a.L) {
+        bytes += 2 * (size_t)a.n * sizeof(double2);
+        if (a.L_smem) bytes += (size_t)a.n * (a.n + 1) * sizeof(double);
+    }
+    return bytes;
+}
+
+int launch_small(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream) {
     const int threads = (int)(((a.n * a.split) + 31) / 32 * 32);
-    const size_t smem = (size_t)a.n * sizeof(double4);
-    if (sc.fam == kFamConical) k_small<kFamConical><<<1, threads, smem, stream>>>(sc, a, tbl_dev);
-    else k_small<kFamGaussian><<<1, threads, smem, stream>>>(sc, a, tbl_dev);
+    const size_t smem = small_smem_bytes(a);
+    auto kern = fam == kFamConical ? k_small<kFamConical> : k_small<kFamGaussian>;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+    }
+    kern<<<(unsigned)a.batch, threads, smem, stream>>>(a, tbl_dev);
+    return (int)cudaGetLastError();
 }
 
 }  // namespace gsb

@@ -222,16 +222,93 @@ def match(spec, q0, target, h: float, epsilon: float, max_iter: int, stop_rule: 
     sysc = system_struct(spec)
     N.check(ctx.lib.gs_match(ctx.handle, ctypes.byref(sysc), ctypes.byref(cfg), n, _ptr(q0), _ptr(target), _ptr(p0),
                              _ptr(endpoint), hist, ctypes.byref(res), _stream_ptr(torch)), "gs_match")
-    diagnosis = None
-    if res.outcome == N.GS_MATCH_CAP:
-        diagnosis = "iteration cap reached before the stopping rule"
-    elif res.outcome == N.GS_MATCH_BLOWUP:
-        diagnosis = "step too large"
-    elif res.outcome == N.GS_MATCH_EVOLVE_FAILED:
-        exc = status_exception(res.status, float(t_final), int(steps))
-        diagnosis = f"step too large ({exc})"
+    diagnosis = _diagnosis(res, t_final, steps)
     return dict(p0=p0, endpoint=endpoint, iterations=int(res.iterations),
                 converged=res.outcome == N.GS_MATCH_CONVERGED,
                 residual_history=tuple(float(hist[i]) for i in range(res.iterations)),
                 hamiltonian=float(res.hamiltonian), final_residual=float(res.final_residual), diagnosis=diagnosis,
                 seconds_device=float(res.seconds_device))
+
+
+def _diagnosis(res: N.MatchResultC, t_final: float, steps: int):
+    if res.outcome == N.GS_MATCH_CAP:
+        return "iteration cap reached before the stopping rule"
+    if res.outcome == N.GS_MATCH_BLOWUP:
+        return "step too large"
+    if res.outcome == N.GS_MATCH_EVOLVE_FAILED:
+        return f"step too large ({status_exception(res.status, float(t_final), int(steps))})"
+    return None
+
+
+def _stack(a, torch, n: int | None = None):
+    """(n, 2) -> shared (stride 0), (B, n, 2) -> per item; returns (tensor, stride in doubles)."""
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(a, np.float64)))
+    t = t.to(device="cuda", dtype=torch.float64).contiguous()
+    if t.dim() == 2:
+        return t, 0
+    return t, int(t[0].numel())
+
+
+def match_batch(specs, cfgs, q0, target, factor=None) -> list:
+    """Independent matches side by side (gs_match_batch).
+
+    specs[b] / cfgs[b]: SystemSpec and a dict (h, epsilon, max_iter, stop_rule, norm, t_final,
+    steps) per item; q0 / target: (n, 2) shared or (B, n, 2); factor: None (momentum update)
+    or the lower Cholesky factor(s) of the Gram matrix, (n, n) shared or (B, n, n) (velocity
+    update).  Returns one dict per item in device.match's format.
+    """
+    torch = _torch()
+    ctx = N.Context.get()
+    B = len(specs)
+    if B != len(cfgs) or B < 1:
+        raise ValueError("specs and cfgs must be non-empty and of equal length")
+    q0, qs = _stack(q0, torch)
+    target, ts = _stack(target, torch)
+    n = q0.shape[-2]
+    fac, fs = (None, 0)
+    if factor is not None:
+        fac = factor.to(device="cuda", dtype=torch.float64).contiguous()
+        fs = 0 if fac.dim() == 2 else n * n
+    items = (N.BatchItem * B)()
+    hmax = 1
+    for b, (spec, c) in enumerate(zip(specs, cfgs)):
+        items[b].system = system_struct(spec)
+        items[b].config = N.MatchConfig(float(c["h"]), float(c["epsilon"]), int(c["max_iter"]),
+                                        _STOP[c["stop_rule"]], _NORM[c["norm"]], int(c["steps"]),
+                                        float(c["t_final"]))
+        hmax = max(hmax, int(c["max_iter"]))
+    p0 = torch.empty((B, n, 2), dtype=torch.float64, device=q0.device)
+    endpoint = torch.empty_like(p0)
+    hist = torch.empty((B, hmax), dtype=torch.float64, device=q0.device)
+    res = (N.MatchResultC * B)()
+    N.check(ctx.lib.gs_match_batch(ctx.handle, items, B, n, _ptr(q0), qs, _ptr(target), ts,
+                                   _ptr(fac) if fac is not None else None, fs, _ptr(p0), _ptr(endpoint), _ptr(hist),
+                                   hmax, res, _stream_ptr(torch)), "gs_match_batch")
+    hist_h = hist.cpu().numpy()
+    out = []
+    for b in range(B):
+        r = res[b]
+        c = cfgs[b]
+        out.append(dict(p0=p0[b], endpoint=endpoint[b], iterations=int(r.iterations),
+                        converged=r.outcome == N.GS_MATCH_CONVERGED,
+                        residual_history=tuple(float(v) for v in hist_h[b, :r.iterations]),
+                        hamiltonian=float(r.hamiltonian), final_residual=float(r.final_residual),
+                        diagnosis=_diagnosis(r, c["t_final"], c["steps"]), seconds_device=float(r.seconds_device)))
+    return out
+
+
+def evolve_batch(spec, q0, p, t_final: float, steps: int):
+    """B independent evolves of one system (gs_evolve_batch): q0 (n, 2) shared or (B, n, 2),
+    p (B, n, 2).  Returns (q (B, n, 2), p (B, n, 2), [exception or None] * B)."""
+    torch = _torch()
+    ctx = N.Context.get()
+    q0, qs = _stack(q0, torch)
+    p = p.to(device="cuda", dtype=torch.float64).clone().contiguous() if isinstance(p, torch.Tensor) else \
+        torch.from_numpy(np.ascontiguousarray(np.asarray(p, np.float64))).cuda()
+    B, n = p.shape[0], p.shape[1]
+    q = torch.empty_like(p)
+    st = (N.Status * B)()
+    sysc = system_struct(spec)
+    N.check(ctx.lib.gs_evolve_batch(ctx.handle, ctypes.byref(sysc), B, n, float(t_final), int(steps), _ptr(q0), qs,
+                                    _ptr(q), _ptr(p), st, _stream_ptr(torch)), "gs_evolve_batch")
+    return q, p, [status_exception(st[b], float(t_final), int(steps)) for b in range(B)]

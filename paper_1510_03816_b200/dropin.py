@@ -9,6 +9,10 @@ callees by name, so every alias must be rebound (SURVEY.md §8(b) "Rebinding poi
     match        geoshoot.shooting.match, geoshoot.analysis.match (analysis.py:23), geoshoot.cli.match
                  (cli.py:58), geoshoot.match
     hamiltonian  geoshoot.particles.hamiltonian, geoshoot.shooting.hamiltonian (shooting.py:30), geoshoot.hamiltonian
+    newton_match geoshoot.shooting.newton_match, geoshoot.newton_match  (batched Jacobian columns)
+    analysis     shape_distance, iso_invariance_check, cluster_test, convergence_sweep, predict,
+                 exact_vs_inexact in geoshoot.analysis, geoshoot.cli (cli.py:24-32), geoshoot
+                 (independent matches batched into one launch)
 
 After ``install()`` the reference's own callers (analysis, cli, newton_match) run their shoots
 on the device, with the reference's exception classes and result types.  ``match`` runs on the
@@ -23,6 +27,7 @@ from __future__ import annotations
 
 import importlib
 
+from . import analysis as _analysis
 from . import errors as _errors
 from . import integrator as _integrator
 from . import particles as _particles
@@ -36,6 +41,14 @@ _ALIASES = {
     "match": ("shooting", "analysis", "cli", ""),
     "hamiltonian": ("particles", "shooting", ""),
     "momenta_from_velocity": ("shooting", ""),
+    # batched analysis: independent matches / shoots side by side
+    "newton_match": ("shooting", ""),
+    "shape_distance": ("analysis", "cli", ""),
+    "iso_invariance_check": ("analysis", ""),
+    "cluster_test": ("analysis", "cli", ""),
+    "convergence_sweep": ("analysis", "cli", ""),
+    "predict": ("analysis", "cli", ""),
+    "exact_vs_inexact": ("analysis", "cli", ""),
 }
 
 
@@ -60,7 +73,8 @@ def install(pkg=None):
         _saved.append((_errors, name, getattr(_errors, name)))
         setattr(_errors, name, getattr(pkg, name))
     _types.use(ParticleState=pkg.ParticleState, EvolveResult=pkg.EvolveResult, EvolveConfig=pkg.EvolveConfig,
-               MatchResult=pkg.MatchResult, LandmarkTemplate=pkg.LandmarkTemplate)
+               MatchResult=pkg.MatchResult, LandmarkTemplate=pkg.LandmarkTemplate,
+               DistanceRecord=pkg.DistanceRecord, ClusterVerdict=pkg.ClusterVerdict, ExactnessRow=pkg.ExactnessRow)
 
     def match(reference, target, cfg):
         """shooting.match on the device, both update spaces (momentum: one device loop;
@@ -69,7 +83,11 @@ def install(pkg=None):
 
     match.original = original_match
     impl = {"rhs": _particles.rhs, "evolve": _integrator.evolve, "match": match,
-            "hamiltonian": _particles.hamiltonian, "momenta_from_velocity": _shooting.momenta_from_velocity}
+            "hamiltonian": _particles.hamiltonian, "momenta_from_velocity": _shooting.momenta_from_velocity,
+            "newton_match": _shooting.newton_match}
+    for fname in ("shape_distance", "iso_invariance_check", "cluster_test", "convergence_sweep", "predict",
+                  "exact_vs_inexact"):
+        impl[fname] = getattr(_analysis, fname)
     for fname, subs in _ALIASES.items():
         for sub in subs:
             mod = _module(pkg, sub)
@@ -88,7 +106,8 @@ def uninstall() -> None:
 
     _types.use(ParticleState=particles.ParticleState, EvolveResult=integrator.EvolveResult,
                EvolveConfig=integrator.EvolveConfig, MatchResult=shooting.MatchResult,
-               LandmarkTemplate=shapes.LandmarkTemplate)
+               LandmarkTemplate=shapes.LandmarkTemplate, DistanceRecord=_analysis.DistanceRecord,
+               ClusterVerdict=_analysis.ClusterVerdict, ExactnessRow=_analysis.ExactnessRow)
 
 
 def installed() -> bool:

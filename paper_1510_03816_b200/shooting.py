@@ -24,7 +24,7 @@ from .integrator import EvolveConfig
 from .particles import SystemSpec
 
 __all__ = ["UpdateSpace", "StopRule", "ResidualNorm", "ShootingConfig", "MatchResult", "match",
-           "contraction_diagnostics", "momenta_from_velocity"]
+           "contraction_diagnostics", "momenta_from_velocity", "newton_match", "gram_factor"]
 
 _BLOWUP_FACTOR = 1e6          # shooting.py:47
 _ILL_CONDITIONED = 1e12       # shooting.py:48
@@ -129,19 +129,23 @@ def match(reference, target, cfg):
 
 
 # --- velocity-space update: Gram solve on the device -----------------------
-def _match_velocity(reference, target, cfg):
-    """shooting.py:218-301 with UpdateSpace.VELOCITY: u <- u + h r, p = K^-1 u (:263-265).
+SMALL_MAX = 512  # gs_small.cu kSmallMax: one persistent CTA per match
 
-    Everything stays on the device: the Gram matrix over q0 comes from libgs_b200 (`gs_gram`,
-    kernels.py:181-197), its Cholesky factor and condition number (2-norm, = the reference's
-    np.linalg.cond for an SPD K) from cuSOLVER through torch.linalg (a library factorisation,
-    once per match), every iteration is one triangular solve pair + one device shoot; the
-    host reads the residual norm.
+
+def gram_factor(spec, q0):
+    """_GramSolver.__init__ (shooting.py:143-152) on the device.
+
+    The Gram matrix over q0 comes from libgs_b200 (`gs_gram`, kernels.py:181-197); its
+    Cholesky factor and 2-norm condition number (= np.linalg.cond for an SPD K, via the
+    eigenvalues) from cuSOLVER through torch.linalg — a library factorisation, once per match.
+    Returns (L, cond, warnings); raises DegenerateConfigurationError when K is not SPD.
     """
     torch = device._torch()
-    q0 = device.as_device(reference.points, torch)
-    tgt = device.as_device(target.points, torch)
-    K = device.gram(cfg.system, q0)
+    K = device.gram(spec, device.as_device(q0, torch))
+    return _factor_of(K, torch)
+
+
+def _factor_of(K, torch):
     evals = torch.linalg.eigvalsh(K)
     amin, amax = float(evals.abs().min()), float(evals.abs().max())
     cond = amax / amin if amin > 0 else math.inf
@@ -154,6 +158,36 @@ def _match_velocity(reference, target, cfg):
     if not (cond < _ILL_CONDITIONED):
         warnings = (f"Gram matrix condition number {cond:.3e} exceeds {_ILL_CONDITIONED:.0e}; "
                     "momenta recovery may lose accuracy",)
+    return L, cond, warnings
+
+
+def _batchable(n: int) -> bool:
+    return n <= SMALL_MAX and device.get_path() != "cell"
+
+
+def match_config_dict(cfg) -> dict:
+    """ShootingConfig -> the per-item dict of device.match_batch."""
+    return dict(h=cfg.h, epsilon=cfg.epsilon, max_iter=cfg.max_iter, stop_rule=_enum_value(cfg.stop_rule),
+                norm=_enum_value(cfg.norm), t_final=cfg.evolve.t_final, steps=cfg.evolve.steps)
+
+
+def _match_velocity(reference, target, cfg):
+    """shooting.py:218-301 with UpdateSpace.VELOCITY: u <- u + h r, p = K^-1 u (:263-265).
+
+    N <= 512: the whole loop — the triangular solve pair of every iteration included — runs in
+    one persistent CTA (gs_match_batch with the Gram factor).  Above that each iteration is
+    one cuSOLVER triangular solve pair (torch.cholesky_solve) plus a device shoot, and the
+    host reads the residual norm.
+    """
+    torch = device._torch()
+    q0 = device.as_device(reference.points, torch)
+    L, _, warnings = gram_factor(cfg.system, q0)
+    if _batchable(reference.n):
+        r = device.match_batch([cfg.system], [match_config_dict(cfg)], q0, target.points, factor=L)[0]
+        return _make_result(r["p0"].cpu().numpy(), r["iterations"], r["converged"], r["residual_history"],
+                            r["hamiltonian"], r["endpoint"].cpu().numpy(), reference, target, r["final_residual"],
+                            r["diagnosis"], warnings)
+    tgt = device.as_device(target.points, torch)
     norm_kind = _enum_value(cfg.norm)
     mdelta = _enum_value(cfg.stop_rule) == "momentum-delta"
     ev = cfg.evolve
@@ -217,6 +251,87 @@ def momenta_from_velocity(kernel, q0, u0) -> np.ndarray:
     if int(info) != 0:
         raise _errors.DegenerateConfigurationError("kernel Gram matrix is not positive definite")
     return torch.cholesky_solve(device.as_device(u0, torch), L).cpu().numpy()
+
+
+def newton_match(reference, target, cfg):
+    """Finite-difference Newton baseline (shooting.py:327-411) with batched Jacobian columns.
+
+    Every iteration needs 2N + 1 shoots; the reference runs the 2N Jacobian columns one after
+    another.  Here the 2N probe momenta come from one multi-right-hand-side Cholesky solve and
+    the 2N column shoots run side by side in ONE persistent launch (gs_evolve_batch, one CTA
+    per column); the dense 2N x 2N Newton system is an LU solve on the device
+    (torch.linalg, cuSOLVER).  Same probe step, same fallback to the feedback update on a
+    singular or unevaluable Jacobian, same stop logic and diagnoses as the reference.
+    """
+    _prepare(reference, target)
+    if _enum_value(cfg.stop_rule) != "residual":
+        raise _errors.ConfigurationError("newton_match supports only the TargetResidual rule")
+    torch = device._torch()
+    n = reference.n
+    q0 = device.as_device(reference.points, torch)
+    tgt = device.as_device(target.points, torch).reshape(-1)
+    L, _, warnings = gram_factor(cfg.system, q0)
+    ev = cfg.evolve
+    norm_kind = _enum_value(cfg.norm)
+
+    def solve(u_flat):  # (..., 2n) -> p (..., n, 2)
+        return torch.cholesky_solve(u_flat.reshape(n, 2), L)
+
+    def shoot(u_flat):
+        q, _, _ = device.evolve(cfg.system, q0, solve(u_flat), ev.t_final, ev.steps, 0)
+        return q.reshape(-1)
+
+    def dnorm(r) -> float:
+        if norm_kind == "max":
+            r2 = r.reshape(-1, 2)
+            return float(torch.hypot(r2[:, 0], r2[:, 1]).max())
+        return float(torch.linalg.vector_norm(r))
+
+    def result(u, history, converged, endpoint, diagnosis):
+        p = solve(u)
+        return _make_result(p.cpu().numpy(), len(history), converged, history,
+                            device.hamiltonian(cfg.system, q0, p), endpoint.reshape(n, 2).cpu().numpy(), reference,
+                            target, dnorm(tgt - endpoint), diagnosis, warnings)
+
+    u = torch.zeros(2 * n, dtype=torch.float64, device=q0.device)
+    endpoint = shoot(u)
+    residual = tgt - endpoint
+    initial_norm = dnorm(residual)
+    history: list = []
+    if initial_norm < cfg.epsilon:
+        return result(u, history, True, endpoint, None)
+    eye = torch.eye(2 * n, dtype=torch.float64, device=q0.device)
+    for _ in range(cfg.max_iter):
+        step = 1e-5 * max(1.0, float(u.abs().max()))
+        probes = u[None, :] + step * eye                      # row j = u + step e_j
+        rhs_cols = probes.reshape(2 * n, n, 2).permute(1, 0, 2).reshape(n, 4 * n)
+        P = torch.cholesky_solve(rhs_cols, L).reshape(n, 2 * n, 2).permute(1, 0, 2).contiguous()
+        cols_q, _, errs = device.evolve_batch(cfg.system, q0, P, ev.t_final, ev.steps)
+        newton_step = None
+        if all(e is None for e in errs):
+            jac = ((cols_q.reshape(2 * n, 2 * n) - endpoint[None, :]) / step).T.contiguous()
+            sol, info = torch.linalg.solve_ex(jac, residual)
+            if int(info) == 0 and bool(torch.isfinite(sol).all()):
+                newton_step = sol
+        elif any(e is not None and not isinstance(e, (_errors.DivergenceError,
+                                                      _errors.DegenerateConfigurationError)) for e in errs):
+            raise next(e for e in errs if e is not None)
+        if newton_step is None:  # singular or unevaluable Jacobian: one feedback update
+            newton_step = residual
+        u = u + cfg.h * newton_step
+        try:
+            endpoint_new = shoot(u)
+        except (_errors.DivergenceError, _errors.DegenerateConfigurationError) as exc:
+            return result(u, history, False, endpoint, f"step too large ({exc})")
+        endpoint = endpoint_new
+        residual = tgt - endpoint
+        value = dnorm(residual)
+        history.append(value)
+        if not math.isfinite(value) or (initial_norm > 0 and value > _BLOWUP_FACTOR * initial_norm):
+            return result(u, history, False, endpoint, "step too large")
+        if value < cfg.epsilon:
+            return result(u, history, True, endpoint, None)
+    return result(u, history, False, endpoint, "iteration cap reached before the stopping rule")
 
 
 def contraction_diagnostics(result) -> list:

@@ -246,6 +246,114 @@ def gen_match(out):
         json.dump(meta, f, indent=1, sort_keys=True)
 
 
+def _cfg_meta(cfg):
+    k = cfg.system.kernel
+    return dict(family=k.family.value, alpha=k.alpha, normalized=k.normalized, sigma2=cfg.system.sigma2, h=cfg.h,
+                epsilon=cfg.epsilon, max_iter=cfg.max_iter, update_space=cfg.update_space.value,
+                stop_rule=cfg.stop_rule.value, norm=cfg.norm.value, t_final=cfg.evolve.t_final,
+                steps=cfg.evolve.steps)
+
+
+def _tpl(arrays, key, t):
+    arrays[key] = t.points
+    return dict(key=key, label=t.label)
+
+
+def gen_analysis(out):
+    """SURVEY.md §8(f2) callers: the reference's analysis.py / newton_match on the inputs of its
+    own tests (test_analysis.py:31-33, 66-77, 139-153, 160-213; test_shooting.py:87-93;
+    test_acceptance.py:196-240, 259-285, 327-340)."""
+    arrays, meta = {}, {}
+    REF = gs.circle(1.0, n=8)
+    TGT = gs.ellipse_rot_shift(1.3, 0.9, 0.0, (0.1, 0.0), n=8)
+    CFG = gs.ShootingConfig(h=0.5, epsilon=1e-6, evolve=gs.EvolveConfig(steps=60))
+    axes = (0.2, 0.4, 0.6, 0.8, 1.0)
+    sweeps = {
+        "sweep_small": (REF, TGT, gs.SweepGrid(alpha2_values=(0.5, 1.0), h_values=(0.4, 0.8, 2.5), n_landmarks=8,
+                                               tolerance=1e-3, max_iter=200)),
+        "sweep_c16": (gs.circle(2.0, n=16), gs.heart4(16), gs.SweepGrid(axes, axes, n_landmarks=16, tolerance=1e-3)),
+        "sweep_g32": (gs.circle(2.0, n=32), gs.heart4(32), gs.SweepGrid(axes, axes, n_landmarks=32,
+                                                                        kernel_family="gaussian")),
+        "sweep_c32": (gs.circle(2.0, n=32), gs.heart4(32), gs.SweepGrid(axes, axes, n_landmarks=32)),
+    }
+    for name, (a, b, grid) in sweeps.items():
+        t0 = time.time()
+        mat = gs.convergence_sweep(a, b, grid)
+        dt = time.time() - t0
+        meta[name] = dict(ref=_tpl(arrays, f"{name}__ref", a), tgt=_tpl(arrays, f"{name}__tgt", b),
+                          alpha2=list(grid.alpha2_values), h=list(grid.h_values), n_landmarks=grid.n_landmarks,
+                          family=grid.kernel_family.value, tolerance=grid.tolerance, max_iter=grid.max_iter,
+                          matrix=mat.tolist(), seconds=dt)
+        print(f"{name}: {mat.tolist()} ({dt:.1f}s)", flush=True)
+
+    clusters = {
+        "cluster_small": (REF, gs.circle(1.0, n=8, label="copy"),
+                          [gs.circle(3.0, n=8, label="big"), gs.heart4(n=8, label="h")],
+                          {"pair": 0.05, "ref_diff": 1.5}, CFG),
+        "cluster_64": (gs.ellipse_rot_shift(4.0, 1.0, 0.0, (0.0, 0.0), 64, label="A"),
+                       gs.ellipse_rot_shift(4.0, 1.05, 0.0, (0.0, 0.0), 64, label="B"),
+                       [gs.circle(2.0, n=64, label="C"), gs.circle(3.0, n=64, label="D")],
+                       {"pair": 0.05, "ref_diff": 1.0},
+                       gs.ShootingConfig(h=0.3, epsilon=1e-3, max_iter=2000)),
+    }
+    for name, (a, b, refs, thr, cfg) in clusters.items():
+        t0 = time.time()
+        v = gs.cluster_test(a, b, refs, thr, cfg)
+        dt = time.time() - t0
+        meta[name] = dict(a=_tpl(arrays, f"{name}__a", a), b=_tpl(arrays, f"{name}__b", b),
+                          refs=[_tpl(arrays, f"{name}__r{i}", r) for i, r in enumerate(refs)], thresholds=thr,
+                          cfg=_cfg_meta(cfg), same_cluster=v.same_cluster,
+                          evidence=[dict(reference_label=e.reference_label, target_label=e.target_label, H=e.H,
+                                         iterations=e.iterations, converged=e.converged) for e in v.evidence],
+                          seconds=dt)
+        print(f"{name}: {v.same_cluster} {[round(e.H, 6) for e in v.evidence]} ({dt:.1f}s)", flush=True)
+
+    newtons = {
+        "newton_small": (REF, TGT, gs.ShootingConfig(h=1.0, epsilon=1e-8, evolve=gs.EvolveConfig(steps=60))),
+        "newton_l2_30": (gs.circle(2.0, n=30), gs.standard_rotated_ellipse(4.0, 1.0, -math.pi / 4, (1.0, 0.0), 30),
+                         gs.ShootingConfig(h=1.0, epsilon=1e-3, max_iter=2000, norm=gs.ResidualNorm.L2)),
+        "newton_cap": (REF, TGT, gs.ShootingConfig(h=1.0, epsilon=1e-12, max_iter=2, evolve=gs.EvolveConfig(steps=60))),
+    }
+    for name, (a, b, cfg) in newtons.items():
+        t0 = time.time()
+        r = gs.newton_match(a, b, cfg)
+        dt = time.time() - t0
+        arrays[f"{name}__p0"] = r.p0
+        arrays[f"{name}__endpoint"] = r.final_template.points
+        arrays[f"{name}__history"] = np.array(r.residual_history, dtype=float)
+        meta[name] = dict(ref=_tpl(arrays, f"{name}__ref", a), tgt=_tpl(arrays, f"{name}__tgt", b),
+                          cfg=_cfg_meta(cfg), iterations=r.iterations, converged=r.converged,
+                          hamiltonian=r.hamiltonian, final_residual=r.final_residual, diagnosis=r.diagnosis,
+                          warnings=list(r.warnings), seconds=dt)
+        print(f"{name}: it={r.iterations} conv={r.converged} H={r.hamiltonian:.12g} ({dt:.1f}s)", flush=True)
+
+    t0 = time.time()
+    rows = gs.exact_vs_inexact(REF, TGT, [0.0, 0.3], CFG, h_by_sigma2={0.3: 0.4})
+    meta["exactness"] = dict(ref=_tpl(arrays, "exactness__ref", REF), tgt=_tpl(arrays, "exactness__tgt", TGT),
+                             cfg=_cfg_meta(CFG), sigma2_values=[0.0, 0.3], h_by_sigma2={"0.3": 0.4},
+                             rows=[dict(sigma2=r.sigma2, h=r.h, H=r.H, final_residual=r.final_residual,
+                                        iterations=r.iterations, converged=r.converged) for r in rows],
+                             seconds=time.time() - t0)
+
+    full = gs.match(REF, TGT, CFG)
+    half = gs.evolve(CFG.system, gs.ParticleState(REF.points, full.p0), gs.EvolveConfig(t_final=0.5, steps=50))
+    partial = gs.LandmarkTemplate(half.final.q, "partial")
+    pcfg = gs.ShootingConfig(h=0.5, epsilon=1e-6, evolve=gs.EvolveConfig(steps=50))
+    pred = gs.predict(REF, partial, 0.5, 1.0, pcfg)
+    arrays["predict__pred"] = pred.points
+    meta["predict"] = dict(ref=_tpl(arrays, "predict__ref", REF), partial=_tpl(arrays, "predict__partial", partial),
+                           t_match=0.5, t_predict=1.0, cfg=_cfg_meta(pcfg), label=pred.label)
+
+    g = gs.PlanarIsometry(angle=math.pi / 3, translation=(0.5, 0.5), reflect_x=True)
+    val = gs.iso_invariance_check(REF, TGT, g, CFG)
+    meta["iso"] = dict(a=_tpl(arrays, "iso__a", REF), b=_tpl(arrays, "iso__b", TGT),
+                       ga=_tpl(arrays, "iso__ga", g.apply(REF)), gb=_tpl(arrays, "iso__gb", g.apply(TGT)),
+                       cfg=_cfg_meta(CFG), value=val)
+    np.savez(os.path.join(out, "analysis_cases.npz"), **arrays)
+    with open(os.path.join(out, "analysis_cases.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+
+
 def gen_errors(out):
     msgs = {}
     q = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 1.0]])
@@ -295,7 +403,7 @@ def main():
     a = ap.parse_args()
     out = HERE
     steps = {"sympy": gen_sympy, "rhs": gen_rhs, "evolve": gen_evolve, "match": gen_match,
-             "errors": gen_errors, "c2": gen_c2}
+             "errors": gen_errors, "c2": gen_c2, "analysis": gen_analysis}
     for name, fn in steps.items():
         if a.only and name not in a.only.split(","):
             continue

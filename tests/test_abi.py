@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for sym in declared_symbols():
         assert hasattr(lib, sym), sym
     assert sorted(_native.EXPORTS) == declared_symbols()
-    assert lib.gs_abi_version() == 1
+    assert lib.gs_abi_version() == 2
     assert b"sm_100a" in lib.gs_version()
 
 
@@ -51,6 +51,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(N.Status) == 32
     assert ctypes.sizeof(N.MatchConfig) == 40
     assert ctypes.sizeof(N.MatchResultC) == 64
+    assert ctypes.sizeof(N.BatchItem) == 80
 
 
 def test_no_device_means_loud_failure():

@@ -1,6 +1,7 @@
 """Host-side logic of the drop-in (no GPU): validation, error messages, templates, configs, rebinding."""
 
 import json
+import math
 import os
 
 import numpy as np
@@ -148,7 +149,9 @@ def test_dropin_rebinds_every_alias_and_restores():
     originals = {(m, f): getattr(getattr(ref, m), f) for m, f in [
         ("particles", "rhs"), ("integrator", "rhs"), ("integrator", "evolve"), ("shooting", "evolve"),
         ("analysis", "evolve"), ("cli", "evolve"), ("shooting", "match"), ("analysis", "match"), ("cli", "match"),
-        ("particles", "hamiltonian"), ("shooting", "hamiltonian")]}
+        ("particles", "hamiltonian"), ("shooting", "hamiltonian"), ("shooting", "newton_match"),
+        ("analysis", "convergence_sweep"), ("cli", "convergence_sweep"), ("analysis", "cluster_test"),
+        ("cli", "cluster_test"), ("analysis", "exact_vs_inexact"), ("analysis", "predict")]}
     dropin.install(ref)
     try:
         assert ref.integrator.rhs is particles.rhs and ref.particles.rhs is particles.rhs and ref.rhs is particles.rhs
@@ -158,6 +161,15 @@ def test_dropin_rebinds_every_alias_and_restores():
         assert ref.shooting.hamiltonian is particles.hamiltonian
         assert gs.errors.DivergenceError is ref.DivergenceError
         assert types.get("EvolveResult") is ref.EvolveResult
+        assert types.get("DistanceRecord") is ref.DistanceRecord
+        assert ref.shooting.newton_match is gs.newton_match is ref.newton_match
+        for f in ("convergence_sweep", "cluster_test", "exact_vs_inexact", "predict", "shape_distance"):
+            assert getattr(ref.analysis, f) is getattr(ref.cli, f) is getattr(ref, f) is getattr(gs, f)
+        grid = ref.SweepGrid((0.5,), (0.4,), n_landmarks=8)
+        with pytest.raises(ref.ConfigurationError, match="thresholds"):  # reference error classes
+            ref.cluster_test(ref.circle(1.0, n=8), ref.circle(1.2, n=8), [ref.circle(2.0, n=8)] * 2,
+                             {"pair": -1, "ref_diff": 1}, ref.ShootingConfig(h=0.5))
+        assert grid.n_landmarks == 8
         if not torch.cuda.is_available():
             st = ref.ParticleState(np.zeros((3, 2)), np.zeros((3, 2)))
             with pytest.raises(N.NativeUnavailable):
@@ -170,3 +182,53 @@ def test_dropin_rebinds_every_alias_and_restores():
         assert getattr(getattr(ref, m), f) is fn
     assert gs.errors.DivergenceError is not ref.DivergenceError
     assert types.get("EvolveResult") is integrator.EvolveResult
+
+
+# --- analysis host logic; no device calls -------------------------------------
+def test_sweep_grid_validation_mirrors_reference():
+    import paper_1510_03816_b200 as gs
+
+    g = gs.SweepGrid((0.5, 1), (0.1,), n_landmarks=8, kernel_family="gaussian")
+    assert g.alpha2_values == (0.5, 1.0) and g.kernel_family is gs.KernelFamily.GAUSSIAN
+    for bad in (dict(alpha2_values=(), h_values=(0.1,)), dict(alpha2_values=(0.5, -1.0), h_values=(0.1,)),
+                dict(alpha2_values=(0.5,), h_values=(0.1,), tolerance=0.0),
+                dict(alpha2_values=(0.5,), h_values=(0.1,), n_landmarks=2),
+                dict(alpha2_values=(0.5,), h_values=(math.inf,)), dict(alpha2_values=(0.5,), h_values=(0.1,),
+                                                                         max_iter=0)):
+        with pytest.raises(gs.ConfigurationError):
+            gs.SweepGrid(**bad)
+
+
+def test_triangle_inequality_audit_host_logic():
+    import paper_1510_03816_b200 as gs
+
+    R = gs.DistanceRecord
+    recs = [R("x", "y", 1.0, 3, True), R("y", "z", 1.5, 3, True), R("x", "z", 4.0, 3, True),
+            R("z", "w", 1.0, 3, False)]
+    rep = gs.triangle_inequality_audit(recs)
+    by = {(e["from"], e["to"], e["via"]): e for e in rep}
+    assert by[("x", "z", "y")]["holds"] is False and by[("x", "z", "y")]["detour"] == 2.5
+    assert by[("z", "x", "y")]["direct"] == 4.0          # reverse-direction fallback
+    assert all("w" not in k for k in by)                 # unconverged records are skipped
+    assert by[("x", "y", "z")]["holds"] is True
+
+
+def test_cluster_and_newton_validate_before_any_device_work():
+    import paper_1510_03816_b200 as gs
+
+    a, b = gs.circle(1.0, n=8), gs.circle(1.1, n=8)
+    cfg = gs.ShootingConfig(h=0.5)
+    with pytest.raises(gs.ConfigurationError, match="at least 2"):
+        gs.cluster_test(a, b, [a], {"pair": 1, "ref_diff": 1}, cfg)
+    with pytest.raises(gs.ConfigurationError, match="missing"):
+        gs.cluster_test(a, b, [a, b], {"pair": 1}, cfg)
+    with pytest.raises(gs.ConfigurationError, match="positive"):
+        gs.cluster_test(a, b, [a, b], {"pair": 0, "ref_diff": 1}, cfg)
+    with pytest.raises(gs.ConfigurationError, match="TargetResidual"):
+        gs.newton_match(a, b, gs.ShootingConfig(h=0.5, stop_rule="momentum-delta"))
+    with pytest.raises(gs.ConfigurationError, match="equal landmark counts"):
+        gs.newton_match(a, gs.circle(1.0, n=9), cfg)
+    with pytest.raises(gs.ConfigurationError, match="t_match"):
+        gs.predict(a, b, 0.0, 0.5, cfg)
+    with pytest.raises(gs.ConfigurationError, match="t_predict"):
+        gs.predict(a, b, 0.5, 0.4, cfg)
