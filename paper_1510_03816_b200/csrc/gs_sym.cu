@@ -21,7 +21,9 @@
 //   * diagonal tiles (I == J) are evaluated one-sided.
 // Why two targets per lane: with one, the per-step shared-memory traffic (rotated 32-byte
 // source records, table lookups, 8 shuffles) saturated the LSU pipe (96% in ncu) before the
-// FP64 pipe; sharing the source read and the shuffles between two targets halves it.
+// FP64 pipe; sharing the source read and the shuffles between two targets halves it.  Each
+// rotation step takes two sources (GS_SYM_SRC2), so a lane runs four independent pair chains
+// against the FP64 latency ("wait" stalls were the top stall reason with two).
 // d == 0 pairs are exact through the lean pair core (gs_device.cuh); interacting coincident
 // particles are re-scanned on the rare flagged tile (reference error, particles.py:92-98).
 // Partials: the I-side of block I over superblock SJ goes to slot SJ, the J-side of block J
@@ -37,7 +39,10 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kST = 64;  // threads per CTA
 #ifndef GS_SYM_MINB      // resident CTAs per SM the register allocation is bounded for (A/B builds)
-#define GS_SYM_MINB 8  // A/B on C2: 8 -> 0.378 ms, 10 -> 0.391 ms, 12 -> 0.401 ms per RHS
+#define GS_SYM_MINB 6  // A/B on C2 (one source per step): 6 -> 0.374 ms, 8 -> 0.377, 10 -> 0.391, 12 -> 0.401
+#endif
+#ifndef GS_SYM_SRC2      // two sources per rotation step: 4 independent pair chains per lane
+#define GS_SYM_SRC2 1    // A/B on C2: 0.364 ms (minb 6, 158 regs) vs 0.383 ms (minb 8, 128 regs) vs 0.374
 #endif
 
 struct Acc {
@@ -146,6 +151,36 @@ __global__ void __launch_bounds__(kST, GS_SYM_MINB) k_dense_sym(const double4* _
                 const int b = (2 * w + ph) & 3;
                 const double4* rot = &s_rot[b][lane];
                 Acc j{0.0, 0.0, 0.0, 0.0};
+#if GS_SYM_SRC2
+                // two sources per step (4 independent pair chains per lane): jA travels with
+                // source (lane + step), jB with source (lane + step + 1); both move 2 lanes
+                Acc jb2{0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+                for (int step = 0; step < 32; step += 2) {
+                    const double4 sa = rot[step];
+                    const double4 sb = rot[step + 1];
+                    two_sided<FAM>(me0, sa, tbl, k1, a0, j, nz0);
+                    two_sided<FAM>(me1, sa, tbl, k1, a1, j, nz1);
+                    two_sided<FAM>(me0, sb, tbl, k1, a0, jb2, nz0);
+                    two_sided<FAM>(me1, sb, tbl, k1, a1, jb2, nz1);
+                    const int src = (lane + 2) & 31;
+                    j.qx = __shfl_sync(kFull, j.qx, src);
+                    j.qy = __shfl_sync(kFull, j.qy, src);
+                    j.px = __shfl_sync(kFull, j.px, src);
+                    j.py = __shfl_sync(kFull, j.py, src);
+                    jb2.qx = __shfl_sync(kFull, jb2.qx, src);
+                    jb2.qy = __shfl_sync(kFull, jb2.qy, src);
+                    jb2.px = __shfl_sync(kFull, jb2.px, src);
+                    jb2.py = __shfl_sync(kFull, jb2.py, src);
+                }
+                {   // jB of lane l belongs to source l + 1: hand it to lane l + 1
+                    const int src = (lane + 31) & 31;
+                    j.qx += __shfl_sync(kFull, jb2.qx, src);
+                    j.qy += __shfl_sync(kFull, jb2.qy, src);
+                    j.px += __shfl_sync(kFull, jb2.px, src);
+                    j.py += __shfl_sync(kFull, jb2.py, src);
+                }
+#else
 #pragma unroll 4
                 for (int step = 0; step < 32; ++step) {
                     const double4 s = rot[step];
@@ -157,6 +192,7 @@ __global__ void __launch_bounds__(kST, GS_SYM_MINB) k_dense_sym(const double4* _
                     j.px = __shfl_sync(kFull, j.px, src);
                     j.py = __shfl_sync(kFull, j.py, src);
                 }
+#endif
                 add_to(&jacc[b * 32 + lane], j);
                 __syncthreads();
             }
