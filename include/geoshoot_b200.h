@@ -157,6 +157,12 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
              const double* q0, const double* target, double* p0_out, double* endpoint_out,
              double* history_out, gs_match_result_t* result, void* stream);
 
+/* particles.velocity_field (particles.py:140-150): u (device, m x 2) = sum_j G(|x_k - q_j|) p_j
+ * at the m sample points x (device, m x 2) for the state q, p (device, n x 2).  Stream-ordered
+ * (does not synchronise); m == 0 is a no-op. */
+int gs_velocity_field(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q,
+                      const double* p, int64_t m, const double* x, double* u, void* stream);
+
 /* ---- batched independent trajectories ---------------------------------
  * Replace the reference's serial loops over independent matches / shoots:
  *   convergence_sweep cells (analysis.py:254-283), cluster_test / shape_distance pairs

@@ -8,6 +8,7 @@ Follows, symbol by symbol:
   error naming the first (i, j) in row-major order and the reference's own dp
   formula ``-(a.sum(1)[:, None] * q - a @ q)`` (``particles.py:116``)
 * ``particles.py:120-131`` hamiltonian (full double sum, no 1/2)
+* ``particles.py:140-150`` velocity_field (kernel-reconstructed velocity at sample points)
 * ``integrator.py:66-121`` fixed-step RK4 with its error re-wrapping
 * ``shooting.py:124-135, 178-179, 218-301`` _norm / _blown_up / match, momentum
   update branch (``shooting.py:266-267``), both stop rules, both norms.
@@ -131,6 +132,17 @@ def hamiltonian(k: Kernel, q: np.ndarray, p: np.ndarray, block: int = 2048) -> f
         kmat = kernel_value(k, np.sqrt(np.sum(diff * diff, axis=-1)))
         total += float(np.sum(p[r0:r1] * (kmat @ p)))
     return total
+
+
+def velocity_field(k: Kernel, q: np.ndarray, p: np.ndarray, x: np.ndarray, block: int = 2048) -> np.ndarray:
+    """particles.py:140-150: u(x_m) = sum_j G(|x_m - q_j|) p_j for an (M, 2) batch x."""
+    x = np.atleast_2d(np.asarray(x, dtype=float))
+    u = np.empty_like(x)
+    for r0 in range(0, x.shape[0], block):
+        r1 = min(x.shape[0], r0 + block)
+        dist = np.sqrt(np.sum((x[r0:r1, None, :] - q[None, :, :]) ** 2, axis=-1))
+        u[r0:r1] = kernel_value(k, dist) @ p
+    return u
 
 
 def evolve(k: Kernel, sigma2: float, q0: np.ndarray, p0: np.ndarray, t_final: float = 1.0,

@@ -9,7 +9,8 @@ reference package itself onto these implementations.  There is no CPU fallback.
 
 from .errors import ConfigurationError, DegenerateConfigurationError, DivergenceError, GeoshootError
 from .kernels import LAMBDA, KernelFamily, KernelSpec, support_radius
-from .particles import (ParticleState, SystemSpec, conserved_quantities, hamiltonian, inexactness_energy, rhs)
+from .particles import (ParticleState, SystemSpec, conserved_quantities, hamiltonian, inexactness_energy, rhs,
+                        velocity_field)
 from .integrator import EvolveConfig, EvolveResult, evolve
 from .shapes import LandmarkTemplate, circle, ellipse_rot_shift
 from .shooting import (MatchResult, ResidualNorm, ShootingConfig, StopRule, UpdateSpace, contraction_diagnostics,
@@ -24,7 +25,7 @@ __version__ = "0.1.0"
 __all__ = [
     "ConfigurationError", "DegenerateConfigurationError", "DivergenceError", "GeoshootError", "LAMBDA",
     "KernelFamily", "KernelSpec", "support_radius", "ParticleState", "SystemSpec", "conserved_quantities",
-    "hamiltonian", "inexactness_energy", "rhs", "EvolveConfig", "EvolveResult", "evolve", "LandmarkTemplate",
+    "hamiltonian", "inexactness_energy", "rhs", "velocity_field", "EvolveConfig", "EvolveResult", "evolve", "LandmarkTemplate",
     "circle", "ellipse_rot_shift", "MatchResult", "ResidualNorm", "ShootingConfig", "StopRule", "UpdateSpace",
     "contraction_diagnostics", "match", "momenta_from_velocity", "newton_match", "get_path", "set_path",
     "DIVERGED", "ClusterVerdict", "DistanceRecord", "ExactnessRow", "SweepGrid", "cluster_test", "convergence_sweep",

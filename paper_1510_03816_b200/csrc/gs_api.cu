@@ -70,6 +70,7 @@ struct gs_context {
     DevBuf<SmallResult> small_res;
     DevBuf<SmallItem> b_items;       // batched launches: per-item constants
     DevBuf<DevStatus> b_st;          // batched evolve: per-item failure records
+    DevBuf<double2> vf_part;         // velocity-field chunk partials
     // profiling: CUDA events around every pair-kernel launch, kernel launch counter
     int prof_on = 0;
     std::vector<cudaEvent_t> prof_events;
@@ -620,7 +621,7 @@ int gs_destroy(gs_context* ctx) {
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
-    ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release();
+    ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release();
     delete ctx;
     return GS_OK;
 }
@@ -1075,6 +1076,25 @@ int gs_gram(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q,
     *bad_i = key == kNoEvent ? -1 : (int64_t)(key / (unsigned long long)n);
     *bad_j = key == kNoEvent ? -1 : (int64_t)(key % (unsigned long long)n);
     return key == kNoEvent ? GS_OK : GS_ERR_COINCIDENT;
+}
+
+int gs_velocity_field(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
+                      int64_t m, const double* x, double* u, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !q || !p || !x || !u || n < 1 || m < 0) return fail(GS_ERR_INVALID, "bad velocity-field args");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (m == 0) return GS_OK;
+    GS_CUDA(cudaSetDevice(ctx->device));
+    GS_CUDA(ctx->S.ensure(n + kStatePad));
+    const DensePlan plan = velocity_plan(n, m, ctx->sm_count);
+    GS_CUDA(ctx->vf_part.ensure((size_t)plan.nchunks * m));
+    k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+    launch_velocity_field(make_const(sys), ctx->S.ptr, n, x, m, plan, ctx->vf_part.ptr, u, ctx->tbl.ptr, s);
+    ctx->launches += 3;
+    ctx->host_pairs += n * m;
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
 }
 
 int gs_stage_path(gs_context* ctx, const gs_system_t* sys, void* stream) {

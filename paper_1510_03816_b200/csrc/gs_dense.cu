@@ -147,6 +147,86 @@ void launch_gram(const SysConst& sc, const double* q, int64_t n, double* K, unsi
 }
 
 // ---------------------------------------------------------------------------------------
+// Velocity field u(x_k) = sum_j G(|x_k - q_j|) p_j at m sample points (particles.py:140-150):
+// the dq half of the pair sum with targets outside the particle set.  Same tiling as
+// k_dense_partial (two sample points per thread, sources through shared memory, source
+// chunks for parallelism at small m); partials per chunk are summed in chunk order.
+template <int FAM>
+__global__ void __launch_bounds__(kDPT, 12) k_velocity_partial(const double4* __restrict__ S, int64_t n,
+                                                               const double* __restrict__ x, int64_t m,
+                                                               int64_t chunk, double k1, double2* __restrict__ part,
+                                                               const double* __restrict__ tbl_g) {
+    __shared__ double s_tbl[kTblWords];
+    __shared__ double4 s_src[kDT];
+    for (int t = threadIdx.x; t < kTblWords; t += kDPT) s_tbl[t] = tbl_g[t];
+    const double* tbl = lane_table(s_tbl);
+    const int64_t k0 = (int64_t)blockIdx.x * kDB + threadIdx.x, k1i = k0 + kDPT;
+    const bool v0 = k0 < m, v1 = k1i < m;
+    const double x0 = v0 ? x[2 * k0] : 1e150 * (threadIdx.x + 1), y0 = v0 ? x[2 * k0 + 1] : 1e150;
+    const double x1 = v1 ? x[2 * k1i] : 1e150 * (threadIdx.x + 1), y1 = v1 ? x[2 * k1i + 1] : -1e150;
+    const int64_t j0 = (int64_t)blockIdx.y * chunk;
+    const int64_t j1 = min(n, j0 + chunk);
+    double ux0 = 0.0, uy0 = 0.0, ux1 = 0.0, uy1 = 0.0;
+    for (int64_t t0 = j0; t0 < j1; t0 += kDT) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kDT; t += kDPT) {
+            const int64_t j = t0 + t;
+            s_src[t] = (j < j1) ? S[j] : far_record(kDB + t);
+        }
+        __syncthreads();
+        const int mm = (int)((j1 - t0) < kDT ? (j1 - t0) : kDT);
+        const int mr = (mm + 3) & ~3;
+#pragma unroll 4
+        for (int jj = 0; jj < mr; ++jj) {
+            const double4 s = s_src[jj];
+            double g0, g1, c;
+            int z;
+            pair_core<FAM>(x0 - s.x, y0 - s.y, 0.0, tbl, k1, g0, c, z);
+            pair_core<FAM>(x1 - s.x, y1 - s.y, 0.0, tbl, k1, g1, c, z);
+            ux0 = fma(g0, s.z, ux0); uy0 = fma(g0, s.w, uy0);
+            ux1 = fma(g1, s.z, ux1); uy1 = fma(g1, s.w, uy1);
+        }
+    }
+    if (v0) part[(int64_t)blockIdx.y * m + k0] = make_double2(ux0, uy0);
+    if (v1) part[(int64_t)blockIdx.y * m + k1i] = make_double2(ux1, uy1);
+}
+
+__global__ void k_velocity_finish(const double2* __restrict__ part, int nchunks, int64_t m, double scale, double* u) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    double sx = 0.0, sy = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        const double2 v = part[(int64_t)c * m + k];
+        sx += v.x; sy += v.y;
+    }
+    u[2 * k] = sx * scale;
+    u[2 * k + 1] = sy * scale;
+}
+
+DensePlan velocity_plan(int64_t n, int64_t m, int sm_count) {
+    const int64_t row_blocks = (m + kDB - 1) / kDB;
+    const int64_t tiles = (n + kDT - 1) / kDT;
+    int64_t nc = ((int64_t)sm_count * 32 + row_blocks - 1) / row_blocks;
+    nc = std::max<int64_t>(1, std::min(nc, tiles));
+    DensePlan p;
+    p.chunk = ((tiles + nc - 1) / nc) * kDT;
+    p.nchunks = (int)((n + p.chunk - 1) / p.chunk);
+    return p;
+}
+
+void launch_velocity_field(const SysConst& sc, const double4* S, int64_t n, const double* x, int64_t m,
+                           const DensePlan& plan, double2* part, double* u, const double* tbl_dev,
+                           cudaStream_t stream) {
+    if (m <= 0) return;
+    dim3 grid((unsigned)((m + kDB - 1) / kDB), (unsigned)plan.nchunks);
+    if (sc.fam == kFamConical)
+        k_velocity_partial<kFamConical><<<grid, kDPT, 0, stream>>>(S, n, x, m, plan.chunk, sc.k1, part, tbl_dev);
+    else
+        k_velocity_partial<kFamGaussian><<<grid, kDPT, 0, stream>>>(S, n, x, m, plan.chunk, sc.k1, part, tbl_dev);
+    k_velocity_finish<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(part, plan.nchunks, m, sc.scale_q, u);
+}
+
+// ---------------------------------------------------------------------------------------
 // Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_finish(SysConst sc, FinishArgs a) {

@@ -57,6 +57,13 @@ void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_
 void launch_gram(const SysConst& sc, const double* q, int64_t n, double* K, unsigned long long* bad,
                  const double* tbl_dev, cudaStream_t stream);
 
+// Velocity field u(x_k) = sum_j G(|x_k - q_j|) p_j at m points x (m x 2) from the packed
+// state S (n records); part holds plan.nchunks * m double2 partials.
+DensePlan velocity_plan(int64_t n, int64_t m, int sm_count);
+void launch_velocity_field(const SysConst& sc, const double4* S, int64_t n, const double* x, int64_t m,
+                           const DensePlan& plan, double2* part, double* u, const double* tbl_dev,
+                           cudaStream_t stream);
+
 // Finish modes
 constexpr int kFinRhs = 0;    // write dq, dp rows ((nrows, 2) AoS)
 constexpr int kFinStage = 1;  // RK4 stage epilogue (integrator.py:98-114)

@@ -169,6 +169,22 @@ def gram(spec, q):
     return K
 
 
+def velocity_field(spec, q, p, x):
+    """particles.velocity_field (particles.py:140-150) on the device: u (M, 2) cuda float64 at the
+    sample points x (M, 2) for the state (q, p)."""
+    torch = _torch()
+    ctx = N.Context.get()
+    q = as_device(q, torch)
+    p = as_device(p, torch)
+    x = as_device(x, torch)
+    m = x.shape[0]
+    u = torch.empty((m, 2), dtype=torch.float64, device=q.device)
+    sysc = system_struct(spec)
+    N.check(ctx.lib.gs_velocity_field(ctx.handle, ctypes.byref(sysc), q.shape[0], _ptr(q), _ptr(p), m, _ptr(x),
+                                      _ptr(u), _stream_ptr(torch)), "gs_velocity_field")
+    return u
+
+
 def n_frames(steps: int, capture_every: int) -> int:
     if capture_every <= 0:
         return 0

@@ -41,6 +41,7 @@ _ALIASES = {
     "match": ("shooting", "analysis", "cli", ""),
     "hamiltonian": ("particles", "shooting", ""),
     "momenta_from_velocity": ("shooting", ""),
+    "velocity_field": ("particles", ""),
     # batched analysis: independent matches / shoots side by side
     "newton_match": ("shooting", ""),
     "shape_distance": ("analysis", "cli", ""),
@@ -84,7 +85,7 @@ def install(pkg=None):
     match.original = original_match
     impl = {"rhs": _particles.rhs, "evolve": _integrator.evolve, "match": match,
             "hamiltonian": _particles.hamiltonian, "momenta_from_velocity": _shooting.momenta_from_velocity,
-            "newton_match": _shooting.newton_match}
+            "newton_match": _shooting.newton_match, "velocity_field": _particles.velocity_field}
     for fname in ("shape_distance", "iso_invariance_check", "cluster_test", "convergence_sweep", "predict",
                   "exact_vs_inexact"):
         impl[fname] = getattr(_analysis, fname)

@@ -354,6 +354,28 @@ def gen_analysis(out):
         json.dump(meta, f, indent=1, sort_keys=True)
 
 
+def gen_vfield(out):
+    """particles.velocity_field (particles.py:140-150) on seeded states: at the landmarks,
+    at random sample points, at a single point; conical and gaussian, normalized or not."""
+    arrays, meta = {}, {}
+    rng = np.random.default_rng(11)
+    cases = {
+        "landmarks10": (gs.circle(1.5, n=10).points, rng.normal(size=(10, 2)), None, spec_of()),
+        "cloud_conical": (rng.uniform(0, 1, (1000, 2)), rng.normal(0, 0.1, (1000, 2)),
+                          rng.uniform(-0.2, 1.2, (777, 2)), spec_of(alpha=0.05 / LAM)),
+        "cloud_gauss": (rng.uniform(0, 1, (600, 2)), rng.normal(0, 0.1, (600, 2)),
+                        rng.uniform(-0.2, 1.2, (300, 2)), spec_of(family="gaussian", alpha=0.07, normalized=False)),
+        "single": (np.array([[0.0, 0.0], [1.0, 0.0]]), np.array([[0.0, 1.0], [1.0, 0.0]]),
+                   np.array([[0.25, -0.5]]), spec_of()),
+    }
+    for name, (q, p, x, spec) in cases.items():
+        x = q if x is None else x
+        u = gs.velocity_field(spec, gs.ParticleState(q, p), x)
+        arrays.update({f"{name}__q": q, f"{name}__p": p, f"{name}__x": x, f"{name}__u": u,
+                       f"{name}__kparams": kparams(spec)})
+    np.savez(os.path.join(out, "vfield_cases.npz"), **arrays)
+
+
 def gen_errors(out):
     msgs = {}
     q = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 1.0]])
@@ -403,7 +425,7 @@ def main():
     a = ap.parse_args()
     out = HERE
     steps = {"sympy": gen_sympy, "rhs": gen_rhs, "evolve": gen_evolve, "match": gen_match,
-             "errors": gen_errors, "c2": gen_c2, "analysis": gen_analysis}
+             "errors": gen_errors, "c2": gen_c2, "analysis": gen_analysis, "vfield": gen_vfield}
     for name, fn in steps.items():
         if a.only and name not in a.only.split(","):
             continue

@@ -422,3 +422,41 @@ def test_config5_cell_rhs_sampled_rows_match_oracle(cuda):
     dqh, dph = dq.cpu().numpy(), dp.cpu().numpy()
     oq, op = native.rhs(_kern(spec), w.sigma2, w.q, p, cutoff=w.sigma)
     assert rel(dqh, oq) <= RHS_TOL and rel(dph, op) <= RHS_TOL
+
+
+VF = cases("vfield_cases.npz")
+
+
+@pytest.mark.parametrize("name", sorted(VF))
+def test_velocity_field_matches_reference(cuda, name):
+    """particles.velocity_field (particles.py:140-150) through gs_velocity_field."""
+    import paper_1510_03816_b200 as gs
+
+    c = VF[name]
+    spec = spec_from(c["kparams"])
+    u = gs.velocity_field(spec, gs.ParticleState(c["q"], c["p"]), c["x"])
+    assert u.shape == c["u"].shape
+    assert rel(u, c["u"]) <= RHS_TOL
+    one = gs.velocity_field(spec, gs.ParticleState(c["q"], c["p"]), c["x"][0])
+    assert one.shape == (2,)
+    np.testing.assert_allclose(one, u[0], rtol=1e-15, atol=0)
+
+
+def test_velocity_field_at_landmarks_is_the_dq_half(cuda):
+    """u(q_i) = dq_i for sigma2 = 0 (particles.py:113 vs 140-150), and a large sample set
+    against the oracle restatement."""
+    import paper_1510_03816_b200 as gs
+    from oracle import restate
+    from oracle.restate import Kernel
+
+    rng = np.random.default_rng(5)
+    n, m = 5000, 3001
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 0.1, (n, 2))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.02))
+    dq, _ = gs.rhs(spec, gs.ParticleState(q, p))
+    u = gs.velocity_field(spec, gs.ParticleState(q, p), q)
+    assert rel(u, dq) <= 1e-13
+    x = rng.uniform(-0.5, 1.5, (m, 2))
+    u = gs.velocity_field(spec, gs.ParticleState(q, p), x)
+    assert rel(u, restate.velocity_field(Kernel(0, 0.02, True), q, p, x)) <= RHS_TOL

@@ -163,6 +163,7 @@ def test_dropin_rebinds_every_alias_and_restores():
         assert types.get("EvolveResult") is ref.EvolveResult
         assert types.get("DistanceRecord") is ref.DistanceRecord
         assert ref.shooting.newton_match is gs.newton_match is ref.newton_match
+        assert ref.particles.velocity_field is gs.velocity_field is ref.velocity_field
         for f in ("convergence_sweep", "cluster_test", "exact_vs_inexact", "predict", "shape_distance"):
             assert getattr(ref.analysis, f) is getattr(ref.cli, f) is getattr(ref, f) is getattr(gs, f)
         grid = ref.SweepGrid((0.5,), (0.4,), n_landmarks=8)
@@ -232,3 +233,24 @@ def test_cluster_and_newton_validate_before_any_device_work():
         gs.predict(a, b, 0.0, 0.5, cfg)
     with pytest.raises(gs.ConfigurationError, match="t_predict"):
         gs.predict(a, b, 0.5, 0.4, cfg)
+
+
+@pytest.mark.skipif(not have_reference, reason="reference package not mounted")
+def test_cli_front_end_runs_the_reference_cli_with_gpu_facts(tmp_path):
+    """the reference's CLI through the drop-in; manifests gain "b200"."""
+    from paper_1510_03816_b200 import cli, dropin
+
+    _reference()
+    out = tmp_path / "c.json"
+    assert cli.main(["shapes", "circle", "--n", "8", "--out", str(out)]) == 0
+    man = json.loads(out.with_suffix(".manifest.json").read_text())
+    assert man["schema"] == "geoshoot.manifest/1"
+    facts = man["extras"]["b200"]
+    assert facts["abi"] == 2 and facts["library"].startswith("geoshoot-b200")
+    assert not dropin.installed()
+    import torch
+
+    if not torch.cuda.is_available():  # the compute commands fail loudly without a device
+        res = tmp_path / "r"
+        with pytest.raises(N.NativeUnavailable):
+            cli.main(["match", str(out), str(out), "--h", "0.3", "--out", str(res)])

@@ -143,3 +143,13 @@ def test_oracle_error_messages_match_reference():
     with pytest.raises(OracleDegenerate) as e:
         native.rhs(k, 0.0, q, p)
     assert str(e.value) == msgs["rhs_coincident_two_groups"]
+
+
+VF = cases("vfield_cases.npz")
+
+
+@pytest.mark.parametrize("name", sorted(VF))
+def test_restate_velocity_field_matches_reference(name):
+    c = VF[name]
+    u = restate.velocity_field(Kernel.from_params(c["kparams"]), c["q"], c["p"], c["x"])
+    assert np.abs(u - c["u"]).max() <= 1e-14 * max(1.0, np.abs(c["u"]).max())
