@@ -142,7 +142,9 @@ def _event_key(st) -> tuple:
 class ShardedSolver:
     """Row-sharded evolve / match across the ranks of ``group`` (default: the world)."""
 
-    def __init__(self, spec, backend=None, group=None):
+    def __init__(self, spec, backend=None, group=None, force_split: bool = False):
+        """``force_split``: take the multi-rank code path (symmetric pair split, reduce-scatter,
+        all-gather) even in a world of one — lets a single GPU exercise the NCCL plumbing."""
         import torch.distributed as dist
 
         self.spec = spec
@@ -151,10 +153,11 @@ class ShardedSolver:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.split = self.world > 1 or (force_split and dist.is_initialized())
 
     # -- collectives (plumbing) -------------------------------------------------------------
     def _allgather_rows(self, S, r0: int, c: int):
-        if self.world > 1:
+        if self.split:
             self.dist.all_gather_into_tensor(S[: c * self.world], S[r0:r0 + c].clone(), group=self.group)
 
     def _reduce_scatter_rows(self, R_rows, R, c: int):
@@ -205,7 +208,7 @@ class ShardedSolver:
         S = self.backend.state(c * W)
         dt = t_final / steps
         sym = False
-        if W > 1 and getattr(self.backend, "supports_sym", False) and self.backend.path() == "dense":
+        if self.split and getattr(self.backend, "supports_sym", False) and self.backend.path() == "dense":
             total = self.backend.sym_parts()
             sym = total > 0
         if sym:

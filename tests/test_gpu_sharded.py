@@ -111,3 +111,58 @@ def test_sharded_match_world1_matches_device_match(cuda):
     assert r["iterations"] == d["iterations"] == 36 and r["converged"]
     assert rel(r["p0"].cpu().numpy(), d["p0"].cpu().numpy()) <= 1e-10
     assert r["hamiltonian"] == pytest.approx(d["hamiltonian"], rel=1e-10)
+
+
+def _nccl_world1():
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        return
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+
+
+def test_sharded_solver_nccl_code_path_world1(cuda):
+    """The exact multi-GPU code path (symmetric pair split, NCCL reduce-scatter of the raw row
+    sums, stage finish, NCCL all-gather of the stage records, first-failure agreement) in a
+    single-process NCCL world: one GPU, nothing waits on another rank."""
+    import torch.distributed as dist
+
+    from paper_1510_03816_b200 import device, sharded
+
+    _nccl_world1()
+    assert dist.get_backend() == "nccl"
+    gs, q, p, spec = _setup(n=5000)
+    solver = sharded.ShardedSolver(spec, force_split=True)
+    qT, pT = solver.evolve(q, p, 1.0, 4)
+    q2, p2, _ = device.evolve(spec, q, p, 1.0, 4)
+    assert rel(qT.cpu().numpy(), q2.cpu().numpy()) <= 1e-13
+    assert rel(pT.cpu().numpy(), p2.cpu().numpy()) <= 1e-13
+    # failures are agreed and re-raised like the single-GPU path
+    qc = q.copy()
+    qc[7] = qc[3]
+    pc = p.copy()
+    with pytest.raises(gs.DegenerateConfigurationError, match="particles 3 and 7 coincide"):
+        solver.evolve(qc, pc, 1.0, 2)
+    # cell path through the same plumbing (rows + all-gather)
+    gs.set_path("cell")
+    try:
+        qT, pT = sharded.ShardedSolver(spec, force_split=True).evolve(q, p, 1.0, 2)
+        q2, p2, _ = device.evolve(spec, q, p, 1.0, 2)
+        assert rel(qT.cpu().numpy(), q2.cpu().numpy()) <= 1e-13
+    finally:
+        gs.set_path("auto")
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c1()
+    spec1 = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
+    r = sharded.ShardedSolver(spec1, force_split=True).match(w.q, w.target, w.h, w.epsilon, w.max_iter, "residual",
+                                                             "max", 1.0, w.steps)
+    assert r["iterations"] == 36 and r["converged"]
