@@ -34,6 +34,9 @@ namespace {
 constexpr int kBB = 256;        // bbox block
 constexpr int kCB = 128;        // pair-kernel threads per CTA
 constexpr int kCL = 32;         // candidate chunk (per-lane list capacity)
+#ifndef GS_CELL_MINB            // resident CTAs per SM the register allocation is bounded for (A/B builds)
+#define GS_CELL_MINB 5  // A/B (C5 / C4 RHS ms): 8 -> 2.79 / 5.40, 6 -> 2.57 / 4.67, 5 -> 2.61 / 4.55, 4 -> 2.62 / 4.49
+#endif
 
 __global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double* red) {
     __shared__ double s[4][kBB];
@@ -203,7 +206,7 @@ __global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, c
 // candidate of the stencil rows and the lanes' sums are xor-butterfly reduced, so every
 // target's summation order is fixed.
 template <int FAM, int TPL>
-__global__ void __launch_bounds__(kCB, 8) k_cell_pair(const double4* __restrict__ Ss, const float2* __restrict__ Sf,
+__global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* __restrict__ Ss, const float2* __restrict__ Sf,
                                                       const unsigned* __restrict__ perm,
                                                       const unsigned* __restrict__ keys_sorted,
                                                       const int* __restrict__ start, const GridParams* __restrict__ gp,
