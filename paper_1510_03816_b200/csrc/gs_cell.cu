@@ -33,7 +33,10 @@ namespace {
 
 constexpr int kBB = 256;        // bbox block
 constexpr int kCB = 128;        // pair-kernel threads per CTA
-constexpr int kCL = 32;         // candidate chunk (per-lane list capacity)
+#ifndef GS_CELL_CL               // candidate chunk = per-lane list capacity (A/B builds)
+#define GS_CELL_CL 32
+#endif
+constexpr int kCL = GS_CELL_CL;
 #ifndef GS_CELL_MINB            // resident CTAs per SM the register allocation is bounded for (A/B builds)
 #define GS_CELL_MINB 5  // A/B (C5 / C4 RHS ms): 8 -> 2.79 / 5.40, 6 -> 2.57 / 4.67, 5 -> 2.61 / 4.55, 4 -> 2.62 / 4.49
 #endif

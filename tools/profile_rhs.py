@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--path", default="auto")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--save", default="", help="write dq, dp of the last RHS to this .npz")
     a = ap.parse_args()
     import torch
 
@@ -33,10 +34,13 @@ def main():
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for k in range(a.reps):
         s.record()
-        device.rhs(spec, q_d, p_d)
+        dq, dp = device.rhs(spec, q_d, p_d)
         e.record()
         torch.cuda.synchronize()
         print(f"{a.config} {a.path} rhs {s.elapsed_time(e):.3f} ms", flush=True)
+
+    if a.save:
+        np.savez(a.save, dq=dq.cpu().numpy(), dp=dp.cpu().numpy())
 
 
 if __name__ == "__main__":
