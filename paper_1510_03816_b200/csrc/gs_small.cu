@@ -14,6 +14,9 @@ namespace gsb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef GS_SMALL_LEAN   // lean pair core + unrolled source loop (A/B builds)
+#define GS_SMALL_LEAN 1
+#endif
 constexpr int kWarps = kSmallThreads / 32;
 
 struct SmallCtx {
@@ -63,6 +66,25 @@ template <int FAM>
 __device__ void small_rhs(const SmallCtx& c, double k1, double4 me, double& sqx, double& sqy, double& spx,
                           double& spy) {
     double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
+#if GS_SMALL_LEAN
+    // lean pair core (gs_device.cuh): d == 0 pairs are exact without selects; the z flag
+    // (integer pipe) sends the rare candidate to the reference's exact coincidence test
+#pragma unroll 4
+    for (int j = c.sub; j < c.n; j += c.split) {
+        const double4 s = c.S[j];
+        const double dx = me.x - s.x, dy = me.y - s.y;
+        const double pdot = fma(me.z, s.z, me.w * s.w);
+        double g, cf;
+        int z;
+        pair_core<FAM>(dx, dy, pdot, c.tbl, k1, g, cf, z);
+        aqx = fma(g, s.z, aqx);
+        aqy = fma(g, s.w, aqy);
+        apx = fma(cf, dx, apx);
+        apy = fma(cf, dy, apy);
+        if (z && c.act && j != c.tgt && pdot != 0.0 && __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) == 0.0)
+            atomicMin(c.key, (unsigned long long)c.tgt * (unsigned long long)c.n + (unsigned long long)j);
+    }
+#else
     for (int j = c.sub; j < c.n; j += c.split) {
         const double4 s = c.S[j];
         double pdot;
@@ -71,6 +93,7 @@ __device__ void small_rhs(const SmallCtx& c, double k1, double4 me, double& sqx,
                 atomicMin(c.key, (unsigned long long)c.tgt * (unsigned long long)c.n + (unsigned long long)j);
         }
     }
+#endif
     for (int off = c.split >> 1; off; off >>= 1) {
         aqx += __shfl_xor_sync(kFull, aqx, off);
         aqy += __shfl_xor_sync(kFull, aqy, off);
