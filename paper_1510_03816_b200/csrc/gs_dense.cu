@@ -228,18 +228,45 @@ void launch_velocity_field(const SysConst& sc, const double4* S, int64_t n, cons
 
 // ---------------------------------------------------------------------------------------
 // Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
-template <int MODE>
-__global__ void __launch_bounds__(256) k_finish(SysConst sc, FinishArgs a) {
-    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (li >= a.nrows) return;
-    if (*((volatile unsigned long long*)&a.st->first_event) < a.event) return;
-    const int64_t i = a.row0 + li;
-    double sqx = 0.0, sqy = 0.0, spx = 0.0, spy = 0.0;
+// Partial sums are reduced by kFinGroups warps per 32 rows: warp w sums slots w, w + 8, ...
+// (coalesced over the rows), warp 0 adds the group sums in group order — a fixed order, and
+// 8x the parallelism of one thread per row walking all slots (the symmetric kernel leaves
+// nsb = 128 slots per row at C2: 67 MB per stage).
+constexpr int kFinRows = 32;
+constexpr int kFinGroups = 8;
+
+__device__ __forceinline__ bool finish_reduce(const FinishArgs& a, int64_t& li, double4& sum) {
+    __shared__ double4 s_part[kFinGroups][kFinRows];
+    const int r = threadIdx.x & (kFinRows - 1), w = threadIdx.x / kFinRows;
+    li = (int64_t)blockIdx.x * kFinRows + r;
+    const bool valid = li < a.nrows;
     const int64_t ps = a.pstride ? a.pstride : a.nrows;
-    for (int c = 0; c < a.nchunks; ++c) {
-        const double4 v = a.part[(int64_t)c * ps + li];
-        sqx += v.x; sqy += v.y; spx += v.z; spy += v.w;
+    double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (valid)
+        for (int c = w; c < a.nchunks; c += kFinGroups) {
+            const double4 v = a.part[(int64_t)c * ps + li];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+    s_part[w][r] = acc;
+    __syncthreads();
+    if (w != 0 || !valid) return false;
+    const int ng = a.nchunks < kFinGroups ? a.nchunks : kFinGroups;
+    sum = s_part[0][r];
+    for (int g = 1; g < ng; ++g) {
+        const double4 v = s_part[g][r];
+        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
     }
+    return true;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish(SysConst sc, FinishArgs a) {
+    int64_t li;
+    double4 sum;
+    if (!finish_reduce(a, li, sum)) return;
+    if (*((volatile unsigned long long*)&a.st->first_event) < a.event) return;  // an earlier failure
+    const int64_t i = a.row0 + li;
+    const double sqx = sum.x, sqy = sum.y, spx = sum.z, spy = sum.w;
     const double4 me = a.S[i];
     // particles.py:113-116: dq = K p (+ sigma2 p), dp = -(sum_j a_ij (q_i - q_j))
     double dqx = sqx * sc.scale_q, dqy = sqy * sc.scale_q;
@@ -291,12 +318,28 @@ __global__ void __launch_bounds__(256) k_finish(SysConst sc, FinishArgs a) {
     if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
 }
 
+// R[i] = the same fixed-order slot sum k_finish forms (multi-GPU symmetric split: the rank's
+// raw row sums before the reduce-scatter), so 1-GPU and N-GPU runs agree bitwise.
+__global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce(FinishArgs a, double4* R) {
+    int64_t li;
+    double4 sum;
+    if (finish_reduce(a, li, sum)) R[li] = sum;
+}
+
+void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream) {
+    if (n <= 0) return;
+    FinishArgs a{};
+    a.part = part; a.nchunks = nslots; a.pstride = pstride; a.nrows = n;
+    k_slot_reduce<<<(unsigned)((n + kFinRows - 1) / kFinRows), kFinRows * kFinGroups, 0, stream>>>(a, R);
+}
+
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream) {
     if (a.nrows <= 0) return;
-    const unsigned blocks = (unsigned)((a.nrows + 255) / 256);
-    if (mode == kFinRhs) k_finish<kFinRhs><<<blocks, 256, 0, stream>>>(sc, a);
-    else if (mode == kFinHam) k_finish<kFinHam><<<blocks, 256, 0, stream>>>(sc, a);
-    else k_finish<kFinStage><<<blocks, 256, 0, stream>>>(sc, a);
+    const unsigned blocks = (unsigned)((a.nrows + kFinRows - 1) / kFinRows);
+    const int threads = kFinRows * kFinGroups;
+    if (mode == kFinRhs) k_finish<kFinRhs><<<blocks, threads, 0, stream>>>(sc, a);
+    else if (mode == kFinHam) k_finish<kFinHam><<<blocks, threads, 0, stream>>>(sc, a);
+    else k_finish<kFinStage><<<blocks, threads, 0, stream>>>(sc, a);
 }
 
 }  // namespace gsb

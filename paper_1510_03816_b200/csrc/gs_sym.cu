@@ -255,21 +255,4 @@ void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* 
                                                                st, event, tbl_dev);
 }
 
-namespace {
-__global__ void k_slot_reduce(const double4* __restrict__ part, int nslots, int64_t pstride, int64_t n, double4* R) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double4 s = make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int c = 0; c < nslots; ++c) {
-        const double4 v = part[(int64_t)c * pstride + i];
-        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-    }
-    R[i] = s;
-}
-}  // namespace
-
-void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream) {
-    if (n > 0) k_slot_reduce<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(part, nslots, pstride, n, R);
-}
-
 }  // namespace gsb
