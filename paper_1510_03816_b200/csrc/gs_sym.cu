@@ -41,6 +41,9 @@ constexpr int kST = 64;  // threads per CTA
 #ifndef GS_SYM_MINB      // resident CTAs per SM the register allocation is bounded for (A/B builds)
 #define GS_SYM_MINB 6  // A/B on C2 (one source per step): 6 -> 0.374 ms, 8 -> 0.377, 10 -> 0.391, 12 -> 0.401
 #endif
+#ifndef GS_SYM_SB        // superblock count above which blocks are grouped (A/B builds)
+#define GS_SYM_SB 128  // A/B on C2 (ms per 100-step solve): 128 -> 152.8, 64 -> 165.4, 32 -> 178.7
+#endif
 #ifndef GS_SYM_SRC2      // two sources per rotation step: 4 independent pair chains per lane
 #define GS_SYM_SRC2 1    // A/B on C2: 0.364 ms (minb 6, 158 regs) vs 0.383 ms (minb 8, 128 regs) vs 0.374
 #endif
@@ -227,7 +230,7 @@ SymPlan sym_plan(int64_t n) {
     SymPlan p;
     p.nb = (int)((n + kDB - 1) / kDB);
     p.G = 1;
-    while ((p.nb + p.G - 1) / p.G > 128 && p.G < kSymMaxG) p.G *= 2;
+    while ((p.nb + p.G - 1) / p.G > GS_SYM_SB && p.G < kSymMaxG) p.G *= 2;
     p.nsb = (p.nb + p.G - 1) / p.G;
     p.pstride = (int64_t)p.nb * kDB;
     p.ok = p.nsb <= 256;
