@@ -238,19 +238,20 @@ constexpr int kFinGroups = 8;
 __device__ __forceinline__ bool finish_reduce(const FinishArgs& a, int64_t& li, double4& sum) {
     __shared__ double4 s_part[kFinGroups][kFinRows];
     const int r = threadIdx.x & (kFinRows - 1), w = threadIdx.x / kFinRows;
+    const int groups = blockDim.x / kFinRows;  // <= kFinGroups, no more than the slots
     li = (int64_t)blockIdx.x * kFinRows + r;
     const bool valid = li < a.nrows;
     const int64_t ps = a.pstride ? a.pstride : a.nrows;
     double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
     if (valid)
-        for (int c = w; c < a.nchunks; c += kFinGroups) {
+        for (int c = w; c < a.nchunks; c += groups) {
             const double4 v = a.part[(int64_t)c * ps + li];
             acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
     s_part[w][r] = acc;
     __syncthreads();
     if (w != 0 || !valid) return false;
-    const int ng = a.nchunks < kFinGroups ? a.nchunks : kFinGroups;
+    const int ng = a.nchunks < groups ? a.nchunks : groups;
     sum = s_part[0][r];
     for (int g = 1; g < ng; ++g) {
         const double4 v = s_part[g][r];
@@ -326,17 +327,22 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce(FinishArg
     if (finish_reduce(a, li, sum)) R[li] = sum;
 }
 
+inline int finish_threads(int nchunks) {
+    const int g = nchunks < 1 ? 1 : (nchunks < kFinGroups ? nchunks : kFinGroups);
+    return g * kFinRows;
+}
+
 void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream) {
     if (n <= 0) return;
     FinishArgs a{};
     a.part = part; a.nchunks = nslots; a.pstride = pstride; a.nrows = n;
-    k_slot_reduce<<<(unsigned)((n + kFinRows - 1) / kFinRows), kFinRows * kFinGroups, 0, stream>>>(a, R);
+    k_slot_reduce<<<(unsigned)((n + kFinRows - 1) / kFinRows), finish_threads(nslots), 0, stream>>>(a, R);
 }
 
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream) {
     if (a.nrows <= 0) return;
     const unsigned blocks = (unsigned)((a.nrows + kFinRows - 1) / kFinRows);
-    const int threads = kFinRows * kFinGroups;
+    const int threads = finish_threads(a.nchunks);
     if (mode == kFinRhs) k_finish<kFinRhs><<<blocks, threads, 0, stream>>>(sc, a);
     else if (mode == kFinHam) k_finish<kFinHam><<<blocks, threads, 0, stream>>>(sc, a);
     else k_finish<kFinStage><<<blocks, threads, 0, stream>>>(sc, a);
