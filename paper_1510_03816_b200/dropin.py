@@ -9,6 +9,9 @@ callees by name, so every alias must be rebound (SURVEY.md §8(b) "Rebinding poi
     match        geoshoot.shooting.match, geoshoot.analysis.match (analysis.py:23), geoshoot.cli.match
                  (cli.py:58), geoshoot.match
     hamiltonian  geoshoot.particles.hamiltonian, geoshoot.shooting.hamiltonian (shooting.py:30), geoshoot.hamiltonian
+    template     geoshoot.shapes.LandmarkTemplate.__post_init__ (shapes.py:45-58: the duplicate check via an
+                 N x N distance matrix, SURVEY §8(b) "template duplicate check") -> an O(N log N) sort-based
+                 check with the same first pair and message, so templates of C4/C5 size can be built
     newton_match geoshoot.shooting.newton_match, geoshoot.newton_match  (batched Jacobian columns)
     analysis     shape_distance, iso_invariance_check, cluster_test, convergence_sweep, predict,
                  exact_vs_inexact in geoshoot.analysis, geoshoot.cli (cli.py:24-32), geoshoot
@@ -31,6 +34,7 @@ from . import analysis as _analysis
 from . import errors as _errors
 from . import integrator as _integrator
 from . import particles as _particles
+from . import shapes as _shapes
 from . import shooting as _shooting
 from . import types as _types
 
@@ -83,6 +87,10 @@ def install(pkg=None):
         return _shooting.match(reference, target, cfg)
 
     match.original = original_match
+    tpl = getattr(_module(pkg, "shapes"), "LandmarkTemplate", None)
+    if tpl is not None:
+        _saved.append((tpl, "__post_init__", tpl.__post_init__))
+        tpl.__post_init__ = _shapes.LandmarkTemplate.__post_init__
     impl = {"rhs": _particles.rhs, "evolve": _integrator.evolve, "match": match,
             "hamiltonian": _particles.hamiltonian, "momenta_from_velocity": _shooting.momenta_from_velocity,
             "newton_match": _shooting.newton_match, "velocity_field": _particles.velocity_field}

@@ -166,6 +166,12 @@ def test_dropin_rebinds_every_alias_and_restores():
         assert ref.particles.velocity_field is gs.velocity_field is ref.velocity_field
         for f in ("convergence_sweep", "cluster_test", "exact_vs_inexact", "predict", "shape_distance"):
             assert getattr(ref.analysis, f) is getattr(ref.cli, f) is getattr(ref, f) is getattr(gs, f)
+        # the reference's own template class, with the O(N log N) duplicate check
+        big = np.random.default_rng(0).uniform(0, 1, (200000, 2))
+        assert ref.LandmarkTemplate(big, "big").n == 200000
+        dup = np.array([[0.0, 0.0], [1.0, 2.0], [3.0, 3.0], [1.0, 2.0], [0.0, 0.0]])
+        with pytest.raises(ref.DegenerateConfigurationError, match=r"landmarks 0 and 4 coincide in template 'dup'"):
+            ref.LandmarkTemplate(dup, "dup")
         grid = ref.SweepGrid((0.5,), (0.4,), n_landmarks=8)
         with pytest.raises(ref.ConfigurationError, match="thresholds"):  # reference error classes
             ref.cluster_test(ref.circle(1.0, n=8), ref.circle(1.2, n=8), [ref.circle(2.0, n=8)] * 2,
