@@ -460,3 +460,38 @@ def test_velocity_field_at_landmarks_is_the_dq_half(cuda):
     x = rng.uniform(-0.5, 1.5, (m, 2))
     u = gs.velocity_field(spec, gs.ParticleState(q, p), x)
     assert rel(u, restate.velocity_field(Kernel(0, 0.02, True), q, p, x)) <= RHS_TOL
+
+
+def _rot90(a):
+    return np.ascontiguousarray(np.column_stack([-a[:, 1], a[:, 0]]))
+
+
+@pytest.mark.parametrize("cfg,path", [("c3", "dense"), ("c5", "cell"), ("c4", "cell")])
+def test_full_size_symmetry_properties(cuda, cfg, path):
+    """Size-independent properties of one RHS at the full BASELINE sizes (beyond any CPU
+    oracle's reach in seconds): translation invariance, equivariance under the exact 90-degree
+    rotation, momentum balance sum_i dp_i = 0 (the i <-> j antisymmetry, particles.py:116),
+    and H = sum_i p_i . dq_i for sigma2 = 0 (particles.py:120-131)."""
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs, device
+
+    w = getattr(configs, cfg)()
+    rng = np.random.default_rng(17)
+    p = w.p if w.p is not None else rng.normal(0, 0.01, w.q.shape)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
+    gs.set_path(path)
+    try:
+        dq, dp = (t.cpu().numpy() for t in device.rhs(spec, w.q, p))
+        shift = np.array([0.25, -0.5])
+        dq_t, dp_t = (t.cpu().numpy() for t in device.rhs(spec, w.q + shift, p))
+        dq_r, dp_r = (t.cpu().numpy() for t in device.rhs(spec, _rot90(w.q), _rot90(p)))
+        H = device.hamiltonian(spec, w.q, p)
+    finally:
+        gs.set_path("auto")
+    # positions move by rounding only (|q| <= 1.5): relative changes at the 1e-15 level
+    assert rel(dq_t, dq) <= 1e-11 and rel(dp_t, dp) <= 1e-10
+    assert rel(dq_r, _rot90(dq)) <= 1e-11 and rel(dp_r, _rot90(dp)) <= 1e-10
+    scale = np.abs(dp).sum(axis=0)
+    assert np.all(np.abs(dp.sum(axis=0)) <= 1e-11 * scale)
+    h_rows = float(np.sum(p * dq))
+    assert H == pytest.approx(h_rows, rel=1e-10)
