@@ -42,6 +42,10 @@ sys.path.insert(0, REPO)
 METRIC = "particle-pair interactions/s in N-particle RHS (fp64)"
 UNIT = "pairs/s"
 W_ALG = 45  # DP-pipe issue slots per ordered pair, libm formulation = 90 flop-equivalents
+# FP64-pipe instructions the implemented kernels issue per evaluated pair (SASS of the inner
+# loops, profiles/r01_history.md): symmetric dense 31 per unordered pair = 15.5 per ordered pair;
+# one-sided / cell-list ~28 per pair.  Used for the kernel's own FP64-pipe utilisation.
+W_IMPL = {"sym": 15.5, "one_sided": 28.0}
 
 
 def parse():
@@ -259,6 +263,7 @@ def main():
     pairs_per_launch = float(pp.value) / max(1, pl.value)
     ach_pairs = pairs_per_launch / (pair_ms_avg / 1e3)
     ach_tflops = ach_pairs * 2 * W_ALG / 1e12
+    w_impl = W_IMPL["sym"] if (a.path == "dense" and w.n >= 1024) else W_IMPL["one_sided"]
     peak = None
     best = None
     for _ in range(3):
@@ -305,7 +310,11 @@ def main():
                                     if a.path == "dense" else "gsb::k_cell_pair"),
                          "avg_launch_ms": pair_ms_avg, "pairs_per_launch": pairs_per_launch,
                          "work_per_pair": f"{W_ALG} DP-pipe slots = {2 * W_ALG} flop-equivalents (SURVEY.md §8(d))",
-                         "peak_source": "measured live: gs_fp64_peak_probe (DFMA chains on all SMs, best of 3)"},
+                         "peak_source": "measured live: gs_fp64_peak_probe (DFMA chains on all SMs, best of 3)",
+                         # the implemented kernel's own FP64-pipe utilisation: issued FP64 slots
+                         # per pair (SASS) x pairs/s against the peak slot rate (= peak / 2)
+                         "fp64_pipe_frac": (ach_pairs * w_impl / (peak * 1e12 / 2)) if peak else None,
+                         "fp64_slots_per_pair_implemented": w_impl},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * w.n * 2 * 8,
                     "d2h_bytes_per_step": 2 * w.n * 2 * 8,
