@@ -19,6 +19,7 @@ from .analysis import (DIVERGED, ClusterVerdict, DistanceRecord, ExactnessRow, S
                        convergence_sweep, exact_vs_inexact, iso_invariance_check, predict, shape_distance,
                        triangle_inequality_audit)
 from .device import get_path, set_path
+from . import dropin  # noqa: E402  (dropin.install() rebinds the reference package)
 
 __version__ = "0.1.0"
 
