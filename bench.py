@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--rk-steps", type=int, default=100)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the multi-GPU code path (ShardedSolver, NCCL) in a one-rank world (testing)")
     return ap.parse_args()
 
 
@@ -205,6 +207,14 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif a.force_sharded:
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(sk.getsockname()[1]))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
     gs.set_path(a.path)
 
     w = configs.c2(a.n)
@@ -213,7 +223,7 @@ def main():
     lib = ctx.lib
     q_d = torch.from_numpy(w.q).cuda()
     p_d = torch.from_numpy(w.p).cuda()
-    solver = sharded.ShardedSolver(spec) if world > 1 else None
+    solver = sharded.ShardedSolver(spec, force_split=a.force_sharded) if (world > 1 or a.force_sharded) else None
 
     def solve():
         if solver is not None:
@@ -324,7 +334,7 @@ def main():
             "extras": extras,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 
