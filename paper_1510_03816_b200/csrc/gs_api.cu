@@ -515,10 +515,23 @@ int run_evolve(gs_context* ctx, const SysConst& sc, double t_final, int steps, i
     return GS_OK;
 }
 
-int small_split(int64_t n) {
-    int split = 1;
-    while (split < 32 && n * split * 2 <= kSmallThreads) split *= 2;
-    return split;
+// CTAs per small-N item: a cluster of kMaxCluster CTAs spreads the rows of one match over
+// that many SMs (GS_B200_CLUSTER overrides; 1 = one CTA per item).
+int small_cluster(int64_t n) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = std::getenv("GS_B200_CLUSTER");
+        const int v = e ? std::atoi(e) : 0;
+        forced = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;  // cluster sizes with a kernel instance
+    }
+    if (forced > 0) return forced;
+    return n >= 64 ? kMaxCluster : 1;
+}
+
+void small_setup(SmallArgs& a, int64_t n) {
+    a.n = n;
+    a.cluster = small_cluster(n);
+    small_threads(n, a.cluster, &a.split);
 }
 
 bool use_small(const gs_system_t* sys, int64_t n) {
@@ -732,7 +745,7 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
     ctx->n = n;
     if (use_small(sys, n)) {
         SmallArgs a{};
-        a.n = n; a.batch = 1; a.split = small_split(n); a.mode = 0;
+        small_setup(a, n); a.batch = 1; a.mode = 0;
         a.item.sc = sc; a.item.t_final = t_final; a.item.steps = steps;
         a.capture_every = capture_every; a.q_in = q; a.p_in = p; a.q_out = q; a.p_out = p; a.frames = frames;
         a.st = ctx->st.ptr;
@@ -786,7 +799,7 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
     if (use_small(sys, n)) {
         GS_CUDA(ctx->hist.ensure(cfg->max_iter));
         SmallArgs a{};
-        a.n = n; a.batch = 1; a.split = small_split(n); a.mode = 1;
+        small_setup(a, n); a.batch = 1; a.mode = 1;
         a.item = small_item(sc, cfg);
         a.q_in = q0; a.target = target; a.q_out = endpoint_out; a.p_out = p0_out;
         a.history = ctx->hist.ptr; a.result = ctx->small_res.ptr; a.st = ctx->st.ptr;
@@ -929,7 +942,7 @@ int gs_match_batch(gs_context* ctx, const gs_batch_item_t* items, int64_t batch,
         if (rc) return rc;
         GS_CUDA(ctx->small_res.ensure(batch));
         SmallArgs a{};
-        a.n = n; a.batch = batch; a.split = small_split(n); a.mode = 1;
+        small_setup(a, n); a.batch = batch; a.mode = 1;
         a.item = host_items[0]; a.items = ctx->b_items.ptr;
         a.q_in = q0; a.q_stride = q0_stride; a.target = target; a.t_stride = target_stride;
         a.q_out = endpoint_out; a.p_out = p0_out;
@@ -994,7 +1007,7 @@ int gs_evolve_batch(gs_context* ctx, const gs_system_t* sys, int64_t batch, int6
     if (use_small(sys, n)) {
         GS_CUDA(ctx->b_st.ensure(batch));
         SmallArgs a{};
-        a.n = n; a.batch = batch; a.split = small_split(n); a.mode = 0;
+        small_setup(a, n); a.batch = batch; a.mode = 0;
         a.item.sc = sc; a.item.t_final = t_final; a.item.steps = steps;
         a.q_in = q_in; a.q_stride = q_stride; a.p_in = p_io; a.q_out = q_out; a.p_out = p_io;
         a.st = ctx->b_st.ptr;

@@ -87,7 +87,8 @@ struct FinishArgs {
 };
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream);
 
-// Small-N persistent kernel: a whole evolve or a whole match in one CTA (n <= kSmallMax).
+// Small-N persistent kernel: a whole evolve or a whole match per thread-block cluster
+// (n <= kSmallMax), see gs_small.cu.
 constexpr int kSmallMax = 512;
 constexpr int kSmallThreads = 512;
 
@@ -113,10 +114,13 @@ struct SmallItem {
     int max_iter, stop_rule, norm;
 };
 
+constexpr int kMaxCluster = 8;  // CTAs per item (portable cluster size)
+
 struct SmallArgs {
     int64_t n;
-    int64_t batch;         // CTAs = items
-    int split;             // lanes per target (power of two <= 32)
+    int64_t batch;         // items; the grid is batch x cluster CTAs
+    int cluster;           // CTAs per item (1..kMaxCluster), one thread-block cluster
+    int split;             // lanes per row (power of two <= 32), see small_threads
     int mode;              // 0 evolve, 1 match
     int capture_every;     // evolve, batch == 1 only
     SmallItem item;        // used when items == null
@@ -142,6 +146,8 @@ struct SmallArgs {
     int L_smem;            // stage L in shared memory (row stride n + 1)
 };
 size_t small_smem_bytes(const SmallArgs& a);
+// Threads per CTA for n rows on `cluster` CTAs; *split = lanes per row.
+int small_threads(int64_t n, int cluster, int* split);
 int launch_small(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream);
 
 }  // namespace gsb

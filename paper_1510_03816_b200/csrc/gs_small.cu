@@ -1,99 +1,152 @@
-// gs_small.cu — one persistent CTA runs a whole evolve or a whole feedback match (n <= 512).
+// gs_small.cu — a whole evolve or a whole feedback match per thread-block cluster (n <= 512).
 //
 // Config 1 (N = 64) is pure latency: a launch per RHS would cost more than the RHS.  Here
-// the reference's complete Algorithm 1 loop (shooting.py:218-301, momentum update
-// :266-267) and its RK4 integrator (integrator.py:66-121) execute inside one kernel:
-// the stage state lives in shared memory, each target row is owned by `split` lanes
-// that share its source sweep (shuffle-reduced in a fixed butterfly order, so every
-// lane ends with identical bits), and the residual norms are block reductions.  The
-// host launches once and reads one result record.
+// the reference's complete Algorithm 1 loop (shooting.py:218-301, both update spaces) and its
+// RK4 integrator (integrator.py:66-121) execute inside one kernel.  One match runs on a
+// cluster of C CTAs (C = 8 by default, C = 1 for tiny n): CTA r owns rows
+// [r*R, (r+1)*R), R = ceil(n/C), and keeps the FULL stage state in its own shared memory.
+// Per RK stage every CTA evaluates its rows against all n sources (`split` lanes per row
+// sharing the source sweep, shuffle-reduced in a fixed butterfly order), computes the next
+// stage input of its rows and stores it into the next-stage buffer of every CTA of the
+// cluster through distributed shared memory; one cluster barrier per stage publishes it.
+// Stage buffers alternate (ping-pong) and the cross-CTA flag / reduction slots alternate by
+// barrier parity, so a CTA running one barrier ahead never overwrites what a slower one still
+// reads.  Residual norms and H are block reductions combined over the cluster in CTA order,
+// so every CTA takes identical decisions.  A batched launch is a grid of such clusters, one
+// per item.
+#include <cooperative_groups.h>
+
 #include "gs_kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gsb {
 
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-#ifndef GS_SMALL_LEAN   // lean pair core + unrolled source loop (A/B builds)
-#define GS_SMALL_LEAN 1
+#ifndef GS_SMALL_UNROLL   // source-loop unroll of the small-N RHS (A/B builds)
+#define GS_SMALL_UNROLL 4
 #endif
+constexpr int kSmallUnroll = GS_SMALL_UNROLL;
 constexpr int kWarps = kSmallThreads / 32;
 
+// Shared memory of the kernel at file scope, so the helpers address it directly instead of
+// through pointers held in registers (the match loop runs at the 128-register limit).
+extern __shared__ double4 s_state[];  // [2][n] ping-pong stage buffers, then the velocity workspace
+__shared__ double s_tbl[kTblWords];
+__shared__ double s_red[kWarps + 1];
+__shared__ double s_dslot[2 * kMaxCluster];              // reduction slots, by barrier parity
+__shared__ unsigned long long s_kslot[2 * kMaxCluster];  // coincidence keys, by barrier parity
+__shared__ int s_bslot[2 * kMaxCluster];                 // non-finite flags, by barrier parity
+__shared__ unsigned long long s_key[3];                  // this CTA's rotating coincidence keys
+__shared__ SmallItem s_item;                             // this item's constants (read on demand)
+
+template <int CL>
 struct SmallCtx {
-    double4* S;            // shared: stage state, n records
-    const double* tbl;     // shared: this lane's copy of the exp table
-    double* red;           // shared: kWarps scratch
-    unsigned long long* key;
+    static constexpr int C = CL;  // CTAs of the cluster (compile time: C = 1 folds away all cluster code)
+    int rank;              // this CTA's rank in the cluster
     int n, split, tgt, sub;
-    bool act;
+    bool act;              // this thread's row exists and is owned by this CTA
+    int parity;            // slot parity (flips at every cluster barrier that uses slots)
 };
 
 __device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
 
-// block-wide reduction of one value per target (lanes with sub != 0 or !act pass identity)
-__device__ double block_reduce(const SmallCtx& c, double v, bool is_max) {
+template <class Ctx>
+__device__ __forceinline__ void cluster_sync(const Ctx& c) {
+    if constexpr (Ctx::C > 1) cg::this_cluster().sync();
+    else __syncthreads();
+}
+
+template <class Ctx, typename T>
+__device__ __forceinline__ T* remote(const Ctx& c, T* p, int r) {
+    if constexpr (Ctx::C > 1) return cg::this_cluster().map_shared_rank(p, r);
+    else return p;
+}
+
+// Stores this row's record into buf[tgt] of every CTA of the cluster (the row's lanes share
+// the stores).  Visible to all after the next cluster barrier.
+template <class Ctx, typename T>
+__device__ __forceinline__ void bcast_row(const Ctx& c, T* buf, const T& v) {
+    if constexpr (Ctx::C == 1) {
+        if (c.act && c.sub == 0) buf[c.tgt] = v;
+    } else {
+        if (!c.act) return;
+        for (int r = c.sub; r < Ctx::C; r += c.split) remote(c, buf, r)[c.tgt] = v;
+    }
+}
+
+// block-wide reduction of one value per row (lanes with sub != 0 or !act pass identity)
+template <class Ctx>
+__device__ double block_reduce(const Ctx& c, double v, bool is_max) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int off = 16; off; off >>= 1) {
         double o = __shfl_xor_sync(kFull, v, off);
         v = is_max ? nanmax(v, o) : v + o;
     }
-    if (lane == 0) c.red[warp] = v;
+    if (lane == 0) s_red[warp] = v;
     __syncthreads();
     if (warp == 0) {
         const int nw = (blockDim.x + 31) >> 5;
-        double w = lane < nw ? c.red[lane] : (is_max ? 0.0 : 0.0);
+        double w = lane < nw ? s_red[lane] : 0.0;
         for (int off = 16; off; off >>= 1) {
             double o = __shfl_xor_sync(kFull, w, off);
             w = is_max ? nanmax(w, o) : w + o;
         }
-        if (lane == 0) c.red[kWarps] = w;
+        if (lane == 0) s_red[kWarps] = w;
     }
     __syncthreads();
-    const double out = c.red[kWarps];
+    const double out = s_red[kWarps];
     __syncthreads();
     return out;
 }
 
-// shooting.py:124-135: MAX = max_i hypot(r_i), L2 = flat 2-norm
-__device__ double block_norm(const SmallCtx& c, double rx, double ry, int kind) {
-    const bool own = c.act && c.sub == 0;
-    if (kind == 0) return block_reduce(c, own ? hypot(rx, ry) : 0.0, true);
-    return sqrt(block_reduce(c, own ? __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)) : 0.0, false));
+// block reduction, then the cluster's CTA values combined in rank order (identical everywhere)
+template <class Ctx>
+__device__ double cluster_reduce(Ctx& c, double v, bool is_max) {
+    v = block_reduce(c, v, is_max);
+    if constexpr (Ctx::C == 1) return v;
+    double* slots = s_dslot + c.parity * kMaxCluster;
+    if (threadIdx.x < (unsigned)c.C) remote(c, slots, (int)threadIdx.x)[c.rank] = v;
+    cluster_sync(c);
+    c.parity ^= 1;
+    double acc = slots[0];
+    for (int r = 1; r < c.C; ++r) acc = is_max ? nanmax(acc, slots[r]) : acc + slots[r];
+    return acc;
 }
 
-// raw sums of the RHS of this lane's target against S (all lanes of the group get them)
-template <int FAM>
-__device__ void small_rhs(const SmallCtx& c, double k1, double4 me, double& sqx, double& sqy, double& spx,
-                          double& spy) {
+// shooting.py:124-135: MAX = max_i hypot(r_i), L2 = flat 2-norm
+template <class Ctx>
+__device__ double cluster_norm(Ctx& c, double rx, double ry, int kind) {
+    const bool own = c.act && c.sub == 0;
+    if (kind == 0) return cluster_reduce(c, own ? hypot(rx, ry) : 0.0, true);
+    return sqrt(cluster_reduce(c, own ? __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)) : 0.0, false));
+}
+
+// raw sums of the RHS of this lane's row against S (all lanes of the row get them).  The lean
+// pair core (gs_device.cuh) makes d == 0 pairs exact without selects; its z flag (integer pipe)
+// sends the rare candidate to the reference's exact coincidence test (particles.py:92-98).
+template <int FAM, class Ctx>
+__device__ void small_rhs(const Ctx& c, const double4* __restrict__ S, double k1, double4 me,
+                          unsigned long long* key, double& sqx, double& sqy, double& spx, double& spy) {
+    const double* tbl = lane_table(s_tbl);
     double aqx = 0.0, aqy = 0.0, apx = 0.0, apy = 0.0;
-#if GS_SMALL_LEAN
-    // lean pair core (gs_device.cuh): d == 0 pairs are exact without selects; the z flag
-    // (integer pipe) sends the rare candidate to the reference's exact coincidence test
-#pragma unroll 4
+#pragma unroll kSmallUnroll
     for (int j = c.sub; j < c.n; j += c.split) {
-        const double4 s = c.S[j];
+        const double4 s = S[j];
         const double dx = me.x - s.x, dy = me.y - s.y;
         const double pdot = fma(me.z, s.z, me.w * s.w);
         double g, cf;
         int z;
-        pair_core<FAM>(dx, dy, pdot, c.tbl, k1, g, cf, z);
+        pair_core<FAM>(dx, dy, pdot, tbl, k1, g, cf, z);
         aqx = fma(g, s.z, aqx);
         aqy = fma(g, s.w, aqy);
         apx = fma(cf, dx, apx);
         apy = fma(cf, dy, apy);
         if (z && c.act && j != c.tgt && pdot != 0.0 && __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) == 0.0)
-            atomicMin(c.key, (unsigned long long)c.tgt * (unsigned long long)c.n + (unsigned long long)j);
+            atomicMin(key, (unsigned long long)c.tgt * (unsigned long long)c.n + (unsigned long long)j);
     }
-#else
-    for (int j = c.sub; j < c.n; j += c.split) {
-        const double4 s = c.S[j];
-        double pdot;
-        if (pair_accum<FAM>(me.x, me.y, me.z, me.w, s.x, s.y, s.z, s.w, c.tbl, k1, aqx, aqy, apx, apy, pdot)) {
-            if (c.act && j != c.tgt && pdot != 0.0)
-                atomicMin(c.key, (unsigned long long)c.tgt * (unsigned long long)c.n + (unsigned long long)j);
-        }
-    }
-#endif
     for (int off = c.split >> 1; off; off >>= 1) {
         aqx += __shfl_xor_sync(kFull, aqx, off);
         aqy += __shfl_xor_sync(kFull, aqy, off);
@@ -103,28 +156,40 @@ __device__ void small_rhs(const SmallCtx& c, double k1, double4 me, double& sqx,
     sqx = aqx; sqy = aqy; spx = apx; spy = apy;
 }
 
-__device__ __forceinline__ void store_frame(const SmallCtx& c, double* frames, int f, const double4& b) {
+template <class Ctx>
+__device__ __forceinline__ void store_frame(const Ctx& c, double* frames, int f, const double4& b) {
     if (frames && c.act && c.sub == 0) reinterpret_cast<double4*>(frames)[(int64_t)f * c.n + c.tgt] = b;
 }
 
-// integrator.py:66-121 on the block.  b: in = initial state, out = final state.
-// Returns kNoEvent or the failure event (step*8 + ev); *c.key holds the pair on coincidence.
-template <int FAM>
-__device__ unsigned long long small_evolve(const SmallCtx& c, const SysConst& sc, double4& b, int steps, double dt,
-                                           int capture_every, double* frames) {
-    if (threadIdx.x == 0) *c.key = kNoEvent;
-    if (c.act && c.sub == 0) c.S[c.tgt] = b;
+// Publishes this CTA's rows of (q, p) as S[0] of every CTA (an evolve's initial state).
+template <class Ctx>
+__device__ __forceinline__ void publish_state(Ctx& c, const double4& b) {
+    bcast_row(c, s_state, b);
+    cluster_sync(c);
+}
+
+// integrator.py:66-121 over the cluster.  Precondition: S[0] holds the initial state of all
+// rows (publish_state).  b: in = this thread's initial row, out = its final row.  Returns
+// kNoEvent or the failure event (step*8 + ev); *key_out = the row-major-first coincident pair.
+template <int FAM, class Ctx>
+__device__ unsigned long long small_evolve(Ctx& c, const SysConst& sc, double4& b, int steps, double dt,
+                                           int capture_every, double* frames, unsigned long long* key_out) {
     int f = 0;
     if (capture_every > 0) store_frame(c, frames, f++, b);
-    __syncthreads();
+    // Barriers per stage: one CTA barrier (C = 1), or one CTA + one cluster barrier.  The
+    // coincidence key rotates over 3 slots: stage k's slot is read right after stage k's
+    // barrier, when stage k - 1's slot (read after the previous barrier) is reset for its next
+    // use by stage k + 2.
+    int cur = 0, k = 0;
     for (int step = 1; step <= steps; ++step) {
         double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
-        for (int s = 0; s < 4; ++s) {
-            const double4 me = c.act ? c.S[c.tgt] : make_double4(0.0, 0.0, 0.0, 0.0);
+        for (int s = 0; s < 4; ++s, ++k) {
+            double4* Sc = s_state + (size_t)cur * c.n;
+            double4* Sn = s_state + (size_t)(cur ^ 1) * c.n;
+            unsigned long long* key = s_key + k % 3;
+            const double4 me = c.act ? Sc[c.tgt] : make_double4(0.0, 0.0, 0.0, 0.0);
             double sqx, sqy, spx, spy;
-            small_rhs<FAM>(c, sc.k1, me, sqx, sqy, spx, spy);
-            __syncthreads();
-            if (*c.key != kNoEvent) return (unsigned long long)step * 8ull + 2ull * s;
+            small_rhs<FAM>(c, Sc, sc.k1, me, key, sqx, sqy, spx, spy);
             double dqx = sqx * sc.scale_q, dqy = sqy * sc.scale_q;
             if (sc.sigma2 != 0.0) {
                 dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
@@ -155,32 +220,55 @@ __device__ unsigned long long small_evolve(const SmallCtx& c, const SysConst& sc
                 nxt.w = __dadd_rn(b.w, __dmul_rn(cc, acc.w));
                 b = nxt;
             }
-            if (c.act && c.sub == 0) c.S[c.tgt] = nxt;
-            const bool bad = c.act && !finite4(nxt.x, nxt.y, nxt.z, nxt.w);
-            if (__syncthreads_or(bad)) return (unsigned long long)step * 8ull + 2ull * s + 1ull;
+            bcast_row(c, Sn, nxt);
+            const int bad = __syncthreads_or(c.act && !finite4(nxt.x, nxt.y, nxt.z, nxt.w));
+            unsigned long long kmin = *key;
+            int anybad = bad;
+            if constexpr (Ctx::C > 1) {  // this CTA's key and flag into every CTA's slots, then the cluster's
+                unsigned long long* ks = s_kslot + c.parity * kMaxCluster;
+                int* bs = s_bslot + c.parity * kMaxCluster;
+                if (threadIdx.x < (unsigned)c.C) {
+                    remote(c, ks, (int)threadIdx.x)[c.rank] = kmin;
+                    remote(c, bs, (int)threadIdx.x)[c.rank] = bad;
+                }
+                cluster_sync(c);
+                c.parity ^= 1;
+                kmin = ks[0];
+                anybad = bs[0];
+                for (int r = 1; r < c.C; ++r) {
+                    kmin = ks[r] < kmin ? ks[r] : kmin;
+                    anybad |= bs[r];
+                }
+            }
+            if (threadIdx.x == 0) s_key[(k + 2) % 3] = kNoEvent;  // stage k - 1's slot, next used by k + 2
+            if (kmin != kNoEvent) {
+                *key_out = kmin;
+                return (unsigned long long)step * 8ull + 2ull * s;
+            }
+            if (anybad) return (unsigned long long)step * 8ull + 2ull * s + 1ull;
+            cur ^= 1;
         }
         if (capture_every > 0 && (step % capture_every == 0 || step == steps)) store_frame(c, frames, f++, b);
     }
     return kNoEvent;
 }
 
-// particles.py:120-131 at (q, p): block sum of p_i . (K p)_i
-template <int FAM>
-__device__ double small_hamiltonian(const SmallCtx& c, const SysConst& sc, double4 b) {
-    if (c.act && c.sub == 0) c.S[c.tgt] = b;
-    if (threadIdx.x == 0) *c.key = kNoEvent;
-    __syncthreads();
+// particles.py:120-131 at (q, p): sum_i p_i . (K p)_i over the cluster.  b = this row's (q0, p).
+template <int FAM, class Ctx>
+__device__ double small_hamiltonian(Ctx& c, const SysConst& sc, double4 b) {
+    publish_state(c, b);
     double sqx, sqy, spx, spy;
-    small_rhs<FAM>(c, sc.k1, b, sqx, sqy, spx, spy);
-    __syncthreads();
+    small_rhs<FAM>(c, s_state, sc.k1, b, s_key + 2, sqx, sqy, spx, spy);  // coincidences are irrelevant to H
     const double v = __dadd_rn(__dmul_rn(b.z, sqx * sc.scale_q), __dmul_rn(b.w, sqy * sc.scale_q));
-    return block_reduce(c, (c.act && c.sub == 0) ? v : 0.0, false);
+    return cluster_reduce(c, (c.act && c.sub == 0) ? v : 0.0, false);
 }
 
-// p = K^-1 u with K = L L^T (shooting.py:157-159, cho_solve): forward substitution L y = u
-// (column-oriented: y_j = v_j / L_jj, then v_i -= L_ij y_j for i > j) into w, backward
-// L^T x = y into w.  One barrier per column; every thread updates rows of the column.
-__device__ void small_chol_solve(const SmallCtx& c, const double* L, int ld, double2* v, double2* w) {
+// p = K^-1 u with K = L L^T (shooting.py:157-159, cho_solve), solved redundantly by every CTA
+// of the cluster (u of all rows is in v): forward substitution L y = u (column-oriented:
+// y_j = v_j / L_jj, then v_i -= L_ij y_j for i > j) into v, backward L^T x = y into w.  One
+// CTA barrier per column; every thread updates rows of the column.
+template <class Ctx>
+__device__ void small_chol_solve(const Ctx& c, const double* L, int ld, double2* v, double2* w) {
     const int n = c.n;
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += blockDim.x) w[t] = v[t];
@@ -216,46 +304,51 @@ __device__ void small_chol_solve(const SmallCtx& c, const double* L, int ld, dou
     }
 }
 
-template <int FAM>
+template <int FAM, int CL>
 __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const double* __restrict__ tbl_g) {
-    extern __shared__ double4 s_state[];
-    __shared__ double s_tbl[kTblWords];
-    __shared__ double s_red[kWarps + 1];
-    __shared__ unsigned long long s_key;
     for (int t = threadIdx.x; t < kTblWords; t += blockDim.x) s_tbl[t] = tbl_g[t];
+    if (threadIdx.x < 3) s_key[threadIdx.x] = kNoEvent;
 
-    const int64_t b = blockIdx.x;
-    const SmallItem item = a.items ? a.items[b] : a.item;
+    constexpr int C = CL;
+    const int64_t b = blockIdx.x / C;  // the item this cluster runs
+    if (threadIdx.x == 0) s_item = a.items ? a.items[b] : a.item;
+    __syncthreads();
+    const SmallItem& item = s_item;
     const SysConst& sc = item.sc;
-    SmallCtx c;
-    c.S = s_state; c.tbl = lane_table(s_tbl); c.red = s_red; c.key = &s_key;
+    SmallCtx<CL> c; c.rank = (int)(blockIdx.x % C); c.parity = 0;
     c.n = (int)a.n; c.split = a.split;
-    c.tgt = threadIdx.x / a.split; c.sub = threadIdx.x % a.split;
-    c.act = c.tgt < c.n;
+    const int R = (c.n + C - 1) / C;
+    const int tl = threadIdx.x / a.split;
+    c.sub = threadIdx.x % a.split;
+    c.tgt = c.rank * R + tl;
+    c.act = tl < R && c.tgt < c.n;
     const int t = c.act ? c.tgt : 0;
     const double dt = item.t_final / item.steps;
     const int64_t own = b * 2 * a.n;  // this item's (n, 2) slice of the per-item outputs
     const double* q_in = a.q_in + b * a.q_stride;
-    __syncthreads();
+    cluster_sync(c);  // table loaded; every CTA of the cluster is running (DSMEM targets exist)
 
     if (a.mode == 0) {  // ------------------------------------------------ evolve
         const double* p_in = a.p_in + own;
         double4 bs = make_double4(q_in[2 * t], q_in[2 * t + 1], p_in[2 * t], p_in[2 * t + 1]);
-        const unsigned long long ev = small_evolve<FAM>(c, sc, bs, item.steps, dt, a.capture_every, a.frames);
+        publish_state(c, bs);
+        unsigned long long key = kNoEvent;
+        const unsigned long long ev = small_evolve<FAM>(c, sc, bs, item.steps, dt, a.capture_every, a.frames, &key);
         if (c.act && c.sub == 0) {
             a.q_out[own + 2 * t] = bs.x; a.q_out[own + 2 * t + 1] = bs.y;
             a.p_out[own + 2 * t] = bs.z; a.p_out[own + 2 * t + 1] = bs.w;
         }
-        if (threadIdx.x == 0) {
+        if (c.rank == 0 && threadIdx.x == 0) {
             a.st[b].first_event = ev;
-            a.st[b].pair_key = (ev != kNoEvent && (ev & 1ull) == 0) ? s_key : kNoEvent;
+            a.st[b].pair_key = (ev != kNoEvent && (ev & 1ull) == 0) ? key : kNoEvent;
         }
+        cluster_sync(c);  // no CTA exits while another may still store into its shared memory
         return;
     }
 
     // ------------------------------------------------------------------ match
-    // velocity workspace after the state records: v, w (n double2 each), then L (smem copy)
-    double2* v = reinterpret_cast<double2*>(s_state + a.n);
+    // velocity workspace after the two state buffers: v, w (n double2 each), then L (smem copy)
+    double2* v = reinterpret_cast<double2*>(s_state + 2 * a.n);
     double2* w = v + a.n;
     const double* L = nullptr;
     int ld = (int)a.n;
@@ -276,7 +369,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const doub
     double px = 0.0, py = 0.0, ux = 0.0, uy = 0.0;
     double ex = qx0, ey = qy0;  // evolve(q0, 0) is exactly q0 (zero momenta: dq = dp = 0)
     double rx = __dsub_rn(yx, ex), ry = __dsub_rn(yy, ey);
-    double nrm = block_norm(c, rx, ry, item.norm);
+    double nrm = cluster_norm(c, rx, ry, item.norm);
     double initial = nrm;
     bool have_initial = (item.stop_rule == 0);
     int outcome = 1, iters = 0, fail_iter = -1;
@@ -289,7 +382,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const doub
             if (L) {  // u <- u + h r; p = K^-1 u (shooting.py:263-265)
                 ux = __dadd_rn(ux, __dmul_rn(item.h, rx));
                 uy = __dadd_rn(uy, __dmul_rn(item.h, ry));
-                if (c.act && c.sub == 0) v[c.tgt] = make_double2(ux, uy);
+                bcast_row(c, v, make_double2(ux, uy));
+                cluster_sync(c);
                 small_chol_solve(c, L, ld, v, w);
                 const double2 pv = w[t];
                 px = pv.x; py = pv.y;
@@ -298,18 +392,20 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const doub
                 py = __dadd_rn(py, __dmul_rn(item.h, ry));
             }
             double4 bs = make_double4(qx0, qy0, px, py);
-            const unsigned long long ev = small_evolve<FAM>(c, sc, bs, item.steps, dt, 0, nullptr);
+            publish_state(c, bs);
+            unsigned long long key = kNoEvent;
+            const unsigned long long ev = small_evolve<FAM>(c, sc, bs, item.steps, dt, 0, nullptr, &key);
             if (ev != kNoEvent) {
                 outcome = 3; fail_event = ev; fail_iter = it + 1;
-                fail_key = ((ev & 1ull) == 0) ? s_key : kNoEvent;
+                fail_key = ((ev & 1ull) == 0) ? key : kNoEvent;
                 break;
             }
             ex = bs.x; ey = bs.y;
             rx = __dsub_rn(yx, ex); ry = __dsub_rn(yy, ey);
-            nrm = block_norm(c, rx, ry, item.norm);
+            nrm = cluster_norm(c, rx, ry, item.norm);
             double value = (item.stop_rule == 0) ? nrm : delta;
             if (!have_initial) { initial = value; have_initial = true; }
-            if (threadIdx.x == 0) history[it] = value;
+            if (c.rank == 0 && threadIdx.x == 0) history[it] = value;
             iters = it + 1;
             if (!isfinite(value) || (initial > 0.0 && value > 1e6 * initial)) { outcome = 2; break; }
             if (value < item.epsilon) { outcome = 0; break; }
@@ -320,18 +416,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const doub
         a.p_out[own + 2 * t] = px; a.p_out[own + 2 * t + 1] = py;
         a.q_out[own + 2 * t] = ex; a.q_out[own + 2 * t + 1] = ey;
     }
-    if (threadIdx.x == 0) {
+    if (c.rank == 0 && threadIdx.x == 0) {
         SmallResult r;
         r.hamiltonian = H; r.final_residual = nrm; r.fail_event = fail_event; r.pair_key = fail_key;
         r.outcome = outcome; r.iterations = iters; r.fail_iter = fail_iter; r.pad = 0;
         a.result[b] = r;
     }
+    cluster_sync(c);
 }
 
 }  // namespace
 
 size_t small_smem_bytes(const SmallArgs& a) {
-    size_t bytes = (size_t)a.n * sizeof(double4);
+    size_t bytes = 2 * (size_t)a.n * sizeof(double4);
     if (a.mode == 1 && a.L) {
         bytes += 2 * (size_t)a.n * sizeof(double2);
         if (a.L_smem) bytes += (size_t)a.n * (a.n + 1) * sizeof(double);
@@ -339,16 +436,45 @@ size_t small_smem_bytes(const SmallArgs& a) {
     return bytes;
 }
 
+int small_threads(int64_t n, int cluster, int* split_out) {
+    const int64_t rows = (n + cluster - 1) / cluster;
+    int split = 1;
+    while (split < 32 && rows * split * 2 <= kSmallThreads) split *= 2;
+    *split_out = split;
+    return (int)(((rows * split) + 31) / 32 * 32);
+}
+
 int launch_small(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream) {
-    const int threads = (int)(((a.n * a.split) + 31) / 32 * 32);
+    int split = 0;
+    const int threads = small_threads(a.n, a.cluster, &split);
+    if (split != a.split) return (int)cudaErrorInvalidValue;
     const size_t smem = small_smem_bytes(a);
-    auto kern = fam == kFamConical ? k_small<kFamConical> : k_small<kFamGaussian>;
+    void (*kern)(SmallArgs, const double*) = nullptr;
+    const bool con = fam == kFamConical;
+    switch (a.cluster) {
+        case 1: kern = con ? k_small<kFamConical, 1> : k_small<kFamGaussian, 1>; break;
+        case 2: kern = con ? k_small<kFamConical, 2> : k_small<kFamGaussian, 2>; break;
+        case 4: kern = con ? k_small<kFamConical, 4> : k_small<kFamGaussian, 4>; break;
+        case 8: kern = con ? k_small<kFamConical, 8> : k_small<kFamGaussian, 8>; break;
+        default: return (int)cudaErrorInvalidValue;
+    }
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
     }
-    kern<<<(unsigned)a.batch, threads, smem, stream>>>(a, tbl_dev);
-    return (int)cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.batch * a.cluster));
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)a.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, kern, a, tbl_dev);
 }
 
 }  // namespace gsb
