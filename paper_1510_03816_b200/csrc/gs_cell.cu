@@ -37,6 +37,9 @@ constexpr int kCB = 128;        // pair-kernel threads per CTA
 #define GS_CELL_CL 32
 #endif
 constexpr int kCL = GS_CELL_CL;
+#ifndef GS_CELL_TPL_MIN         // minimum lanes per target (A/B builds)
+#define GS_CELL_TPL_MIN 4  // A/B (C5 / C4 RHS ms): 1 -> 2.61 / 4.48, 2 -> 2.57 / 3.94, 4 -> 2.57 / 3.62, 8 -> 2.64 / 3.48, 16 -> 2.87 / 3.36
+#endif
 #ifndef GS_CELL_MINB            // resident CTAs per SM the register allocation is bounded for (A/B builds)
 #define GS_CELL_MINB 5  // A/B (C5 / C4 RHS ms): 8 -> 2.79 / 5.40, 6 -> 2.57 / 4.67, 5 -> 2.61 / 4.55, 4 -> 2.62 / 4.49
 #endif
@@ -344,7 +347,7 @@ void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t ro
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int tpl = 1;  // lanes per target: enough threads to cover every SM ~8 warps deep
+    int tpl = GS_CELL_TPL_MIN;  // lanes per target: enough threads to cover every SM ~8 warps deep
     while (tpl < 16 && n * tpl < (int64_t)sms * 1024) tpl *= 2;
     const unsigned blocks = (unsigned)((n * tpl + kCB - 1) / kCB);
 #define GS_CELL_LAUNCH(F, T)                                                                                   \
