@@ -71,6 +71,9 @@ struct gs_context {
     DevBuf<SmallItem> b_items;       // batched launches: per-item constants
     DevBuf<DevStatus> b_st;          // batched evolve: per-item failure records
     DevBuf<double2> vf_part;         // velocity-field chunk partials
+    // rank split of the symmetric kernel: slots written per row superblock for the cached range
+    DevBuf<int> sym_slots, sym_counts;
+    int64_t sym_key_n = -1, sym_key_b = -1, sym_key_e = -1;
     // profiling: CUDA events around every pair-kernel launch, kernel launch counter
     int prof_on = 0;
     std::vector<cudaEvent_t> prof_events;
@@ -634,7 +637,8 @@ int gs_destroy(gs_context* ctx) {
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
-    ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release();
+    ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release(); ctx->sym_slots.release();
+    ctx->sym_counts.release();
     delete ctx;
     return GS_OK;
 }
@@ -1136,14 +1140,37 @@ int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, in
     GS_CUDA(cudaSetDevice(ctx->device));
     const SymPlan sp = sym_plan(n);
     GS_CUDA(ctx->part.ensure((size_t)sp.nsb * (size_t)sp.pstride));
-    GS_CUDA(cudaMemsetAsync(ctx->part.ptr, 0, (size_t)sp.nsb * (size_t)sp.pstride * sizeof(double4), s));
+    if (ctx->sym_key_n != n || ctx->sym_key_b != part_begin || ctx->sym_key_e != part_end) {
+        // Each (slot, row) is written by exactly one superblock pair: tile (X, Y) stores the
+        // I-side sums of X's rows in slot Y and the J-side sums of Y's rows in slot X.  List,
+        // per row superblock, the slots this rank's pairs write (ascending); the reduction reads
+        // only those, so the buffer needs no clearing.
+        const int nsb = sp.nsb;
+        std::vector<unsigned char> hit((size_t)nsb * nsb, 0);
+        for (long long t = part_begin; t < part_end; ++t) {
+            long long SI, SJ;
+            sym_pair_of(t, nsb, &SI, &SJ);
+            hit[(size_t)SI * nsb + SJ] = 1;
+            hit[(size_t)SJ * nsb + SI] = 1;
+        }
+        std::vector<int> slots((size_t)nsb * nsb, 0), counts(nsb, 0);
+        for (int X = 0; X < nsb; ++X)
+            for (int Y = 0; Y < nsb; ++Y)
+                if (hit[(size_t)X * nsb + Y]) slots[(size_t)X * nsb + counts[X]++] = Y;
+        GS_CUDA(ctx->sym_slots.ensure(slots.size()));
+        GS_CUDA(ctx->sym_counts.ensure(counts.size()));
+        GS_CUDA(cudaMemcpy(ctx->sym_slots.ptr, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice));
+        GS_CUDA(cudaMemcpy(ctx->sym_counts.ptr, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
+        ctx->sym_key_n = n; ctx->sym_key_b = part_begin; ctx->sym_key_e = part_end;
+    }
     const SysConst sc = make_const(sys);
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg;
     if (ctx->prof_on) prof_mark(ctx, s);
     launch_dense_sym(sc, ctx->S.ptr, n, ctx->part.ptr, sp.pstride, ctx->st.ptr, ev, ctx->tbl.ptr, s, part_begin,
                      part_end);
     if (ctx->prof_on) prof_mark(ctx, s);
-    launch_slot_reduce(ctx->part.ptr, sp.nsb, sp.pstride, n, reinterpret_cast<double4*>(R), s);
+    launch_slot_reduce_list(ctx->part.ptr, sp.pstride, n, sp.G * kDB, sp.nsb, ctx->sym_slots.ptr,
+                            ctx->sym_counts.ptr, reinterpret_cast<double4*>(R), s);
     ctx->launches += 2;
     ctx->pair_launches++;
     ctx->host_pairs += (long long)((double)n * (double)n * (double)(part_end - part_begin) / (double)total);

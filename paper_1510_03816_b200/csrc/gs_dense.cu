@@ -327,6 +327,46 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce(FinishArg
     if (finish_reduce(a, li, sum)) R[li] = sum;
 }
 
+// Rank-split variant: rows of superblock X sum only the slots the rank's superblock pairs wrote
+// (slots[X * nsb + k], k < counts[X], ascending), in the same grouped order as finish_reduce;
+// untouched slots are neither cleared nor read.
+__global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce_list(const double4* __restrict__ part,
+                                                                            int64_t pstride, int64_t n,
+                                                                            int rows_per_sb, int nsb,
+                                                                            const int* __restrict__ slots,
+                                                                            const int* __restrict__ counts,
+                                                                            double4* R) {
+    __shared__ double4 s_part[kFinGroups][kFinRows];
+    const int r = threadIdx.x & (kFinRows - 1), w = threadIdx.x / kFinRows;
+    const int64_t li = (int64_t)blockIdx.x * kFinRows + r;
+    const bool valid = li < n;
+    const int X = valid ? (int)(li / rows_per_sb) : 0;
+    const int cnt = valid ? counts[X] : 0;
+    const int* list = slots + (size_t)X * nsb;
+    double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int k = w; k < cnt; k += kFinGroups) {
+        const double4 v = part[(int64_t)list[k] * pstride + li];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    s_part[w][r] = acc;
+    __syncthreads();
+    if (w != 0 || !valid) return;
+    const int ng = cnt < kFinGroups ? cnt : kFinGroups;
+    double4 sum = ng > 0 ? s_part[0][r] : make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int g = 1; g < ng; ++g) {
+        const double4 v = s_part[g][r];
+        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+    }
+    R[li] = sum;
+}
+
+void launch_slot_reduce_list(const double4* part, int64_t pstride, int64_t n, int rows_per_sb, int nsb,
+                             const int* slots, const int* counts, double4* R, cudaStream_t stream) {
+    if (n <= 0) return;
+    k_slot_reduce_list<<<(unsigned)((n + kFinRows - 1) / kFinRows), kFinRows * kFinGroups, 0, stream>>>(
+        part, pstride, n, rows_per_sb, nsb, slots, counts, R);
+}
+
 inline int finish_threads(int nchunks) {
     const int g = nchunks < 1 ? 1 : (nchunks < kFinGroups ? nchunks : kFinGroups);
     return g * kFinRows;

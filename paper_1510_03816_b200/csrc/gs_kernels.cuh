@@ -52,6 +52,11 @@ void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* 
                       long long cta1 = -1);
 // R[i] = sum over slots of part[slot * pstride + i] (fixed order), i < n.
 void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream);
+// The same over the slots listed per row superblock (a rank's share of the superblock pairs).
+void launch_slot_reduce_list(const double4* part, int64_t pstride, int64_t n, int rows_per_sb, int nsb,
+                             const int* slots, const int* counts, double4* R, cudaStream_t stream);
+// Superblock pair (SI, SJ), SI <= SJ, of work item t (row-major over the upper triangle).
+void sym_pair_of(long long t, int nsb, long long* SI, long long* SJ);
 
 // Gram matrix of the kernel over q (n x n row-major), first coincident pair -> *bad (i*n+j).
 void launch_gram(const SysConst& sc, const double* q, int64_t n, double* K, unsigned long long* bad,

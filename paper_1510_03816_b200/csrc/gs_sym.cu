@@ -237,6 +237,18 @@ SymPlan sym_plan(int64_t n) {
     return p;
 }
 
+void sym_pair_of(long long t, int nsb, long long* SI, long long* SJ) {
+    auto row_start = [nsb](long long r) { return r * nsb - r * (r - 1) / 2; };
+    long long lo = 0, hi = nsb - 1;  // largest r with row_start(r) <= t
+    while (lo < hi) {
+        const long long mid = (lo + hi + 1) / 2;
+        if (row_start(mid) <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    *SI = lo;
+    *SJ = lo + (t - row_start(lo));
+}
+
 long long sym_ctas(int64_t n) {
     const SymPlan p = sym_plan(n);
     return (long long)p.nsb * (p.nsb + 1) / 2;
