@@ -240,16 +240,7 @@ def momenta_from_velocity(kernel, q0, u0) -> np.ndarray:
     if q0.shape != u0.shape or q0.ndim != 2 or q0.shape[1] != 2:
         raise ValueError(f"q0 and u0 must both have shape (N, 2), got {q0.shape} and {u0.shape}")
     torch = device._torch()
-
-    class _Spec:
-        pass
-
-    spec = _Spec()
-    spec.kernel, spec.sigma2 = kernel, 0.0
-    K = device.gram(spec, device.as_device(q0, torch))
-    L, info = torch.linalg.cholesky_ex(K)
-    if int(info) != 0:
-        raise _errors.DegenerateConfigurationError("kernel Gram matrix is not positive definite")
+    L, _, _ = gram_factor(SystemSpec(kernel=kernel), q0)
     return torch.cholesky_solve(device.as_device(u0, torch), L).cpu().numpy()
 
 
