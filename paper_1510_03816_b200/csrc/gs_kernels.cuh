@@ -35,7 +35,7 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
 
 // Symmetric all-pairs RHS of all n rows (single rank, gs_sym.cu): each unordered pair once;
 // row i gets nsb partials part[slot * pstride + i], pstride = nb * kDB.
-constexpr int kSymMaxG = 4;
+constexpr int kSymMaxG = 8;  // 8 blocks per superblock: symmetric dense up to N = 256 * 8 * 128 = 262144
 struct SymPlan {
     int nb;           // 128-row blocks
     int G;            // blocks per superblock

@@ -466,7 +466,7 @@ def _rot90(a):
     return np.ascontiguousarray(np.column_stack([-a[:, 1], a[:, 0]]))
 
 
-@pytest.mark.parametrize("cfg,path", [("c3", "dense"), ("c5", "cell"), ("c4", "cell")])
+@pytest.mark.parametrize("cfg,path", [("c3", "dense"), ("c5", "cell"), ("c4", "cell"), ("c4", "dense")])
 def test_full_size_symmetry_properties(cuda, cfg, path):
     """Size-independent properties of one RHS at the full BASELINE sizes (beyond any CPU
     oracle's reach in seconds): translation invariance, equivariance under the exact 90-degree
