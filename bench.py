@@ -340,7 +340,8 @@ def main():
 
 
 def run_extras(a, gs, device, configs, torch):
-    """Secondary figures of BASELINE's metric pair: one C2 RHS; C1 seconds per feedback iteration."""
+    """Secondary figures of BASELINE's metric pair: one C2 RHS, one C5 cell-list RHS, C1 seconds
+    per feedback iteration."""
     out = {}
     w = configs.c2(a.n)
     spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
@@ -356,6 +357,40 @@ def run_extras(a, gs, device, configs, torch):
     e.record()
     torch.cuda.synchronize()
     out["c2_rhs_ms"] = s.elapsed_time(e) / reps
+    # C5 cell-list RHS at the first feedback shoot's state (SURVEY §8(d) cell-list roofline:
+    # accepted pairs/s x 45 slots against the FP64 peak)
+    import ctypes
+
+    from paper_1510_03816_b200 import _native as N
+
+    w5 = configs.c5()
+    spec5 = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w5.alpha), sigma2=w5.sigma2)
+    q5 = torch.from_numpy(w5.q).cuda()
+    p5 = torch.from_numpy(w5.h * (w5.target - w5.q)).cuda()
+    path0 = device.get_path()
+    device.set_path("cell")
+    try:
+        for _ in range(2):
+            device.rhs(spec5, q5, p5)
+        ctx = N.Context.get()
+        pm, pl, ll, pp = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        ctx.lib.gs_profile_enable(ctx.handle, 1)
+        ctx.lib.gs_profile_read(ctx.handle, ctypes.byref(pm), ctypes.byref(pl), ctypes.byref(ll), ctypes.byref(pp), 1)
+        s.record()
+        for _ in range(3):
+            device.rhs(spec5, q5, p5)
+        e.record()
+        torch.cuda.synchronize()
+        ctx.lib.gs_profile_read(ctx.handle, ctypes.byref(pm), ctypes.byref(pl), ctypes.byref(ll), ctypes.byref(pp), 1)
+        ctx.lib.gs_profile_enable(ctx.handle, 0)
+    finally:
+        device.set_path(path0)
+    rhs_ms = s.elapsed_time(e) / 3
+    acc = pp.value / 3
+    out["c5_cell_rhs_ms"] = rhs_ms
+    out["c5_cell_pair_kernel_ms"] = pm.value / max(1, pl.value)
+    out["c5_accepted_pairs_per_rhs"] = acc
+    out["c5_cell_pairs_per_s"] = acc / (rhs_ms / 1e3)
     c1 = configs.c1()
     spec1 = gs.SystemSpec(kernel=gs.KernelSpec(alpha=c1.alpha))
     cfg = gs.ShootingConfig(h=c1.h, epsilon=c1.epsilon, max_iter=c1.max_iter, update_space="momentum",
