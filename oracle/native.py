@@ -114,7 +114,7 @@ def evolve(k: Kernel, sigma2: float, q0: np.ndarray, p0: np.ndarray, t_final: fl
 
 
 def match_momentum(k: Kernel, sigma2: float, q0, target, h, epsilon, max_iter, stop_rule="residual",
-                   norm_kind="max", t_final=1.0, steps=100, cutoff: float = 0.0) -> dict:
+                   norm_kind="max", t_final=1.0, steps=100, cutoff: float = 0.0, update_space="momentum") -> dict:
     ev = lambda qq, pp: evolve(k, sigma2, qq, pp, t_final, steps, cutoff)[0]
     return restate.match_momentum(k, sigma2, q0, target, h, epsilon, max_iter, stop_rule, norm_kind,
-                                  t_final, steps, evolve_fn=ev)
+                                  t_final, steps, evolve_fn=ev, update_space=update_space)

@@ -10,8 +10,9 @@ Follows, symbol by symbol:
 * ``particles.py:120-131`` hamiltonian (full double sum, no 1/2)
 * ``particles.py:140-150`` velocity_field (kernel-reconstructed velocity at sample points)
 * ``integrator.py:66-121`` fixed-step RK4 with its error re-wrapping
-* ``shooting.py:124-135, 178-179, 218-301`` _norm / _blown_up / match, momentum
-  update branch (``shooting.py:266-267``), both stop rules, both norms.
+* ``shooting.py:124-135, 178-179, 218-301`` _norm / _blown_up / match, both update spaces
+  (momentum ``:266-267``; velocity ``:138-159, 263-265`` with scipy's Cholesky, as the reference),
+  both stop rules, both norms.
 
 Row blocking changes only the BLAS blocking of the row-block products, so the
 results agree with the reference to rounding (pinned in tests/test_oracle.py).
@@ -189,16 +190,29 @@ def norm(kind: str, vec: np.ndarray) -> float:
     return float(np.linalg.norm(arr.ravel()))
 
 
+def gram_matrix(k: Kernel, q: np.ndarray) -> np.ndarray:
+    """kernels.py:181-197: K_ij = G(|q_i - q_j|)."""
+    return kernel_value(k, np.sqrt(np.sum((q[:, None, :] - q[None, :, :]) ** 2, axis=-1)))
+
+
 def match_momentum(k: Kernel, sigma2: float, q0: np.ndarray, target: np.ndarray, h: float,
                    epsilon: float, max_iter: int, stop_rule: str = "residual", norm_kind: str = "max",
-                   t_final: float = 1.0, steps: int = 100, evolve_fn=None) -> dict:
-    """shooting.py:218-301 with update_space = MOMENTUM (p <- p + h r, shooting.py:266-267).
+                   t_final: float = 1.0, steps: int = 100, evolve_fn=None, update_space: str = "momentum") -> dict:
+    """shooting.py:218-301: update_space MOMENTUM (p <- p + h r, shooting.py:266-267) or VELOCITY
+    (u <- u + h r, p = K^-1 u with the Cholesky factor of the Gram matrix over q0 computed once,
+    shooting.py:138-159, 263-265).
 
     Returns the MatchResult fields (hamiltonian included, shooting.py:182-207).
     """
     ev = evolve_fn or (lambda qq, pp: evolve(k, sigma2, qq, pp, t_final, steps)[0])
     n = q0.shape[0]
     p = np.zeros((n, 2))
+    u = np.zeros((n, 2))
+    factor = None
+    if update_space == "velocity":
+        from scipy.linalg import cho_factor, cho_solve
+
+        factor = cho_factor(gram_matrix(k, q0), lower=True)
 
     def result(history, converged, endpoint, diagnosis):
         return dict(p0=p, iterations=len(history), converged=converged, residual_history=tuple(history),
@@ -215,7 +229,11 @@ def match_momentum(k: Kernel, sigma2: float, q0: np.ndarray, target: np.ndarray,
             return result(history, True, endpoint, None)
     for _ in range(max_iter):
         delta = h * norm(norm_kind, residual)
-        p = p + h * residual
+        if factor is not None:
+            u = u + h * residual
+            p = cho_solve(factor, u)
+        else:
+            p = p + h * residual
         try:
             endpoint_new = ev(q0, p)
         except (OracleDivergence, OracleDegenerate) as exc:

@@ -495,3 +495,27 @@ def test_full_size_symmetry_properties(cuda, cfg, path):
     assert np.all(np.abs(dp.sum(axis=0)) <= 1e-11 * scale)
     h_rows = float(np.sum(p * dq))
     assert H == pytest.approx(h_rows, rel=1e-10)
+
+
+@pytest.mark.parametrize("space", ["velocity", "momentum"])
+def test_general_path_match_both_spaces_match_oracle(cuda, space):
+    """N = 600 > 512: the general device loop (momentum: gs_match's host-driven device loop;
+    velocity: device Gram + cuSOLVER factor + device shoots) against the oracle's Algorithm 1."""
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+    from oracle.restate import Kernel
+
+    n = 600
+    ref = gs.circle(1.0, n=n)
+    tgt = gs.ellipse_rot_shift(1.05, 0.96, 0.0, (0.01, 0.0), n=n)
+    alpha = 0.02
+    h = 0.5 if space == "velocity" else 0.3
+    cfg = gs.ShootingConfig(h=h, epsilon=1e-7, max_iter=200, update_space=space,
+                            evolve=gs.EvolveConfig(steps=10), system=gs.SystemSpec(kernel=gs.KernelSpec(alpha=alpha)))
+    r = gs.match(ref, tgt, cfg)
+    o = native.match_momentum(Kernel(0, alpha, True), 0.0, ref.points, tgt.points, h, 1e-7, 200, "residual", "max",
+                              1.0, 10, update_space=space)
+    assert r.converged and o["converged"]
+    assert r.iterations == o["iterations"]
+    assert np.abs(r.p0 - o["p0"]).max() <= 1e-8 * np.abs(o["p0"]).max()
+    assert r.hamiltonian == pytest.approx(o["hamiltonian"], rel=1e-8)

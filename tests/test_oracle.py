@@ -96,11 +96,13 @@ def _kernel(meta):
     return Kernel(0 if meta["family"] == "conical" else 1, meta["alpha"], meta["normalized"])
 
 
-@pytest.mark.parametrize("name", sorted(n for n, m in MATCH_META.items() if m["update_space"] == "momentum"))
+@pytest.mark.parametrize("name", sorted(n for n, m in MATCH_META.items() if not m.get("warnings")))
 def test_oracle_match_matches_reference(name):
+    """Both update spaces (the ill-conditioned velocity case carries the factorisation error of
+    a cond ~1e16 Gram matrix and is pinned on the device side by its warning only)."""
     m, c = MATCH_META[name], MATCH[name]
     out = native.match_momentum(_kernel(m), m["sigma2"], c["ref"], c["tgt"], m["h"], m["epsilon"], m["max_iter"],
-                                m["stop_rule"], m["norm"], m["t_final"], m["steps"])
+                                m["stop_rule"], m["norm"], m["t_final"], m["steps"], update_space=m["update_space"])
     assert out["iterations"] == m["iterations"]
     assert out["converged"] == m["converged"]
     if m["diagnosis"] and m["diagnosis"].startswith("step too large"):
