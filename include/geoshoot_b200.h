@@ -240,6 +240,32 @@ int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, in
 int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt,
                     const double* R_rows, void* stream);
 
+/* ---- fused stage exchange over peer memory (multi-GPU symmetric split, opt-in) ---------------
+ * Replaces the NCCL reduce-scatter + all-gather of a stage: the stage
+ * epilogue of this rank's rows reads every rank's raw row sums over NVLink and stores each new
+ * 32-byte stage record straight into every rank's S.  Per stage: gs_p2p_pairs (waits for the
+ * previous stage's records, this rank's superblock pairs, signals "sums ready"), gs_p2p_finish
+ * (waits for all ranks' sums, epilogue + stores, signals "records written"); gs_p2p_sync after
+ * the last stage.  Signals are monotonic counters in each rank's memory (system-scope atomics);
+ * waits give up after GS_B200_P2P_TIMEOUT_S (default 10 s) and count it in gs_p2p_timeouts —
+ * a lost signal costs a timeout, never a hang.  Requires an open stage session (gs_stage_begin).
+ *   gs_p2p_local    : allocates this rank's sums buffer (rows_all records) and counters (zeroed);
+ *                     returns the device pointers of S, R and the counters
+ *   gs_p2p_export   : the same, as 3 cudaIpcMemHandle_t (3 x 64 bytes) for the other ranks
+ *   gs_p2p_import   : opens every rank's handles (world x 3 x 64 bytes, rank order)
+ *   gs_p2p_set_peers: sets the ranks' pointers directly (one process driving several contexts) */
+int gs_p2p_local(gs_context* ctx, int64_t rows_all, void** S, void** R, void** flags);
+int gs_p2p_export(gs_context* ctx, int64_t rows_all, void* handles);
+int gs_p2p_import(gs_context* ctx, int world, int rank, const void* handles_all);
+int gs_p2p_set_peers(gs_context* ctx, int world, int rank, void* const* S, void* const* R, void* const* F);
+int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, int64_t part_begin,
+                 int64_t part_end, void* stream);
+int gs_p2p_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt,
+                  void* stream);
+int gs_p2p_sync(gs_context* ctx, void* stream);
+int gs_p2p_timeouts(gs_context* ctx, int64_t* timeouts);
+int gs_p2p_close(gs_context* ctx);
+
 /* Profiling: with profiling enabled, every launch of the pair kernel (the dense or cell-list
  * RHS sweep, or the persistent small-N kernel) is bracketed by CUDA events on its stream;
  * gs_profile_read returns their summed device time (ms), the number of pair-kernel launches,

@@ -34,7 +34,8 @@ EXPORTS = (
     "gs_status_fetch", "gs_status_reset", "gs_hamiltonian", "gs_evolve", "gs_match", "gs_stage_begin",
     "gs_stage_run", "gs_stage_state", "gs_stage_end", "gs_fp64_peak_probe", "gs_profile_enable",
     "gs_profile_read", "gs_stage_path", "gs_sym_parts", "gs_stage_pairs_sym", "gs_stage_finish", "gs_gram",
-    "gs_match_batch", "gs_evolve_batch", "gs_velocity_field",
+    "gs_match_batch", "gs_evolve_batch", "gs_velocity_field", "gs_p2p_local", "gs_p2p_export", "gs_p2p_import",
+    "gs_p2p_set_peers", "gs_p2p_pairs", "gs_p2p_finish", "gs_p2p_sync", "gs_p2p_timeouts", "gs_p2p_close",
 )
 
 
@@ -126,6 +127,15 @@ def load(path: str = LIB_PATH):
             "gs_evolve_batch": ([_vp, P(System), _i64, _i64, ctypes.c_double, ctypes.c_int32, _dp, _i64, _dp, _dp,
                                  P(Status), _vp], ctypes.c_int),
             "gs_velocity_field": ([_vp, P(System), _i64, _dp, _dp, _i64, _dp, _dp, _vp], ctypes.c_int),
+            "gs_p2p_local": ([_vp, _i64, P(_vp), P(_vp), P(_vp)], ctypes.c_int),
+            "gs_p2p_export": ([_vp, _i64, _vp], ctypes.c_int),
+            "gs_p2p_import": ([_vp, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
+            "gs_p2p_set_peers": ([_vp, ctypes.c_int, ctypes.c_int, P(_vp), P(_vp), P(_vp)], ctypes.c_int),
+            "gs_p2p_pairs": ([_vp, P(System), ctypes.c_int32, ctypes.c_int32, _i64, _i64, _vp], ctypes.c_int),
+            "gs_p2p_finish": ([_vp, P(System), ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _vp], ctypes.c_int),
+            "gs_p2p_sync": ([_vp, _vp], ctypes.c_int),
+            "gs_p2p_timeouts": ([_vp, P(_i64)], ctypes.c_int),
+            "gs_p2p_close": ([_vp], ctypes.c_int),
             "gs_profile_enable": ([_vp, ctypes.c_int32], ctypes.c_int),
             "gs_profile_read": ([_vp, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64),
                                  ctypes.c_int32], ctypes.c_int),

@@ -74,6 +74,19 @@ struct gs_context {
     // rank split of the symmetric kernel: slots written per row superblock for the cached range
     DevBuf<int> sym_slots, sym_counts;
     int64_t sym_key_n = -1, sym_key_b = -1, sym_key_e = -1;
+    // fused stage exchange over peer memory (gs_p2p_*): this rank's raw row sums, the signal
+    // counters ([0] sums ready, [1] stage records written, [2] wait timeouts) and the ranks' pointers
+    struct P2P {
+        int world = 0, rank = 0;
+        DevBuf<double4> R;
+        DevBuf<unsigned long long> flags;
+        DevBuf<const double4*> Rp;
+        DevBuf<double4*> Sp;
+        DevBuf<unsigned long long*> Fp;
+        std::vector<void*> opened;       // IPC mappings to close
+        unsigned long long epoch = 0;    // stages completed since the peers were set
+        long long timeout_ns = 10000000000ll;
+    } p2p;
     // profiling: CUDA events around every pair-kernel launch, kernel launch counter
     int prof_on = 0;
     std::vector<cudaEvent_t> prof_events;
@@ -637,6 +650,8 @@ int gs_destroy(gs_context* ctx) {
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
+    gs_p2p_close(ctx);
+    ctx->p2p.R.release(); ctx->p2p.flags.release(); ctx->p2p.Rp.release(); ctx->p2p.Sp.release(); ctx->p2p.Fp.release();
     ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release(); ctx->sym_slots.release();
     ctx->sym_counts.release();
     delete ctx;
@@ -1127,8 +1142,8 @@ int64_t gs_sym_parts(int64_t n) {
     return (p.ok && n >= kSymMinN) ? (int64_t)sym_ctas(n) : 0;
 }
 
-int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
-                       int64_t part_end, double* R, void* stream) {
+static int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
+                          int64_t part_end, double* R, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || ctx->n < 1 || !R) return fail(GS_ERR_INVALID, "no stage session");
     int rc = check_system(sys);
@@ -1178,6 +1193,11 @@ int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, in
     return GS_OK;
 }
 
+int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
+                       int64_t part_end, double* R, void* stream) {
+    return pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, R, stream);
+}
+
 int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt,
                     const double* R_rows, void* stream) {
     if (!ctx || ctx->n < 1) return fail(GS_ERR_INVALID, "no stage session");
@@ -1194,6 +1214,162 @@ int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32
     launch_finish(kFinStage, make_const(sys), fa, (cudaStream_t)stream);
     ctx->launches++;
     GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+// ---- fused stage exchange over peer memory (multi-GPU, symmetric split) -----------------
+// Per stage: [wait: previous stage's records from all ranks] -> this rank's superblock pairs ->
+// raw row sums into R -> signal "sums ready" to every rank -> wait for all ranks' signals ->
+// epilogue of this rank's rows reading every rank's R and storing the new records into every
+// rank's S (k_finish_p2p) -> signal "records written".  Counters only grow (targets are
+// multiples of the world size), waits give up after a timeout and count it (gs_p2p_timeouts),
+// so a lost signal costs a timeout, never a hang.
+namespace {
+
+__global__ void k_p2p_signal(unsigned long long* const* Fp, int world, int which) {
+    __threadfence_system();
+    if ((int)threadIdx.x < world) atomicAdd_system(Fp[threadIdx.x] + which, 1ull);
+}
+
+__global__ void k_p2p_wait(unsigned long long* flags, int which, unsigned long long target, long long timeout_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*((volatile unsigned long long*)&flags[which]) < target) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if ((long long)(t - t0) > timeout_ns) {
+            atomicAdd(&flags[2], 1ull);
+            break;
+        }
+        __nanosleep(256);
+    }
+    __threadfence_system();
+}
+
+}  // namespace
+
+int gs_p2p_local(gs_context* ctx, int64_t rows_all, void** S, void** R, void** flags) {
+    if (!ctx || ctx->n < 1 || !S || !R || !flags) return fail(GS_ERR_INVALID, "no stage session");
+    if (rows_all < ctx->n) return fail(GS_ERR_INVALID, "rows_all < n");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    GS_CUDA(ctx->p2p.R.ensure(rows_all));
+    GS_CUDA(ctx->p2p.flags.ensure(4));
+    GS_CUDA(cudaMemset(ctx->p2p.flags.ptr, 0, 4 * sizeof(unsigned long long)));
+    *S = ctx->S.ptr; *R = ctx->p2p.R.ptr; *flags = ctx->p2p.flags.ptr;
+    if (const char* e = std::getenv("GS_B200_P2P_TIMEOUT_S")) ctx->p2p.timeout_ns = (long long)(std::atof(e) * 1e9);
+    return GS_OK;
+}
+
+int gs_p2p_export(gs_context* ctx, int64_t rows_all, void* handles) {
+    if (!handles) return fail(GS_ERR_INVALID, "handles is NULL");
+    void* ptr[3];
+    int rc = gs_p2p_local(ctx, rows_all, &ptr[0], &ptr[1], &ptr[2]);
+    if (rc) return rc;
+    for (int k = 0; k < 3; ++k)
+        GS_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handles) + k, ptr[k]));
+    return GS_OK;
+}
+
+int gs_p2p_set_peers(gs_context* ctx, int world, int rank, void* const* S, void* const* R, void* const* F) {
+    if (!ctx || world < 1 || world > 32 || rank < 0 || rank >= world || !S || !R || !F)
+        return fail(GS_ERR_INVALID, "bad peer set");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    GS_CUDA(ctx->p2p.Sp.ensure(world));
+    GS_CUDA(ctx->p2p.Rp.ensure(world));
+    GS_CUDA(ctx->p2p.Fp.ensure(world));
+    GS_CUDA(cudaMemcpy(ctx->p2p.Sp.ptr, S, world * sizeof(void*), cudaMemcpyHostToDevice));
+    GS_CUDA(cudaMemcpy(ctx->p2p.Rp.ptr, R, world * sizeof(void*), cudaMemcpyHostToDevice));
+    GS_CUDA(cudaMemcpy(ctx->p2p.Fp.ptr, F, world * sizeof(void*), cudaMemcpyHostToDevice));
+    ctx->p2p.world = world; ctx->p2p.rank = rank; ctx->p2p.epoch = 0;
+    return GS_OK;
+}
+
+int gs_p2p_close(gs_context* ctx) {
+    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
+    cudaSetDevice(ctx->device);
+    for (void* p : ctx->p2p.opened) cudaIpcCloseMemHandle(p);
+    ctx->p2p.opened.clear();
+    ctx->p2p.world = 0;
+    return GS_OK;
+}
+
+int gs_p2p_import(gs_context* ctx, int world, int rank, const void* handles_all) {
+    if (!ctx || !handles_all || world < 1 || world > 32 || rank < 0 || rank >= world)
+        return fail(GS_ERR_INVALID, "bad peer import");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    gs_p2p_close(ctx);
+    const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(handles_all);
+    std::vector<void*> S(world), R(world), F(world);
+    for (int w = 0; w < world; ++w) {
+        void** dst[3] = {&S[w], &R[w], &F[w]};
+        if (w == rank) {
+            S[w] = ctx->S.ptr; R[w] = ctx->p2p.R.ptr; F[w] = ctx->p2p.flags.ptr;
+            continue;
+        }
+        for (int k = 0; k < 3; ++k) {
+            GS_CUDA(cudaIpcOpenMemHandle(dst[k], h[3 * w + k], cudaIpcMemLazyEnablePeerAccess));
+            ctx->p2p.opened.push_back(*dst[k]);
+        }
+    }
+    return gs_p2p_set_peers(ctx, world, rank, S.data(), R.data(), F.data());
+}
+
+int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
+                 int64_t part_end, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers (gs_p2p_import / gs_p2p_set_peers)");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    {
+        auto& P = ctx->p2p;
+        if (P.epoch > 0)  // every rank's records of the previous stage are in S
+            k_p2p_wait<<<1, 1, 0, s>>>(P.flags.ptr, 1, P.epoch * (unsigned long long)P.world, P.timeout_ns);
+        int rc = pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, reinterpret_cast<double*>(P.R.ptr), stream);
+        if (rc) return rc;
+        k_p2p_signal<<<1, 32, 0, s>>>(P.Fp.ptr, P.world, 0);
+        ctx->launches += 2;
+    }
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_p2p_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers (gs_p2p_import / gs_p2p_set_peers)");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (stg < 0 || stg > 3 || step < 1) return fail(GS_ERR_INVALID, "bad stage index");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    auto& P = ctx->p2p;
+    k_p2p_wait<<<1, 1, 0, s>>>(P.flags.ptr, 0, (P.epoch + 1) * (unsigned long long)P.world, P.timeout_ns);
+    FinishArgs fa{};
+    fa.nrows = ctx->row1 - ctx->row0; fa.row0 = ctx->row0;
+    fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr; fa.stage = stg; fa.dt = dt; fa.st = ctx->st.ptr;
+    fa.event = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg + 1ull;
+    launch_finish_p2p(make_const(sys), fa, P.Rp.ptr, P.Sp.ptr, P.world, s);
+    k_p2p_signal<<<1, 32, 0, s>>>(P.Fp.ptr, P.world, 1);
+    P.epoch++;
+    ctx->launches += 3;
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_p2p_sync(gs_context* ctx, void* stream) {
+    if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    auto& P = ctx->p2p;
+    k_p2p_wait<<<1, 1, 0, (cudaStream_t)stream>>>(P.flags.ptr, 1, P.epoch * (unsigned long long)P.world,
+                                                   P.timeout_ns);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+int gs_p2p_timeouts(gs_context* ctx, int64_t* out) {
+    if (!ctx || !out) return fail(GS_ERR_INVALID, "NULL argument");
+    unsigned long long v = 0;
+    if (ctx->p2p.flags.ptr) {
+        GS_CUDA(cudaSetDevice(ctx->device));
+        GS_CUDA(cudaMemcpy(&v, ctx->p2p.flags.ptr + 2, sizeof(v), cudaMemcpyDeviceToHost));
+    }
+    *out = (int64_t)v;
     return GS_OK;
 }
 

@@ -228,6 +228,42 @@ void launch_velocity_field(const SysConst& sc, const double4* S, int64_t n, cons
 
 // ---------------------------------------------------------------------------------------
 // Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
+// RK4 stage epilogue of row li in the reference's evaluation order (integrator.py:98-114):
+//   stage inputs q + (0.5 dt) k_s, q + dt k_3; combine q + (dt/6) (((k1 + 2k2) + 2k3) + k4).
+// Updates the row's accumulator / base records and returns the next stage input.
+__device__ __forceinline__ double4 stage_update(const FinishArgs& a, int64_t li, double dqx, double dqy, double dpx,
+                                                double dpy) {
+    double4 b = a.B[li];
+    double4 acc;
+    double4 nxt;
+    if (a.stage == 0) {
+        acc = make_double4(dqx, dqy, dpx, dpy);
+    } else {
+        acc = a.A[li];
+        const double w = (a.stage == 3) ? 1.0 : 2.0;
+        acc.x = __dadd_rn(acc.x, __dmul_rn(w, dqx));
+        acc.y = __dadd_rn(acc.y, __dmul_rn(w, dqy));
+        acc.z = __dadd_rn(acc.z, __dmul_rn(w, dpx));
+        acc.w = __dadd_rn(acc.w, __dmul_rn(w, dpy));
+    }
+    if (a.stage < 3) {
+        const double c = (a.stage == 2) ? a.dt : 0.5 * a.dt;
+        nxt.x = __dadd_rn(b.x, __dmul_rn(c, dqx));
+        nxt.y = __dadd_rn(b.y, __dmul_rn(c, dqy));
+        nxt.z = __dadd_rn(b.z, __dmul_rn(c, dpx));
+        nxt.w = __dadd_rn(b.w, __dmul_rn(c, dpy));
+        a.A[li] = acc;
+    } else {
+        const double c = a.dt / 6.0;
+        nxt.x = __dadd_rn(b.x, __dmul_rn(c, acc.x));
+        nxt.y = __dadd_rn(b.y, __dmul_rn(c, acc.y));
+        nxt.z = __dadd_rn(b.z, __dmul_rn(c, acc.z));
+        nxt.w = __dadd_rn(b.w, __dmul_rn(c, acc.w));
+        a.B[li] = nxt;
+    }
+    return nxt;
+}
+
 // Partial sums are reduced by kFinGroups warps per 32 rows: warp w sums slots w, w + 8, ...
 // (coalesced over the rows), warp 0 adds the group sums in group order — a fixed order, and
 // 8x the parallelism of one thread per row walking all slots (the symmetric kernel leaves
@@ -285,36 +321,7 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish(SysConst sc, F
         a.ham[li] = __dadd_rn(__dmul_rn(me.z, sqx * sc.scale_q), __dmul_rn(me.w, sqy * sc.scale_q));
         return;
     }
-    // RK4 stage epilogue in the reference's evaluation order (integrator.py:98-114):
-    //   stage inputs q + (0.5 dt) k_s, q + dt k_3; combine q + (dt/6) (((k1 + 2k2) + 2k3) + k4)
-    double4 b = a.B[li];
-    double4 acc;
-    double4 nxt;
-    if (a.stage == 0) {
-        acc = make_double4(dqx, dqy, dpx, dpy);
-    } else {
-        acc = a.A[li];
-        const double w = (a.stage == 3) ? 1.0 : 2.0;
-        acc.x = __dadd_rn(acc.x, __dmul_rn(w, dqx));
-        acc.y = __dadd_rn(acc.y, __dmul_rn(w, dqy));
-        acc.z = __dadd_rn(acc.z, __dmul_rn(w, dpx));
-        acc.w = __dadd_rn(acc.w, __dmul_rn(w, dpy));
-    }
-    if (a.stage < 3) {
-        const double c = (a.stage == 2) ? a.dt : 0.5 * a.dt;
-        nxt.x = __dadd_rn(b.x, __dmul_rn(c, dqx));
-        nxt.y = __dadd_rn(b.y, __dmul_rn(c, dqy));
-        nxt.z = __dadd_rn(b.z, __dmul_rn(c, dpx));
-        nxt.w = __dadd_rn(b.w, __dmul_rn(c, dpy));
-        a.A[li] = acc;
-    } else {
-        const double c = a.dt / 6.0;
-        nxt.x = __dadd_rn(b.x, __dmul_rn(c, acc.x));
-        nxt.y = __dadd_rn(b.y, __dmul_rn(c, acc.y));
-        nxt.z = __dadd_rn(b.z, __dmul_rn(c, acc.z));
-        nxt.w = __dadd_rn(b.w, __dmul_rn(c, acc.w));
-        a.B[li] = nxt;
-    }
+    const double4 nxt = stage_update(a, li, dqx, dqy, dpx, dpy);
     a.S[i] = nxt;
     if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
 }
@@ -377,6 +384,41 @@ void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_
     FinishArgs a{};
     a.part = part; a.nchunks = nslots; a.pstride = pstride; a.nrows = n;
     k_slot_reduce<<<(unsigned)((n + kFinRows - 1) / kFinRows), finish_threads(nslots), 0, stream>>>(a, R);
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused stage exchange over peer memory (multi-GPU, symmetric split): the RK4 epilogue of this
+// rank's rows reads every rank's raw row sums through NVLink (rank order: deterministic) and
+// stores each finished 32-byte stage record straight into every rank's copy of S — the
+// reduce-scatter and the all-gather of the NCCL path, done by the epilogue itself.
+__global__ void __launch_bounds__(256) k_finish_p2p(SysConst sc, FinishArgs a, const double4* const* __restrict__ Rp,
+                                                    double4* const* __restrict__ Sp, int world) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= a.nrows) return;
+    if (*((volatile unsigned long long*)&a.st->first_event) < a.event) return;  // an earlier failure
+    const int64_t i = a.row0 + li;
+    double4 sum = Rp[0][i];
+    for (int w = 1; w < world; ++w) {
+        const double4 v = Rp[w][i];
+        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+    }
+    const double4 me = a.S[i];
+    double dqx = sum.x * sc.scale_q, dqy = sum.y * sc.scale_q;
+    if (sc.sigma2 != 0.0) {
+        dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
+        dqy = __dadd_rn(dqy, __dmul_rn(sc.sigma2, me.w));
+    }
+    const double dpx = sum.z * sc.scale_p, dpy = sum.w * sc.scale_p;
+    const double4 nxt = stage_update(a, li, dqx, dqy, dpx, dpy);
+    for (int w = 0; w < world; ++w) Sp[w][i] = nxt;
+    __threadfence_system();  // the stores reach the peers before this rank's "S written" signal
+    if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
+}
+
+void launch_finish_p2p(const SysConst& sc, const FinishArgs& a, const double4* const* Rp, double4* const* Sp,
+                       int world, cudaStream_t stream) {
+    if (a.nrows <= 0) return;
+    k_finish_p2p<<<(unsigned)((a.nrows + 255) / 256), 256, 0, stream>>>(sc, a, Rp, Sp, world);
 }
 
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream) {

@@ -91,6 +91,11 @@ struct FinishArgs {
     unsigned long long event;
 };
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream);
+// Stage epilogue of rows [row0, row0 + nrows) from the raw row sums of all `world` ranks
+// (Rp[w], full length, summed in rank order), storing each new stage record into Sp[w] of
+// every rank (peer memory).
+void launch_finish_p2p(const SysConst& sc, const FinishArgs& a, const double4* const* Rp, double4* const* Sp,
+                       int world, cudaStream_t stream);
 
 // Small-N persistent kernel: a whole evolve or a whole match per thread-block cluster
 // (n <= kSmallMax), see gs_small.cu.

@@ -60,13 +60,14 @@ def rhs_rows(spec, q, p, r0: int, r1: int):
 
 
 class DeviceStageBackend:
-    """gs_stage_* of libgs_b200.so on this rank's GPU."""
+    """gs_stage_* of libgs_b200.so on this rank's GPU (``ctx``: a library context, default the
+    process's context for the current device)."""
 
-    def __init__(self, spec):
+    def __init__(self, spec, ctx=None):
         import torch
 
         self.torch = torch
-        self.ctx = N.Context.get()
+        self.ctx = ctx or N.Context.get()
         self.sysc = device.system_struct(spec)
         self.n = 0
 
@@ -121,6 +122,47 @@ class DeviceStageBackend:
         N.check(self.ctx.lib.gs_status_fetch(self.ctx.handle, ctypes.byref(st), self._s()), "gs_status_fetch")
         return st
 
+    # -- fused stage exchange over peer memory (gs_p2p_*, opt-in) ---------------------------
+    supports_p2p = True
+
+    def state_ptr(self) -> int:
+        return int(self.ctx.lib.gs_stage_state(self.ctx.handle) or 0)
+
+    def p2p_local(self, rows_all: int):
+        """(S, R, counters) device pointers of this rank (counters zeroed)."""
+        ptr = [ctypes.c_void_p() for _ in range(3)]
+        N.check(self.ctx.lib.gs_p2p_local(self.ctx.handle, rows_all, *(ctypes.byref(x) for x in ptr)), "gs_p2p_local")
+        return tuple(int(x.value) for x in ptr)
+
+    def p2p_export(self, rows_all: int) -> bytes:
+        buf = ctypes.create_string_buffer(3 * 64)
+        N.check(self.ctx.lib.gs_p2p_export(self.ctx.handle, rows_all, buf), "gs_p2p_export")
+        return buf.raw
+
+    def p2p_import(self, world: int, rank: int, handles: bytes):
+        N.check(self.ctx.lib.gs_p2p_import(self.ctx.handle, world, rank, handles), "gs_p2p_import")
+
+    def p2p_set_peers(self, world: int, rank: int, S, R, F):
+        arr = ctypes.c_void_p * world
+        N.check(self.ctx.lib.gs_p2p_set_peers(self.ctx.handle, world, rank, arr(*S), arr(*R), arr(*F)),
+                "gs_p2p_set_peers")
+
+    def p2p_pairs(self, step: int, stage: int, b: int, e: int):
+        N.check(self.ctx.lib.gs_p2p_pairs(self.ctx.handle, ctypes.byref(self.sysc), step, stage, b, e, self._s()),
+                "gs_p2p_pairs")
+
+    def p2p_finish(self, step: int, stage: int, dt: float):
+        N.check(self.ctx.lib.gs_p2p_finish(self.ctx.handle, ctypes.byref(self.sysc), step, stage, dt, self._s()),
+                "gs_p2p_finish")
+
+    def p2p_sync(self):
+        N.check(self.ctx.lib.gs_p2p_sync(self.ctx.handle, self._s()), "gs_p2p_sync")
+
+    def p2p_timeouts(self) -> int:
+        v = ctypes.c_int64()
+        N.check(self.ctx.lib.gs_p2p_timeouts(self.ctx.handle, ctypes.byref(v)), "gs_p2p_timeouts")
+        return int(v.value)
+
 
 def _wrap_device_ptr(torch, ptr: int, shape):
     """Zero-copy float64 CUDA tensor over a library-owned device pointer."""
@@ -142,9 +184,15 @@ def _event_key(st) -> tuple:
 class ShardedSolver:
     """Row-sharded evolve / match across the ranks of ``group`` (default: the world)."""
 
-    def __init__(self, spec, backend=None, group=None, force_split: bool = False):
+    def __init__(self, spec, backend=None, group=None, force_split: bool = False, p2p: bool | None = None):
         """``force_split``: take the multi-rank code path (symmetric pair split, reduce-scatter,
-        all-gather) even in a world of one — lets a single GPU exercise the NCCL plumbing."""
+        all-gather) even in a world of one — lets a single GPU exercise the NCCL plumbing.
+        ``p2p`` (default: environment GS_B200_P2P=1): exchange the stage over peer memory
+        (gs_p2p_*: the epilogue reads every rank's row sums and stores the new records into every
+        rank's S over NVLink) instead of NCCL's reduce-scatter + all-gather; on any wait timeout
+        the evolve is redone on the NCCL path and peer exchange is switched off."""
+        import os
+
         import torch.distributed as dist
 
         self.spec = spec
@@ -154,6 +202,10 @@ class ShardedSolver:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.split = self.world > 1 or (force_split and dist.is_initialized())
+        if p2p is None:
+            p2p = os.environ.get("GS_B200_P2P", "0") == "1"
+        self.p2p = bool(p2p) and getattr(self.backend, "supports_p2p", False)
+        self._p2p_key = None
 
     # -- collectives (plumbing) -------------------------------------------------------------
     def _allgather_rows(self, S, r0: int, c: int):
@@ -213,6 +265,8 @@ class ShardedSolver:
             sym = total > 0
         if sym:
             b, e = self.rank * total // W, (self.rank + 1) * total // W
+            if self.p2p:
+                return self._evolve_p2p(q, p, t_final, steps, n, c, b, e, S)
             R = self.backend.new_partials(c * W)
             R_rows = self.backend.new_partials(c)
         for step in range(1, steps + 1):
@@ -224,6 +278,37 @@ class ShardedSolver:
                 else:
                     self.backend.run(step, s, dt)
                 self._allgather_rows(S, r0, c)
+        self._raise_first_failure(t_final, steps)
+        return S[:n, 0:2].clone(), S[:n, 2:4].clone()
+
+    def _p2p_setup(self, n: int, c: int):
+        """Exchange the ranks' buffer handles once per stage session (a collective)."""
+        key = (n, c, self.backend.state_ptr())
+        if self._p2p_key == key:
+            return
+        handles = self.backend.p2p_export(c * self.world)
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, handles, group=self.group)
+        self.backend.p2p_import(self.world, self.rank, b"".join(allh))
+        self.dist.barrier(group=self.group)
+        self._p2p_key = key
+
+    def _evolve_p2p(self, q, p, t_final, steps, n, c, b, e, S):
+        torch = _torch_of(self.backend)
+        self._p2p_setup(n, c)
+        before = self.backend.p2p_timeouts()
+        dt = t_final / steps
+        for step in range(1, steps + 1):
+            for s in range(4):
+                self.backend.p2p_pairs(step, s, b, e)
+                self.backend.p2p_finish(step, s, dt)
+        self.backend.p2p_sync()
+        lost = torch.tensor([float(self.backend.p2p_timeouts() - before)], dtype=torch.float64,
+                            device=_dev_of(self.backend))
+        self._allreduce(lost, self.dist.ReduceOp.MAX if self.world > 1 else None)
+        if float(lost[0]) > 0:  # a signal never arrived: redo this evolve on the NCCL path
+            self.p2p = False
+            return self.evolve(q, p, t_final, steps)
         self._raise_first_failure(t_final, steps)
         return S[:n, 0:2].clone(), S[:n, 2:4].clone()
 

@@ -166,3 +166,81 @@ def test_sharded_solver_nccl_code_path_world1(cuda):
     r = sharded.ShardedSolver(spec1, force_split=True).match(w.q, w.target, w.h, w.epsilon, w.max_iter, "residual",
                                                              "max", 1.0, w.steps)
     assert r["iterations"] == 36 and r["converged"]
+
+
+def _two_rank_emulation(n=5000, steps=3, only_rank0=False):
+    """Two library contexts on one GPU play ranks 0 and 1 of the peer-memory exchange, driven
+    in stream order (every wait is satisfied by work queued before it: nothing spins on a
+    kernel that has not run)."""
+    import torch
+
+    from paper_1510_03816_b200 import _native as N
+    from paper_1510_03816_b200 import sharded
+
+    gs, q, p, spec = _setup(n=n)
+    W = 2
+    c = (n + W - 1) // W
+    be = [sharded.DeviceStageBackend(spec, ctx=N.Context(0)) for _ in range(W)]
+    for r, b in enumerate(be):
+        r0, r1, _ = sharded.row_split(n, W, r)
+        b.begin(q, p, r0, r1)
+    ptrs = [b.p2p_local(c * W) for b in be]
+    S, R, F = ([x[k] for x in ptrs] for k in range(3))
+    for r, b in enumerate(be):
+        b.p2p_set_peers(W, r, S, R, F)
+    total = be[0].sym_parts()
+    ranges = [(r * total // W, (r + 1) * total // W) for r in range(W)]
+    dt = 1.0 / steps
+    active = be[:1] if only_rank0 else be
+    for step in range(1, steps + 1):
+        for s in range(4):
+            for r, b in enumerate(active):
+                b.p2p_pairs(step, s, *ranges[r])
+            for b in active:
+                b.p2p_finish(step, s, dt)
+    for b in active:
+        b.p2p_sync()
+    torch.cuda.synchronize()
+    return gs, q, p, spec, be
+
+
+def test_peer_exchange_two_ranks_emulated(cuda):
+    """gs_p2p_*: the fused epilogue + peer stores of two ranks reproduce the single-GPU evolve,
+    and both ranks end with identical full states."""
+    from paper_1510_03816_b200 import device
+
+    gs, q, p, spec, be = _two_rank_emulation()
+    n = q.shape[0]
+    SA, SB = be[0].state(n).clone(), be[1].state(n).clone()
+    assert be[0].p2p_timeouts() == 0 and be[1].p2p_timeouts() == 0
+    np.testing.assert_array_equal(SA.cpu().numpy(), SB.cpu().numpy())
+    q2, p2, _ = device.evolve(spec, q, p, 1.0, 3)
+    # the ranks' row sums are added in rank order instead of the one-GPU slot order: rounding only
+    assert rel(SA[:, 0:2].cpu().numpy(), q2.cpu().numpy()) <= 1e-13
+    assert rel(SA[:, 2:4].cpu().numpy(), p2.cpu().numpy()) <= 1e-11
+
+
+def test_peer_exchange_lost_signal_times_out(cuda, monkeypatch):
+    """A rank whose peer never signals gives up after the timeout (no hang) and counts it."""
+    monkeypatch.setenv("GS_B200_P2P_TIMEOUT_S", "0.02")
+    gs, q, p, spec, be = _two_rank_emulation(n=3000, steps=1, only_rank0=True)
+    assert be[0].p2p_timeouts() > 0
+
+
+def test_sharded_solver_peer_exchange_world1(cuda):
+    """ShardedSolver's peer-exchange path (handle export / import, pairs, fused finish, sync,
+    timeout agreement) in a one-process NCCL world."""
+    from paper_1510_03816_b200 import device, sharded
+
+    _nccl_world1()
+    gs, q, p, spec = _setup(n=5000)
+    solver = sharded.ShardedSolver(spec, force_split=True, p2p=True)
+    qT, pT = solver.evolve(q, p, 1.0, 4)
+    assert solver.p2p  # no timeout, still on the peer path
+    q2, p2, _ = device.evolve(spec, q, p, 1.0, 4)
+    assert rel(qT.cpu().numpy(), q2.cpu().numpy()) <= 1e-13
+    assert rel(pT.cpu().numpy(), p2.cpu().numpy()) <= 1e-13
+    qc = q.copy()
+    qc[7] = qc[3]
+    with pytest.raises(gs.DegenerateConfigurationError, match="particles 3 and 7 coincide"):
+        solver.evolve(qc, p, 1.0, 2)
