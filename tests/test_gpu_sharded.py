@@ -244,3 +244,45 @@ def test_sharded_solver_peer_exchange_world1(cuda):
     qc[7] = qc[3]
     with pytest.raises(gs.DegenerateConfigurationError, match="particles 3 and 7 coincide"):
         solver.evolve(qc, p, 1.0, 2)
+
+
+def _ipc_worker(rank, world, port, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1510_03816_b200 import sharded
+
+    gs, q, p, spec = _setup(n=2000)
+    be = sharded.DeviceStageBackend(spec)
+    r0, r1, c = sharded.row_split(2000, world, rank)
+    be.begin(q, p, r0, r1)
+    handles = be.p2p_export(c * world)
+    allh = [None] * world
+    dist.all_gather_object(allh, handles)
+    be.p2p_import(world, rank, b"".join(allh))  # opens the other process's buffers (CUDA IPC)
+    dist.barrier()
+    be.ctx.lib.gs_p2p_close(be.ctx.handle)
+    with open(f"{out}.{rank}", "w") as f:
+        f.write("ok")
+    dist.destroy_process_group()
+
+
+def test_peer_handles_open_across_processes(cuda, tmp_path):
+    """The IPC handle exchange of the peer-memory path between two processes (no kernel waits
+    on the other process: only the mapping is exercised)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "ipc")
+    mp.spawn(_ipc_worker, args=(2, port, out), nprocs=2, join=True)
+    for r in range(2):
+        assert open(f"{out}.{r}").read() == "ok"
