@@ -240,7 +240,7 @@ int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, in
 int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt,
                     const double* R_rows, void* stream);
 
-/* ---- fused stage exchange over peer memory (multi-GPU symmetric split, opt-in) ---------------
+/* ---- fused stage exchange over peer memory (multi-GPU symmetric split) ----------------------
  * Replaces the NCCL reduce-scatter + all-gather of a stage: the stage
  * epilogue of this rank's rows reads every rank's raw row sums over NVLink and stores each new
  * 32-byte stage record straight into every rank's S.  Per stage: gs_p2p_pairs (waits for the

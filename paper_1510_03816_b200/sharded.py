@@ -187,7 +187,7 @@ class ShardedSolver:
     def __init__(self, spec, backend=None, group=None, force_split: bool = False, p2p: bool | None = None):
         """``force_split``: take the multi-rank code path (symmetric pair split, reduce-scatter,
         all-gather) even in a world of one — lets a single GPU exercise the NCCL plumbing.
-        ``p2p`` (default: environment GS_B200_P2P=1): exchange the stage over peer memory
+        ``p2p`` (default: on when world > 1, see GS_B200_P2P): exchange the stage over peer memory
         (gs_p2p_*: the epilogue reads every rank's row sums and stores the new records into every
         rank's S over NVLink) instead of NCCL's reduce-scatter + all-gather; on any wait timeout
         the evolve is redone on the NCCL path and peer exchange is switched off."""
@@ -202,8 +202,9 @@ class ShardedSolver:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.split = self.world > 1 or (force_split and dist.is_initialized())
-        if p2p is None:
-            p2p = os.environ.get("GS_B200_P2P", "0") == "1"
+        if p2p is None:  # default: on across GPUs; GS_B200_P2P=0 switches it off, =1 forces it on
+            env = os.environ.get("GS_B200_P2P", "")
+            p2p = env == "1" or (env != "0" and self.world > 1)
         self.p2p = bool(p2p) and getattr(self.backend, "supports_p2p", False)
         self._p2p_key = None
 
@@ -265,10 +266,10 @@ class ShardedSolver:
             sym = total > 0
         if sym:
             b, e = self.rank * total // W, (self.rank + 1) * total // W
-            if self.p2p:
-                return self._evolve_p2p(q, p, t_final, steps, n, c, b, e, S)
             R = self.backend.new_partials(c * W)
             R_rows = self.backend.new_partials(c)
+            if self.p2p and self._p2p_ready(q, p, n, c, r0, r1, b, e, S, R, R_rows, dt):
+                return self._evolve_p2p(q, p, t_final, steps, n, c, b, e, S, r0, r1)
         for step in range(1, steps + 1):
             for s in range(4):
                 if sym:
@@ -281,21 +282,60 @@ class ShardedSolver:
         self._raise_first_failure(t_final, steps)
         return S[:n, 0:2].clone(), S[:n, 2:4].clone()
 
-    def _p2p_setup(self, n: int, c: int):
-        """Exchange the ranks' buffer handles once per stage session (a collective)."""
+    def _agree(self, ok: bool) -> bool:
+        """All ranks' verdict (MIN over ranks)."""
+        torch = _torch_of(self.backend)
+        t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=_dev_of(self.backend))
+        self._allreduce(t, self.dist.ReduceOp.MIN if self.world > 1 else None)
+        return float(t[0]) > 0.5
+
+    def _p2p_ready(self, q, p, n, c, r0, r1, b, e, S, R, R_rows, dt) -> bool:
+        """Once per stage session (a collective): exchange the ranks' buffer handles, then run
+        the first stage both ways — NCCL reduce-scatter + all-gather, and the peer-memory
+        exchange — from the same state and keep the peer path only if every rank got the same
+        records (1e-12) without a timeout.  Any failure switches peer exchange off everywhere."""
+        torch = _torch_of(self.backend)
         key = (n, c, self.backend.state_ptr())
         if self._p2p_key == key:
-            return
-        handles = self.backend.p2p_export(c * self.world)
+            return True
+        ok = True
+        try:
+            handles = self.backend.p2p_export(c * self.world)
+        except Exception:
+            ok, handles = False, b""
         allh = [None] * self.world
         self.dist.all_gather_object(allh, handles, group=self.group)
-        self.backend.p2p_import(self.world, self.rank, b"".join(allh))
-        self.dist.barrier(group=self.group)
+        ok = self._agree(ok and all(len(h) == len(handles) and h for h in allh))
+        if ok:
+            try:
+                self.backend.p2p_import(self.world, self.rank, b"".join(allh))
+            except Exception:
+                ok = False
+            ok = self._agree(ok)
+        if ok:  # one stage both ways from (q, p)
+            self.backend.pairs_sym(1, 0, b, e, R)
+            self._reduce_scatter_rows(R_rows, R, c)
+            self.backend.finish(1, 0, dt, R_rows)
+            self._allgather_rows(S, r0, c)
+            ref = S[:n].clone()
+            self.backend.begin(q, p, r0, r1)
+            before = self.backend.p2p_timeouts()
+            self.backend.p2p_pairs(1, 0, b, e)
+            self.backend.p2p_finish(1, 0, dt)
+            self.backend.p2p_sync()
+            got = S[:n]
+            scale = float(ref.abs().max()) or 1.0
+            same = bool(torch.isfinite(got).all()) and float((got - ref).abs().max()) <= 1e-12 * scale
+            ok = self._agree(same and self.backend.p2p_timeouts() == before)
+            self.backend.begin(q, p, r0, r1)
+        if not ok:
+            self.p2p = False
+            return False
         self._p2p_key = key
+        return True
 
-    def _evolve_p2p(self, q, p, t_final, steps, n, c, b, e, S):
+    def _evolve_p2p(self, q, p, t_final, steps, n, c, b, e, S, r0, r1):
         torch = _torch_of(self.backend)
-        self._p2p_setup(n, c)
         before = self.backend.p2p_timeouts()
         dt = t_final / steps
         for step in range(1, steps + 1):
