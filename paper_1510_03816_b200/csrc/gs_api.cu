@@ -83,6 +83,7 @@ struct gs_context {
         DevBuf<const double4*> Rp;
         DevBuf<double4*> Sp;
         DevBuf<unsigned long long*> Fp;
+        DevBuf<unsigned> done;           // block-completion counters of the signalling kernels
         std::vector<void*> opened;       // IPC mappings to close
         unsigned long long epoch = 0;    // stages completed since the peers were set
         long long timeout_ns = 10000000000ll;
@@ -651,7 +652,7 @@ int gs_destroy(gs_context* ctx) {
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     gs_p2p_close(ctx);
-    ctx->p2p.R.release(); ctx->p2p.flags.release(); ctx->p2p.Rp.release(); ctx->p2p.Sp.release(); ctx->p2p.Fp.release();
+    ctx->p2p.R.release(); ctx->p2p.flags.release(); ctx->p2p.done.release(); ctx->p2p.Rp.release(); ctx->p2p.Sp.release(); ctx->p2p.Fp.release();
     ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release(); ctx->sym_slots.release();
     ctx->sym_counts.release();
     delete ctx;
@@ -1143,7 +1144,8 @@ int64_t gs_sym_parts(int64_t n) {
 }
 
 static int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
-                          int64_t part_end, double* R, void* stream) {
+                          int64_t part_end, double* R, void* stream,
+                          PeerSignal sig = PeerSignal{nullptr, 0, 0, nullptr}) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || ctx->n < 1 || !R) return fail(GS_ERR_INVALID, "no stage session");
     int rc = check_system(sys);
@@ -1185,7 +1187,7 @@ static int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step,
                      part_end);
     if (ctx->prof_on) prof_mark(ctx, s);
     launch_slot_reduce_list(ctx->part.ptr, sp.pstride, n, sp.G * kDB, sp.nsb, ctx->sym_slots.ptr,
-                            ctx->sym_counts.ptr, reinterpret_cast<double4*>(R), s);
+                            ctx->sym_counts.ptr, reinterpret_cast<double4*>(R), s, sig);
     ctx->launches += 2;
     ctx->pair_launches++;
     ctx->host_pairs += (long long)((double)n * (double)n * (double)(part_end - part_begin) / (double)total);
@@ -1226,15 +1228,11 @@ int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32
 // so a lost signal costs a timeout, never a hang.
 namespace {
 
-__global__ void k_p2p_signal(unsigned long long* const* Fp, int world, int which) {
-    __threadfence_system();
-    if ((int)threadIdx.x < world) atomicAdd_system(Fp[threadIdx.x] + which, 1ull);
-}
-
 __global__ void k_p2p_wait(unsigned long long* flags, int which, unsigned long long target, long long timeout_ns) {
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (*((volatile unsigned long long*)&flags[which]) < target) {
+    while (*((volatile unsigned long long*)&flags[which]) < target &&
+           *((volatile unsigned long long*)&flags[2]) == 0) {  // after one timeout nobody waits
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if ((long long)(t - t0) > timeout_ns) {
             atomicAdd(&flags[2], 1ull);
@@ -1254,6 +1252,8 @@ int gs_p2p_local(gs_context* ctx, int64_t rows_all, void** S, void** R, void** f
     GS_CUDA(ctx->p2p.R.ensure(rows_all));
     GS_CUDA(ctx->p2p.flags.ensure(4));
     GS_CUDA(cudaMemset(ctx->p2p.flags.ptr, 0, 4 * sizeof(unsigned long long)));
+    GS_CUDA(ctx->p2p.done.ensure(2));
+    GS_CUDA(cudaMemset(ctx->p2p.done.ptr, 0, 2 * sizeof(unsigned)));
     *S = ctx->S.ptr; *R = ctx->p2p.R.ptr; *flags = ctx->p2p.flags.ptr;
     if (const char* e = std::getenv("GS_B200_P2P_TIMEOUT_S")) ctx->p2p.timeout_ns = (long long)(std::atof(e) * 1e9);
     return GS_OK;
@@ -1320,12 +1320,14 @@ int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
     GS_CUDA(cudaSetDevice(ctx->device));
     {
         auto& P = ctx->p2p;
-        if (P.epoch > 0)  // every rank's records of the previous stage are in S
+        if (P.epoch > 0) {  // every rank's records of the previous stage are in S
             k_p2p_wait<<<1, 1, 0, s>>>(P.flags.ptr, 1, P.epoch * (unsigned long long)P.world, P.timeout_ns);
-        int rc = pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, reinterpret_cast<double*>(P.R.ptr), stream);
+            ctx->launches++;
+        }
+        // the slot reduction's last CTA signals "sums ready" to every rank
+        int rc = pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, reinterpret_cast<double*>(P.R.ptr), stream,
+                                PeerSignal{P.Fp.ptr, P.world, 0, P.done.ptr});
         if (rc) return rc;
-        k_p2p_signal<<<1, 32, 0, s>>>(P.Fp.ptr, P.world, 0);
-        ctx->launches += 2;
     }
     GS_CUDA(cudaGetLastError());
     return GS_OK;
@@ -1339,15 +1341,16 @@ int gs_p2p_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t
     if (stg < 0 || stg > 3 || step < 1) return fail(GS_ERR_INVALID, "bad stage index");
     GS_CUDA(cudaSetDevice(ctx->device));
     auto& P = ctx->p2p;
-    k_p2p_wait<<<1, 1, 0, s>>>(P.flags.ptr, 0, (P.epoch + 1) * (unsigned long long)P.world, P.timeout_ns);
     FinishArgs fa{};
     fa.nrows = ctx->row1 - ctx->row0; fa.row0 = ctx->row0;
     fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr; fa.stage = stg; fa.dt = dt; fa.st = ctx->st.ptr;
     fa.event = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg + 1ull;
-    launch_finish_p2p(make_const(sys), fa, P.Rp.ptr, P.Sp.ptr, P.world, s);
-    k_p2p_signal<<<1, 32, 0, s>>>(P.Fp.ptr, P.world, 1);
+    // waits (every CTA) for all ranks' "sums ready", its last CTA signals "records written"
+    launch_finish_p2p(make_const(sys), fa, P.Rp.ptr, P.Sp.ptr, P.world,
+                      PeerWait{P.flags.ptr, 0, (P.epoch + 1) * (unsigned long long)P.world, P.timeout_ns},
+                      PeerSignal{P.Fp.ptr, P.world, 1, P.done.ptr + 1}, s);
     P.epoch++;
-    ctx->launches += 3;
+    ctx->launches++;
     GS_CUDA(cudaGetLastError());
     return GS_OK;
 }

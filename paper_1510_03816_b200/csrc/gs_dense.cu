@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce_list(cons
                                                                             int rows_per_sb, int nsb,
                                                                             const int* __restrict__ slots,
                                                                             const int* __restrict__ counts,
-                                                                            double4* R) {
+                                                                            double4* R, PeerSignal sig) {
     __shared__ double4 s_part[kFinGroups][kFinRows];
     const int r = threadIdx.x & (kFinRows - 1), w = threadIdx.x / kFinRows;
     const int64_t li = (int64_t)blockIdx.x * kFinRows + r;
@@ -357,21 +357,24 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce_list(cons
     }
     s_part[w][r] = acc;
     __syncthreads();
-    if (w != 0 || !valid) return;
-    const int ng = cnt < kFinGroups ? cnt : kFinGroups;
-    double4 sum = ng > 0 ? s_part[0][r] : make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int g = 1; g < ng; ++g) {
-        const double4 v = s_part[g][r];
-        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+    if (w == 0 && valid) {
+        const int ng = cnt < kFinGroups ? cnt : kFinGroups;
+        double4 sum = ng > 0 ? s_part[0][r] : make_double4(0.0, 0.0, 0.0, 0.0);
+        for (int g = 1; g < ng; ++g) {
+            const double4 v = s_part[g][r];
+            sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+        }
+        R[li] = sum;
     }
-    R[li] = sum;
+    block_signal_last(sig);
 }
 
 void launch_slot_reduce_list(const double4* part, int64_t pstride, int64_t n, int rows_per_sb, int nsb,
-                             const int* slots, const int* counts, double4* R, cudaStream_t stream) {
+                             const int* slots, const int* counts, double4* R, cudaStream_t stream,
+                             PeerSignal sig) {
     if (n <= 0) return;
     k_slot_reduce_list<<<(unsigned)((n + kFinRows - 1) / kFinRows), kFinRows * kFinGroups, 0, stream>>>(
-        part, pstride, n, rows_per_sb, nsb, slots, counts, R);
+        part, pstride, n, rows_per_sb, nsb, slots, counts, R, sig);
 }
 
 inline int finish_threads(int nchunks) {
@@ -392,33 +395,35 @@ void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_
 // stores each finished 32-byte stage record straight into every rank's copy of S — the
 // reduce-scatter and the all-gather of the NCCL path, done by the epilogue itself.
 __global__ void __launch_bounds__(256) k_finish_p2p(SysConst sc, FinishArgs a, const double4* const* __restrict__ Rp,
-                                                    double4* const* __restrict__ Sp, int world) {
+                                                    double4* const* __restrict__ Sp, int world, PeerWait wt,
+                                                    PeerSignal sig) {
+    block_wait(wt);  // every rank's row sums of this stage are in place
     const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (li >= a.nrows) return;
-    if (*((volatile unsigned long long*)&a.st->first_event) < a.event) return;  // an earlier failure
-    const int64_t i = a.row0 + li;
-    double4 sum = Rp[0][i];
-    for (int w = 1; w < world; ++w) {
-        const double4 v = Rp[w][i];
-        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+    if (li < a.nrows && !(*((volatile unsigned long long*)&a.st->first_event) < a.event)) {
+        const int64_t i = a.row0 + li;
+        double4 sum = Rp[0][i];
+        for (int w = 1; w < world; ++w) {
+            const double4 v = Rp[w][i];
+            sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+        }
+        const double4 me = a.S[i];
+        double dqx = sum.x * sc.scale_q, dqy = sum.y * sc.scale_q;
+        if (sc.sigma2 != 0.0) {
+            dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
+            dqy = __dadd_rn(dqy, __dmul_rn(sc.sigma2, me.w));
+        }
+        const double dpx = sum.z * sc.scale_p, dpy = sum.w * sc.scale_p;
+        const double4 nxt = stage_update(a, li, dqx, dqy, dpx, dpy);
+        for (int w = 0; w < world; ++w) Sp[w][i] = nxt;
+        if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
     }
-    const double4 me = a.S[i];
-    double dqx = sum.x * sc.scale_q, dqy = sum.y * sc.scale_q;
-    if (sc.sigma2 != 0.0) {
-        dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
-        dqy = __dadd_rn(dqy, __dmul_rn(sc.sigma2, me.w));
-    }
-    const double dpx = sum.z * sc.scale_p, dpy = sum.w * sc.scale_p;
-    const double4 nxt = stage_update(a, li, dqx, dqy, dpx, dpy);
-    for (int w = 0; w < world; ++w) Sp[w][i] = nxt;
-    __threadfence_system();  // the stores reach the peers before this rank's "S written" signal
-    if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
+    block_signal_last(sig);  // after the last CTA's stores: "records written" to every rank
 }
 
 void launch_finish_p2p(const SysConst& sc, const FinishArgs& a, const double4* const* Rp, double4* const* Sp,
-                       int world, cudaStream_t stream) {
-    if (a.nrows <= 0) return;
-    k_finish_p2p<<<(unsigned)((a.nrows + 255) / 256), 256, 0, stream>>>(sc, a, Rp, Sp, world);
+                       int world, PeerWait wait, PeerSignal sig, cudaStream_t stream) {
+    const int64_t rows = a.nrows > 0 ? a.nrows : 1;  // one CTA at least: it carries the signal
+    k_finish_p2p<<<(unsigned)((rows + 255) / 256), 256, 0, stream>>>(sc, a, Rp, Sp, world, wait, sig);
 }
 
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream) {

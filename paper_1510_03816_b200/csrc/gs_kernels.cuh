@@ -52,9 +52,61 @@ void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* 
                       long long cta1 = -1);
 // R[i] = sum over slots of part[slot * pstride + i] (fixed order), i < n.
 void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream);
-// The same over the slots listed per row superblock (a rank's share of the superblock pairs).
+// Peer-memory signalling fused into kernels (gs_p2p_*).  PeerWait: every CTA waits until its
+// own counter flags[which] reaches target (gives up after timeout_ns, counted in flags[2]; once
+// a timeout happened nobody waits any more).  PeerSignal: the last CTA to finish adds 1 to
+// counter `which` of every rank (system-scope, after a system fence), using `done` (zero
+// between launches) to detect it.  A null pointer disables either.
+struct PeerWait {
+    unsigned long long* flags;
+    int which;
+    unsigned long long target;
+    long long timeout_ns;
+};
+struct PeerSignal {
+    unsigned long long* const* Fp;
+    int world, which;
+    unsigned int* done;
+};
+
+__device__ __forceinline__ void block_wait(const PeerWait& w) {
+    if (!w.flags) return;
+    if (threadIdx.x == 0) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (*((volatile unsigned long long*)&w.flags[w.which]) < w.target &&
+               *((volatile unsigned long long*)&w.flags[2]) == 0) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if ((long long)(t - t0) > w.timeout_ns) {
+                atomicAdd(&w.flags[2], 1ull);
+                break;
+            }
+            __nanosleep(128);
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void block_signal_last(const PeerSignal& s) {
+    if (!s.Fp) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // this CTA's stores (local and peer) are visible system-wide
+        const unsigned prev = atomicAdd(s.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *s.done = 0;
+            __threadfence_system();
+            for (int r = 0; r < s.world; ++r) atomicAdd_system(s.Fp[r] + s.which, 1ull);
+        }
+    }
+}
+
+// The same over the slots listed per row superblock (a rank's share of the superblock pairs);
+// `sig` (optional) signals the peers once all of R is written.
 void launch_slot_reduce_list(const double4* part, int64_t pstride, int64_t n, int rows_per_sb, int nsb,
-                             const int* slots, const int* counts, double4* R, cudaStream_t stream);
+                             const int* slots, const int* counts, double4* R, cudaStream_t stream,
+                             PeerSignal sig = PeerSignal{nullptr, 0, 0, nullptr});
 // Superblock pair (SI, SJ), SI <= SJ, of work item t (row-major over the upper triangle).
 void sym_pair_of(long long t, int nsb, long long* SI, long long* SJ);
 
@@ -95,7 +147,7 @@ void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream
 // (Rp[w], full length, summed in rank order), storing each new stage record into Sp[w] of
 // every rank (peer memory).
 void launch_finish_p2p(const SysConst& sc, const FinishArgs& a, const double4* const* Rp, double4* const* Sp,
-                       int world, cudaStream_t stream);
+                       int world, PeerWait wait, PeerSignal sig, cudaStream_t stream);
 
 // Small-N persistent kernel: a whole evolve or a whole match per thread-block cluster
 // (n <= kSmallMax), see gs_small.cu.
