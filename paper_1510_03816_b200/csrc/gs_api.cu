@@ -1145,7 +1145,8 @@ int64_t gs_sym_parts(int64_t n) {
 
 static int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
                           int64_t part_end, double* R, void* stream,
-                          PeerSignal sig = PeerSignal{nullptr, 0, 0, nullptr}) {
+                          PeerSignal sig = PeerSignal{nullptr, 0, 0, nullptr},
+                          PeerWait wait = PeerWait{nullptr, 0, 0, 0}) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || ctx->n < 1 || !R) return fail(GS_ERR_INVALID, "no stage session");
     int rc = check_system(sys);
@@ -1184,7 +1185,7 @@ static int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step,
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg;
     if (ctx->prof_on) prof_mark(ctx, s);
     launch_dense_sym(sc, ctx->S.ptr, n, ctx->part.ptr, sp.pstride, ctx->st.ptr, ev, ctx->tbl.ptr, s, part_begin,
-                     part_end);
+                     part_end, wait);
     if (ctx->prof_on) prof_mark(ctx, s);
     launch_slot_reduce_list(ctx->part.ptr, sp.pstride, n, sp.G * kDB, sp.nsb, ctx->sym_slots.ptr,
                             ctx->sym_counts.ptr, reinterpret_cast<double4*>(R), s, sig);
@@ -1320,11 +1321,13 @@ int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
     GS_CUDA(cudaSetDevice(ctx->device));
     {
         auto& P = ctx->p2p;
-        if (P.epoch > 0) {  // every rank's records of the previous stage are in S
+        // one waiting thread for every rank's records of the previous stage (waiting in each of
+        // the pair kernel's thousands of CTAs cost more: 164.8 vs 159.5 ms per C2 solve), then
+        // the pairs; the slot reduction's last CTA signals "sums ready" to every rank
+        if (P.epoch > 0) {
             k_p2p_wait<<<1, 1, 0, s>>>(P.flags.ptr, 1, P.epoch * (unsigned long long)P.world, P.timeout_ns);
             ctx->launches++;
         }
-        // the slot reduction's last CTA signals "sums ready" to every rank
         int rc = pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, reinterpret_cast<double*>(P.R.ptr), stream,
                                 PeerSignal{P.Fp.ptr, P.world, 0, P.done.ptr});
         if (rc) return rc;

@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* 
     __shared__ double s_tbl[kTblWords];
     __shared__ int s_list[kCL][kCB];
     __shared__ unsigned long long s_acc_count;
-    if (*((volatile unsigned long long*)&st->first_event) < event) return;
+    // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
     for (int t = threadIdx.x; t < kTblWords; t += kCB) s_tbl[t] = tbl_g[t];
     const double* tbl = lane_table(s_tbl);
     if (threadIdx.x == 0) s_acc_count = 0;

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kDPT, 12) k_dense_partial(const double4* __res
                                                             unsigned long long event, const double* __restrict__ tbl_g) {
     __shared__ double s_tbl[kTblWords];
     __shared__ double4 s_src[kDT];
-    if (*((volatile unsigned long long*)&st->first_event) < event) return;  // an earlier failure
+    // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
     for (int t = threadIdx.x; t < kTblWords; t += kDPT) s_tbl[t] = tbl_g[t];
     const double* tbl = lane_table(s_tbl);
 

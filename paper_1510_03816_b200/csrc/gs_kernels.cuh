@@ -33,25 +33,6 @@ void launch_dense_partial(const SysConst& sc, const double4* S, int64_t n, int64
                           const DensePlan& plan, double4* part, DevStatus* st, unsigned long long event,
                           const double* tbl_dev, cudaStream_t stream);
 
-// Symmetric all-pairs RHS of all n rows (single rank, gs_sym.cu): each unordered pair once;
-// row i gets nsb partials part[slot * pstride + i], pstride = nb * kDB.
-constexpr int kSymMaxG = 8;  // 8 blocks per superblock: symmetric dense up to N = 256 * 8 * 128 = 262144
-struct SymPlan {
-    int nb;           // 128-row blocks
-    int G;            // blocks per superblock
-    int nsb;          // superblocks = partial slots per row
-    int64_t pstride;  // nb * kDB
-    bool ok;          // partial buffer stays bounded (nsb <= 256)
-};
-SymPlan sym_plan(int64_t n);
-long long sym_ctas(int64_t n);  // work items (superblock pairs) of one symmetric RHS
-// CTAs [cta0, cta1) of the superblock-pair list (cta1 < 0: all).  A multi-GPU rank runs its
-// share of the list; the slots of the other ranks' items must be zero in `part`.
-void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
-                      unsigned long long event, const double* tbl_dev, cudaStream_t stream, long long cta0 = 0,
-                      long long cta1 = -1);
-// R[i] = sum over slots of part[slot * pstride + i] (fixed order), i < n.
-void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream);
 // Peer-memory signalling fused into kernels (gs_p2p_*).  PeerWait: every CTA waits until its
 // own counter flags[which] reaches target (gives up after timeout_ns, counted in flags[2]; once
 // a timeout happened nobody waits any more).  PeerSignal: the last CTA to finish adds 1 to
@@ -102,6 +83,25 @@ __device__ __forceinline__ void block_signal_last(const PeerSignal& s) {
     }
 }
 
+// Symmetric all-pairs RHS of all n rows (single rank, gs_sym.cu): each unordered pair once;
+// row i gets nsb partials part[slot * pstride + i], pstride = nb * kDB.
+constexpr int kSymMaxG = 8;  // 8 blocks per superblock: symmetric dense up to N = 256 * 8 * 128 = 262144
+struct SymPlan {
+    int nb;           // 128-row blocks
+    int G;            // blocks per superblock
+    int nsb;          // superblocks = partial slots per row
+    int64_t pstride;  // nb * kDB
+    bool ok;          // partial buffer stays bounded (nsb <= 256)
+};
+SymPlan sym_plan(int64_t n);
+long long sym_ctas(int64_t n);  // work items (superblock pairs) of one symmetric RHS
+// CTAs [cta0, cta1) of the superblock-pair list (cta1 < 0: all).  A multi-GPU rank runs its
+// share of the list; the slots of the other ranks' items must be zero in `part`.
+void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
+                      unsigned long long event, const double* tbl_dev, cudaStream_t stream, long long cta0 = 0,
+                      long long cta1 = -1, PeerWait wait = PeerWait{nullptr, 0, 0, 0});
+// R[i] = sum over slots of part[slot * pstride + i] (fixed order), i < n.
+void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream);
 // The same over the slots listed per row superblock (a rank's share of the superblock pairs);
 // `sig` (optional) signals the peers once all of R is written.
 void launch_slot_reduce_list(const double4* part, int64_t pstride, int64_t n, int rows_per_sb, int nsb,

@@ -96,11 +96,13 @@ template <int FAM>
 __global__ void __launch_bounds__(kST, GS_SYM_MINB) k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, int G,
                                                        int nsb, long long cta0, double k1, double4* __restrict__ part,
                                                        int64_t pstride, DevStatus* st, unsigned long long event,
-                                                       const double* __restrict__ tbl_g) {
+                                                       const double* __restrict__ tbl_g, PeerWait wait) {
     __shared__ double s_tbl[kTblWords];
     __shared__ double4 s_rot[4][64];     // sub-block b of J twice: s_rot[b][k] = record 32 b + (k & 31)
     extern __shared__ double4 s_acc[];   // G * kDB records
-    if (*((volatile unsigned long long*)&st->first_event) < event) return;
+    // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
+    block_wait(wait);  // multi-GPU peer exchange: every rank's records of the previous stage are in S
     for (int t = threadIdx.x; t < kTblWords; t += kST) s_tbl[t] = tbl_g[t];
     const double* tbl = lane_table(s_tbl);
 
@@ -256,7 +258,7 @@ long long sym_ctas(int64_t n) {
 
 void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* part, int64_t pstride, DevStatus* st,
                       unsigned long long event, const double* tbl_dev, cudaStream_t stream, long long cta0,
-                      long long cta1) {
+                      long long cta1, PeerWait wait) {
     const SymPlan p = sym_plan(n);
     if (cta1 < 0) cta1 = sym_ctas(n);
     if (cta1 <= cta0) return;
@@ -264,10 +266,10 @@ void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* 
     const size_t smem = (size_t)p.G * kDB * sizeof(double4);
     if (sc.fam == kFamConical)
         k_dense_sym<kFamConical><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, cta0, sc.k1, part, pstride, st,
-                                                              event, tbl_dev);
+                                                              event, tbl_dev, wait);
     else
         k_dense_sym<kFamGaussian><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, cta0, sc.k1, part, pstride,
-                                                               st, event, tbl_dev);
+                                                               st, event, tbl_dev, wait);
 }
 
 }  // namespace gsb
