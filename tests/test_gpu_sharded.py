@@ -168,17 +168,16 @@ def test_sharded_solver_nccl_code_path_world1(cuda):
     assert r["iterations"] == 36 and r["converged"]
 
 
-def _two_rank_emulation(n=5000, steps=3, only_rank0=False):
-    """Two library contexts on one GPU play ranks 0 and 1 of the peer-memory exchange, driven
-    in stream order (every wait is satisfied by work queued before it: nothing spins on a
-    kernel that has not run)."""
+def _two_rank_emulation(n=5000, steps=3, only_rank0=False, W=2):
+    """W library contexts on one GPU play the ranks of the peer-memory exchange, driven in
+    stream order (every wait is satisfied by work queued before it: nothing spins on a kernel
+    that has not run)."""
     import torch
 
     from paper_1510_03816_b200 import _native as N
     from paper_1510_03816_b200 import sharded
 
     gs, q, p, spec = _setup(n=n)
-    W = 2
     c = (n + W - 1) // W
     be = [sharded.DeviceStageBackend(spec, ctx=N.Context(0)) for _ in range(W)]
     for r, b in enumerate(be):
@@ -204,16 +203,17 @@ def _two_rank_emulation(n=5000, steps=3, only_rank0=False):
     return gs, q, p, spec, be
 
 
-def test_peer_exchange_two_ranks_emulated(cuda):
-    """gs_p2p_*: the fused epilogue + peer stores of two ranks reproduce the single-GPU evolve,
-    and both ranks end with identical full states."""
+@pytest.mark.parametrize("W,n", [(2, 5000), (3, 4999)])
+def test_peer_exchange_two_ranks_emulated(cuda, W, n):
+    """gs_p2p_*: the fused epilogue + peer stores of W ranks (uneven split for W = 3) reproduce
+    the single-GPU evolve, and all ranks end with identical full states."""
     from paper_1510_03816_b200 import device
 
-    gs, q, p, spec, be = _two_rank_emulation()
-    n = q.shape[0]
-    SA, SB = be[0].state(n).clone(), be[1].state(n).clone()
-    assert be[0].p2p_timeouts() == 0 and be[1].p2p_timeouts() == 0
-    np.testing.assert_array_equal(SA.cpu().numpy(), SB.cpu().numpy())
+    gs, q, p, spec, be = _two_rank_emulation(n=n, W=W)
+    SA = be[0].state(n).clone()
+    for b in be:
+        assert b.p2p_timeouts() == 0
+        np.testing.assert_array_equal(b.state(n).cpu().numpy(), SA.cpu().numpy())
     q2, p2, _ = device.evolve(spec, q, p, 1.0, 3)
     # the ranks' row sums are added in rank order instead of the one-GPU slot order: rounding only
     assert rel(SA[:, 0:2].cpu().numpy(), q2.cpu().numpy()) <= 1e-13
