@@ -312,7 +312,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (BASELINE configs[1] recipe: uniform [0,1]^2 seed 0, N(0,0.01^2) seed 1)",
-            "config": dict(arm_config(a, w.n), parallelism=f"rows{world}",
+            "config": dict(arm_config(a, w.n), parallelism=(
+                f"rows{world}" if solver is None else
+                f"{'pair-split' if a.path == 'dense' else 'rows'}{world}+{'p2p' if solver.p2p else 'nccl'}"),
                            l2="flushed between timed steps (256 MB write)"),
             "roofline": {"bound": "fp64", "achieved": ach_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach_tflops / peak if peak else None, "traffic": traffic,
