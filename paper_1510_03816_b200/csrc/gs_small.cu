@@ -29,6 +29,12 @@ constexpr unsigned kFull = 0xffffffffu;
 #define GS_SMALL_UNROLL 4
 #endif
 constexpr int kSmallUnroll = GS_SMALL_UNROLL;
+#ifndef GS_SMALL_ASYNC       // per-stage exchange by st.async + mbarriers (A/B: 0 = cluster barriers)
+#define GS_SMALL_ASYNC 1
+#endif
+#ifndef GS_CLUSTER_PTX_BAR   // explicit aligned cluster barrier instead of cg::this_cluster().sync() (A/B)
+#define GS_CLUSTER_PTX_BAR 1
+#endif
 constexpr int kWarps = kSmallThreads / 32;
 
 // Shared memory of the kernel at file scope, so the helpers address it directly instead of
@@ -41,6 +47,7 @@ __shared__ unsigned long long s_kslot[2 * kMaxCluster];  // coincidence keys, by
 __shared__ int s_bslot[2 * kMaxCluster];                 // non-finite flags, by barrier parity
 __shared__ unsigned long long s_key[3];                  // this CTA's rotating coincidence keys
 __shared__ SmallItem s_item;                             // this item's constants (read on demand)
+__shared__ __align__(8) unsigned long long s_mbar[2];    // per next-stage buffer: DSMEM arrivals
 
 template <int CL>
 struct SmallCtx {
@@ -49,20 +56,84 @@ struct SmallCtx {
     int n, split, tgt, sub;
     bool act;              // this thread's row exists and is owned by this CTA
     int parity;            // slot parity (flips at every cluster barrier that uses slots)
+    unsigned ph[2];        // phase parity of s_mbar[0 / 1] (identical in every thread and CTA)
 };
 
 __device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
 
 template <class Ctx>
 __device__ __forceinline__ void cluster_sync(const Ctx& c) {
-    if constexpr (Ctx::C > 1) cg::this_cluster().sync();
-    else __syncthreads();
+    if constexpr (Ctx::C > 1) {
+#if GS_CLUSTER_PTX_BAR
+        // all threads arrive (release: this CTA's DSMEM / shared stores become visible to the
+        // cluster) and wait (acquire); the .aligned forms: every thread executes them together
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#else
+        cg::this_cluster().sync();
+#endif
+    } else {
+        __syncthreads();
+    }
 }
 
 template <class Ctx, typename T>
 __device__ __forceinline__ T* remote(const Ctx& c, T* p, int r) {
     if constexpr (Ctx::C > 1) return cg::this_cluster().map_shared_rank(p, r);
     else return p;
+}
+
+// ---- DSMEM transfers tracked by mbarriers (the per-stage exchange, C > 1) -----------------
+// A stage's records and flags go to every CTA with st.async, each store counted in bytes on
+// the receiving CTA's mbarrier of that buffer (complete_tx); a CTA proceeds when its barrier
+// has seen all n x 32 + C x 12 bytes — no cluster-wide barrier and none of its GPU-scope
+// fences / L1 invalidation per stage.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 5000000000ull) __trap();  // a lost transfer: fail the launch, never hang
+    }
+}
+
+__device__ __forceinline__ void st_async_rec(uint32_t raddr, const double4& v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr), "d"(v.x), "d"(v.y), "r"(rbar) : "memory");
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr + 16), "d"(v.z), "d"(v.w), "r"(rbar) : "memory");
+}
+
+__device__ __forceinline__ void st_async_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(raddr), "l"(v), "r"(rbar) : "memory");
+}
+
+__device__ __forceinline__ void st_async_u32(uint32_t raddr, unsigned v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 ::"r"(raddr), "r"(v), "r"(rbar) : "memory");
 }
 
 // Stores this row's record into buf[tgt] of every CTA of the cluster (the row's lanes share
@@ -220,25 +291,49 @@ __device__ unsigned long long small_evolve(Ctx& c, const SysConst& sc, double4& 
                 nxt.w = __dadd_rn(b.w, __dmul_rn(cc, acc.w));
                 b = nxt;
             }
-            bcast_row(c, Sn, nxt);
-            const int bad = __syncthreads_or(c.act && !finite4(nxt.x, nxt.y, nxt.z, nxt.w));
-            unsigned long long kmin = *key;
-            int anybad = bad;
-            if constexpr (Ctx::C > 1) {  // this CTA's key and flag into every CTA's slots, then the cluster's
+            unsigned long long kmin;
+            int anybad;
+            if constexpr (Ctx::C > 1) {
+#if GS_SMALL_ASYNC
+                // records and flags to every CTA by st.async, counted on its mbarrier of buffer nb
+                const int nb = cur ^ 1;
+                unsigned long long* bar = &s_mbar[nb];
+                if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(c.n * 32 + Ctx::C * 12));
+                if (c.act)
+                    for (int r = c.sub; r < Ctx::C; r += c.split)
+                        st_async_rec(mapa_u32(smem_u32(&Sn[c.tgt]), r), nxt, mapa_u32(smem_u32(bar), r));
+                const int bad = __syncthreads_or(c.act && !finite4(nxt.x, nxt.y, nxt.z, nxt.w));
+                unsigned long long* ks = s_kslot + nb * kMaxCluster;
+                int* bs = s_bslot + nb * kMaxCluster;
+                if (threadIdx.x < (unsigned)Ctx::C) {
+                    const uint32_t rb = mapa_u32(smem_u32(bar), (int)threadIdx.x);
+                    st_async_u64(mapa_u32(smem_u32(&ks[c.rank]), (int)threadIdx.x), *key, rb);
+                    st_async_u32(mapa_u32(smem_u32(&bs[c.rank]), (int)threadIdx.x), (unsigned)bad, rb);
+                }
+                mbar_wait(bar, c.ph[nb]);
+                c.ph[nb] ^= 1u;
+#else
+                bcast_row(c, Sn, nxt);
+                const int bad = __syncthreads_or(c.act && !finite4(nxt.x, nxt.y, nxt.z, nxt.w));
                 unsigned long long* ks = s_kslot + c.parity * kMaxCluster;
                 int* bs = s_bslot + c.parity * kMaxCluster;
                 if (threadIdx.x < (unsigned)c.C) {
-                    remote(c, ks, (int)threadIdx.x)[c.rank] = kmin;
+                    remote(c, ks, (int)threadIdx.x)[c.rank] = *key;
                     remote(c, bs, (int)threadIdx.x)[c.rank] = bad;
                 }
                 cluster_sync(c);
                 c.parity ^= 1;
+#endif
                 kmin = ks[0];
                 anybad = bs[0];
                 for (int r = 1; r < c.C; ++r) {
                     kmin = ks[r] < kmin ? ks[r] : kmin;
                     anybad |= bs[r];
                 }
+            } else {
+                bcast_row(c, Sn, nxt);
+                anybad = __syncthreads_or(c.act && !finite4(nxt.x, nxt.y, nxt.z, nxt.w));
+                kmin = *key;
             }
             if (threadIdx.x == 0) s_key[(k + 2) % 3] = kNoEvent;  // stage k - 1's slot, next used by k + 2
             if (kmin != kNoEvent) {
@@ -308,6 +403,11 @@ template <int FAM, int CL>
 __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const double* __restrict__ tbl_g) {
     for (int t = threadIdx.x; t < kTblWords; t += blockDim.x) s_tbl[t] = tbl_g[t];
     if (threadIdx.x < 3) s_key[threadIdx.x] = kNoEvent;
+    if (CL > 1 && threadIdx.x == 0) {  // DSMEM arrival barriers, visible to the cluster after its first sync
+        mbar_init(&s_mbar[0]);
+        mbar_init(&s_mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     constexpr int C = CL;
     const int64_t b = blockIdx.x / C;  // the item this cluster runs
@@ -315,7 +415,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a, const doub
     __syncthreads();
     const SmallItem& item = s_item;
     const SysConst& sc = item.sc;
-    SmallCtx<CL> c; c.rank = (int)(blockIdx.x % C); c.parity = 0;
+    SmallCtx<CL> c;
+    c.ph[0] = 0; c.ph[1] = 0; c.rank = (int)(blockIdx.x % C); c.parity = 0;
     c.n = (int)a.n; c.split = a.split;
     const int R = (c.n + C - 1) / C;
     const int tl = threadIdx.x / a.split;
