@@ -545,7 +545,23 @@ int small_threads(int64_t n, int cluster, int* split_out) {
     return (int)(((rows * split) + 31) / 32 * 32);
 }
 
+static int launch_small_cluster(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream);
+
+// A cluster launch the device cannot place (shared memory / cluster resources) falls back to
+// one CTA per item: same results to rounding, never a failed match.
 int launch_small(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream) {
+    int rc = launch_small_cluster(fam, a, tbl_dev, stream);
+    if (rc != 0 && a.cluster > 1) {
+        (void)cudaGetLastError();
+        SmallArgs b = a;
+        b.cluster = 1;
+        small_threads(b.n, 1, &b.split);
+        rc = launch_small_cluster(fam, b, tbl_dev, stream);
+    }
+    return rc;
+}
+
+static int launch_small_cluster(int fam, const SmallArgs& a, const double* tbl_dev, cudaStream_t stream) {
     int split = 0;
     const int threads = small_threads(a.n, a.cluster, &split);
     if (split != a.split) return (int)cudaErrorInvalidValue;
