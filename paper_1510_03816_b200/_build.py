@@ -19,8 +19,9 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libgs_b200.so")
-SOURCES = ["gs_dense.cu", "gs_sym.cu", "gs_small.cu", "gs_cell.cu", "gs_api.cu"]
-HEADERS = ["gs_device.cuh", "gs_kernels.cuh", "gs_cell.cuh", os.path.join("..", "..", "include", "geoshoot_b200.h")]
+SOURCES = ["gs_dense.cu", "gs_sym.cu", "gs_small.cu", "gs_cell.cu", "gs_api.cu", "gs_batch.cu", "gs_p2p.cu"]
+HEADERS = ["gs_device.cuh", "gs_kernels.cuh", "gs_cell.cuh", "gs_context.cuh",
+           os.path.join("..", "..", "include", "geoshoot_b200.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

@@ -1,23 +1,17 @@
-// gs_api.cu — C ABI of libgs_b200.so (include/geoshoot_b200.h).
+// gs_api.cu — C ABI of libgs_b200.so (include/geoshoot_b200.h): context, RHS, Hamiltonian,
+// velocity field, evolve, match, Gram matrix, stage API, profiling.
 //
 // Host-side orchestration of the device path: argument validation with the reference's
-// error contract, workspaces owned by an opaque context, the RK4 stage loop
-// (integrator.py:95-119) and the feedback loop (shooting.py:259-301, momentum update).
-// The numerics all run in the kernels of gs_dense.cu / gs_small.cu / gs_cell.cu.
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include "../../include/geoshoot_b200.h"
-#include "gs_cell.cuh"
-#include "gs_kernels.cuh"
+// error contract, workspaces owned by an opaque context (gs_context.cuh), the RK4 stage loop
+// (integrator.py:95-119) and the feedback loop (shooting.py:259-301).  The numerics all run in
+// the kernels of gs_dense.cu / gs_sym.cu / gs_small.cu / gs_cell.cu; batched trajectories are in
+// gs_batch.cu, the multi-GPU peer-memory exchange in gs_p2p.cu.
+#include "gs_context.cuh"
 
 using namespace gsb;
+using namespace gsapi;
 
-namespace {
+namespace gsapi {
 
 thread_local std::string g_last_error;
 
@@ -26,105 +20,7 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
-#define GS_CUDA(call)                                                                                   \
-    do {                                                                                                \
-        cudaError_t e_ = (call);                                                                        \
-        if (e_ != cudaSuccess)                                                                          \
-            return fail(GS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));               \
-    } while (0)
 
-template <typename T>
-struct DevBuf {
-    T* ptr = nullptr;
-    size_t cap = 0;  // elements
-    cudaError_t ensure(size_t n) {
-        if (n <= cap) return cudaSuccess;
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        cap = 0;
-        cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
-        if (e == cudaSuccess) cap = n;
-        return e;
-    }
-    void release() {
-        if (ptr) cudaFree(ptr);
-        ptr = nullptr;
-        cap = 0;
-    }
-};
-
-}  // namespace
-
-struct gs_context {
-    int device = 0;
-    int sm_count = 148;
-    DevBuf<double> tbl;
-    DevBuf<DevStatus> st;
-    DevStatus* st_host = nullptr;   // pinned
-    double* scal_host = nullptr;    // pinned scratch (16 doubles)
-    // stage session
-    DevBuf<double4> S, B, A, part;
-    int64_t n = 0, row0 = 0, row1 = 0;
-    // match / reductions
-    DevBuf<double> q0, tgt, p, resid, red, ham, hist, scal;
-    DevBuf<SmallResult> small_res;
-    DevBuf<SmallItem> b_items;       // batched launches: per-item constants
-    DevBuf<DevStatus> b_st;          // batched evolve: per-item failure records
-    DevBuf<double2> vf_part;         // velocity-field chunk partials
-    // rank split of the symmetric kernel: slots written per row superblock for the cached range
-    DevBuf<int> sym_slots, sym_counts;
-    int64_t sym_key_n = -1, sym_key_b = -1, sym_key_e = -1;
-    // fused stage exchange over peer memory (gs_p2p_*): this rank's raw row sums, the signal
-    // counters ([0] sums ready, [1] stage records written, [2] wait timeouts) and the ranks' pointers
-    struct P2P {
-        int world = 0, rank = 0;
-        DevBuf<double4> R;
-        DevBuf<unsigned long long> flags;
-        DevBuf<const double4*> Rp;
-        DevBuf<double4*> Sp;
-        DevBuf<unsigned long long*> Fp;
-        DevBuf<unsigned> done;           // block-completion counters of the signalling kernels
-        std::vector<void*> opened;       // IPC mappings to close
-        unsigned long long epoch = 0;    // stages completed since the peers were set
-        long long timeout_ns = 10000000000ll;
-    } p2p;
-    // profiling: CUDA events around every pair-kernel launch, kernel launch counter
-    int prof_on = 0;
-    std::vector<cudaEvent_t> prof_events;
-    size_t prof_used = 0;
-    long long launches = 0;
-    long long pair_launches = 0;
-    long long host_pairs = 0;     // dense / small-kernel pair count (known on the host)
-    // cell list (gs_cell.cu)
-    DevBuf<unsigned> c_keys, c_keys_sorted, c_vals, c_perm;
-    DevBuf<int> c_start;
-    DevBuf<double4> c_Ss;
-    DevBuf<float2> c_Sf;
-    DevBuf<double> c_bbox;
-    DevBuf<GridParams> c_gp;
-    DevBuf<unsigned char> c_cub;
-    DevBuf<unsigned long long> c_acc;   // accepted pairs (profiling)
-    DevBuf<unsigned long long> gram_bad;  // gs_gram's first coincident pair
-    size_t c_cub_bytes = 0;
-    int cell_on = 0;                    // path of the current call
-    // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds
-    struct Graph {
-        cudaGraphExec_t exec = nullptr;
-        std::vector<double> key;
-        std::vector<cudaEvent_t> ev;    // profiling events captured inside the graph
-        long long launches = 0, pair_launches = 0, host_pairs = 0;
-    } graph;
-    std::vector<cudaEvent_t>* capture_events = nullptr;  // non-null while capturing
-    cudaStream_t cap_stream = nullptr;
-    int graphs_on = 1;
-    int sym_on = 1;                     // symmetric dense kernel for full-row RHS
-    double prof_ms_acc = 0.0;           // pair-kernel time already harvested (graph replays)
-};
-
-namespace {
-
-constexpr int kRedBlocks = 512;
-constexpr int64_t kStatePad = 64;  // spare records after S for equal-size all-gather slices
 
 int check_system(const gs_system_t* sys) {
     if (!sys) return fail(GS_ERR_INVALID, "system is NULL");
@@ -272,7 +168,6 @@ __global__ void k_fp64_probe(double* out, int iters) {
     if (r == 12345.678) out[0] = r;  // never true; keeps the chains alive
 }
 
-inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 int ensure_session(gs_context* ctx, int64_t n, int64_t nrows) {
     const DensePlan plan = dense_plan(n, ctx->sm_count);
@@ -565,7 +460,6 @@ SmallItem small_item(const SysConst& sc, const gs_match_config_t* cfg) {
     return it;
 }
 
-// shooting.py:66-100 / integrator.py:35-43 validation of one (system, match config) item
 int check_match(const gs_system_t* sys, const gs_match_config_t* cfg) {
     int rc = check_system(sys);
     if (rc) return rc;
@@ -598,7 +492,60 @@ void small_to_result(const SmallResult& r, int64_t n, gs_match_result_t* out) {
     }
 }
 
-}  // namespace
+
+int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
+                   int64_t part_end, double* R, void* stream, PeerSignal sig, PeerWait wait) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || ctx->n < 1 || !R) return fail(GS_ERR_INVALID, "no stage session");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    const int64_t n = ctx->n, total = gs_sym_parts(n);
+    if (total == 0) return fail(GS_ERR_UNSUPPORTED, "symmetric split not available for this n");
+    if (stg < 0 || stg > 3 || step < 1 || part_begin < 0 || part_end > total || part_begin > part_end)
+        return fail(GS_ERR_INVALID, "bad stage / part range");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const SymPlan sp = sym_plan(n);
+    GS_CUDA(ctx->part.ensure((size_t)sp.nsb * (size_t)sp.pstride));
+    if (ctx->sym_key_n != n || ctx->sym_key_b != part_begin || ctx->sym_key_e != part_end) {
+        // Each (slot, row) is written by exactly one superblock pair: tile (X, Y) stores the
+        // I-side sums of X's rows in slot Y and the J-side sums of Y's rows in slot X.  List,
+        // per row superblock, the slots this rank's pairs write (ascending); the reduction reads
+        // only those, so the buffer needs no clearing.
+        const int nsb = sp.nsb;
+        std::vector<unsigned char> hit((size_t)nsb * nsb, 0);
+        for (long long t = part_begin; t < part_end; ++t) {
+            long long SI, SJ;
+            sym_pair_of(t, nsb, &SI, &SJ);
+            hit[(size_t)SI * nsb + SJ] = 1;
+            hit[(size_t)SJ * nsb + SI] = 1;
+        }
+        std::vector<int> slots((size_t)nsb * nsb, 0), counts(nsb, 0);
+        for (int X = 0; X < nsb; ++X)
+            for (int Y = 0; Y < nsb; ++Y)
+                if (hit[(size_t)X * nsb + Y]) slots[(size_t)X * nsb + counts[X]++] = Y;
+        GS_CUDA(ctx->sym_slots.ensure(slots.size()));
+        GS_CUDA(ctx->sym_counts.ensure(counts.size()));
+        GS_CUDA(cudaMemcpy(ctx->sym_slots.ptr, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice));
+        GS_CUDA(cudaMemcpy(ctx->sym_counts.ptr, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
+        ctx->sym_key_n = n; ctx->sym_key_b = part_begin; ctx->sym_key_e = part_end;
+    }
+    const SysConst sc = make_const(sys);
+    const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg;
+    if (ctx->prof_on) prof_mark(ctx, s);
+    launch_dense_sym(sc, ctx->S.ptr, n, ctx->part.ptr, sp.pstride, ctx->st.ptr, ev, ctx->tbl.ptr, s, part_begin,
+                     part_end, wait);
+    if (ctx->prof_on) prof_mark(ctx, s);
+    launch_slot_reduce_list(ctx->part.ptr, sp.pstride, n, sp.G * kDB, sp.nsb, ctx->sym_slots.ptr,
+                            ctx->sym_counts.ptr, reinterpret_cast<double4*>(R), s, sig);
+    ctx->launches += 2;
+    ctx->pair_launches++;
+    ctx->host_pairs += (long long)((double)n * (double)n * (double)(part_end - part_begin) / (double)total);
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+}
+
+
+}  // namespace gsapi
 
 // ======================================================================================
 extern "C" {
@@ -912,148 +859,6 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
     return GS_OK;
 }
 
-// ---- batched trajectories --------------------------------------------
-// One CTA per item of a persistent small-N launch: convergence-sweep cells, cluster-test
-// pairs, exact-vs-inexact rows (gs_match_batch) and Newton Jacobian columns (gs_evolve_batch)
-// run side by side instead of one after another.  Above kSmallMax (or on the cell path) the
-// items run one after another through the general path.
-namespace {
-
-constexpr size_t kSmemBudget = 220 * 1024;  // dynamic shared memory one CTA may claim
-
-int upload_items(gs_context* ctx, const std::vector<SmallItem>& items, cudaStream_t s) {
-    GS_CUDA(ctx->b_items.ensure(items.size()));
-    GS_CUDA(cudaMemcpyAsync(ctx->b_items.ptr, items.data(), items.size() * sizeof(SmallItem), cudaMemcpyHostToDevice,
-                            s));
-    return GS_OK;
-}
-
-}  // namespace
-
-int gs_match_batch(gs_context* ctx, const gs_batch_item_t* items, int64_t batch, int64_t n, const double* q0,
-                   int64_t q0_stride, const double* target, int64_t target_stride, const double* gram_factor,
-                   int64_t factor_stride, double* p0_out, double* endpoint_out, double* history_out,
-                   int64_t history_stride, gs_match_result_t* results, void* stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    if (!ctx || !items || !results || !history_out) return fail(GS_ERR_INVALID, "NULL argument");
-    if (batch < 1) return fail(GS_ERR_INVALID, "batch must be >= 1");
-    if (n < 1 || !q0 || !target || !p0_out || !endpoint_out)
-        return fail(GS_ERR_INVALID, "templates must have shape (N, 2), N >= 1");
-    if (q0_stride < 0 || target_stride < 0 || factor_stride < 0)
-        return fail(GS_ERR_INVALID, "strides must be >= 0");
-    bool small = n <= kSmallMax;
-    std::vector<SmallItem> host_items((size_t)batch);
-    for (int64_t b = 0; b < batch; ++b) {
-        int rc = check_match(&items[b].system, &items[b].config);
-        if (rc) return fail(rc, "item " + std::to_string(b) + ": " + g_last_error);
-        if (items[b].system.family != items[0].system.family)
-            return fail(GS_ERR_INVALID, "all items of a batch must use the same kernel family");
-        if (history_stride < items[b].config.max_iter)
-            return fail(GS_ERR_INVALID, "history_stride must be >= every item's max_iter");
-        small = small && use_small(&items[b].system, n);
-        host_items[b] = small_item(make_const(&items[b].system), &items[b].config);
-    }
-    GS_CUDA(cudaSetDevice(ctx->device));
-    cudaEvent_t e0, e1;
-    GS_CUDA(cudaEventCreate(&e0));
-    GS_CUDA(cudaEventCreate(&e1));
-    GS_CUDA(cudaEventRecord(e0, s));
-    if (small) {
-        int rc = upload_items(ctx, host_items, s);
-        if (rc) return rc;
-        GS_CUDA(ctx->small_res.ensure(batch));
-        SmallArgs a{};
-        small_setup(a, n); a.batch = batch; a.mode = 1;
-        a.item = host_items[0]; a.items = ctx->b_items.ptr;
-        a.q_in = q0; a.q_stride = q0_stride; a.target = target; a.t_stride = target_stride;
-        a.q_out = endpoint_out; a.p_out = p0_out;
-        a.history = history_out; a.hist_stride = history_stride; a.result = ctx->small_res.ptr;
-        a.L = gram_factor; a.L_stride = factor_stride;
-        if (gram_factor) {
-            a.L_smem = 1;
-            if (small_smem_bytes(a) > kSmemBudget) a.L_smem = 0;
-        }
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
-        GS_CUDA((cudaError_t)launch_small(items[0].system.family, a, ctx->tbl.ptr, s));
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
-        ctx->launches++;
-        ctx->pair_launches++;
-        GS_CUDA(cudaEventRecord(e1, s));
-        std::vector<SmallResult> r((size_t)batch);
-        GS_CUDA(cudaMemcpyAsync(r.data(), ctx->small_res.ptr, batch * sizeof(SmallResult), cudaMemcpyDeviceToHost, s));
-        GS_CUDA(cudaStreamSynchronize(s));
-        for (int64_t b = 0; b < batch; ++b) {
-            small_to_result(r[b], n, &results[b]);
-            ctx->host_pairs += (long long)(r[b].iterations + (r[b].outcome == GS_MATCH_EVOLVE_FAILED)) * 4LL *
-                                   items[b].config.steps * n * n + n * n;
-        }
-    } else {
-        if (gram_factor)
-            return fail(GS_ERR_UNSUPPORTED, "velocity-space batches need N <= 512 on the dense path");
-        std::vector<double> hist((size_t)history_stride);
-        for (int64_t b = 0; b < batch; ++b) {
-            int rc = gs_match(ctx, &items[b].system, &items[b].config, n, q0 + b * q0_stride,
-                              target + b * target_stride, p0_out + b * 2 * n, endpoint_out + b * 2 * n, hist.data(),
-                              &results[b], stream);
-            if (rc) return fail(rc, "item " + std::to_string(b) + ": " + g_last_error);
-            if (results[b].iterations > 0)
-                GS_CUDA(cudaMemcpyAsync(history_out + b * history_stride, hist.data(),
-                                        results[b].iterations * sizeof(double), cudaMemcpyHostToDevice, s));
-        }
-        GS_CUDA(cudaEventRecord(e1, s));
-    }
-    GS_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    for (int64_t b = 0; b < batch; ++b) results[b].seconds_device = ms * 1e-3;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return GS_OK;
-}
-
-int gs_evolve_batch(gs_context* ctx, const gs_system_t* sys, int64_t batch, int64_t n, double t_final, int32_t steps,
-                    const double* q_in, int64_t q_stride, double* q_out, double* p_io, gs_status_t* status,
-                    void* stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    if (!ctx || !status) return fail(GS_ERR_INVALID, "NULL argument");
-    int rc = check_system(sys);
-    if (rc) return rc;
-    if (batch < 1) return fail(GS_ERR_INVALID, "batch must be >= 1");
-    if (n < 1 || !q_in || !q_out || !p_io) return fail(GS_ERR_INVALID, "q and p must have shape (N, 2), N >= 1");
-    if (q_stride < 0) return fail(GS_ERR_INVALID, "q_stride must be >= 0");
-    if (!(t_final > 0.0) || !std::isfinite(t_final)) return fail(GS_ERR_INVALID, "t_final must be positive");
-    if (steps < 1) return fail(GS_ERR_INVALID, "steps must be >= 1");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    const SysConst sc = make_const(sys);
-    if (use_small(sys, n)) {
-        GS_CUDA(ctx->b_st.ensure(batch));
-        SmallArgs a{};
-        small_setup(a, n); a.batch = batch; a.mode = 0;
-        a.item.sc = sc; a.item.t_final = t_final; a.item.steps = steps;
-        a.q_in = q_in; a.q_stride = q_stride; a.p_in = p_io; a.q_out = q_out; a.p_out = p_io;
-        a.st = ctx->b_st.ptr;
-        ctx->host_pairs += 4LL * steps * n * n * batch;
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
-        GS_CUDA((cudaError_t)launch_small(sc.fam, a, ctx->tbl.ptr, s));
-        if (ctx->prof_on) cudaEventRecord(prof_event(ctx), s);
-        ctx->launches++;
-        ctx->pair_launches++;
-        std::vector<DevStatus> d((size_t)batch);
-        GS_CUDA(cudaMemcpyAsync(d.data(), ctx->b_st.ptr, batch * sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-        GS_CUDA(cudaStreamSynchronize(s));
-        for (int64_t b = 0; b < batch; ++b) decode_status(d[b], n, &status[b]);
-        return GS_OK;
-    }
-    for (int64_t b = 0; b < batch; ++b) {
-        GS_CUDA(cudaMemcpyAsync(q_out + b * 2 * n, q_in + b * q_stride, 2 * n * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s));
-        rc = gs_evolve(ctx, sys, n, t_final, steps, 0, q_out + b * 2 * n, p_io + b * 2 * n, nullptr, &status[b],
-                       stream);
-        if (rc == GS_ERR_CUDA || rc == GS_ERR_INVALID || rc == GS_ERR_UNSUPPORTED) return rc;
-    }
-    return GS_OK;
-}
-
 // ---- stage API ------------------------------------------------------------------------
 int gs_stage_begin(gs_context* ctx, int64_t n, const double* q, const double* p, int64_t row0, int64_t row1,
                    void* stream) {
@@ -1144,59 +949,6 @@ int64_t gs_sym_parts(int64_t n) {
     return (p.ok && n >= kSymMinN) ? (int64_t)sym_ctas(n) : 0;
 }
 
-static int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
-                          int64_t part_end, double* R, void* stream,
-                          PeerSignal sig = PeerSignal{nullptr, 0, 0, nullptr},
-                          PeerWait wait = PeerWait{nullptr, 0, 0, 0}) {
-    cudaStream_t s = (cudaStream_t)stream;
-    if (!ctx || ctx->n < 1 || !R) return fail(GS_ERR_INVALID, "no stage session");
-    int rc = check_system(sys);
-    if (rc) return rc;
-    const int64_t n = ctx->n, total = gs_sym_parts(n);
-    if (total == 0) return fail(GS_ERR_UNSUPPORTED, "symmetric split not available for this n");
-    if (stg < 0 || stg > 3 || step < 1 || part_begin < 0 || part_end > total || part_begin > part_end)
-        return fail(GS_ERR_INVALID, "bad stage / part range");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    const SymPlan sp = sym_plan(n);
-    GS_CUDA(ctx->part.ensure((size_t)sp.nsb * (size_t)sp.pstride));
-    if (ctx->sym_key_n != n || ctx->sym_key_b != part_begin || ctx->sym_key_e != part_end) {
-        // Each (slot, row) is written by exactly one superblock pair: tile (X, Y) stores the
-        // I-side sums of X's rows in slot Y and the J-side sums of Y's rows in slot X.  List,
-        // per row superblock, the slots this rank's pairs write (ascending); the reduction reads
-        // only those, so the buffer needs no clearing.
-        const int nsb = sp.nsb;
-        std::vector<unsigned char> hit((size_t)nsb * nsb, 0);
-        for (long long t = part_begin; t < part_end; ++t) {
-            long long SI, SJ;
-            sym_pair_of(t, nsb, &SI, &SJ);
-            hit[(size_t)SI * nsb + SJ] = 1;
-            hit[(size_t)SJ * nsb + SI] = 1;
-        }
-        std::vector<int> slots((size_t)nsb * nsb, 0), counts(nsb, 0);
-        for (int X = 0; X < nsb; ++X)
-            for (int Y = 0; Y < nsb; ++Y)
-                if (hit[(size_t)X * nsb + Y]) slots[(size_t)X * nsb + counts[X]++] = Y;
-        GS_CUDA(ctx->sym_slots.ensure(slots.size()));
-        GS_CUDA(ctx->sym_counts.ensure(counts.size()));
-        GS_CUDA(cudaMemcpy(ctx->sym_slots.ptr, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice));
-        GS_CUDA(cudaMemcpy(ctx->sym_counts.ptr, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
-        ctx->sym_key_n = n; ctx->sym_key_b = part_begin; ctx->sym_key_e = part_end;
-    }
-    const SysConst sc = make_const(sys);
-    const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg;
-    if (ctx->prof_on) prof_mark(ctx, s);
-    launch_dense_sym(sc, ctx->S.ptr, n, ctx->part.ptr, sp.pstride, ctx->st.ptr, ev, ctx->tbl.ptr, s, part_begin,
-                     part_end, wait);
-    if (ctx->prof_on) prof_mark(ctx, s);
-    launch_slot_reduce_list(ctx->part.ptr, sp.pstride, n, sp.G * kDB, sp.nsb, ctx->sym_slots.ptr,
-                            ctx->sym_counts.ptr, reinterpret_cast<double4*>(R), s, sig);
-    ctx->launches += 2;
-    ctx->pair_launches++;
-    ctx->host_pairs += (long long)((double)n * (double)n * (double)(part_end - part_begin) / (double)total);
-    GS_CUDA(cudaGetLastError());
-    return GS_OK;
-}
-
 int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
                        int64_t part_end, double* R, void* stream) {
     return pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, R, stream);
@@ -1218,165 +970,6 @@ int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32
     launch_finish(kFinStage, make_const(sys), fa, (cudaStream_t)stream);
     ctx->launches++;
     GS_CUDA(cudaGetLastError());
-    return GS_OK;
-}
-
-// ---- fused stage exchange over peer memory (multi-GPU, symmetric split) -----------------
-// Per stage: [wait: previous stage's records from all ranks] -> this rank's superblock pairs ->
-// raw row sums into R -> signal "sums ready" to every rank -> wait for all ranks' signals ->
-// epilogue of this rank's rows reading every rank's R and storing the new records into every
-// rank's S (k_finish_p2p) -> signal "records written".  Counters only grow (targets are
-// multiples of the world size), waits give up after a timeout and count it (gs_p2p_timeouts),
-// so a lost signal costs a timeout, never a hang.
-namespace {
-
-__global__ void k_p2p_wait(unsigned long long* flags, int which, unsigned long long target, long long timeout_ns) {
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (*((volatile unsigned long long*)&flags[which]) < target &&
-           *((volatile unsigned long long*)&flags[2]) == 0) {  // after one timeout nobody waits
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if ((long long)(t - t0) > timeout_ns) {
-            atomicAdd(&flags[2], 1ull);
-            break;
-        }
-        __nanosleep(256);
-    }
-    __threadfence_system();
-}
-
-}  // namespace
-
-int gs_p2p_local(gs_context* ctx, int64_t rows_all, void** S, void** R, void** flags) {
-    if (!ctx || ctx->n < 1 || !S || !R || !flags) return fail(GS_ERR_INVALID, "no stage session");
-    if (rows_all < ctx->n) return fail(GS_ERR_INVALID, "rows_all < n");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    GS_CUDA(ctx->p2p.R.ensure(rows_all));
-    GS_CUDA(ctx->p2p.flags.ensure(4));
-    GS_CUDA(cudaMemset(ctx->p2p.flags.ptr, 0, 4 * sizeof(unsigned long long)));
-    GS_CUDA(ctx->p2p.done.ensure(2));
-    GS_CUDA(cudaMemset(ctx->p2p.done.ptr, 0, 2 * sizeof(unsigned)));
-    *S = ctx->S.ptr; *R = ctx->p2p.R.ptr; *flags = ctx->p2p.flags.ptr;
-    if (const char* e = std::getenv("GS_B200_P2P_TIMEOUT_S")) ctx->p2p.timeout_ns = (long long)(std::atof(e) * 1e9);
-    return GS_OK;
-}
-
-int gs_p2p_export(gs_context* ctx, int64_t rows_all, void* handles) {
-    if (!handles) return fail(GS_ERR_INVALID, "handles is NULL");
-    void* ptr[3];
-    int rc = gs_p2p_local(ctx, rows_all, &ptr[0], &ptr[1], &ptr[2]);
-    if (rc) return rc;
-    for (int k = 0; k < 3; ++k)
-        GS_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handles) + k, ptr[k]));
-    return GS_OK;
-}
-
-int gs_p2p_set_peers(gs_context* ctx, int world, int rank, void* const* S, void* const* R, void* const* F) {
-    if (!ctx || world < 1 || world > 32 || rank < 0 || rank >= world || !S || !R || !F)
-        return fail(GS_ERR_INVALID, "bad peer set");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    GS_CUDA(ctx->p2p.Sp.ensure(world));
-    GS_CUDA(ctx->p2p.Rp.ensure(world));
-    GS_CUDA(ctx->p2p.Fp.ensure(world));
-    GS_CUDA(cudaMemcpy(ctx->p2p.Sp.ptr, S, world * sizeof(void*), cudaMemcpyHostToDevice));
-    GS_CUDA(cudaMemcpy(ctx->p2p.Rp.ptr, R, world * sizeof(void*), cudaMemcpyHostToDevice));
-    GS_CUDA(cudaMemcpy(ctx->p2p.Fp.ptr, F, world * sizeof(void*), cudaMemcpyHostToDevice));
-    ctx->p2p.world = world; ctx->p2p.rank = rank; ctx->p2p.epoch = 0;
-    return GS_OK;
-}
-
-int gs_p2p_close(gs_context* ctx) {
-    if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
-    cudaSetDevice(ctx->device);
-    for (void* p : ctx->p2p.opened) cudaIpcCloseMemHandle(p);
-    ctx->p2p.opened.clear();
-    ctx->p2p.world = 0;
-    return GS_OK;
-}
-
-int gs_p2p_import(gs_context* ctx, int world, int rank, const void* handles_all) {
-    if (!ctx || !handles_all || world < 1 || world > 32 || rank < 0 || rank >= world)
-        return fail(GS_ERR_INVALID, "bad peer import");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    gs_p2p_close(ctx);
-    const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(handles_all);
-    std::vector<void*> S(world), R(world), F(world);
-    for (int w = 0; w < world; ++w) {
-        void** dst[3] = {&S[w], &R[w], &F[w]};
-        if (w == rank) {
-            S[w] = ctx->S.ptr; R[w] = ctx->p2p.R.ptr; F[w] = ctx->p2p.flags.ptr;
-            continue;
-        }
-        for (int k = 0; k < 3; ++k) {
-            GS_CUDA(cudaIpcOpenMemHandle(dst[k], h[3 * w + k], cudaIpcMemLazyEnablePeerAccess));
-            ctx->p2p.opened.push_back(*dst[k]);
-        }
-    }
-    return gs_p2p_set_peers(ctx, world, rank, S.data(), R.data(), F.data());
-}
-
-int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
-                 int64_t part_end, void* stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers (gs_p2p_import / gs_p2p_set_peers)");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    {
-        auto& P = ctx->p2p;
-        // one waiting thread for every rank's records of the previous stage (waiting in each of
-        // the pair kernel's thousands of CTAs cost more: 164.8 vs 159.5 ms per C2 solve), then
-        // the pairs; the slot reduction's last CTA signals "sums ready" to every rank
-        if (P.epoch > 0) {
-            k_p2p_wait<<<1, 1, 0, s>>>(P.flags.ptr, 1, P.epoch * (unsigned long long)P.world, P.timeout_ns);
-            ctx->launches++;
-        }
-        int rc = pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, reinterpret_cast<double*>(P.R.ptr), stream,
-                                PeerSignal{P.Fp.ptr, P.world, 0, P.done.ptr});
-        if (rc) return rc;
-    }
-    GS_CUDA(cudaGetLastError());
-    return GS_OK;
-}
-
-int gs_p2p_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt, void* stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers (gs_p2p_import / gs_p2p_set_peers)");
-    int rc = check_system(sys);
-    if (rc) return rc;
-    if (stg < 0 || stg > 3 || step < 1) return fail(GS_ERR_INVALID, "bad stage index");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    auto& P = ctx->p2p;
-    FinishArgs fa{};
-    fa.nrows = ctx->row1 - ctx->row0; fa.row0 = ctx->row0;
-    fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr; fa.stage = stg; fa.dt = dt; fa.st = ctx->st.ptr;
-    fa.event = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg + 1ull;
-    // waits (every CTA) for all ranks' "sums ready", its last CTA signals "records written"
-    launch_finish_p2p(make_const(sys), fa, P.Rp.ptr, P.Sp.ptr, P.world,
-                      PeerWait{P.flags.ptr, 0, (P.epoch + 1) * (unsigned long long)P.world, P.timeout_ns},
-                      PeerSignal{P.Fp.ptr, P.world, 1, P.done.ptr + 1}, s);
-    P.epoch++;
-    ctx->launches++;
-    GS_CUDA(cudaGetLastError());
-    return GS_OK;
-}
-
-int gs_p2p_sync(gs_context* ctx, void* stream) {
-    if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers");
-    GS_CUDA(cudaSetDevice(ctx->device));
-    auto& P = ctx->p2p;
-    k_p2p_wait<<<1, 1, 0, (cudaStream_t)stream>>>(P.flags.ptr, 1, P.epoch * (unsigned long long)P.world,
-                                                   P.timeout_ns);
-    GS_CUDA(cudaGetLastError());
-    return GS_OK;
-}
-
-int gs_p2p_timeouts(gs_context* ctx, int64_t* out) {
-    if (!ctx || !out) return fail(GS_ERR_INVALID, "NULL argument");
-    unsigned long long v = 0;
-    if (ctx->p2p.flags.ptr) {
-        GS_CUDA(cudaSetDevice(ctx->device));
-        GS_CUDA(cudaMemcpy(&v, ctx->p2p.flags.ptr + 2, sizeof(v), cudaMemcpyDeviceToHost));
-    }
-    *out = (int64_t)v;
     return GS_OK;
 }
 
@@ -1441,3 +1034,4 @@ int gs_fp64_peak_probe(gs_context* ctx, int32_t iters, double* ms, double* flops
 }
 
 }  // extern "C"
+
