@@ -29,6 +29,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #define GS_SMALL_UNROLL 4
 #endif
 constexpr int kSmallUnroll = GS_SMALL_UNROLL;
+#ifndef GS_SMALL_MAXSPLIT    // lanes per row at most (A/B builds)
+#define GS_SMALL_MAXSPLIT 32
+#endif
 #ifndef GS_SMALL_ASYNC       // per-stage exchange by st.async + mbarriers (A/B: 0 = cluster barriers)
 #define GS_SMALL_ASYNC 1
 #endif
@@ -540,7 +543,8 @@ size_t small_smem_bytes(const SmallArgs& a) {
 int small_threads(int64_t n, int cluster, int* split_out) {
     const int64_t rows = (n + cluster - 1) / cluster;
     int split = 1;
-    while (split < 32 && rows * split * 2 <= kSmallThreads) split *= 2;
+    // lanes per row: a power of two <= 32, no more than the sources (n), within the CTA size
+    while (split < GS_SMALL_MAXSPLIT && split * 2 <= n && rows * split * 2 <= kSmallThreads) split *= 2;
     *split_out = split;
     return (int)(((rows * split) + 31) / 32 * 32);
 }
