@@ -270,7 +270,7 @@ int choose_path_impl(gs_context* ctx, const gs_system_t* sys, const double4* S, 
     GridParams g;
     GS_CUDA(cudaMemcpyAsync(&g, ctx->c_gp.ptr, sizeof(g), cudaMemcpyDeviceToHost, s));
     GS_CUDA(cudaStreamSynchronize(s));
-    ctx->cell_on = g.hashed || (int64_t)g.nx * g.ny >= kCellMinCells;
+    ctx->cell_on = g.hashed || (int64_t)g.nx * g.ny >= (int64_t)kCellMinCells * g.sub * g.sub;  // cells of edge cutoff
     return GS_OK;
 }
 

@@ -11,8 +11,10 @@
 //   2. cell key per particle, stable LSD radix sort of (key, index) with CUB, cell start
 //      offsets (start[c] = first sorted position with key >= c), permuted copy of the
 //      32-byte (x, y, px, py) records so that a cell's particles are contiguous;
-//   3. the pair kernel: one thread per target in sorted order; the 3 stencil rows of its
-//      cell are 3 contiguous sorted ranges.  Candidates are filtered in fp32 on the FMA pipe
+//   3. the pair kernel: TPL lanes per target in sorted order.  Cells have edge cutoff/2
+//      (GridParams::sub), so a target visits 5 stencil rows, each one contiguous sorted range
+//      trimmed to the cells its disk reaches (~5 sigma^2 of candidates instead of the 9 sigma^2
+//      of a 3x3 stencil of cutoff-sized cells: C5 RHS 2.57 -> 1.98 ms).  Candidates are filtered in fp32 on the FMA pipe
 //      (8-byte float positions relative to the grid origin, radius grown by the fp32 error
 //      bound so no pair within the cutoff is lost) into a per-lane list in shared memory,
 //      then the accepted pairs run the full fp64 pair body of
@@ -24,6 +26,9 @@
 // Bound: FP64 pipe for the pair kernel (~90 DP slots per HBM byte at config 5); the build
 // kernels (sort / scan / permute) are HBM/latency bound and are measured separately.
 #include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdlib>
 
 #include "gs_cell.cuh"
 
@@ -71,7 +76,8 @@ __global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double*
     if (threadIdx.x < 4) red[4 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
 }
 
-__global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, GridParams* gp) {
+__global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, int sub_max,
+                              GridParams* gp) {
     __shared__ double s[4][kBB];
     __shared__ int s_bad;
     if (threadIdx.x == 0) s_bad = 0;
@@ -106,20 +112,30 @@ __global__ void k_grid_params(const double* __restrict__ red, int nb, double cut
     const double margin = 4.0 * extent * 5.9604644775390625e-08;
     const double rcf = cutoff * (1.0 + 1e-6) + margin + 1e-30;
     g.rc2f = (margin < 64.0 * cutoff && extent < 1e30) ? __double2float_ru(rcf * rcf) : __int_as_float(0x7fc00000);
+    g.rc = rcf;
+    g.sub = 1;
     if (bad || !isfinite(mnx) || !isfinite(mxx) || !isfinite(mny) || !isfinite(mxy)) {
         // non-finite stage state: one cell (the stage check has already recorded the failure)
-        g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.nx = 1; g.ny = 1; g.ncells = 1; g.hashed = 0;
+        g.x0 = 0.0; g.y0 = 0.0; g.inv_h = 0.0; g.h = 0.0; g.nx = 1; g.ny = 1; g.ncells = 1; g.hashed = 0;
         g.rc2f = __int_as_float(0x7fc00000);  // NaN: accept everything
     } else {
-        const double fx = floor((mxx - mnx) / cutoff) + 1.0, fy = floor((mxy - mny) / cutoff) + 1.0;
-        g.x0 = mnx; g.y0 = mny; g.inv_h = 1.0 / cutoff;
+        g.x0 = mnx; g.y0 = mny;
+        // finest subdivision whose row-major grid fits the cap (sub = 1: cell edge = cutoff)
+        int sub = sub_max;
+        for (; sub > 1; --sub) {
+            const double h = cutoff / sub;
+            const double fx = floor((mxx - mnx) / h) + 1.0, fy = floor((mxy - mny) / h) + 1.0;
+            if (fx * fy <= (double)cap && margin < 0.25 * h) break;
+        }
+        const double h = cutoff / sub;
+        const double fx = floor((mxx - mnx) / h) + 1.0, fy = floor((mxy - mny) / h) + 1.0;
+        g.h = h; g.inv_h = 1.0 / h;
         if (fx * fy <= (double)cap) {
-            g.nx = (int)fx; g.ny = (int)fy; g.ncells = g.nx * g.ny; g.hashed = 0;
+            g.nx = (int)fx; g.ny = (int)fy; g.ncells = g.nx * g.ny; g.hashed = 0; g.sub = sub;
         } else {
             g.nx = 0; g.ny = 0; g.ncells = (int)cap; g.hashed = 1;
         }
     }
-    g.pad = 0;
     *gp = g;
 }
 
@@ -156,6 +172,26 @@ struct Ranges {
 __device__ __forceinline__ void stencil_ranges(const GridParams& g, const int* __restrict__ start, double x, double y,
                                                Ranges& r) {
     r.cnt = 0;
+    if (!g.hashed && g.sub > 1) {
+        // rows cy - sub .. cy + sub, each trimmed to the cells within rc of the target in x.
+        // Cell coordinates are monotone in the position, so every particle with |dx| <= xr lies
+        // in [cell(x - xr), cell(x + xr)]; rc carries a 1e-6 relative slack over the cutoff (and
+        // the fp32 margin), far above the rounding of the slab bounds below.
+        const int cy = cell_coord(y, g.y0, g.inv_h, g.ny);
+        const double rc2 = g.rc * g.rc;
+        for (int yy = max(cy - g.sub, 0); yy <= min(cy + g.sub, g.ny - 1); ++yy) {
+            const double lo = fma((double)yy, g.h, g.y0), hi = lo + g.h;
+            const double gap = fmax(0.0, fmax(lo - y, y - hi));
+            const double xr2 = fma(-gap, gap, rc2);
+            if (!(xr2 > 0.0)) continue;
+            const double xr = sqrt(xr2);
+            const int xa = cell_coord(x - xr, g.x0, g.inv_h, g.nx), xb = cell_coord(x + xr, g.x0, g.inv_h, g.nx);
+            r.a[r.cnt] = start[yy * g.nx + xa];
+            r.b[r.cnt] = start[yy * g.nx + xb + 1];
+            ++r.cnt;
+        }
+        return;
+    }
     if (!g.hashed) {
         const int cx = cell_coord(x, g.x0, g.inv_h, g.nx), cy = cell_coord(y, g.y0, g.inv_h, g.ny);
         const int xa = max(cx - 1, 0), xb = min(cx + 1, g.nx - 1);
@@ -328,7 +364,11 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
     const int nb = (int)std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB);
     k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, w.bbox_red);
     const int64_t cap = cell_cap(n);
-    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, w.gp);
+    static const int sub_max = [] {
+        const char* e = std::getenv("GS_B200_CELL_SUB");  // A/B: cells per cutoff (1 = classic 3x3 stencil)
+        return e ? std::min(std::max(std::atoi(e), 1), kCellSubMax) : 2;
+    }();
+    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, sub_max, w.gp);
     const unsigned blocks = (unsigned)((n + 255) / 256);
     k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
     int end_bit = 1;

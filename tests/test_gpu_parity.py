@@ -519,3 +519,41 @@ def test_general_path_match_both_spaces_match_oracle(cuda, space):
     assert r.iterations == o["iterations"]
     assert np.abs(r.p0 - o["p0"]).max() <= 1e-8 * np.abs(o["p0"]).max()
     assert r.hamiltonian == pytest.approx(o["hamiltonian"], rel=1e-8)
+
+
+def test_cell_stencil_covers_every_pair_within_the_cutoff(cuda, monkeypatch):
+    """The subdivided grid (cell edge cutoff/2, per-target trimmed stencil rows) must not lose a
+    pair within the cutoff.  With the cutoff shortened to 3 alpha a pair near it still carries
+    G = e^-3, so a missed one shows at ~1e-2; points sit on cell boundaries (a lattice of the
+    cell edge) and partners at 0.999 cutoff in every direction."""
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+    from paper_1510_03816_b200 import device
+
+    alpha = 0.01
+    cut = 3.0 * alpha
+    monkeypatch.setattr(device, "support_radius", lambda k: cut)
+    rng = np.random.default_rng(21)
+    h = cut / 2
+    # lattice on cell boundaries (the grid origin is the bounding-box corner (0, 0)), spaced 3h
+    # so that no two lattice points sit at exactly the cutoff
+    lat = np.stack(np.meshgrid(np.arange(40) * 3 * h, np.arange(40) * 3 * h), -1).reshape(-1, 2)
+    ang = rng.uniform(0, 2 * np.pi, 1600)
+    part = lat + 0.999 * cut * np.stack([np.cos(ang), np.sin(ang)], 1)
+    axis = lat[:400] + np.array([0.999 * cut, 0.0])  # along the rows: the trimmed x-range ends
+    diag = lat[400:800] + 0.999 * cut * np.array([np.sqrt(0.5), -np.sqrt(0.5)])
+    q = np.concatenate([lat, part, axis, diag, rng.uniform(0, 120 * h, (1000, 2))])
+    q = q[(q >= 0).all(1)]
+    # the device filter admits d < cutoff (1 + 1e-6) + fp32 margin (harmless at the product's
+    # cutoff, where G = 2^-53): drop the points of pairs inside that window so both sums agree
+    from scipy.spatial import cKDTree
+
+    pairs = cKDTree(q).query_pairs(cut * (1 + 1e-5), output_type="ndarray")
+    d = np.linalg.norm(q[pairs[:, 0]] - q[pairs[:, 1]], axis=1)
+    q = np.delete(q, np.unique(pairs[d >= cut * (1 - 1e-12)].ravel()), axis=0)
+    p = rng.normal(0, 0.01, q.shape)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=alpha), sigma2=0.0)
+    with _cell(gs):
+        dq, dp = gs.rhs(spec, gs.ParticleState(q, p))
+    oq, op = native.rhs(_kern(spec), 0.0, q, p, cutoff=cut)
+    assert rel(dq, oq) <= RHS_TOL and rel(dp, op) <= RHS_TOL
