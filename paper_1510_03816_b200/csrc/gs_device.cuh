@@ -54,13 +54,19 @@ struct DevStatus {
     unsigned long long pair_key;
 };
 
+// Constants of the pair core in the constant bank: FP64 instructions take them as c[][] operands
+// instead of re-materialising 64-bit literals into (uniform) registers inside the hot loops
+// (k_cell_pair's body: 123 -> 115 instructions per two pairs; results bitwise unchanged).
+enum { kCbC1, kCbC2, kCbC3, kCbC4, kCbC5, kCb0375, kCbMagicK, kCbTinyR2, kCbN };
+static __constant__ double gs_cb[kCbN] = {kC1, kC2, kC3, kC4, kC5, 0.375, 6755399441055744.0 + 1073741824.0, 1e-200};
+
 __device__ __forceinline__ double rsqrt_refined(double x) {
     double y0;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
     // cubic correction: y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2
     double h = x * y0;
     double e = fma(-h, y0, 1.0);
-    double t = fma(e, 0.375, 0.5);
+    double t = fma(e, gs_cb[kCb0375], 0.5);
     double ye = y0 * e;
     return fma(ye, t, y0);
 }
@@ -73,15 +79,16 @@ __device__ __forceinline__ double rsqrt_refined(double x) {
 constexpr double kRoundMagicK = 6755399441055744.0 + 1073741824.0;
 constexpr int kMagicHi = 0x43380000;
 __device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ tbl) {
-    double s = y + kRoundMagicK;
-    double kd = s - kRoundMagicK;
+    double s = y + gs_cb[kCbMagicK];
+    double kd = s - gs_cb[kCbMagicK];
     double u = y - kd;
     const int k = __double2loint(s) - (1 << 30);
     const bool ok = ((__double2hiint(s) ^ kMagicHi) | ((k - kKMin) >> 31)) == 0;  // one predicate
     double t = tbl[(k & (kTbl - 1)) * kTblRep];
     int n = k >> kTblBits;
     double tn = __hiloint2double(__double2hiint(t) + (n << 20), __double2loint(t));
-    double e1 = u * fma(fma(fma(fma(kC5, u, kC4), u, kC3), u, kC2), u, kC1);
+    double e1 = u * fma(fma(fma(fma(gs_cb[kCbC5], u, gs_cb[kCbC4]), u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u,
+                        gs_cb[kCbC1]);
     double g = fma(tn, e1, tn);
     return ok ? g : 0.0;
 }
@@ -104,7 +111,7 @@ constexpr double kTinyR2 = 1e-200;
 template <int FAM>
 __device__ __forceinline__ void pair_core(double dx, double dy, double pdot, const double* __restrict__ tbl, double k1,
                                           double& g, double& c, int& z) {
-    const double r2 = fma(dx, dx, fma(dy, dy, kTinyR2));
+    const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
     z = ((__double2hiint(r2) ^ __double2hiint(kTinyR2)) | (__double2loint(r2) ^ __double2loint(kTinyR2))) == 0;
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
