@@ -92,8 +92,14 @@ __device__ __forceinline__ void add_to(double4* dst, const Acc& a) {
     *dst = v;
 }
 
+#ifdef GS_SYM_MAXREG  // A/B on C2 (ms per RHS): 160 regs (6 CTAs/SM) 0.366, 152 -> 0.378, 144 (7 CTAs/SM) -> 0.381, 136 -> 0.397
+#define GS_SYM_BOUNDS __maxnreg__(GS_SYM_MAXREG)
+#else
+#define GS_SYM_BOUNDS __launch_bounds__(kST, GS_SYM_MINB)
+#endif
+
 template <int FAM>
-__global__ void __launch_bounds__(kST, GS_SYM_MINB) k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, int G,
+__global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t n, int nb, int G,
                                                        int nsb, long long cta0, double k1, double4* __restrict__ part,
                                                        int64_t pstride, DevStatus* st, unsigned long long event,
                                                        const double* __restrict__ tbl_g, PeerWait wait) {
