@@ -32,6 +32,9 @@ constexpr int kSmallUnroll = GS_SMALL_UNROLL;
 #ifndef GS_SMALL_MAXSPLIT    // lanes per row at most (A/B builds)
 #define GS_SMALL_MAXSPLIT 32
 #endif
+#ifndef GS_SMALL_RS          // reduce-scatter + all-gather of a row's four sums (A/B: 0 = plain butterfly)
+#define GS_SMALL_RS 1
+#endif
 #ifndef GS_SMALL_ASYNC       // per-stage exchange by st.async + mbarriers (A/B: 0 = cluster barriers)
 #define GS_SMALL_ASYNC 1
 #endif
@@ -221,6 +224,27 @@ __device__ void small_rhs(const Ctx& c, const double4* __restrict__ S, double k1
         if (z && c.act && j != c.tgt && pdot != 0.0 && __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) == 0.0)
             atomicMin(key, (unsigned long long)c.tgt * (unsigned long long)c.n + (unsigned long long)j);
     }
+#if GS_SMALL_RS
+    if (c.split >= 4) {
+        // reduce-scatter, then all-gather: the first level swaps two of the four sums, the second
+        // one, the rest one each — 12 + 8 shuffles of 32-bit halves instead of 8 per level (the
+        // SHFL pipe bounded the plain butterfly at 32 lanes per row).  Fixed order: deterministic.
+        const int oa = c.split >> 1, ob = c.split >> 2;
+        const bool ha = (c.sub & oa) != 0, hb = (c.sub & ob) != 0;
+        const double k0 = ha ? apx : aqx, k1 = ha ? apy : aqy;   // kept: components 2ha, 2ha + 1
+        const double s0 = ha ? aqx : apx, s1 = ha ? aqy : apy;
+        const double m0 = k0 + __shfl_xor_sync(kFull, s0, oa);
+        const double m1 = k1 + __shfl_xor_sync(kFull, s1, oa);
+        double m = (hb ? m1 : m0) + __shfl_xor_sync(kFull, hb ? m0 : m1, ob);  // component 2ha + hb
+        for (int off = ob >> 1; off; off >>= 1) m += __shfl_xor_sync(kFull, m, off);
+        const int base = (threadIdx.x & 31) & ~(c.split - 1), low = c.sub & (ob - 1);
+        sqx = __shfl_sync(kFull, m, base | low);
+        sqy = __shfl_sync(kFull, m, base | ob | low);
+        spx = __shfl_sync(kFull, m, base | oa | low);
+        spy = __shfl_sync(kFull, m, base | oa | ob | low);
+        return;
+    }
+#endif
     for (int off = c.split >> 1; off; off >>= 1) {
         aqx += __shfl_xor_sync(kFull, aqx, off);
         aqy += __shfl_xor_sync(kFull, aqy, off);
