@@ -46,7 +46,7 @@ constexpr int kCL = GS_CELL_CL;
 #define GS_CELL_TPL_MIN 4  // A/B (C5 / C4 RHS ms): 1 -> 2.61 / 4.48, 2 -> 2.57 / 3.94, 4 -> 2.57 / 3.62, 8 -> 2.64 / 3.48, 16 -> 2.87 / 3.36
 #endif
 #ifndef GS_CELL_MINB            // resident CTAs per SM the register allocation is bounded for (A/B builds)
-#define GS_CELL_MINB 6  // A/B (C5 / C4 RHS ms), 3x3 stencil: 8 -> 2.79 / 5.40, 6 -> 2.57 / 4.67, 5 -> 2.61 / 4.55, 4 -> 2.62 / 4.49; half-size cells: 6 -> 1.91 / 2.76, 5 -> 1.98 / 2.75, 4 -> 1.98 / 2.75
+#define GS_CELL_MINB 7  // A/B (C5 / C4 RHS ms), 3x3 stencil: 8 -> 2.79 / 5.40, 6 -> 2.57 / 4.67, 5 -> 2.61 / 4.55, 4 -> 2.62 / 4.49; half-size cells: 8 -> 1.95 / 2.90, 7 -> 1.85 / 2.75, 6 -> 1.91 / 2.76, 5 -> 1.98 / 2.75, 4 -> 1.98 / 2.75
 #endif
 
 __global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double* red) {
