@@ -231,6 +231,7 @@ CellWs cell_ws(gs_context* ctx) {
     w.keys = ctx->c_keys.ptr; w.keys_sorted = ctx->c_keys_sorted.ptr; w.vals = ctx->c_vals.ptr;
     w.perm = ctx->c_perm.ptr; w.start = ctx->c_start.ptr; w.Ss = ctx->c_Ss.ptr; w.Sf = ctx->c_Sf.ptr; w.bbox_red = ctx->c_bbox.ptr;
     w.gp = ctx->c_gp.ptr; w.cub_temp = ctx->c_cub.ptr; w.cub_bytes = ctx->c_cub_bytes;
+    w.tlist = ctx->c_tlist.ptr; w.nsel = ctx->c_nsel.ptr;
     return w;
 }
 
@@ -240,6 +241,8 @@ int ensure_cell(gs_context* ctx, int64_t n) {
     GS_CUDA(ctx->c_start.ensure(cell_cap(n) + 1));
     GS_CUDA(ctx->c_bbox.ensure(4 * kCellBboxBlocks));
     GS_CUDA(ctx->c_gp.ensure(1));
+    GS_CUDA(ctx->c_tlist.ensure(n));
+    GS_CUDA(ctx->c_nsel.ensure(1));
     GS_CUDA(ctx->c_acc.ensure(1));
     const size_t bytes = cell_cub_bytes(n);
     GS_CUDA(ctx->c_cub.ensure(bytes));

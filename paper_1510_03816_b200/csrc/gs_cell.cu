@@ -250,7 +250,7 @@ __global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, c
 template <int FAM, int TPL>
 __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* __restrict__ Ss, const float2* __restrict__ Sf,
                                                       const unsigned* __restrict__ perm,
-                                                      const unsigned* __restrict__ keys_sorted,
+                                                      const int* __restrict__ tlist, int64_t nt,
                                                       const int* __restrict__ start, const GridParams* __restrict__ gp,
                                                       int64_t n, int64_t row0, int64_t row1, double k1,
                                                       double4* __restrict__ part, DevStatus* st,
@@ -267,9 +267,11 @@ __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* 
     __syncthreads();
 
     const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
-    const int64_t k = (int64_t)blockIdx.x * (kCB / TPL) + threadIdx.x / TPL;
-    const bool valid = k < n;
-    const int64_t kk = valid ? k : 0;
+    // target t of this launch: sorted position t (all rows), or tlist[t] (a rank's rows, in
+    // sorted order: the rank's warps only carry its own targets)
+    const int64_t t = (int64_t)blockIdx.x * (kCB / TPL) + threadIdx.x / TPL;
+    const bool valid = t < nt;
+    const int64_t kk = valid ? (tlist ? (int64_t)tlist[t] : t) : 0;
     const int64_t i = (int64_t)perm[kk];
     const bool active = valid && i >= row0 && i < row1;
     const GridParams g = *gp;
@@ -345,11 +347,13 @@ __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* 
 
 }  // namespace
 
+size_t cell_select_bytes(int64_t n);
+
 size_t cell_cub_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
                                     (const unsigned*)nullptr, (unsigned*)nullptr, (int)n, 0, 32);
-    return bytes;
+    return std::max(bytes, cell_select_bytes(n));
 }
 
 int64_t cell_cap(int64_t n) {
@@ -382,17 +386,51 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
     return 0;
 }
 
+namespace {
+// perm[k] in [row0, row1): the sorted positions of a rank's target rows
+struct InRows {
+    const unsigned* perm;
+    int64_t row0, row1;
+    __device__ __forceinline__ bool operator()(const int& k) const {
+        const int64_t i = (int64_t)perm[k];
+        return i >= row0 && i < row1;
+    }
+};
+}  // namespace
+
+size_t cell_select_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceSelect::If(nullptr, bytes, cub::CountingInputIterator<int>(0), (int*)nullptr, (int*)nullptr, (int)n,
+                          InRows{nullptr, 0, 0});
+    return bytes;
+}
+
 void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t row0, int64_t row1, double4* part,
                       DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
                       cudaStream_t stream) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int tpl = GS_CELL_TPL_MIN;  // lanes per target: enough threads to cover every SM ~8 warps deep
+    // A row range (multi-GPU rank): compact the rank's targets in sorted order first, so no warp
+    // carries other ranks' targets (over all n sorted positions nearly every warp would hold
+    // one of this rank's rows at 8 ranks, and a warp costs its slowest target).
+    const bool partial = row0 > 0 || row1 < n;
+    const int* tlist = nullptr;
+    const int64_t nt = partial ? row1 - row0 : n;
+    if (partial) {
+        size_t bytes = w.cub_bytes;
+        cub::DeviceSelect::If(w.cub_temp, bytes, cub::CountingInputIterator<int>(0), w.tlist, w.nsel, (int)n,
+                              InRows{w.perm, row0, row1}, stream);
+        tlist = w.tlist;
+    }
+    if (nt <= 0) return;
+    // lanes per target: enough threads to cover every SM ~8 warps deep.  Chosen from n, not nt,
+    // so a row's lane split and summation order do not depend on the number of ranks.
+    int tpl = GS_CELL_TPL_MIN;
     while (tpl < 16 && n * tpl < (int64_t)sms * 1024) tpl *= 2;
-    const unsigned blocks = (unsigned)((n * tpl + kCB - 1) / kCB);
+    const unsigned blocks = (unsigned)((nt * tpl + kCB - 1) / kCB);
 #define GS_CELL_LAUNCH(F, T)                                                                                   \
-    k_cell_pair<F, T><<<blocks, kCB, 0, stream>>>(w.Ss, w.Sf, w.perm, w.keys_sorted, w.start, w.gp, n, row0,  \
+    k_cell_pair<F, T><<<blocks, kCB, 0, stream>>>(w.Ss, w.Sf, w.perm, tlist, nt, w.start, w.gp, n, row0,      \
                                                   row1, sc.k1, part, st, event, tbl_dev, accepted)
 #define GS_CELL_FAM(F)                                    \
     switch (tpl) {                                        \

@@ -38,7 +38,9 @@ struct CellWs {
     float2* Sf;             // n: fp32 positions relative to the grid origin, sorted order
     double* bbox_red;       // 4 * kCellBboxBlocks
     GridParams* gp;         // 1
-    void* cub_temp;
+    int* tlist;             // n: sorted positions of a rank's target rows (row-range launches)
+    int* nsel;              // 1: CUB select output count
+    void* cub_temp;         // shared by the radix sort and the target select (same stream)
     size_t cub_bytes;
 };
 

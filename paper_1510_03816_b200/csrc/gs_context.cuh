@@ -104,6 +104,7 @@ struct gs_context {
     DevBuf<float2> c_Sf;
     DevBuf<double> c_bbox;
     DevBuf<GridParams> c_gp;
+    DevBuf<int> c_tlist, c_nsel;
     DevBuf<unsigned char> c_cub;
     DevBuf<unsigned long long> c_acc;   // accepted pairs (profiling)
     DevBuf<unsigned long long> gram_bad;  // gs_gram's first coincident pair

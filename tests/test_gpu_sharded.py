@@ -286,3 +286,26 @@ def test_peer_handles_open_across_processes(cuda, tmp_path):
     mp.spawn(_ipc_worker, args=(2, port, out), nprocs=2, join=True)
     for r in range(2):
         assert open(f"{out}.{r}").read() == "ok"
+
+
+def test_cell_rows_of_a_rank_equal_the_full_cell_rhs(cuda):
+    """The cell path of one rank (rows [r0, r1) of an uneven split) evaluates only its own
+    targets, compacted in cell order (no warp carries another rank's rows), and every row keeps
+    the summation order of the full-row launch: the slices are bitwise the full RHS."""
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import sharded
+
+    rng = np.random.default_rng(31)
+    n = 40000
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 0.01, (n, 2))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.02 / gs.LAMBDA), sigma2=0.1)
+    gs.set_path("cell")
+    try:
+        dq, dp = sharded.rhs_rows(spec, q, p, 0, n)
+        cuts = [0, 7001, 7002, 23000, n]
+        parts = [sharded.rhs_rows(spec, q, p, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    finally:
+        gs.set_path("auto")
+    np.testing.assert_array_equal(np.concatenate([a.cpu().numpy() for a, _ in parts]), dq.cpu().numpy())
+    np.testing.assert_array_equal(np.concatenate([b.cpu().numpy() for _, b in parts]), dp.cpu().numpy())
