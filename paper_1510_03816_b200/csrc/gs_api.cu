@@ -440,8 +440,9 @@ int small_cluster(int64_t n) {
         forced = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;  // cluster sizes with a kernel instance
     }
     if (forced > 0) return forced;
-    // A/B (st.async exchange): N = 64 -> 8 CTAs best; N = 16..32 -> 4; N = 8 -> 1
-    return n >= 64 ? kMaxCluster : (n >= 16 ? 4 : 1);
+    // A/B (st.async exchange, ms per feedback iteration): N = 64 -> 8 CTAs best (16, non-portable:
+    // no faster); N = 60 (100 RK4 steps) 8 -> 0.57, 4 -> 0.67; N = 30: 8 -> 0.49, 4 -> 0.48; N = 8 -> 1
+    return n >= 48 ? kMaxCluster : (n >= 16 ? 4 : 1);
 }
 
 void small_setup(SmallArgs& a, int64_t n) {
