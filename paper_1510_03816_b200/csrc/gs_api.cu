@@ -127,6 +127,35 @@ __global__ void k_residual(const double* __restrict__ src, int stride, const dou
     if (threadIdx.x == 0) red[blockIdx.x] = s[0];
 }
 
+// One decision of Algorithm 1 on the device (shooting.py:259-301, as the host loop in gs_match):
+// delta = h * |r| from BEFORE the update, value = |Y - X(T)| or delta, blow-up / convergence /
+// cap, history; then the WHILE node's condition for the next iteration.
+__global__ void k_match_decide(MatchLoop* L, const double* __restrict__ scal, const DevStatus* __restrict__ st,
+                               double* hist, double h, double eps, int max_iter, int stop_rule,
+                               cudaGraphConditionalHandle cond) {
+    MatchLoop m = *L;
+    bool stop = false;
+    if (st->first_event != kNoEvent) {  // the shoot failed: last finite endpoint, new p (shooting.py:269-276)
+        m.outcome = GS_MATCH_EVOLVE_FAILED;
+        m.fail_it = m.it + 1;
+        stop = true;
+    } else {
+        const double delta = h * m.nrm;
+        const double nrm = scal[0];
+        const double value = stop_rule == GS_STOP_TARGET_RESIDUAL ? nrm : delta;
+        if (!m.have_initial) { m.initial = value; m.have_initial = 1; }
+        hist[m.it] = value;
+        m.iters = m.it + 1;
+        m.nrm = nrm;
+        if (!isfinite(value) || (m.initial > 0.0 && value > 1e6 * m.initial)) { m.outcome = GS_MATCH_BLOWUP; stop = true; }
+        else if (value < eps) { m.outcome = GS_MATCH_CONVERGED; stop = true; }
+        else if (m.it + 1 >= max_iter) { m.outcome = GS_MATCH_CAP; stop = true; }
+        m.it += 1;
+    }
+    *L = m;
+    cudaGraphSetConditional(cond, stop ? 0u : 1u);
+}
+
 // deterministic final reduction of `m` partials; kind: 0 max, 1 sum -> sqrt, 2 plain sum
 __global__ void k_reduce_final(const double* __restrict__ red, int m, int kind, double* out, DevStatus* st) {
     __shared__ double s[512];
@@ -359,7 +388,9 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
     return {(double)ctx->n, (double)ctx->row0, (double)ctx->row1, (double)steps, dt, (double)ctx->cell_on,
             (double)ctx->prof_on, (double)sc.fam, sc.k1, sc.scale_q, sc.scale_p, sc.sigma2, sc.cutoff,
             P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr), P(ctx->c_Sf.ptr),
-            P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr)};
+            P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr),
+            P(ctx->c_keys_sorted.ptr), P(ctx->c_vals.ptr), P(ctx->c_bbox.ptr), P(ctx->c_gp.ptr), P(ctx->c_tlist.ptr),
+            P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes};
 }
 
 // integrator.py:95-119 as one CUDA graph (4 x steps stages, ~2 kernels per dense stage and
@@ -569,6 +600,7 @@ int gs_create(gs_context** out, int device) {
     ctx->device = device;
     if (const char* g = std::getenv("GS_B200_GRAPHS")) ctx->graphs_on = std::atoi(g) != 0;
     if (const char* g = std::getenv("GS_B200_SYM")) ctx->sym_on = std::atoi(g) != 0;
+    if (const char* g = std::getenv("GS_B200_DEVLOOP")) ctx->devloop_on = std::atoi(g) != 0;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
     // 2^(j/kTbl), j = 0..kTbl-1, rounded from long double, replicated kTblRep times interleaved
@@ -580,6 +612,7 @@ int gs_create(gs_context** out, int device) {
     if (e == cudaSuccess) e = ctx->st.ensure(1);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->st_host, sizeof(DevStatus));
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->scal_host, 16 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->mloop_host, sizeof(MatchLoop));
     if (e == cudaSuccess) e = ctx->scal.ensure(16);
     if (e == cudaSuccess) e = ctx->small_res.ensure(1);
     if (e != cudaSuccess) {
@@ -598,6 +631,9 @@ int gs_destroy(gs_context* ctx) {
     ctx->red.release(); ctx->ham.release(); ctx->hist.release(); ctx->scal.release(); ctx->small_res.release();
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
     if (ctx->scal_host) cudaFreeHost(ctx->scal_host);
+    if (ctx->mloop_host) cudaFreeHost(ctx->mloop_host);
+    if (ctx->mgraph.exec) cudaGraphExecDestroy(ctx->mgraph.exec);
+    ctx->mloop.release(); ctx->ep.release(); ctx->c_tlist.release(); ctx->c_nsel.release();
     graph_reset(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
@@ -749,6 +785,101 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
     return rc;
 }
 
+// The whole feedback loop as ONE graph launch: a conditional WHILE node whose body is an
+// iteration (momentum update, 4 x steps RK stages, residual, norm, k_match_decide); the
+// device decides when to stop, the host reads the outcome once at the end.  Returns
+// GS_ERR_UNSUPPORTED when the runtime cannot build conditional nodes (the caller then runs the
+// host-driven loop).
+int match_device_loop(gs_context* ctx, const SysConst& sc, const gs_match_config_t* cfg, int64_t n,
+                      double* endpoint_out, int nb, int red_kind, double nrm0, cudaStream_t s, MatchLoop* out) {
+    GS_CUDA(ctx->mloop.ensure(1));
+    GS_CUDA(ctx->hist.ensure(cfg->max_iter));
+    GS_CUDA(ctx->ep.ensure(2 * n));
+    if (!ctx->cap_stream) GS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    const double dt = cfg->t_final / cfg->steps;
+    // everything the loop graph bakes in (the evolve's key + the loop's constants and buffers)
+    std::vector<double> key = graph_key(ctx, sc, dt, cfg->steps);
+    auto P = [](const void* p) { return (double)(uintptr_t)p; };
+    for (double v : {cfg->h, cfg->epsilon, (double)cfg->max_iter, (double)cfg->stop_rule, (double)cfg->norm, (double)nb,
+                     (double)red_kind, P(ctx->q0.ptr), P(ctx->p.ptr), P(ctx->resid.ptr), P(ctx->tgt.ptr),
+                     P(ctx->red.ptr), P(ctx->scal.ptr), P(ctx->mloop.ptr), P(ctx->hist.ptr), P(ctx->ep.ptr)})
+        key.push_back(v);
+    if (!ctx->mgraph.exec || ctx->mgraph.key != key) {
+        if (ctx->mgraph.exec) cudaGraphExecDestroy(ctx->mgraph.exec);
+        ctx->mgraph = gs_context::LoopGraph();
+        cudaGraph_t g = nullptr;
+        GS_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle cond;
+        cudaGraphNode_t node;
+        cudaGraphNodeParams np = {};
+        if (cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+            (void)cudaGetLastError();
+            cudaGraphDestroy(g);
+            return GS_ERR_UNSUPPORTED;
+        }
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = cond;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        if (cudaGraphAddNode(&node, g, nullptr, 0, &np) != cudaSuccess) {
+            (void)cudaGetLastError();
+            cudaGraphDestroy(g);
+            return GS_ERR_UNSUPPORTED;
+        }
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        const long long l0 = ctx->launches, pl0 = ctx->pair_launches, hp0 = ctx->host_pairs;
+        cudaStream_t c = ctx->cap_stream;
+        cudaError_t e = cudaStreamBeginCaptureToGraph(c, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+            cudaGraphDestroy(g);
+            return fail(GS_ERR_CUDA, std::string("loop capture: ") + cudaGetErrorString(e));
+        }
+        k_match_begin<<<nblk(n), 256, 0, c>>>(ctx->q0.ptr, ctx->p.ptr, ctx->resid.ptr, cfg->h, n, ctx->S.ptr,
+                                              ctx->B.ptr);
+        k_status_reset<<<1, 1, 0, c>>>(ctx->st.ptr);
+        for (int step = 1; step <= cfg->steps; ++step)
+            for (int st = 0; st < 4; ++st) stage(ctx, sc, step, st, dt, c);
+        k_residual<<<nb, 256, 0, c>>>(reinterpret_cast<const double*>(ctx->B.ptr), 4, ctx->tgt.ptr, n, ctx->ep.ptr,
+                                      ctx->resid.ptr, cfg->norm, ctx->red.ptr, ctx->st.ptr);
+        k_reduce_final<<<1, 512, 0, c>>>(ctx->red.ptr, nb, red_kind, ctx->scal.ptr, ctx->st.ptr);
+        k_match_decide<<<1, 1, 0, c>>>(ctx->mloop.ptr, ctx->scal.ptr, ctx->st.ptr, ctx->hist.ptr, cfg->h,
+                                       cfg->epsilon, cfg->max_iter, cfg->stop_rule, cond);
+        cudaGraph_t captured = nullptr;
+        e = cudaStreamEndCapture(c, &captured);
+        ctx->mgraph.launches = ctx->launches - l0 + 4;
+        ctx->mgraph.pair_launches = ctx->pair_launches - pl0;
+        ctx->mgraph.host_pairs = ctx->host_pairs - hp0;
+        ctx->launches = l0; ctx->pair_launches = pl0; ctx->host_pairs = hp0;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&ctx->mgraph.exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            ctx->mgraph = gs_context::LoopGraph();
+            return fail(GS_ERR_CUDA, std::string("loop graph: ") + cudaGetErrorString(e));
+        }
+        ctx->mgraph.key = key;
+    }
+    MatchLoop m{};
+    m.outcome = GS_MATCH_CAP;
+    m.nrm = nrm0;
+    m.initial = nrm0;
+    m.have_initial = cfg->stop_rule == GS_STOP_TARGET_RESIDUAL;
+    *ctx->mloop_host = m;
+    cudaError_t e = cudaMemcpyAsync(ctx->mloop.ptr, ctx->mloop_host, sizeof(MatchLoop), cudaMemcpyHostToDevice, s);
+    // the graph's endpoint buffer starts from the initial shoot's endpoint (kept on a failure)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->ep.ptr, endpoint_out, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaGraphLaunch(ctx->mgraph.exec, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(endpoint_out, ctx->ep.ptr, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->mloop_host, ctx->mloop.ptr, sizeof(MatchLoop), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(GS_ERR_CUDA, std::string("loop graph launch: ") + cudaGetErrorString(e));
+    *out = *ctx->mloop_host;
+    const long long its = out->iters + (out->outcome == GS_MATCH_EVOLVE_FAILED);
+    ctx->launches += its * ctx->mgraph.launches;
+    ctx->pair_launches += its * ctx->mgraph.pair_launches;
+    ctx->host_pairs += its * ctx->mgraph.host_pairs;
+    return GS_OK;
+}
+
 int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* cfg, int64_t n, const double* q0,
              const double* target, double* p0_out, double* endpoint_out, double* history_out,
              gs_match_result_t* result, void* stream) {
@@ -812,9 +943,30 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         double initial = nrm;
         bool have_initial = cfg->stop_rule == GS_STOP_TARGET_RESIDUAL;
         int outcome = GS_MATCH_CAP, iters = 0;
+        bool done = false;
         if (cfg->stop_rule == GS_STOP_TARGET_RESIDUAL && nrm < cfg->epsilon) {
             outcome = GS_MATCH_CONVERGED;
-        } else {
+            done = true;
+        } else if (ctx->devloop_on && !ctx->prof_on) {
+            MatchLoop m{};
+            rc = match_device_loop(ctx, sc, cfg, n, endpoint_out, nb, red_kind, nrm, s, &m);
+            if (rc != GS_OK && rc != GS_ERR_UNSUPPORTED) return rc;
+            if (rc == GS_OK) {
+                done = true;
+                outcome = m.outcome;
+                iters = m.iters;
+                nrm = m.nrm;
+                if (iters > 0)
+                    GS_CUDA(cudaMemcpy(history_out, ctx->hist.ptr, iters * sizeof(double), cudaMemcpyDeviceToHost));
+                if (outcome == GS_MATCH_EVOLVE_FAILED) {
+                    gs_status_t st;
+                    if (fetch_status(ctx, s, n, &st) == GS_ERR_CUDA) return GS_ERR_CUDA;
+                    result->status = st;
+                    result->status.iteration = m.fail_it;
+                }
+            }
+        }
+        if (!done) {
             for (int it = 0; it < cfg->max_iter; ++it) {
                 const double delta = cfg->h * nrm;
                 k_match_begin<<<nblk(n), 256, 0, s>>>(ctx->q0.ptr, ctx->p.ptr, ctx->resid.ptr, cfg->h, n, ctx->S.ptr,

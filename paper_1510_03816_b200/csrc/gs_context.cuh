@@ -57,6 +57,13 @@ struct DevBuf {
 using gsapi::DevBuf;
 using namespace gsb;  // internal header: the context holds the kernels' types
 
+// State of the device-resident feedback loop (gs_match, n above the small-N kernel): what the
+// host loop of shooting.py:259-301 keeps in locals, kept on the device between iterations.
+struct MatchLoop {
+    int it, iters, outcome, have_initial, fail_it, pad;
+    double initial, nrm;
+};
+
 struct gs_context {
     int device = 0;
     int sm_count = 148;
@@ -64,12 +71,15 @@ struct gs_context {
     DevBuf<DevStatus> st;
     DevStatus* st_host = nullptr;   // pinned
     double* scal_host = nullptr;    // pinned scratch (16 doubles)
+    MatchLoop* mloop_host = nullptr; // pinned
     // stage session
     DevBuf<double4> S, B, A, part;
     int64_t n = 0, row0 = 0, row1 = 0;
     // match / reductions
     DevBuf<double> q0, tgt, p, resid, red, ham, hist, scal;
     DevBuf<SmallResult> small_res;
+    DevBuf<MatchLoop> mloop;
+    DevBuf<double> ep;               // the loop graph's endpoint buffer
     DevBuf<SmallItem> b_items;       // batched launches: per-item constants
     DevBuf<DevStatus> b_st;          // batched evolve: per-item failure records
     DevBuf<double2> vf_part;         // velocity-field chunk partials
@@ -117,9 +127,16 @@ struct gs_context {
         std::vector<cudaEvent_t> ev;    // profiling events captured inside the graph
         long long launches = 0, pair_launches = 0, host_pairs = 0;
     } graph;
+    // the device-resident feedback loop (conditional WHILE graph), re-launched while its key holds
+    struct LoopGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::vector<double> key;
+        long long launches = 0, pair_launches = 0, host_pairs = 0;  // per iteration
+    } mgraph;
     std::vector<cudaEvent_t>* capture_events = nullptr;  // non-null while capturing
     cudaStream_t cap_stream = nullptr;
     int graphs_on = 1;
+    int devloop_on = 1;                 // large-N matches as one conditional-WHILE graph
     int sym_on = 1;                     // symmetric dense kernel for full-row RHS
     double prof_ms_acc = 0.0;           // pair-kernel time already harvested (graph replays)
 };
