@@ -44,6 +44,10 @@ constexpr int kST = 64;  // threads per CTA
 #ifndef GS_SYM_SB        // superblock count above which blocks are grouped (A/B builds)
 #define GS_SYM_SB 128  // A/B on C2 (ms per 100-step solve): 128 -> 152.8, 64 -> 165.4, 32 -> 178.7
 #endif
+#ifndef GS_SYM_UNROLL     // unroll of the two-source rotation loop (16 trips)
+#define GS_SYM_UNROLL 2  // A/B on C2 (ms per RHS): 2 -> 0.365, 4 -> 0.375, 8 -> 0.420 (fewer moves, slower)
+#endif
+constexpr int kSymUnroll = GS_SYM_UNROLL;
 #ifndef GS_SYM_SRC2      // two sources per rotation step: 4 independent pair chains per lane
 #define GS_SYM_SRC2 1    // A/B on C2: 0.364 ms (minb 6, 158 regs) vs 0.383 ms (minb 8, 128 regs) vs 0.374
 #endif
@@ -166,7 +170,7 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                 // two sources per step (4 independent pair chains per lane): jA travels with
                 // source (lane + step), jB with source (lane + step + 1); both move 2 lanes
                 Acc jb2{0.0, 0.0, 0.0, 0.0};
-#pragma unroll 2
+#pragma unroll kSymUnroll
                 for (int step = 0; step < 32; step += 2) {
                     const double4 sa = rot[step];
                     const double4 sb = rot[step + 1];
