@@ -306,7 +306,12 @@ int choose_path_impl(gs_context* ctx, const gs_system_t* sys, const double4* S, 
     return GS_OK;
 }
 
-constexpr int64_t kSymMinN = 1024;
+// Below this N the symmetric kernel's 128 x 128 tiles leave most SMs idle (N = 1024: 36 CTAs)
+// and the one-sided kernel with fine source chunks is faster (us per RK stage, one-sided vs
+// symmetric: N = 1024 15.7 vs 23.7, 2048 21.6 vs 24.6, 4096 51.2 vs 37.2).
+constexpr int64_t kSymMinN = 3072;
+// Multi-GPU: the ranks' shares of the symmetric pair list (gs_sym_parts) from this N on.
+constexpr int64_t kSymSplitMinN = 1024;
 
 bool use_sym(const gs_context* ctx, int64_t n, int64_t row0, int64_t nrows) {
     return ctx->sym_on && !ctx->cell_on && row0 == 0 && nrows == n && n >= kSymMinN && sym_plan(n).ok;
@@ -1102,7 +1107,7 @@ int gs_stage_path(gs_context* ctx, const gs_system_t* sys, void* stream) {
 
 int64_t gs_sym_parts(int64_t n) {
     const SymPlan p = sym_plan(n);
-    return (p.ok && n >= kSymMinN) ? (int64_t)sym_ctas(n) : 0;
+    return (p.ok && n >= kSymSplitMinN) ? (int64_t)sym_ctas(n) : 0;
 }
 
 int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,

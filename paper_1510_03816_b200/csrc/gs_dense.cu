@@ -23,14 +23,18 @@
 namespace gsb {
 
 DensePlan dense_plan(int64_t n, int sm_count) {
+    // Source chunks of a multiple of kCG sources, enough of them for ~32 CTAs per SM: at mid N
+    // (a few thousand particles) whole kDT tiles would leave a handful of CTAs with long serial
+    // source loops (N = 600: 15 CTAs, 59 us per RHS).  Depends on n and the SM count only, so a
+    // row's summation order does not depend on the row split.
+    constexpr int64_t kCG = 32;
     const int64_t row_blocks = (n + kDB - 1) / kDB;
-    const int64_t tiles = (n + kDT - 1) / kDT;
+    const int64_t units = (n + kCG - 1) / kCG;
     const int64_t want_ctas = (int64_t)sm_count * 32;
     int64_t nc = (want_ctas + row_blocks - 1) / row_blocks;
-    nc = std::max<int64_t>(1, std::min(nc, tiles));
-    int64_t chunk_tiles = (tiles + nc - 1) / nc;
+    nc = std::max<int64_t>(1, std::min(nc, units));
     DensePlan p;
-    p.chunk = chunk_tiles * kDT;
+    p.chunk = ((units + nc - 1) / nc) * kCG;
     p.nchunks = (int)((n + p.chunk - 1) / p.chunk);
     return p;
 }
@@ -80,14 +84,14 @@ __global__ void __launch_bounds__(kDPT, 12) k_dense_partial(const double4* __res
 
     Row a0{0.0, 0.0, 0.0, 0.0, 0}, a1{0.0, 0.0, 0.0, 0.0, 0};
     for (int64_t t0 = j0; t0 < j1; t0 += kDT) {
+        const int m = (int)((j1 - t0) < kDT ? (j1 - t0) : kDT);
+        const int mr = (m + 3) & ~3;
         __syncthreads();
-        for (int t = threadIdx.x; t < kDT; t += kDPT) {
+        for (int t = threadIdx.x; t < mr; t += kDPT) {
             const int64_t j = t0 + t;
             s_src[t] = (j < j1) ? S[j] : far_record(kDB + t);  // far, p = 0: contributes exactly 0
         }
         __syncthreads();
-        const int m = (int)((j1 - t0) < kDT ? (j1 - t0) : kDT);
-        const int mr = (m + 3) & ~3;
 #pragma unroll 4
         for (int jj = 0; jj < mr; ++jj) {
             const double4 s = s_src[jj];
