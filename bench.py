@@ -165,7 +165,7 @@ def reference_arm(a):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs[1] recipe, seeds 0/1)",
         "config": dict(arm_config(a, w.n), parallelism="host cores",
                        sample=f"rows [0,{rows}) of one RHS per step (same pairs/s metric)"),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"rows [0,{rows}) of one C2 RHS per step via oracle/restate.py (numpy, "
                                    "bitwise equal to geoshoot.rhs; elementwise on 1 core, BLAS on "
                                    f"{cores} threads)"},
@@ -175,6 +175,17 @@ def reference_arm(a):
 
 
 # ---------------------------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_port(w, spec_alpha, c1=None):
     """The C/OpenMP oracle port on all host cores, one RK4 step (4 RHS) of C2; with `c1`, also
     the reference's Algorithm 1 (numpy restatement, bitwise the reference) on config 1 — the
@@ -188,7 +199,7 @@ def cpu_baseline_port(w, spec_alpha, c1=None):
     dt = time.perf_counter() - t0
     out = {"value": 4.0 * w.n * w.n / dt, "unit": UNIT, "cores": threads, "kind": "port",
            "sample": f"one RK4 step (4 dense RHS, N={w.n}) of C2 through oracle/gs_oracle.c (OpenMP, libm exp)",
-           "seconds": dt}
+           "seconds": dt, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
     if c1 is not None:
         from oracle import restate
 
