@@ -45,7 +45,10 @@ constexpr int kCL = GS_CELL_CL;
 #ifndef GS_CELL_TPL_MIN         // minimum lanes per target (A/B builds)
 #define GS_CELL_TPL_MIN 4  // A/B (C5 / C4 RHS ms): 1 -> 2.61 / 4.48, 2 -> 2.57 / 3.94, 4 -> 2.57 / 3.62, 8 -> 2.64 / 3.48, 16 -> 2.87 / 3.36
 #endif
-#ifndef GS_CELL_MINB            // resident CTAs per SM the register allocation is bounded for (A/B builds)
+#ifndef GS_CELL_PREFETCH  // software-pipelined record loads in the pair loop (A/B builds)
+#define GS_CELL_PREFETCH 0  // A/B (C5 / C4 RHS ms vs 1.855 / 2.76): minb 7 -> 2.00 / 3.01, 6 -> 2.01 / 2.93, 5 -> 2.01 / 2.84 (bitwise equal)
+#endif
+#ifndef GS_CELL_MINB           // resident CTAs per SM the register allocation is bounded for (A/B builds)
 #define GS_CELL_MINB 7  // A/B (C5 / C4 RHS ms), 3x3 stencil: 8 -> 2.79 / 5.40, 6 -> 2.57 / 4.67, 5 -> 2.61 / 4.55, 4 -> 2.62 / 4.49; half-size cells: 8 -> 1.95 / 2.90, 7 -> 1.85 / 2.75, 6 -> 1.91 / 2.76, 5 -> 1.98 / 2.75, 4 -> 1.98 / 2.75
 #endif
 
@@ -296,9 +299,18 @@ __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* 
                     if (!(fmaf(dx, dx, dy * dy) >= g.rc2f)) s_list[cnt++][threadIdx.x] = j;  // NaN: keep
                 }
                 nacc += cnt;
+#if GS_CELL_PREFETCH
+                // the next accepted record is loaded while the current pair is evaluated
+                double4 s_nx = cnt > 0 ? Ss[s_list[0][threadIdx.x]] : me;
+#endif
                 for (int u = 0; u < cnt; ++u) {
+#if GS_CELL_PREFETCH
+                    const double4 s = s_nx;
+                    if (u + 1 < cnt) s_nx = Ss[s_list[u + 1][threadIdx.x]];
+#else
                     const int j = s_list[u][threadIdx.x];
                     const double4 s = Ss[j];
+#endif
                     const double dx = me.x - s.x, dy = me.y - s.y;
                     const double pdot = fma(me.z, s.z, me.w * s.w);
                     double gk, c;
