@@ -260,3 +260,17 @@ def test_cli_front_end_runs_the_reference_cli_with_gpu_facts(tmp_path):
         res = tmp_path / "r"
         with pytest.raises(N.NativeUnavailable):
             cli.main(["match", str(out), str(out), "--h", "0.3", "--out", str(res)])
+
+
+def test_input_validation_matches_reference():
+    """Malformed inputs (empty, ragged, wrong shape, non-finite, mismatched, bad configs,
+    duplicate landmarks) raise the reference's exception types with its messages
+    (tests/golden/validation.json, made by tests/golden/make_validation.py from the reference)."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_validation import outcomes
+
+    want = json.load(open(os.path.join(GOLDEN, "validation.json")))
+    got = outcomes(gs)
+    assert got == want
