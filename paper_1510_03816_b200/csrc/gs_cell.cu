@@ -230,6 +230,42 @@ __global__ void k_cell_keys(const double4* __restrict__ S, int64_t n, const Grid
     vals[i] = (unsigned)i;
 }
 
+// Small-n sort (n <= kSortSmallMax): the whole (key, index) sort in ONE CTA (CUB BlockRadixSort,
+// stable, blocked arrangement in index order) instead of the four device-wide radix launches
+// (histogram, scan, two onesweep passes) that dominate a small cloud's cell build.  Pad slots
+// carry the largest key and follow every real element (stability), so positions [0, n) hold
+// exactly the device sort's (key, index) order: results are bitwise unchanged.
+#ifndef GS_SORT_SMALL_RB          // radix bits per block pass (A/B builds)
+#define GS_SORT_SMALL_RB 4
+#endif
+constexpr int kSortSmallThreads = 1024;
+constexpr int kSortSmallItems = 16;
+constexpr int64_t kSortSmallMax = (int64_t)kSortSmallThreads * kSortSmallItems;
+using SortSmall = cub::BlockRadixSort<unsigned, kSortSmallThreads, kSortSmallItems, unsigned, GS_SORT_SMALL_RB>;
+
+__global__ void __launch_bounds__(kSortSmallThreads, 1) k_sort_small(const unsigned* __restrict__ keys, int n,
+                                                                     int end_bit, unsigned* keys_sorted,
+                                                                     unsigned* perm) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& tmp = *reinterpret_cast<typename SortSmall::TempStorage*>(smem_raw);
+    unsigned k[kSortSmallItems], v[kSortSmallItems];
+#pragma unroll
+    for (int t = 0; t < kSortSmallItems; ++t) {
+        const int i = threadIdx.x * kSortSmallItems + t;
+        k[t] = i < n ? keys[i] : 0xffffffffu;
+        v[t] = (unsigned)i;
+    }
+    SortSmall(tmp).SortBlockedToStriped(k, v, 0, end_bit);
+#pragma unroll
+    for (int t = 0; t < kSortSmallItems; ++t) {
+        const int i = t * kSortSmallThreads + threadIdx.x;
+        if (i < n) {
+            keys_sorted[i] = k[t];
+            perm[i] = v[t];
+        }
+    }
+}
+
 // start[c] = first sorted position whose key >= c, for c in [0, ncells]; permuted records
 __global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, const unsigned* __restrict__ perm,
                                      const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
@@ -389,10 +425,22 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
     k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
     int end_bit = 1;
     while ((1ll << end_bit) < cap) ++end_bit;
-    size_t bytes = w.cub_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(w.cub_temp, bytes, w.keys, w.keys_sorted, w.vals, w.perm,
-                                                    (int)n, 0, end_bit, stream);
-    if (e != cudaSuccess) return (int)e;
+    static const int64_t small_max = [] {
+        const char* e = std::getenv("GS_B200_SORT_SMALL_MAX");  // A/B: 0 = always the device-wide sort
+        return e ? std::min<int64_t>(std::atoll(e), kSortSmallMax) : kSortSmallMax;
+    }();
+    if (n <= small_max) {
+        static const bool attr_ok = cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)sizeof(typename SortSmall::TempStorage)) == cudaSuccess;
+        if (!attr_ok) return (int)cudaErrorInvalidConfiguration;
+        k_sort_small<<<1, kSortSmallThreads, sizeof(typename SortSmall::TempStorage), stream>>>(
+            w.keys, (int)n, end_bit, w.keys_sorted, w.perm);
+    } else {
+        size_t bytes = w.cub_bytes;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(w.cub_temp, bytes, w.keys, w.keys_sorted, w.vals, w.perm,
+                                                        (int)n, 0, end_bit, stream);
+        if (e != cudaSuccess) return (int)e;
+    }
     k_cell_start_permute<<<(unsigned)((n + 1 + 255) / 256), 256, 0, stream>>>(w.keys_sorted, w.perm, S, n, w.gp,
                                                                             w.start, w.Ss, w.Sf);
     return 0;
