@@ -45,6 +45,9 @@ constexpr int kCL = GS_CELL_CL;
 #ifndef GS_CELL_TPL_MIN         // minimum lanes per target (A/B builds)
 #define GS_CELL_TPL_MIN 4  // A/B (C5 / C4 RHS ms): 1 -> 2.61 / 4.48, 2 -> 2.57 / 3.94, 4 -> 2.57 / 3.62, 8 -> 2.64 / 3.48, 16 -> 2.87 / 3.36
 #endif
+#ifndef GS_CELL_TPL_DEPTH  // lanes per target grow until n * lanes >= SMs * this (A/B builds)
+#define GS_CELL_TPL_DEPTH 512  // A/B (bench --path cell, ms per 100-step solve, 1024 -> 512): n = 12000 34.5 -> 30.8, 16384 37.1 -> 33.7 (256: 34.9), 30000 50.3 -> 48.0
+#endif
 #ifndef GS_CELL_PREFETCH  // software-pipelined record loads in the pair loop (A/B builds)
 #define GS_CELL_PREFETCH 0  // A/B (C5 / C4 RHS ms vs 1.855 / 2.76): minb 7 -> 2.00 / 3.01, 6 -> 2.01 / 2.93, 5 -> 2.01 / 2.84 (bitwise equal)
 #endif
@@ -487,7 +490,7 @@ void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t ro
     // lanes per target: enough threads to cover every SM ~8 warps deep.  Chosen from n, not nt,
     // so a row's lane split and summation order do not depend on the number of ranks.
     int tpl = GS_CELL_TPL_MIN;
-    while (tpl < 16 && n * tpl < (int64_t)sms * 1024) tpl *= 2;
+    while (tpl < 16 && n * tpl < (int64_t)sms * GS_CELL_TPL_DEPTH) tpl *= 2;
     const unsigned blocks = (unsigned)((nt * tpl + kCB - 1) / kCB);
 #define GS_CELL_LAUNCH(F, T)                                                                                   \
     k_cell_pair<F, T><<<blocks, kCB, 0, stream>>>(w.Ss, w.Sf, w.perm, tlist, nt, w.start, w.gp, n, row0,      \
