@@ -39,7 +39,7 @@ namespace {
 constexpr int kBB = 256;        // bbox block
 constexpr int kCB = 128;        // pair-kernel threads per CTA
 #ifndef GS_CELL_CL               // candidate chunk = per-lane list capacity (A/B builds)
-#define GS_CELL_CL 32
+#define GS_CELL_CL 32  // A/B at 7 CTAs/SM (C5 / C4 RHS ms): 24 -> 1.95 / 2.79, 32 -> 1.86 / 2.77, 40 -> 1.86 / 2.80, 48 -> 1.96 / 2.95
 #endif
 constexpr int kCL = GS_CELL_CL;
 #ifndef GS_CELL_TPL_MIN         // minimum lanes per target (A/B builds)
