@@ -21,8 +21,8 @@
  *     context's GPU; "host" pointers are ordinary host memory.
  *   - All GPU work is ordered on the caller's `stream` (a cudaStream_t passed as void*;
  *     NULL = legacy default stream).  Functions that must report a numerical outcome
- *     (status, match result) synchronise that stream before returning; gs_rhs_async and
- *     the gs_stage_* calls never synchronise.
+ *     (status, match result) synchronise that stream before returning; gs_rhs_rows,
+ *     gs_velocity_field and the gs_stage_* / gs_p2p_* calls never synchronise.
  *   - The library owns only the workspaces inside a gs_context; the caller owns every
  *     buffer it passes.  One context per concurrent caller; no global mutable state
  *     beyond a thread-local last-error string.
@@ -60,7 +60,8 @@ extern "C" {
 #define GS_FAMILY_GAUSSIAN 1
 
 /* pair-sum strategy */
-#define GS_PATH_AUTO 0   /* cell list when the support radius is small against the point cloud */
+#define GS_PATH_AUTO 0   /* cell list when N >= 2048, the bounding box spans >= 25 support-radius cells and
+                            holds >= 4 particles per such cell on average; dense otherwise */
 #define GS_PATH_DENSE 1  /* all N^2 pairs, the reference's own semantics (no truncation) */
 #define GS_PATH_CELL 2   /* pairs with d_ij < cutoff only (KD-1: G(cutoff) = 2^-53) */
 

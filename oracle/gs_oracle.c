@@ -70,12 +70,18 @@ static inline int pair_term(const go_params* k, long i, long j, const double* q,
 
 /* Cells of edge = cutoff, hashed into nb (power of two >= 2n) buckets by the bits of the double
  * cell coordinate floor(x / cutoff): no bounding box, so a flung-apart (diverging) state costs
- * the same as a compact one.  Pairs are still decided by the exact distance test. */
+ * the same as a compact one.  Pairs are still decided by the exact distance test.
+ * The particles are counting-sorted by bucket (stable: ascending index inside a bucket) and
+ * copied in that order, and targets are processed in that order, so a target's candidate
+ * loads are contiguous; each target still sums bucket by bucket (stencil order dy, dx) and,
+ * inside a bucket, in ascending particle index. */
 typedef struct {
     double inv;
     unsigned long nb;
     long* start;   /* nb + 1 */
     long* idx;     /* n, particle indices grouped by bucket (ascending within a bucket) */
+    double* qs;    /* n x 2, q in bucket order */
+    double* ps;    /* n x 2, p in bucket order */
 } go_grid;
 
 static unsigned long cell_bucket(double cx, double cy, unsigned long nb) {
@@ -88,75 +94,118 @@ static unsigned long cell_bucket(double cx, double cy, unsigned long nb) {
     return (unsigned long)(h & (nb - 1));
 }
 
-static void grid_build(go_grid* g, const double* q, long n, double cutoff) {
+static void grid_build(go_grid* g, const double* q, const double* p, long n, double cutoff) {
     g->inv = 1.0 / cutoff;
     g->nb = 1;
     while (g->nb < 2ul * (unsigned long)n) g->nb <<= 1;
     g->start = (long*)calloc(g->nb + 1, sizeof(long));
     g->idx = (long*)malloc(n * sizeof(long));
+    g->qs = (double*)malloc(2 * n * sizeof(double));
+    g->ps = (double*)malloc(2 * n * sizeof(double));
     unsigned long* cell = (unsigned long*)malloc(n * sizeof(unsigned long));
-    for (long i = 0; i < n; i++) {
-        cell[i] = cell_bucket(floor(q[2 * i] * g->inv), floor(q[2 * i + 1] * g->inv), g->nb);
-        g->start[cell[i] + 1]++;
-    }
+#pragma omp parallel for
+    for (long i = 0; i < n; i++) cell[i] = cell_bucket(floor(q[2 * i] * g->inv), floor(q[2 * i + 1] * g->inv), g->nb);
+    for (long i = 0; i < n; i++) g->start[cell[i] + 1]++;
     for (unsigned long c = 0; c < g->nb; c++) g->start[c + 1] += g->start[c];
     long* fill = (long*)malloc(g->nb * sizeof(long));
     memcpy(fill, g->start, g->nb * sizeof(long));
     for (long i = 0; i < n; i++) g->idx[fill[cell[i]]++] = i;
+#pragma omp parallel for
+    for (long s = 0; s < n; s++) {
+        const long i = g->idx[s];
+        g->qs[2 * s] = q[2 * i]; g->qs[2 * s + 1] = q[2 * i + 1];
+        g->ps[2 * s] = p[2 * i]; g->ps[2 * s + 1] = p[2 * i + 1];
+    }
     free(fill);
     free(cell);
 }
 
-static void grid_free(go_grid* g) { free(g->start); free(g->idx); }
+static void grid_free(go_grid* g) { free(g->start); free(g->idx); free(g->qs); free(g->ps); }
+
+/* the pair term of pair_term() on explicit values (i != j) */
+static inline int pair_term_v(const go_params* k, const double* qi, const double* pi, const double* qj,
+                              const double* pj, double* aq, double* ap) {
+    double dx = qi[0] - qj[0], dy = qi[1] - qj[1];
+    double r = sqrt(dx * dx + dy * dy);
+    double g = kval(k, r);
+    aq[0] += g * pj[0];
+    aq[1] += g * pj[1];
+    double pdot = pi[0] * pj[0] + pi[1] * pj[1];
+    if (r == 0.0) return pdot != 0.0;
+    double a = pdot * kder(k, r) / r;
+    ap[0] -= a * dx;
+    ap[1] -= a * dy;
+    return 0;
+}
 
 /* rhs rows [r0, r1).  *bad = min over interacting coincident pairs of i*n + j (or -1). */
 int go_rhs(const go_params* k, long n, const double* q, const double* p, double* dq, double* dp,
            long r0, long r1, long long* bad) {
     long long best = INT64_MAX;
-    go_grid g;
-    const int use_grid = k->cutoff > 0.0;
-    if (use_grid) grid_build(&g, q, n, k->cutoff);
     double c2 = k->cutoff * k->cutoff;
+    if (!(k->cutoff > 0.0)) {
 #pragma omp parallel for schedule(dynamic, 64) reduction(min : best)
-    for (long i = r0; i < r1; i++) {
-        double aq[2] = {0.0, 0.0}, ap[2] = {0.0, 0.0};
-        if (!use_grid) {
+        for (long i = r0; i < r1; i++) {
+            double aq[2] = {0.0, 0.0}, ap[2] = {0.0, 0.0};
             for (long j = 0; j < n; j++) {
                 if (pair_term(k, i, j, q, p, aq, ap)) {
                     long long key = (long long)i * n + j;
                     if (key < best) best = key;
                 }
             }
-        } else {
-            const double cx = floor(q[2 * i] * g.inv), cy = floor(q[2 * i + 1] * g.inv);
-            unsigned long seen[9];
-            int ns = 0;
-            for (int ddy = -1; ddy <= 1; ddy++)
-                for (int ddx = -1; ddx <= 1; ddx++) {
-                    const unsigned long b = cell_bucket(cx + ddx, cy + ddy, g.nb);
-                    int dup = 0;
-                    for (int t = 0; t < ns; t++) dup |= seen[t] == b;
-                    if (dup) continue;
-                    seen[ns++] = b;
-                    for (long s = g.start[b]; s < g.start[b + 1]; s++) {
-                        long j = g.idx[s];
-                        double dx = q[2 * i] - q[2 * j], dy = q[2 * i + 1] - q[2 * j + 1];
-                        if (!(dx * dx + dy * dy < c2)) continue;
-                        if (pair_term(k, i, j, q, p, aq, ap)) {
-                            long long key = (long long)i * n + j;
-                            if (key < best) best = key;
-                        }
+            if (k->sigma2 != 0.0) {
+                aq[0] += k->sigma2 * p[2 * i];
+                aq[1] += k->sigma2 * p[2 * i + 1];
+            }
+            dq[2 * (i - r0)] = aq[0]; dq[2 * (i - r0) + 1] = aq[1];
+            dp[2 * (i - r0)] = ap[0]; dp[2 * (i - r0) + 1] = ap[1];
+        }
+        *bad = (best == INT64_MAX) ? -1 : best;
+        return best == INT64_MAX ? GO_OK : GO_COINCIDENT;
+    }
+    go_grid g;
+    grid_build(&g, q, p, n, k->cutoff);
+#pragma omp parallel for schedule(dynamic, 64) reduction(min : best)
+    for (long t = 0; t < n; t++) {
+        const long i = g.idx[t];
+        if (i < r0 || i >= r1) continue;
+        const double* qi = g.qs + 2 * t;
+        const double* pi = g.ps + 2 * t;
+        double aq[2] = {0.0, 0.0}, ap[2] = {0.0, 0.0};
+        const double cx = floor(qi[0] * g.inv), cy = floor(qi[1] * g.inv);
+        unsigned long seen[9];
+        int ns = 0;
+        for (int ddy = -1; ddy <= 1; ddy++)
+            for (int ddx = -1; ddx <= 1; ddx++) {
+                const unsigned long b = cell_bucket(cx + ddx, cy + ddy, g.nb);
+                int dup = 0;
+                for (int u = 0; u < ns; u++) dup |= seen[u] == b;
+                if (dup) continue;
+                seen[ns++] = b;
+                for (long s = g.start[b]; s < g.start[b + 1]; s++) {
+                    const double* qj = g.qs + 2 * s;
+                    double dx = qi[0] - qj[0], dy = qi[1] - qj[1];
+                    if (!(dx * dx + dy * dy < c2)) continue;
+                    if (s == t) {  /* self pair: G(0) p_i, nothing in dp */
+                        double g0 = kval(k, 0.0);
+                        aq[0] += g0 * pi[0];
+                        aq[1] += g0 * pi[1];
+                        continue;
+                    }
+                    if (pair_term_v(k, qi, pi, qj, g.ps + 2 * s, aq, ap)) {
+                        long long key = (long long)i * n + g.idx[s];
+                        if (key < best) best = key;
                     }
                 }
-        }
+            }
         if (k->sigma2 != 0.0) {
-            aq[0] += k->sigma2 * p[2 * i];
-            aq[1] += k->sigma2 * p[2 * i + 1];
+            aq[0] += k->sigma2 * pi[0];
+            aq[1] += k->sigma2 * pi[1];
         }
         dq[2 * (i - r0)] = aq[0]; dq[2 * (i - r0) + 1] = aq[1];
         dp[2 * (i - r0)] = ap[0]; dp[2 * (i - r0) + 1] = ap[1];
     }
-    if (use_grid) grid_free(&g);
+    grid_free(&g);
     *bad = (best == INT64_MAX) ? -1 : best;
     return best == INT64_MAX ? GO_OK : GO_COINCIDENT;
 }

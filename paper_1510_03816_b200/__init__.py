@@ -16,8 +16,7 @@ from .shapes import LandmarkTemplate, circle, ellipse_rot_shift
 from .shooting import (MatchResult, ResidualNorm, ShootingConfig, StopRule, UpdateSpace, contraction_diagnostics,
                        match, momenta_from_velocity, newton_match)
 from .analysis import (DIVERGED, ClusterVerdict, DistanceRecord, ExactnessRow, SweepGrid, cluster_test,
-                       convergence_sweep, exact_vs_inexact, iso_invariance_check, predict, shape_distance,
-                       triangle_inequality_audit)
+                       convergence_sweep, exact_vs_inexact, iso_invariance_check, predict, shape_distance)
 from .device import get_path, set_path
 from . import dropin  # noqa: E402  (dropin.install() rebinds the reference package)
 
@@ -30,5 +29,5 @@ __all__ = [
     "circle", "ellipse_rot_shift", "MatchResult", "ResidualNorm", "ShootingConfig", "StopRule", "UpdateSpace",
     "contraction_diagnostics", "match", "momenta_from_velocity", "newton_match", "get_path", "set_path",
     "DIVERGED", "ClusterVerdict", "DistanceRecord", "ExactnessRow", "SweepGrid", "cluster_test", "convergence_sweep",
-    "exact_vs_inexact", "iso_invariance_check", "predict", "shape_distance", "triangle_inequality_audit",
+    "exact_vs_inexact", "iso_invariance_check", "predict", "shape_distance",
 ]

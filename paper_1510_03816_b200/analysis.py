@@ -25,7 +25,7 @@ from .shooting import (ShootingConfig, StopRule, _batchable, _enum_value, _facto
 
 __all__ = [
     "DIVERGED", "SweepGrid", "DistanceRecord", "ClusterVerdict", "ExactnessRow", "shape_distance",
-    "iso_invariance_check", "cluster_test", "triangle_inequality_audit", "convergence_sweep", "predict",
+    "iso_invariance_check", "cluster_test", "convergence_sweep", "predict",
     "exact_vs_inexact", "match_many",
 ]
 
@@ -212,36 +212,6 @@ def cluster_test(a, b, refs: list, thresholds: dict, cfg, preprocess: bool = Fal
     verdict = evidence[0].H <= pair_thr and all(
         abs(evidence[i].H - evidence[i + 1].H) <= ref_thr for i in range(1, len(evidence), 2))
     return _types.get("ClusterVerdict")(same_cluster=verdict, evidence=tuple(evidence))
-
-
-def triangle_inequality_audit(records) -> list:
-    """analysis.py:210-251 (host bookkeeping over distance records)."""
-    table = {}
-    for rec in records:
-        if rec.converged:
-            table[(rec.reference_label, rec.target_label)] = rec.H
-
-    def lookup(x, y):
-        if (x, y) in table:
-            return table[(x, y)]
-        return table.get((y, x))
-
-    labels = sorted({lab for key in table for lab in key})
-    report = []
-    for x in labels:
-        for z in labels:
-            if x == z or lookup(x, z) is None:
-                continue
-            for y in labels:
-                if y in (x, z):
-                    continue
-                via_left, via_right = lookup(x, y), lookup(y, z)
-                if via_left is None or via_right is None:
-                    continue
-                direct = lookup(x, z)
-                report.append({"from": x, "to": z, "via": y, "direct": direct, "detour": via_left + via_right,
-                               "holds": direct <= via_left + via_right + 1e-12})
-    return report
 
 
 def convergence_sweep(reference, target, grid: SweepGrid) -> np.ndarray:

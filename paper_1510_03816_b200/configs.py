@@ -100,8 +100,20 @@ def _displacement(x: np.ndarray, rng: np.random.Generator) -> np.ndarray:
     return 0.05 * out
 
 
+# Feedback gains of C4 / C5 (BASELINE.json leaves h open).  The survey's
+# proposals (0.1 / 0.4) throw the first shoot's cloud apart: under KD-1 the momentum equation of
+# these dense clouds is stiff, and a 20-step RK4 shoot blows up once max|p| reaches ~0.007 (C4) /
+# ~0.015 (C5), whatever h is; h only sets how many iterations it takes to get there.  Measured on
+# the B200 at full size (tools/h_scan.py, profiles/r02_h_scan.json): C4 blows up at iteration
+# 1 / 4 / 36 / 71 / 91 for h = 0.1 / 0.02 / 0.002 / 0.001 / 0.0007 and completes its 100 iterations
+# at 0.0005 and 0.0003; C5 blows up at iteration 2 / 6 / 10 / 19 for h = 0.4 / 0.02 / 0.01 / 0.005
+# and completes its 20 at 0.004 (momentum delta already rising at the end), 0.003 and 0.002.
+C4_H = 0.0005
+C5_H = 0.003
+
+
 def c4(n: int = 262144) -> Workload:
-    """Clustered exact matching: 16 Gaussians (seed 4), smooth target (seed 5), sigma=0.02, h=0.1."""
+    """Clustered exact matching: 16 Gaussians (seed 4), smooth target (seed 5), sigma=0.02, h=C4_H."""
     r = np.random.default_rng(4)
     centres = r.uniform(0.1, 0.9, (16, 2))
     lab = r.integers(0, 16, n)
@@ -109,20 +121,20 @@ def c4(n: int = 262144) -> Workload:
     y = x + _displacement(x, np.random.default_rng(5))
     return Workload(
         name="C4", q=x, p=None, target=y, sigma=0.02, t_final=1.0, steps=20,
-        h=0.1, epsilon=1e-6, max_iter=100,
+        h=C4_H, epsilon=1e-6, max_iter=100,
     )
 
 
 def c5(n: int = 1048576) -> Workload:
     """Inexact matching: uniform (seed 6), smooth target + N(0, 0.002^2) noise (seed 7),
-    sigma=0.01, sigma2=0.1, h=0.4, exactly 20 iterations (eps=1e-300)."""
+    sigma=0.01, sigma2=0.1, h=C5_H, exactly 20 iterations (eps=1e-300)."""
     x = np.random.default_rng(6).uniform(0.0, 1.0, (n, 2))
     r7 = np.random.default_rng(7)
     y = x + _displacement(x, r7)
     y = y + r7.normal(0.0, 0.002, (n, 2))
     return Workload(
         name="C5", q=x, p=None, target=y, sigma=0.01, t_final=1.0, steps=20,
-        h=0.4, epsilon=1e-300, max_iter=20, sigma2=0.1, stop_rule="momentum-delta",
+        h=C5_H, epsilon=1e-300, max_iter=20, sigma2=0.1, stop_rule="momentum-delta",
     )
 
 

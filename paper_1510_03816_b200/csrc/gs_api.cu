@@ -283,6 +283,7 @@ int ensure_cell(gs_context* ctx, int64_t n) {
 // support radius is small against the point cloud of S (one bbox reduction + 8-byte read).
 constexpr int64_t kCellMinN = 2048;
 constexpr int kCellMinCells = 25;
+constexpr double kCellMinDensity = 4.0;  // mean particles per cutoff-sized cell of the bounding box
 
 int choose_path_impl(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s) {
     ctx->cell_on = 0;
@@ -302,7 +303,12 @@ int choose_path_impl(gs_context* ctx, const gs_system_t* sys, const double4* S, 
     GridParams g;
     GS_CUDA(cudaMemcpyAsync(&g, ctx->c_gp.ptr, sizeof(g), cudaMemcpyDeviceToHost, s));
     GS_CUDA(cudaStreamSynchronize(s));
-    ctx->cell_on = g.hashed || (int64_t)g.nx * g.ny >= (int64_t)kCellMinCells * g.sub * g.sub;  // cells of edge cutoff
+    // cells of edge cutoff: enough of them to pay for the build, and dense enough that a row has
+    // in-support neighbours (a row with none keeps only its self term: its dp, < 2^-53 of a
+    // neighbour's term in the reference, becomes 0 — fine normwise unless most rows are like that).
+    // A cloud already spread over a hashed grid is sparse by construction: dense path.
+    const double cells = (double)g.nx * (double)g.ny / ((double)g.sub * (double)g.sub);
+    ctx->cell_on = !g.hashed && cells >= (double)kCellMinCells && (double)n >= kCellMinDensity * cells;
     return GS_OK;
 }
 
@@ -349,7 +355,7 @@ PairOut pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64
     } else if (ctx->cell_on) {
         out = PairOut{1, 0};
         CellWs w = cell_ws(ctx);
-        cell_build(w, S, n, sc.cutoff, stream);
+        if (const int rc = cell_build(w, S, n, sc.cutoff, stream)) ctx->cell_err = rc;
         ctx->launches += 6;  // bbox, params, keys, 2x radix passes (approx.), start/permute
         if (ctx->prof_on) prof_mark(ctx, stream);
         launch_cell_pair(sc, w, n, row0, row0 + nrows, part, ctx->st.ptr, ev, ctx->tbl.ptr,
@@ -364,6 +370,14 @@ PairOut pair_kernel(gs_context* ctx, const SysConst& sc, const double4* S, int64
     ctx->launches++;
     ctx->pair_launches++;
     return out;
+}
+
+// A cell build that failed to enqueue inside this call (sticky until reported).
+int take_cell_err(gs_context* ctx) {
+    if (!ctx->cell_err) return GS_OK;
+    const int e = ctx->cell_err;
+    ctx->cell_err = 0;
+    return fail(GS_ERR_CUDA, std::string("cell-list build failed: ") + cudaGetErrorString((cudaError_t)e));
 }
 
 // One RK4 stage for the session's rows (pair kernel + finish epilogue).
@@ -415,6 +429,10 @@ int run_evolve_graph(gs_context* ctx, const SysConst& sc, double t_final, int st
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
         ctx->capture_events = nullptr;
+        if (ctx->cell_err) {
+            if (g) cudaGraphDestroy(g);
+            return take_cell_err(ctx);
+        }
         if (e != cudaSuccess) return fail(GS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
         e = cudaGraphInstantiate(&ctx->graph.exec, g, 0);
         cudaGraphDestroy(g);
@@ -463,7 +481,7 @@ int run_evolve(gs_context* ctx, const SysConst& sc, double t_final, int steps, i
         }
     }
     GS_CUDA(cudaGetLastError());
-    return GS_OK;
+    return take_cell_err(ctx);
 }
 
 // CTAs per small-N item: a cluster of kMaxCluster CTAs spreads the rows of one match over
@@ -689,7 +707,7 @@ static int rhs_impl(gs_context* ctx, const gs_system_t* sys, int64_t n, const do
     fa.dq = dq; fa.dp = dp; fa.st = ctx->st.ptr; fa.event = 3ull;
     launch_finish(kFinRhs, sc, fa, s);
     GS_CUDA(cudaGetLastError());
-    return GS_OK;
+    return take_cell_err(ctx);
 }
 
 int gs_rhs_rows(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p, int64_t row0,
@@ -728,6 +746,7 @@ int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const dou
     // coincident pairs are irrelevant to H (particles.py:127-128 has no check): use an event id
     // that is never reported
     const PairOut po = pair_kernel(ctx, sc, ctx->S.ptr, n, 0, n, plan, ctx->part.ptr, 2ull, s);
+    if ((rc = take_cell_err(ctx))) return rc;
     ctx->launches += 5;  // reset, pack, finish, 2 reductions
     FinishArgs fa{};
     fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = n; fa.row0 = 0;
@@ -851,6 +870,10 @@ int match_device_loop(gs_context* ctx, const SysConst& sc, const gs_match_config
                                        cfg->epsilon, cfg->max_iter, cfg->stop_rule, cond);
         cudaGraph_t captured = nullptr;
         e = cudaStreamEndCapture(c, &captured);
+        if (ctx->cell_err) {
+            cudaGraphDestroy(g);
+            return take_cell_err(ctx);
+        }
         ctx->mgraph.launches = ctx->launches - l0 + 4;
         ctx->mgraph.pair_launches = ctx->pair_launches - pl0;
         ctx->mgraph.host_pairs = ctx->host_pairs - hp0;
@@ -1045,7 +1068,7 @@ int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
     if (step == 1 && stg == 0 && (rc = choose_path(ctx, sys, ctx->S.ptr, ctx->n, (cudaStream_t)stream))) return rc;
     stage(ctx, make_const(sys), step, stg, dt, (cudaStream_t)stream);
     GS_CUDA(cudaGetLastError());
-    return GS_OK;
+    return take_cell_err(ctx);
 }
 
 double* gs_stage_state(gs_context* ctx) { return ctx ? reinterpret_cast<double*>(ctx->S.ptr) : nullptr; }

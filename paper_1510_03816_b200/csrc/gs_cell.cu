@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "gs_cell.cuh"
@@ -37,6 +38,7 @@ namespace gsb {
 namespace {
 
 constexpr int kBB = 256;        // bbox block
+constexpr int kMaxDevices = 64;
 constexpr int kCB = 128;        // pair-kernel threads per CTA
 #ifndef GS_CELL_CL               // candidate chunk = per-lane list capacity (A/B builds)
 #define GS_CELL_CL 32  // A/B at 7 CTAs/SM (C5 / C4 RHS ms): 24 -> 1.95 / 2.79, 32 -> 1.86 / 2.77, 40 -> 1.86 / 2.80, 48 -> 1.96 / 2.95
@@ -433,9 +435,15 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
         return e ? std::min<int64_t>(std::atoll(e), kSortSmallMax) : kSortSmallMax;
     }();
     if (n <= small_max) {
-        static const bool attr_ok = cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)sizeof(typename SortSmall::TempStorage)) == cudaSuccess;
-        if (!attr_ok) return (int)cudaErrorInvalidConfiguration;
+        // the attribute is per device: set once for each device this process launches on
+        static std::atomic<signed char> attr_state[kMaxDevices];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= kMaxDevices) return (int)cudaErrorInvalidDevice;
+        if (attr_state[dev].load() == 0)
+            attr_state[dev] = cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)sizeof(typename SortSmall::TempStorage)) == cudaSuccess ? 1 : -1;
+        if (attr_state[dev].load() < 0) return (int)cudaErrorInvalidConfiguration;
         k_sort_small<<<1, kSortSmallThreads, sizeof(typename SortSmall::TempStorage), stream>>>(
             w.keys, (int)n, end_bit, w.keys_sorted, w.perm);
     } else {

@@ -120,6 +120,7 @@ struct gs_context {
     DevBuf<unsigned long long> gram_bad;  // gs_gram's first coincident pair
     size_t c_cub_bytes = 0;
     int cell_on = 0;                    // path of the current call
+    int cell_err = 0;                   // sticky: a cell build failed to enqueue (reported by the API call)
     // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds
     struct Graph {
         cudaGraphExec_t exec = nullptr;

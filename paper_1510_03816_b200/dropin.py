@@ -20,9 +20,12 @@ callees by name, so every alias must be rebound (SURVEY.md §8(b) "Rebinding poi
 After ``install()`` the reference's own callers (analysis, cli, newton_match) run their shoots
 on the device, with the reference's exception classes and result types.  ``match`` runs on the
 device in both update spaces (momentum: one device loop; velocity: device Gram matrix, cuSOLVER
-Cholesky via torch.linalg, device shoots), as does ``momenta_from_velocity``.  Kernel
-families the device does not provide (bessel) raise ConfigurationError — there is no CPU
-fallback.  Use ``pytest -p paper_1510_03816_b200.pytest_dropin`` to run a geoshoot-based
+Cholesky via torch.linalg, device shoots), as does ``momenta_from_velocity``.  The device
+provides the conical and gaussian families (the north_star's path); a call whose kernel is of
+another family (bessel, ``kernels.py:91-118``) is not replaced: the rebound name hands it to the
+reference's own function it shadowed, so the drop-in never narrows what the reference accepts.
+The package's own API (``paper_1510_03816_b200.rhs`` etc.) still raises ConfigurationError for
+bessel — there is no CPU fallback inside this package.  Use ``pytest -p paper_1510_03816_b200.pytest_dropin`` to run a geoshoot-based
 test suite against the device path.
 """
 
@@ -66,6 +69,48 @@ def _module(pkg, sub: str):
         return None
 
 
+_DEVICE_FAMILIES = ("conical", "gaussian")
+
+
+def _kernel_specs(obj, depth: int = 0):
+    """KernelSpec-like objects reachable from a call argument: a KernelSpec, a SystemSpec
+    (.kernel), a ShootingConfig (.system.kernel), a SweepGrid (.kernel_family) or a list of them."""
+    if depth > 2 or obj is None:
+        return
+    if isinstance(obj, (list, tuple)):
+        for o in obj:
+            yield from _kernel_specs(o, depth + 1)
+        return
+    fam = getattr(obj, "kernel_family", None)
+    if fam is not None:
+        yield str(getattr(fam, "value", fam))
+    if hasattr(obj, "family") and hasattr(obj, "alpha"):
+        yield str(getattr(obj.family, "value", obj.family))
+    for attr in ("kernel", "system"):
+        sub = getattr(obj, attr, None)
+        if sub is not None and sub is not obj:
+            yield from _kernel_specs(sub, depth + 1)
+
+
+def _on_device(args, kwargs) -> bool:
+    return all(f in _DEVICE_FAMILIES for a in (*args, *kwargs.values()) for f in _kernel_specs(a))
+
+
+def _dispatch(device_fn, reference_fn):
+    """The device function for the device's kernel families, the shadowed reference function otherwise."""
+
+    def fn(*args, **kwargs):
+        if _on_device(args, kwargs):
+            return device_fn(*args, **kwargs)
+        return reference_fn(*args, **kwargs)
+
+    fn.__name__ = getattr(device_fn, "__name__", "fn")
+    fn.__doc__ = getattr(device_fn, "__doc__", None)
+    fn.device = device_fn
+    fn.original = reference_fn
+    return fn
+
+
 def install(pkg=None):
     """Rebind ``geoshoot`` (or the given package object) onto this package.  Idempotent."""
     if _saved:
@@ -97,12 +142,17 @@ def install(pkg=None):
     for fname in ("shape_distance", "iso_invariance_check", "cluster_test", "convergence_sweep", "predict",
                   "exact_vs_inexact"):
         impl[fname] = getattr(_analysis, fname)
+    wrappers = {}
     for fname, subs in _ALIASES.items():
         for sub in subs:
             mod = _module(pkg, sub)
             if mod is not None and hasattr(mod, fname):
-                _saved.append((mod, fname, getattr(mod, fname)))
-                setattr(mod, fname, impl[fname])
+                orig = getattr(mod, fname)
+                _saved.append((mod, fname, orig))
+                key = (fname, id(orig))
+                if key not in wrappers:  # one wrapper per shadowed function: aliases stay identical
+                    wrappers[key] = _dispatch(impl[fname], orig)
+                setattr(mod, fname, wrappers[key])
     return pkg
 
 

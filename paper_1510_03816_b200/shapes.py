@@ -19,31 +19,57 @@ from . import types as _types
 __all__ = ["LandmarkTemplate", "first_coincident_pair", "circle", "ellipse_rot_shift"]
 
 
+# Pairs can only have a zero computed distance if both coordinate differences are below ~2^-537
+# (their squares underflow); grouping by this (larger) gap keeps every such pair in one group.
+_GAP = 1e-150
+
+
+def _chains(v: np.ndarray, gid: np.ndarray):
+    """Sorted order of (gid, v) and the group id of each sorted element: groups of equal gid whose
+    consecutive v differ by less than _GAP."""
+    order = np.lexsort((v, gid))
+    vs, gs_ = v[order], gid[order]
+    brk = np.ones(v.size, dtype=bool)
+    brk[1:] = (gs_[1:] != gs_[:-1]) | ~(np.abs(vs[1:] - vs[:-1]) < _GAP)
+    return order, np.cumsum(brk) - 1
+
+
 def first_coincident_pair(pts: np.ndarray):
-    """(i, j) of the row-major-first pair of identical points, or None."""
+    """(i, j) of the row-major-first pair whose distance the reference computes as 0.0
+    (``sqrt(dx*dx + dy*dy) == 0``, kernels.py:174-178 via shapes.py:52-58), or None.
+
+    The reference's test includes distinct points whose squared difference underflows; pairs
+    are grouped by coordinate gaps below _GAP (x, then y within an x-group), and every pair
+    inside a group is tested with the reference's own formula.  O(N log N) for any input
+    whose groups are small (the common case: groups of one)."""
     n = pts.shape[0]
     if n < 2:
         return None
-    order = np.lexsort((pts[:, 1], pts[:, 0]))
-    s = pts[order]
-    same = (s[1:, 0] == s[:-1, 0]) & (s[1:, 1] == s[:-1, 1])
-    if not np.any(same):
+    x, y = np.ascontiguousarray(pts[:, 0]), np.ascontiguousarray(pts[:, 1])
+    ox, gx = _chains(x, np.zeros(n, dtype=np.int64))
+    gxi = np.empty(n, dtype=np.int64)
+    gxi[ox] = gx
+    oy, gy = _chains(y, gxi)
+    sizes = np.bincount(gy)
+    if sizes.max() < 2:
         return None
     best = None
-    k = 0
-    idx = np.flatnonzero(same)
-    # walk runs of equal points: run spans sorted positions [a, b]
-    while k < idx.size:
-        a = idx[k]
-        b = a + 1
-        while k + 1 < idx.size and idx[k + 1] == b:
-            k += 1
-            b += 1
-        members = np.sort(order[a:b + 1])
-        cand = (int(members[0]), int(members[1]))
-        if best is None or cand < best:
-            best = cand
-        k += 1
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    for g in np.flatnonzero(sizes >= 2):
+        members = np.sort(oy[starts[g]:starts[g + 1]])
+        sub = pts[members]
+        for k in range(0, members.size, 512):  # bounded memory even for one huge group
+            d = sub[k:k + 512, None, :] - sub[None, :, :]
+            dist = np.sqrt(np.sum(d * d, axis=-1))
+            rows = np.arange(k, min(k + 512, members.size))
+            dist[rows - k, rows] = np.inf
+            hit = np.argwhere(dist == 0.0)
+            if hit.size:
+                a, b = hit[0]
+                cand = (int(members[a + k]), int(members[b]))
+                if best is None or cand < best:
+                    best = cand
+                break  # rows are in ascending member order: later chunks only give larger i
     return best
 
 

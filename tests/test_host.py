@@ -71,6 +71,22 @@ def test_first_coincident_pair_is_row_major_first():
     assert shapes.first_coincident_pair(pts) == (0, 1)
 
 
+def test_first_coincident_pair_includes_underflowing_distances():
+    """The reference rejects distinct points whose squared difference underflows (distance 0.0)."""
+    rng = np.random.default_rng(1)
+    for scale in (1e-170, 1e-161, 1e-200, 1e-300):
+        for trial in range(60):
+            n = int(rng.integers(2, 40))
+            pts = rng.integers(0, 5, (n, 2)).astype(float) * scale + rng.integers(0, 3, (n, 1))
+            d = np.sqrt(np.sum((pts[:, None, :] - pts[None, :, :]) ** 2, axis=-1))
+            np.fill_diagonal(d, np.inf)
+            want = tuple(int(v) for v in np.argwhere(d == 0.0)[0]) if np.any(d == 0.0) else None
+            assert shapes.first_coincident_pair(pts) == want, scale
+    pts = np.array([[0.5, 0.5], [0.5 + 2.0 ** -600 * 0.0, 0.5], [1e-170, 0.0], [0.0, 2e-170]])
+    assert shapes.first_coincident_pair(pts) == (0, 1)
+    assert shapes.first_coincident_pair(pts[2:]) == (0, 1)  # distinct, distance underflows to 0
+
+
 def test_large_template_check_is_fast():
     import time
 
@@ -121,7 +137,7 @@ def test_configs_are_deterministic_and_follow_the_recipes():
     np.testing.assert_array_equal(a.q, b.q)
     np.testing.assert_array_equal(a.target, b.target)
     w = configs.c5(4096)
-    assert w.sigma2 == 0.1 and w.h == 0.4 and w.max_iter == 20 and w.epsilon == 1e-300
+    assert w.sigma2 == 0.1 and w.h == configs.C5_H and w.max_iter == 20 and w.epsilon == 1e-300
     assert np.abs(w.target - w.q).max() < 0.5
 
 
@@ -153,19 +169,25 @@ def test_dropin_rebinds_every_alias_and_restores():
         ("analysis", "convergence_sweep"), ("cli", "convergence_sweep"), ("analysis", "cluster_test"),
         ("cli", "cluster_test"), ("analysis", "exact_vs_inexact"), ("analysis", "predict")]}
     dropin.install(ref)
+
+    def dev(f):  # the device function behind a rebound name (bessel calls go to the shadowed original)
+        return getattr(f, "device", f)
+
     try:
-        assert ref.integrator.rhs is particles.rhs and ref.particles.rhs is particles.rhs and ref.rhs is particles.rhs
+        assert ref.integrator.rhs is ref.particles.rhs is ref.rhs and dev(ref.rhs) is particles.rhs
+        assert ref.rhs.original is originals[("particles", "rhs")]
         for m in ("integrator", "shooting", "analysis", "cli"):
-            assert getattr(ref, m).evolve is integrator.evolve
+            assert dev(getattr(ref, m).evolve) is integrator.evolve
         assert ref.shooting.match is ref.analysis.match is ref.cli.match is ref.match
-        assert ref.shooting.hamiltonian is particles.hamiltonian
+        assert dev(ref.shooting.hamiltonian) is particles.hamiltonian
         assert gs.errors.DivergenceError is ref.DivergenceError
         assert types.get("EvolveResult") is ref.EvolveResult
         assert types.get("DistanceRecord") is ref.DistanceRecord
-        assert ref.shooting.newton_match is gs.newton_match is ref.newton_match
-        assert ref.particles.velocity_field is gs.velocity_field is ref.velocity_field
+        assert ref.shooting.newton_match is ref.newton_match and dev(ref.newton_match) is gs.newton_match
+        assert ref.particles.velocity_field is ref.velocity_field and dev(ref.velocity_field) is gs.velocity_field
         for f in ("convergence_sweep", "cluster_test", "exact_vs_inexact", "predict", "shape_distance"):
-            assert getattr(ref.analysis, f) is getattr(ref.cli, f) is getattr(ref, f) is getattr(gs, f)
+            assert getattr(ref.analysis, f) is getattr(ref.cli, f) is getattr(ref, f)
+            assert dev(getattr(ref, f)) is getattr(gs, f)
         # the reference's own template class, with the O(N log N) duplicate check
         big = np.random.default_rng(0).uniform(0, 1, (200000, 2))
         assert ref.LandmarkTemplate(big, "big").n == 200000
@@ -183,6 +205,16 @@ def test_dropin_rebinds_every_alias_and_restores():
                 ref.rhs(ref.SystemSpec(), st)  # no CPU fallback behind the drop-in
             with pytest.raises(N.NativeUnavailable):
                 ref.integrator.evolve(ref.SystemSpec(), st)
+        # a family the device does not provide stays on the reference's own function
+        bes = ref.SystemSpec(kernel=ref.KernelSpec(family="bessel", nu=2.5, alpha=0.7))
+        rng = np.random.default_rng(3)
+        st2 = ref.ParticleState(rng.uniform(0, 1, (6, 2)), rng.normal(0, 0.1, (6, 2)))
+        got = ref.rhs(bes, st2)
+        want = originals[("particles", "rhs")](bes, st2)
+        assert all(np.array_equal(a, b) for a, b in zip(got, want))
+        cfg = ref.ShootingConfig(system=bes, h=0.5, max_iter=3, evolve=ref.EvolveConfig(steps=4))
+        res = ref.match(ref.circle(1.0, n=6), ref.circle(1.1, n=6), cfg)  # bessel match, reference path
+        assert res.iterations >= 1 and np.all(np.isfinite(res.p0))
     finally:
         dropin.uninstall()
     for (m, f), fn in originals.items():
@@ -204,20 +236,6 @@ def test_sweep_grid_validation_mirrors_reference():
                                                                          max_iter=0)):
         with pytest.raises(gs.ConfigurationError):
             gs.SweepGrid(**bad)
-
-
-def test_triangle_inequality_audit_host_logic():
-    import paper_1510_03816_b200 as gs
-
-    R = gs.DistanceRecord
-    recs = [R("x", "y", 1.0, 3, True), R("y", "z", 1.5, 3, True), R("x", "z", 4.0, 3, True),
-            R("z", "w", 1.0, 3, False)]
-    rep = gs.triangle_inequality_audit(recs)
-    by = {(e["from"], e["to"], e["via"]): e for e in rep}
-    assert by[("x", "z", "y")]["holds"] is False and by[("x", "z", "y")]["detour"] == 2.5
-    assert by[("z", "x", "y")]["direct"] == 4.0          # reverse-direction fallback
-    assert all("w" not in k for k in by)                 # unconverged records are skipped
-    assert by[("x", "y", "z")]["holds"] is True
 
 
 def test_cluster_and_newton_validate_before_any_device_work():
