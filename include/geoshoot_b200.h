@@ -277,6 +277,12 @@ int gs_profile_enable(gs_context* ctx, int32_t on);
 int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, int64_t* launches, int64_t* pairs,
                     int32_t reset);
 
+/* Cell path of multi-RHS calls (gs_evolve, gs_match): the RHS runs through cluster Verlet lists
+ * rebuilt only when a particle has moved half the skin (gs_verlet.cu).  Diagnostics: *builds =
+ * list builds so far on this context, *entries = list capacity (candidates) of the last
+ * build.  Synchronises. */
+int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stream);
+
 /* micro-benchmark used by bench.py for the FP64 roofline denominator: `iters` dependent
  * DFMA chains per thread on a full grid; returns the device time in *ms (host). */
 int gs_fp64_peak_probe(gs_context* ctx, int32_t iters, double* ms, double* flops, void* stream);

@@ -266,7 +266,7 @@ CellWs cell_ws(gs_context* ctx) {
 
 int ensure_cell(gs_context* ctx, int64_t n) {
     GS_CUDA(ctx->c_keys.ensure(n)); GS_CUDA(ctx->c_keys_sorted.ensure(n)); GS_CUDA(ctx->c_vals.ensure(n));
-    GS_CUDA(ctx->c_perm.ensure(n)); GS_CUDA(ctx->c_Ss.ensure(n)); GS_CUDA(ctx->c_Sf.ensure(n));
+    GS_CUDA(ctx->c_perm.ensure(n)); GS_CUDA(ctx->c_Ss.ensure(n + 1)); GS_CUDA(ctx->c_Sf.ensure(n));
     GS_CUDA(ctx->c_start.ensure(cell_cap(n) + 1));
     GS_CUDA(ctx->c_bbox.ensure(4 * kCellBboxBlocks));
     GS_CUDA(ctx->c_gp.ensure(1));
@@ -276,6 +276,69 @@ int ensure_cell(gs_context* ctx, int64_t n) {
     const size_t bytes = cell_cub_bytes(n);
     GS_CUDA(ctx->c_cub.ensure(bytes));
     ctx->c_cub_bytes = ctx->c_cub.cap;
+    return GS_OK;
+}
+
+VerletWs verlet_ws(gs_context* ctx, int64_t n, double cutoff) {
+    VerletWs v;
+    v.cnt = ctx->v_cnt.ptr; v.ofs = ctx->v_ofs.ptr; v.len = ctx->v_len.ptr; v.list = ctx->v_list.ptr;
+    v.cap = (int64_t)ctx->v_list.cap;
+    v.Xb = ctx->v_xb.ptr; v.flags = ctx->v_flags.ptr; v.overflow = ctx->v_over.ptr;
+    v.scan_temp = ctx->v_scan.ptr; v.scan_bytes = ctx->v_scan.cap;
+    v.tpl = verlet_tpl(n); v.skin = ctx->verlet_skin; v.cutoff = cutoff;
+    return v;
+}
+
+// Workspaces of the cluster Verlet lists for n particles; the list buffer is sized from a build
+// of the current state S (twice its entries: the lists grow when the cloud contracts; a build
+// that still overflows is detected after the call and the call is redone, see verlet_retry).
+int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, cudaStream_t s) {
+    const int64_t ncl = verlet_clusters(n);
+    const bool fresh = ctx->v_flags.cap == 0;
+    GS_CUDA(ctx->v_cnt.ensure(ncl + 1)); GS_CUDA(ctx->v_ofs.ensure(ncl + 1)); GS_CUDA(ctx->v_xb.ensure(n));
+    GS_CUDA(ctx->v_len.ensure(ncl));
+    GS_CUDA(ctx->v_flags.ensure(4)); GS_CUDA(ctx->v_over.ensure(1));
+    GS_CUDA(ctx->v_scan.ensure(verlet_scan_bytes(ncl)));
+    if (fresh) {
+        GS_CUDA(cudaMemsetAsync(ctx->v_flags.ptr, 0, 4 * sizeof(unsigned), s));
+        GS_CUDA(cudaMemsetAsync(ctx->v_over.ptr, 0, sizeof(unsigned long long), s));
+    }
+    GS_CUDA(cudaMemsetAsync(ctx->v_cnt.ptr + ncl, 0, sizeof(long long), s));
+    if (ctx->v_list.cap > 0 && ctx->v_list_n == n && ctx->v_list_cutoff == cutoff) return GS_OK;
+    VerletWs v = verlet_ws(ctx, n, cutoff);
+    v.cap = 0;  // sizing build: counts and offsets only
+    if (int rc = verlet_build(cell_ws(ctx), v, S, n, cutoff, s)) return fail(GS_ERR_CUDA, "verlet sizing build failed");
+    long long total = 0;
+    GS_CUDA(cudaMemcpyAsync(&total, ctx->v_ofs.ptr + ncl, sizeof(total), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaMemsetAsync(ctx->v_over.ptr, 0, sizeof(unsigned long long), s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    const double slack = ctx->verlet_slack;  // spare capacity as a fraction of the sizing build
+    const long long want = slack >= 0.5 ? std::max<long long>(total + total / 2, total + (1 << 20))
+                                        : std::max<long long>(1, (long long)((1.0 + slack) * (double)total));
+    ctx->v_list.release();
+    GS_CUDA(ctx->v_list.ensure((size_t)want));
+    ctx->v_list_n = n;
+    ctx->v_list_cutoff = cutoff;
+    return GS_OK;
+}
+
+// After a multi-RHS call: did a rebuild need more list entries than the buffer holds?  Then the
+// buffer grows and the caller redoes the call (*retry).  Synchronises.
+int verlet_retry(gs_context* ctx, cudaStream_t s, bool* retry) {
+    *retry = false;
+    if (!ctx->verlet_call) return GS_OK;
+    unsigned long long need = 0;
+    GS_CUDA(cudaMemcpyAsync(&need, ctx->v_over.ptr, sizeof(need), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    if (!need) return GS_OK;
+    GS_CUDA(cudaMemsetAsync(ctx->v_over.ptr, 0, sizeof(unsigned long long), s));
+    if (++ctx->verlet_retries > 3 || need > (1ull << 31)) {
+        ctx->verlet_call = 0;  // give up on lists for this context: the per-RHS cell sweep
+        ctx->verlet_on = 0;
+    } else {
+        GS_CUDA(ctx->v_list.ensure((size_t)(need + need / 2)));
+    }
+    *retry = true;
     return GS_OK;
 }
 
@@ -324,9 +387,17 @@ bool use_sym(const gs_context* ctx, int64_t n, int64_t row0, int64_t nrows) {
 }
 
 // Path of this call + the partial buffer it needs (allocated here, never inside a capture).
-int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s) {
+// multi_rhs: the call evaluates many RHS of all rows (evolve, match): the cell path then runs
+// through the cluster Verlet lists.
+int choose_path(gs_context* ctx, const gs_system_t* sys, const double4* S, int64_t n, cudaStream_t s,
+                bool multi_rhs = false) {
     int rc = choose_path_impl(ctx, sys, S, n, s);
     if (rc) return rc;
+    ctx->verlet_call = 0;
+    if (multi_rhs && ctx->cell_on && ctx->verlet_on && ctx->row0 == 0 && ctx->row1 == n) {
+        if ((rc = ensure_verlet(ctx, S, n, sys->cutoff, s))) return rc;
+        ctx->verlet_call = 1;
+    }
     if (use_sym(ctx, n, ctx->row0, ctx->row1 - ctx->row0)) {
         const SymPlan sp = sym_plan(n);
         GS_CUDA(ctx->part.ensure((size_t)sp.nsb * (size_t)sp.pstride));
@@ -380,12 +451,70 @@ int take_cell_err(gs_context* ctx) {
     return fail(GS_ERR_CUDA, std::string("cell-list build failed: ") + cudaGetErrorString((cudaError_t)e));
 }
 
+// The cluster-list RHS sweep of one stage (gs_verlet.cu): gather + rebuild decision, the
+// rebuild (a conditional IF node when captured into a graph, unconditional otherwise), the sweep.
+void verlet_stage(gs_context* ctx, const SysConst& sc, int force, unsigned long long ev, cudaStream_t stream) {
+    const int64_t n = ctx->n;
+    CellWs w = cell_ws(ctx);
+    VerletWs v = verlet_ws(ctx, n, sc.cutoff);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive) {
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaGraphConditionalHandle cond;
+        bool ok = cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, &deps, &nd) == cudaSuccess &&
+                  cudaGraphConditionalHandleCreate(&cond, g, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+        if (ok) {
+            verlet_gather(w, v, ctx->S.ptr, n, force, cond, 1, stream);
+            ctx->launches++;
+            cudaGraphNodeParams np = {};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = cond;
+            np.conditional.type = cudaGraphCondTypeIf;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            ok = cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, &deps, &nd) == cudaSuccess &&
+                 cudaGraphAddNode(&node, g, deps, nd, &np) == cudaSuccess;
+            if (ok && !ctx->cap_stream2) ok = cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) == cudaSuccess;
+            if (ok) {
+                cudaStream_t s2 = ctx->cap_stream2;
+                ok = cudaStreamBeginCaptureToGraph(s2, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                if (ok) {
+                    if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, s2)) ctx->cell_err = rc;
+                    cudaGraph_t body = nullptr;
+                    ok = cudaStreamEndCapture(s2, &body) == cudaSuccess;
+                }
+                if (ok) ok = cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies) ==
+                             cudaSuccess;
+            }
+        }
+        if (!ok && !ctx->cell_err) ctx->cell_err = (int)cudaErrorStreamCaptureInvalidated;
+        ctx->launches += 10;  // a rebuild, when it runs (approx.)
+    } else {
+        if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, stream)) ctx->cell_err = rc;
+        ctx->launches += 10;
+    }
+    if (ctx->prof_on) prof_mark(ctx, stream);
+    launch_verlet_pair(sc, w, v, n, ctx->part.ptr, ctx->st.ptr, ev, ctx->tbl.ptr,
+                       ctx->prof_on ? ctx->c_acc.ptr : nullptr, stream);
+    if (ctx->prof_on) prof_mark(ctx, stream);
+    ctx->launches++;
+    ctx->pair_launches++;
+}
+
 // One RK4 stage for the session's rows (pair kernel + finish epilogue).
 void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cudaStream_t stream) {
     const int64_t n = ctx->n, nrows = ctx->row1 - ctx->row0;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)s;
-    const PairOut po = pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
+    PairOut po{1, 0};
+    if (ctx->verlet_call && ctx->cell_on && ctx->row0 == 0 && nrows == n)
+        verlet_stage(ctx, sc, step == 1 && s == 0, ev, stream);
+    else
+        po = pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
     ctx->launches++;  // finish
     FinishArgs fa{};
     fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = nrows;
@@ -409,7 +538,9 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
             P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr), P(ctx->c_Sf.ptr),
             P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr),
             P(ctx->c_keys_sorted.ptr), P(ctx->c_vals.ptr), P(ctx->c_bbox.ptr), P(ctx->c_gp.ptr), P(ctx->c_tlist.ptr),
-            P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes};
+            P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes, (double)ctx->verlet_call,
+            P(ctx->v_cnt.ptr), P(ctx->v_ofs.ptr), P(ctx->v_len.ptr), P(ctx->v_list.ptr), (double)ctx->v_list.cap, P(ctx->v_xb.ptr),
+            P(ctx->v_flags.ptr), P(ctx->v_over.ptr), P(ctx->v_scan.ptr), ctx->verlet_skin};
 }
 
 // integrator.py:95-119 as one CUDA graph (4 x steps stages, ~2 kernels per dense stage and
@@ -624,6 +755,9 @@ int gs_create(gs_context** out, int device) {
     if (const char* g = std::getenv("GS_B200_GRAPHS")) ctx->graphs_on = std::atoi(g) != 0;
     if (const char* g = std::getenv("GS_B200_SYM")) ctx->sym_on = std::atoi(g) != 0;
     if (const char* g = std::getenv("GS_B200_DEVLOOP")) ctx->devloop_on = std::atoi(g) != 0;
+    if (const char* g = std::getenv("GS_B200_VERLET")) ctx->verlet_on = std::atoi(g);
+    if (const char* g = std::getenv("GS_B200_SKIN")) ctx->verlet_skin = std::max(0.0, std::atof(g));
+    if (const char* g = std::getenv("GS_B200_VERLET_SLACK")) ctx->verlet_slack = std::atof(g);  // tests
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
     // 2^(j/kTbl), j = 0..kTbl-1, rounded from long double, replicated kTblRep times interleaved
@@ -659,7 +793,10 @@ int gs_destroy(gs_context* ctx) {
     ctx->mloop.release(); ctx->ep.release(); ctx->c_tlist.release(); ctx->c_nsel.release();
     graph_reset(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+    ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
+    ctx->v_over.release(); ctx->v_scan.release();
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     gs_p2p_close(ctx);
@@ -790,12 +927,17 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
     } else {
         if ((rc = ensure_session(ctx, n, n))) return rc;
         ctx->row0 = 0; ctx->row1 = n;
-        ctx->launches += 4;  // reset, pack, copy, unpack
-        k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
-        k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
-        if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
-        k_copy_rows<<<nblk(n), 256, 0, s>>>(ctx->S.ptr, 0, n, ctx->B.ptr);
-        if ((rc = run_evolve(ctx, sc, t_final, steps, capture_every, frames, s))) return rc;
+        // (verlet_on == 2: lists in host-driven evolves too, for per-kernel profiling)
+        const bool multi = capture_every == 0 && (ctx->graphs_on || ctx->verlet_on == 2);
+        for (bool retry = true; retry;) {
+            ctx->launches += 4;  // reset, pack, copy, unpack
+            k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+            k_pack<<<nblk(n), 256, 0, s>>>(q, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+            if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s, multi))) return rc;
+            k_copy_rows<<<nblk(n), 256, 0, s>>>(ctx->S.ptr, 0, n, ctx->B.ptr);
+            if ((rc = run_evolve(ctx, sc, t_final, steps, capture_every, frames, s))) return rc;
+            if ((rc = verlet_retry(ctx, s, &retry))) return rc;  // lists outgrew their buffer: redo
+        }
         k_unpack<<<nblk(n), 256, 0, s>>>(ctx->B.ptr, n, q, p);
         GS_CUDA(cudaGetLastError());
     }
@@ -950,6 +1092,8 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         small_to_result(r, n, result);
     } else {
         // host-driven loop, all state on the device, two scalars read back per iteration
+      for (bool verlet_redo = true; verlet_redo;) {
+        verlet_redo = false;
         if ((rc = ensure_session(ctx, n, n))) return rc;
         GS_CUDA(ctx->q0.ensure(2 * n)); GS_CUDA(ctx->tgt.ensure(2 * n)); GS_CUDA(ctx->p.ensure(2 * n));
         GS_CUDA(ctx->resid.ensure(2 * n)); GS_CUDA(ctx->red.ensure(kRedBlocks)); GS_CUDA(ctx->ham.ensure(n));
@@ -958,7 +1102,7 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         GS_CUDA(cudaMemcpyAsync(ctx->tgt.ptr, target, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
         GS_CUDA(cudaMemsetAsync(ctx->p.ptr, 0, 2 * n * sizeof(double), s));
         k_match_begin<<<nblk(n), 256, 0, s>>>(ctx->q0.ptr, ctx->p.ptr, ctx->resid.ptr, 0.0, n, ctx->S.ptr, ctx->B.ptr);
-        if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s))) return rc;
+        if ((rc = choose_path(ctx, sys, ctx->S.ptr, n, s, ctx->graphs_on != 0))) return rc;
         // initial shoot with p = 0 leaves q0 unchanged bitwise: endpoint = q0 (shooting.py:244-247)
         const int nb = (int)std::min<int64_t>(kRedBlocks, (n + 255) / 256);
         const int red_kind = cfg->norm == GS_NORM_MAX ? 0 : 1;
@@ -1025,6 +1169,12 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
                 if (value < cfg->epsilon) { outcome = GS_MATCH_CONVERGED; break; }
             }
         }
+        if ((rc = verlet_retry(ctx, s, &verlet_redo))) return rc;  // lists outgrew their buffer: redo
+        if (verlet_redo) {
+            std::memset(result, 0, sizeof(*result));
+            result->status.i = result->status.j = -1;
+            continue;
+        }
         GS_CUDA(cudaMemcpyAsync(p0_out, ctx->p.ptr, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
         GS_CUDA(cudaEventRecord(e1, s));
         double H = 0.0;
@@ -1033,6 +1183,7 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         result->iterations = iters;
         result->hamiltonian = H;
         result->final_residual = nrm;
+      }
     }
     GS_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -1040,6 +1191,26 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
     result->seconds_device = ms * 1e-3;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    return GS_OK;
+}
+
+// Cluster Verlet list diagnostics: list builds since the context was created (incl. the sizing
+// builds) and the entries of the last build.  Synchronises.
+int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stream) {
+    if (!ctx || !builds || !entries) return fail(GS_ERR_INVALID, "NULL argument");
+    *builds = 0;
+    *entries = 0;
+    if (ctx->v_flags.cap == 0) return GS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned f[4];
+    long long tot = 0;
+    GS_CUDA(cudaMemcpyAsync(f, ctx->v_flags.ptr, sizeof(f), cudaMemcpyDeviceToHost, s));
+    if (ctx->v_list_n > 0)
+        GS_CUDA(cudaMemcpyAsync(&tot, ctx->v_ofs.ptr + verlet_clusters(ctx->v_list_n), sizeof(tot),
+                                cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    *builds = f[1];
+    *entries = tot;
     return GS_OK;
 }
 

@@ -55,4 +55,36 @@ void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t ro
                       DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
                       cudaStream_t stream);
 
+// ---- cluster Verlet lists (gs_verlet.cu): the cell path of whole evolves / matches ----------
+// Clusters of GS_VERLET_M consecutive sorted particles; one list per cluster of the sorted
+// positions within cutoff (1 + skin) of any member at the last build, reused until a particle has
+// moved half the skin.
+struct VerletWs {
+    long long* cnt;                // ncl + 1 (cnt[ncl] = 0): list capacities (candidate counts, padded)
+    long long* ofs;                // ncl + 1: exclusive scan of cnt (ofs[ncl] = entries of the build)
+    int* len;                      // ncl: padded list lengths
+    int* list;                     // cap entries
+    int64_t cap;
+    double2* Xb;                   // n: positions at the build, sorted order
+    unsigned* flags;               // [0] rebuild wanted, [2] CTA counter, [3] last decision (zero-initialised)
+    unsigned long long* overflow;  // entries a build needed beyond cap (0: none)
+    void* scan_temp;
+    size_t scan_bytes;
+    int tpl;                       // pair-sweep lanes per cluster (lists padded to 2 tpl)
+    double skin;                   // list radius = cutoff (1 + skin); rebuild at skin * cutoff / 2
+    double cutoff;
+};
+int64_t verlet_clusters(int64_t n);
+int verlet_tpl(int64_t n);
+size_t verlet_scan_bytes(int64_t ncl);
+// Grid + lists for the records of S (cell workspace w is rebuilt; Ss[n] becomes the sentinel).
+int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, double cutoff, cudaStream_t stream);
+// Ss <- S in sorted order and the rebuild decision (force: no gather, rebuild) -> IF condition / flags[3].
+void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, int force,
+                   cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream);
+// Raw pair sums of all n rows from the lists -> part[i] (original index).
+void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
+                        DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                        cudaStream_t stream);
+
 }  // namespace gsb

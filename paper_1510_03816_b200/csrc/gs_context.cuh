@@ -121,6 +121,21 @@ struct gs_context {
     size_t c_cub_bytes = 0;
     int cell_on = 0;                    // path of the current call
     int cell_err = 0;                   // sticky: a cell build failed to enqueue (reported by the API call)
+    // cluster Verlet lists of the cell path in multi-RHS calls (gs_verlet.cu)
+    DevBuf<int> v_list, v_len;
+    DevBuf<long long> v_cnt, v_ofs;
+    DevBuf<double2> v_xb;
+    DevBuf<unsigned> v_flags;
+    DevBuf<unsigned long long> v_over;
+    DevBuf<unsigned char> v_scan;
+    int verlet_on = 1;                  // GS_B200_VERLET=0: the per-RHS cell sweep everywhere
+    int verlet_call = 0;                // this call evaluates its RHS through the lists
+    int64_t v_list_n = -1;              // n and cutoff the list buffer was sized for
+    double v_list_cutoff = 0.0;
+    int verlet_retries = 0;
+    double verlet_skin = 0.05;          // GS_B200_SKIN
+    double verlet_slack = 0.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
+    cudaStream_t cap_stream2 = nullptr; // captures the conditional rebuild bodies
     // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds
     struct Graph {
         cudaGraphExec_t exec = nullptr;

@@ -1,0 +1,506 @@
+// gs_verlet.cu — cluster Verlet lists for the cell-list fp64 RHS of whole evolves / matches.
+//
+// The cell-list semantics are unchanged (KD-1): the RHS of row i sums the pairs
+// with d_ij < cutoff (particles.py:79-117 restricted to the kernel's numerical support).  What
+// changes is how the pairs are found:
+//
+//   build (only when needed): the cell grid of gs_cell.cu (bbox, keys, sort, start/permute) is
+//   built for the list radius rl = cutoff (1 + skin); consecutive sorted particles form clusters
+//   of M targets; every cluster gets ONE list of the sorted positions of all sources within rl of
+//   any of its members (fp32 filter grown by its error bound, canonical order: stencil row, then
+//   sorted position), padded to a multiple of 2 TPL entries with a sentinel far record.
+//
+//   every RHS: the records of the stage are gathered into sorted order; a particle that moved more
+//   than skin * cutoff / 2 since the build triggers a rebuild (a pair now closer than the cutoff
+//   was closer than rl at the build: both particles moved less than half the skin); then TPL lanes
+//   per cluster walk its list two sources at a time, each source evaluated against all M members
+//   with the fp64 pair core of gs_device.cuh and masked to d^2 < cutoff^2 exactly (so the sum is
+//   over the same pairs as a fresh cell sweep, whenever the list was built).
+//
+// Why: the per-RHS cell sweep (gs_cell.cu) spends its issue slots on the fp32 candidate filter and
+// idles lanes whose filtered lists are short; here the filter runs once per rebuild, every lane of
+// a cluster has the same trip count, each 32-byte source load feeds M bodies (LSU traffic / M) and
+// the M x 2 independent pair chains per lane hide the FP64 latency.  The cost is the masked skin
+// pairs (~(1 + skin)^2 - 1 of the accepted ones) and the union of the M members' neighbourhoods.
+//
+// In a CUDA graph the rebuild is a conditional IF node whose condition the gather kernel sets, so
+// an RHS that does not need a rebuild runs 3 kernels: gather, pair sweep, stage epilogue.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "gs_cell.cuh"
+
+namespace gsb {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kVB = 128;     // pair-sweep threads per CTA
+constexpr int kVBB = 128;    // list-build threads per CTA
+constexpr int kTplB = 32;    // list-build lanes per cluster: one warp (warp-uniform range loop, no divergence)
+#ifndef GS_VERLET_MINB       // resident CTAs per SM the pair sweep's registers are bounded for (A/B)
+#define GS_VERLET_MINB 3
+#endif
+#ifndef GS_VERLET_M          // targets per cluster (A/B builds)
+#define GS_VERLET_M 2
+#endif
+#ifndef GS_VERLET_PF         // L2 prefetch distance of the list, in trips (A/B)
+#define GS_VERLET_PF 8
+#endif
+#ifndef GS_VERLET_DEPTH      // lanes per cluster grow until clusters * lanes >= SMs * this (A/B)
+#define GS_VERLET_DEPTH 1024
+#endif
+constexpr int kVM = GS_VERLET_M;
+
+struct Acc {
+    double qx, qy, px, py;
+};
+
+// exp2_tbl with an extra acceptance predicate (the cutoff mask): G = 0 outside.
+__device__ __forceinline__ double exp2_tbl_in(double y, const double* __restrict__ tbl, bool in) {
+    double s = y + gs_cb[kCbMagicK];
+    double kd = s - gs_cb[kCbMagicK];
+    double u = y - kd;
+    const int k = __double2loint(s) - (1 << 30);
+    const bool ok = ((__double2hiint(s) ^ kMagicHi) | ((k - kKMin) >> 31)) == 0;
+    double t = tbl[(k & (kTbl - 1)) * kTblRep];
+    int nn = k >> kTblBits;
+    double tn = __hiloint2double(__double2hiint(t) + (nn << 20), __double2loint(t));
+    double e1 = u * fma(fma(fma(fma(gs_cb[kCbC5], u, gs_cb[kCbC4]), u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u,
+                        gs_cb[kCbC1]);
+    double g = fma(tn, e1, tn);
+    return (ok && in) ? g : 0.0;
+}
+
+// One ordered pair (target me <- source s), masked to d^2 < cutoff^2 (rc2b = bits of cutoff^2:
+// non-negative doubles order like their bit patterns, so the test is one 64-bit integer compare).
+// nz counts pairs whose d^2 has the high word of the 1e-200 offset (d == 0: the self pair and any
+// coincident particle; a superset, the rare re-scan decides exactly).
+template <int FAM, bool COUNT>
+__device__ __forceinline__ void vbody(const double4& me, const double4& s, const double* __restrict__ tbl, double k1,
+                                      long long rc2b, Acc& a, int& nz, int& nin) {
+    const double dx = me.x - s.x, dy = me.y - s.y;
+    const double pdot = fma(me.z, s.z, me.w * s.w);
+    const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
+    const long long r2b = __double_as_longlong(r2);
+    const bool in = r2b < rc2b;
+    nz += __double2hiint(r2) == __double2hiint(kTinyR2);
+    if (COUNT) nin += in;
+    double g, c;
+    if (FAM == kFamConical) {
+        const double rs = rsqrt_refined(r2);
+        g = exp2_tbl_in((r2 * rs) * k1, tbl, in);
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl_in(r2 * k1, tbl, in);
+        c = pdot * g;
+    }
+    a.qx = fma(g, s.z, a.qx);
+    a.qy = fma(g, s.w, a.qy);
+    a.px = fma(c, dx, a.px);
+    a.py = fma(c, dy, a.py);
+}
+
+template <int FAM, int TPL, bool COUNT>
+__global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
+    k_verlet_pair(const double4* __restrict__ Ss, const int* __restrict__ list, const long long* __restrict__ ofs,
+                  const int* __restrict__ len,
+                  const unsigned* __restrict__ perm, int64_t n, int64_t cl0, int64_t cl1, double k1, long long rc2b,
+                  double4* __restrict__ part, int64_t row0, DevStatus* st, unsigned long long event,
+                  const double* __restrict__ tbl_g, unsigned long long* accepted) {
+    __shared__ double s_tbl[kTblWords];
+    __shared__ unsigned long long s_acc_count;
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
+    for (int t = threadIdx.x; t < kTblWords; t += kVB) s_tbl[t] = tbl_g[t];
+    if (threadIdx.x == 0) s_acc_count = 0;
+    __syncthreads();
+    const double* tbl = lane_table(s_tbl);
+
+    const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
+    const int64_t c = cl0 + (int64_t)blockIdx.x * (kVB / TPL) + threadIdx.x / TPL;
+    const bool valid = c < cl1;
+    double4 me[kVM];
+    Acc a[kVM];
+    int nz[kVM];
+#pragma unroll
+    for (int m = 0; m < kVM; ++m) {
+        const int64_t k = c * kVM + m;
+        me[m] = (valid && k < n) ? Ss[k] : far_record(m);
+        a[m] = Acc{0.0, 0.0, 0.0, 0.0};
+        nz[m] = 0;
+    }
+    int nin = 0;
+    const long long beg = valid ? ofs[c] : 0, end = valid ? beg + len[c] : 0;
+    // software pipeline: source records two trips ahead (unrolled by three, so the prefetched
+    // records rotate through three register sets without moves), list entries three trips ahead,
+    // and an L2 prefetch of the list GS_VERLET_PF trips ahead.  Past the end the sentinel n is
+    // loaded: always a valid address.  Lists are padded to 2 TPL entries per trip.
+    const int2 sent = make_int2((int)n, (int)n);
+    const long long step = 2 * TPL;
+    long long e = beg + 2 * sub;
+    auto ldl = [&](long long x) { return x < end ? __ldg(reinterpret_cast<const int2*>(list + x)) : sent; };
+    int2 j = ldl(e);
+    double4 a0 = Ss[j.x], a1 = Ss[j.y];
+    j = ldl(e + step);
+    double4 b0 = Ss[j.x], b1 = Ss[j.y];
+    int2 jc = ldl(e + 2 * step);
+    double4 c0, c1;
+    while (true) {
+        if (e >= end) break;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(list + e + GS_VERLET_PF * step));
+        c0 = Ss[jc.x]; c1 = Ss[jc.y];
+        jc = ldl(e + 3 * step);
+#pragma unroll
+        for (int m = 0; m < kVM; ++m) {
+            vbody<FAM, COUNT>(me[m], a0, tbl, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], a1, tbl, k1, rc2b, a[m], nz[m], nin);
+        }
+        e += step;
+        if (e >= end) break;
+        a0 = Ss[jc.x]; a1 = Ss[jc.y];
+        jc = ldl(e + 3 * step);
+#pragma unroll
+        for (int m = 0; m < kVM; ++m) {
+            vbody<FAM, COUNT>(me[m], b0, tbl, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], b1, tbl, k1, rc2b, a[m], nz[m], nin);
+        }
+        e += step;
+        if (e >= end) break;
+        b0 = Ss[jc.x]; b1 = Ss[jc.y];
+        jc = ldl(e + 3 * step);
+#pragma unroll
+        for (int m = 0; m < kVM; ++m) {
+            vbody<FAM, COUNT>(me[m], c0, tbl, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], c1, tbl, k1, rc2b, a[m], nz[m], nin);
+        }
+        e += step;
+    }
+#pragma unroll
+    for (int m = 0; m < kVM; ++m) {
+        for (int off = TPL >> 1; off; off >>= 1) {
+            nz[m] += __shfl_xor_sync(kFull, nz[m], off);
+            a[m].qx += __shfl_xor_sync(kFull, a[m].qx, off);
+            a[m].qy += __shfl_xor_sync(kFull, a[m].qy, off);
+            a[m].px += __shfl_xor_sync(kFull, a[m].px, off);
+            a[m].py += __shfl_xor_sync(kFull, a[m].py, off);
+        }
+    }
+    if (valid && sub == 0) {
+#pragma unroll
+        for (int m = 0; m < kVM; ++m) {
+            const int64_t k = c * kVM + m;
+            if (k >= n) continue;
+            const int64_t i = (int64_t)perm[k];
+            if (nz[m] > 1) {  // rare: a coincident particle among the list (reference error, particles.py:92-98)
+                for (long long e = beg; e < end; ++e) {
+                    const int j = list[e];
+                    if (j >= n) continue;
+                    const int64_t jo = (int64_t)perm[j];
+                    if (jo == i) continue;
+                    const double4 s = Ss[j];
+                    const double dx = me[m].x - s.x, dy = me[m].y - s.y;
+                    if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) != 0.0) continue;
+                    if (fma(me[m].z, s.z, me[m].w * s.w) != 0.0)
+                        record_event(st, event, (unsigned long long)(i * n + jo));
+                }
+            }
+            part[i - row0] = make_double4(a[m].qx, a[m].qy, a[m].px, a[m].py);
+        }
+    }
+    if (COUNT) {
+        unsigned long long v = (unsigned long long)nin;
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc_count, v);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_acc_count) atomicAdd(accepted, s_acc_count);
+    }
+}
+
+// ---- list build ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int vcell(double v, double v0, double inv_h, int nmax) {
+    int c = (int)floor((v - v0) * inv_h);
+    return min(max(c, 0), nmax - 1);
+}
+
+__device__ __forceinline__ double vcellf(double v, double v0, double inv_h) { return floor((v - v0) * inv_h); }
+
+__device__ __forceinline__ unsigned vhash(double cx, double cy, int ncells) {
+    unsigned long long h = (unsigned long long)__double_as_longlong(cx + 0.0) * 0x9E3779B97F4A7C15ull ^
+                           (unsigned long long)__double_as_longlong(cy + 0.0) * 0xC2B2AE3D27D4EB4Full;
+    h ^= h >> 31;
+    return (unsigned)h & (unsigned)(ncells - 1);
+}
+
+// The cluster's candidates: the union of its members' stencils (gs_cell.cu stencil_ranges),
+// generated range by range.  Row-major grid: per stencil row one contiguous sorted range spanning
+// every member's trimmed x-range (cells between two consecutive sorted members of one row are
+// empty; in other rows the span may add candidates the filter rejects).  Hashed grid: the
+// deduplicated buckets of all members' 3 x 3 stencils.  One warp per cluster: every range is
+// swept 32 candidates per round, so the loop is warp-uniform.
+struct ClusterMembers {
+    double mx[kVM], my[kVM];
+    float fx[kVM], fy[kVM];
+    int nm;
+};
+
+template <typename F>
+__device__ __forceinline__ void for_each_range(const GridParams& g, const int* __restrict__ start,
+                                               const ClusterMembers& cm, F&& f) {
+    if (!g.hashed) {
+        const int sub = g.sub;
+        int cy[kVM];
+        int lo = g.ny, hi = -1;
+#pragma unroll
+        for (int m = 0; m < kVM; ++m) {
+            cy[m] = m < cm.nm ? vcell(cm.my[m], g.y0, g.inv_h, g.ny) : 0;
+            if (m < cm.nm) { lo = min(lo, cy[m]); hi = max(hi, cy[m]); }
+        }
+        const double rc2 = g.rc * g.rc;
+        for (int yy = max(lo - sub, 0); yy <= min(hi + sub, g.ny - 1); ++yy) {
+            int xa = g.nx, xb = -1;
+#pragma unroll
+            for (int m = 0; m < kVM; ++m) {
+                if (m >= cm.nm || yy < cy[m] - sub || yy > cy[m] + sub) continue;
+                int a, b;
+                if (sub > 1) {
+                    const double ylo = fma((double)yy, g.h, g.y0), yhi = ylo + g.h;
+                    const double gap = fmax(0.0, fmax(ylo - cm.my[m], cm.my[m] - yhi));
+                    const double xr2 = fma(-gap, gap, rc2);
+                    if (!(xr2 > 0.0)) continue;
+                    const double xr = sqrt(xr2);
+                    a = vcell(cm.mx[m] - xr, g.x0, g.inv_h, g.nx);
+                    b = vcell(cm.mx[m] + xr, g.x0, g.inv_h, g.nx);
+                } else {
+                    const int cx = vcell(cm.mx[m], g.x0, g.inv_h, g.nx);
+                    a = max(cx - 1, 0);
+                    b = min(cx + 1, g.nx - 1);
+                }
+                xa = min(xa, a);
+                xb = max(xb, b);
+            }
+            if (xb >= xa) f(start[yy * g.nx + xa], start[yy * g.nx + xb + 1]);
+        }
+        return;
+    }
+    for (int m = 0; m < cm.nm; ++m) {
+        const double cx = vcellf(cm.mx[m], g.x0, g.inv_h), cy = vcellf(cm.my[m], g.y0, g.inv_h);
+        for (int t = 0; t < 9; ++t) {
+            const unsigned key = vhash(cx + (t % 3 - 1), cy + (t / 3 - 1), g.ncells);
+            bool dup = false;  // the bucket already came up for an earlier (member, cell)?
+            for (int m2 = 0; m2 <= m && !dup; ++m2) {
+                const double cx2 = vcellf(cm.mx[m2], g.x0, g.inv_h), cy2 = vcellf(cm.my[m2], g.y0, g.inv_h);
+                for (int t2 = 0; t2 < (m2 == m ? t : 9); ++t2)
+                    dup |= vhash(cx2 + (t2 % 3 - 1), cy2 + (t2 / 3 - 1), g.ncells) == key;
+            }
+            if (!dup) f(start[key], start[key + 1]);
+        }
+    }
+}
+
+__device__ __forceinline__ void load_members(const double4* __restrict__ Ss, const float2* __restrict__ Sf, int64_t n,
+                                             int64_t c, ClusterMembers& cm) {
+    cm.nm = 0;
+#pragma unroll
+    for (int m = 0; m < kVM; ++m) {
+        const int64_t k = c * kVM + m;
+        if (k < n) {
+            const double4 v = Ss[k];
+            cm.mx[m] = v.x; cm.my[m] = v.y;
+            const float2 f = Sf[k];
+            cm.fx[m] = f.x; cm.fy[m] = f.y;
+            cm.nm = m + 1;
+        } else {
+            cm.mx[m] = cm.my[m] = 0.0;
+            cm.fx[m] = cm.fy[m] = 0.0f;
+        }
+    }
+}
+
+// Capacity of cluster c's list: its candidate count (every range's length), padded to `pad` — an
+// upper bound of the filtered list, found without touching a candidate (one thread per cluster).
+__global__ void __launch_bounds__(256) k_verlet_caps(const float2* __restrict__ Sf, const double4* __restrict__ Ss,
+                                                     const int* __restrict__ start, const GridParams* __restrict__ gp,
+                                                     int64_t n, int64_t ncl, int pad, long long* cap) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncl) return;
+    const GridParams g = *gp;
+    ClusterMembers cm;
+    load_members(Ss, Sf, n, c, cm);
+    long long total = 0;
+    for_each_range(g, start, cm, [&](int a, int b) { total += b - a; });
+    cap[c] = (total + pad - 1) / pad * pad;
+}
+
+// list[ofs[c] ...] = the sorted positions within the list radius of any member, in canonical order
+// (ballot compaction, one warp per cluster), padded to a multiple of `pad` with n (the sentinel far
+// record Ss[n]); len[c] = the padded length; Xb[k] = positions at the build.
+__global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__ Sf, const double4* __restrict__ Ss,
+                                                      const int* __restrict__ start, const GridParams* __restrict__ gp,
+                                                      int64_t n, int64_t ncl, int pad, const long long* __restrict__ ofs,
+                                                      int* len, int* list, int64_t cap, double2* Xb,
+                                                      unsigned long long* overflow) {
+    const int sub = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * (kVBB / kTplB) + threadIdx.x / kTplB;
+    if (c >= ncl) return;  // warp-uniform
+    const GridParams g = *gp;
+    ClusterMembers cm;
+    load_members(Ss, Sf, n, c, cm);
+#pragma unroll
+    for (int m = 0; m < kVM; ++m)
+        if (sub == m && m < cm.nm) Xb[c * kVM + m] = make_double2(cm.mx[m], cm.my[m]);
+    const int64_t obase = ofs[c];
+    const bool ok = ofs[ncl] <= cap;  // the list buffer holds the whole build
+    if (!ok) {  // no list: the sweep reads nothing (the call is redone with a larger buffer)
+        if (sub == 0) {
+            atomicMax(overflow, (unsigned long long)ofs[ncl]);
+            len[c] = 0;
+        }
+        return;
+    }
+    const float rc2f = g.rc2f;
+    int count = 0;
+    for_each_range(g, start, cm, [&](int a, int b) {
+        for (int base = a; base < b; base += kTplB) {
+            const int pos = base + sub;
+            bool acc = false;
+            if (pos < b) {
+                const float2 f = Sf[pos];
+                float d2 = INFINITY;
+#pragma unroll
+                for (int m = 0; m < kVM; ++m) {
+                    const float dx = cm.fx[m] - f.x, dy = cm.fy[m] - f.y;
+                    const float dm = fmaf(dx, dx, dy * dy);
+                    d2 = m < cm.nm ? fminf(d2, dm) : d2;
+                }
+                acc = !(d2 >= rc2f);  // NaN radius (filter off): keep
+            }
+            const unsigned bal = __ballot_sync(kFull, acc);
+            if (acc) list[obase + count + __popc(bal & ((1u << sub) - 1))] = pos;
+            count += __popc(bal);
+        }
+    });
+    const int padded = (count + pad - 1) / pad * pad;
+    for (int e = count + sub; e < padded; e += kTplB) list[obase + e] = (int)n;  // padding: sentinel
+    if (sub == 0) len[c] = padded;
+}
+
+// Gather of the stage records into sorted order + the rebuild trigger.  The last CTA decides:
+// rebuild if forced or any particle moved more than half the skin since the build; in a graph
+// it sets the IF node's condition, otherwise flags[3] (host-driven paths always rebuild).
+__global__ void __launch_bounds__(256) k_verlet_gather(const double4* __restrict__ S, const unsigned* __restrict__ perm,
+                                                       int64_t n, double4* Ss, const double2* __restrict__ Xb,
+                                                       double thr2, unsigned* flags, int force,
+                                                       cudaGraphConditionalHandle cond, int use_cond) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool need = false;
+    if (!force && k < n) {
+        const double4 v = S[perm[k]];
+        Ss[k] = v;
+        const double2 b = Xb[k];
+        const double dx = v.x - b.x, dy = v.y - b.y;
+        need = fma(dx, dx, dy * dy) > thr2;
+    }
+    if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&flags[0], 1u);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&flags[2], 1u);
+        if (prev == gridDim.x - 1) {
+            const unsigned f = force ? 1u : atomicExch(&flags[0], 0u);
+            flags[0] = 0u;
+            flags[2] = 0u;
+            flags[1] += f;  // builds so far (diagnostics)
+            if (use_cond) cudaGraphSetConditional(cond, f);
+            flags[3] = f;
+        }
+    }
+}
+
+__global__ void k_verlet_sentinel(double4* Ss, int64_t n) { Ss[n] = far_record(0); }
+
+}  // namespace
+
+int verlet_tpl(int64_t n) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ncl = (n + kVM - 1) / kVM;
+    static const int depth = [] {
+        const char* e = std::getenv("GS_B200_VERLET_DEPTH");
+        return e ? std::max(1, std::atoi(e)) : GS_VERLET_DEPTH;
+    }();
+    static const int tpl_min = [] {
+        const char* e = std::getenv("GS_B200_VERLET_TPL");  // A/B: minimum lanes per cluster
+        const int v = e ? std::atoi(e) : 4;
+        return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 4;
+    }();
+    int tpl = tpl_min;
+    while (tpl < 16 && ncl * tpl < (int64_t)sms * depth) tpl *= 2;
+    return tpl;
+}
+
+int64_t verlet_clusters(int64_t n) { return (n + kVM - 1) / kVM; }
+
+size_t verlet_scan_bytes(int64_t ncl) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const long long*)nullptr, (long long*)nullptr, (int)(ncl + 1));
+    return bytes;
+}
+
+int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, double cutoff, cudaStream_t stream) {
+    const double rl = cutoff * (1.0 + v.skin);
+    int rc = cell_build(w, S, n, rl, stream);
+    if (rc) return rc;
+    k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, n);
+    const int64_t ncl = verlet_clusters(n);
+    const int pad = 2 * v.tpl;
+    k_verlet_caps<<<(unsigned)((ncl + 255) / 256), 256, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.cnt);
+    size_t bytes = v.scan_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(v.scan_temp, bytes, v.cnt, v.ofs, (int)(ncl + 1), stream);
+    if (e != cudaSuccess) return (int)e;
+    const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
+    k_verlet_fill<<<blocks, kVBB, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.ofs, v.len, v.list, v.cap,
+                                               v.Xb, v.overflow);
+    return (int)cudaGetLastError();
+}
+
+void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, int force,
+                   cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream) {
+    const double thr = 0.5 * v.skin * v.cutoff;
+    k_verlet_gather<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(S, w.perm, n, w.Ss, v.Xb, thr * thr * (1.0 - 1e-9),
+                                                                     v.flags, force, cond, use_cond);
+}
+
+void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
+                        DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                        cudaStream_t stream) {
+    const int64_t ncl = verlet_clusters(n);
+    const double rc2 = sc.cutoff * sc.cutoff;
+    long long rc2b;
+    memcpy(&rc2b, &rc2, sizeof(rc2b));
+    const int tpl = v.tpl;
+    const unsigned blocks = (unsigned)((ncl * tpl + kVB - 1) / kVB);
+#define GS_V_LAUNCH(F, T)                                                                                  \
+    if (accepted)                                                                                          \
+        k_verlet_pair<F, T, true><<<blocks, kVB, 0, stream>>>(w.Ss, v.list, v.ofs, v.len, w.perm, n, 0, ncl, sc.k1,  \
+                                                              rc2b, part, 0, st, event, tbl_dev, accepted);  \
+    else                                                                                                   \
+        k_verlet_pair<F, T, false><<<blocks, kVB, 0, stream>>>(w.Ss, v.list, v.ofs, v.len, w.perm, n, 0, ncl, sc.k1, \
+                                                               rc2b, part, 0, st, event, tbl_dev, accepted)
+#define GS_V_FAM(F)                           \
+    switch (tpl) {                            \
+        case 1: GS_V_LAUNCH(F, 1); break;     \
+        case 2: GS_V_LAUNCH(F, 2); break;     \
+        case 4: GS_V_LAUNCH(F, 4); break;     \
+        case 8: GS_V_LAUNCH(F, 8); break;     \
+        default: GS_V_LAUNCH(F, 16); break;   \
+    }
+    if (sc.fam == kFamConical) { GS_V_FAM(kFamConical) }
+    else { GS_V_FAM(kFamGaussian) }
+#undef GS_V_FAM
+#undef GS_V_LAUNCH
+}
+
+}  // namespace gsb

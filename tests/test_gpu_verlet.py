@@ -1,0 +1,125 @@
+"""The cluster Verlet lists of the cell path (gs_verlet.cu) against the per-RHS cell sweep and the
+C oracle: same pairs (d < cutoff), so the same sums up to summation order — for evolves that reuse
+a list over many RHS, rebuild it when particles move, outgrow the list buffer, or hit a
+coincident interacting pair (particles.py:92-98, integrator.py:102-105)."""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+class _Env:
+    """A fresh library context created under the given environment (read at gs_create)."""
+
+    def __init__(self, **env):
+        self.env = env
+
+    def __enter__(self):
+        from paper_1510_03816_b200 import _native as N
+
+        self.N = N
+        self.saved = {k: os.environ.get(k) for k in self.env}
+        os.environ.update({k: str(v) for k, v in self.env.items()})
+        self.ctxs = N.Context._by_device
+        N.Context._by_device = {}
+        return N
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        self.N.Context._by_device = self.ctxs
+
+
+def _stats(N):
+    ctx = N.Context.get()
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    N.check(ctx.lib.gs_cell_stats(ctx.handle, ctypes.byref(b), ctypes.byref(e), None), "gs_cell_stats")
+    return b.value, e.value
+
+
+def _evolve(gs, spec, q, p, steps, **env):
+    from paper_1510_03816_b200 import device
+
+    with _Env(**env) as N:
+        gs.set_path("cell")
+        try:
+            out = gs.evolve(spec, gs.ParticleState(q, p), gs.EvolveConfig(t_final=steps / 20, steps=steps))
+            st = _stats(N)
+        finally:
+            gs.set_path("auto")
+    return out.final.q, out.final.p, st
+
+
+def test_lists_equal_the_cell_sweep_and_rebuild_when_particles_move(cuda):
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c5(65536)
+    p = 0.05 * (w.target - w.q)  # large enough that the 8-step shoot moves particles past half the skin
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    qv, pv, (builds, cap) = _evolve(gs, spec, w.q, p, 8)
+    qs, ps, _ = _evolve(gs, spec, w.q, p, 8, GS_B200_VERLET=0)
+    assert rel(qv, qs) <= TOL and rel(pv, ps) <= TOL
+    assert builds >= 3  # sizing build + forced first build + at least one displacement rebuild
+    assert cap > 0
+
+
+def test_lists_match_the_oracle_on_the_clustered_cloud(cuda):
+    import paper_1510_03816_b200 as gs
+    from oracle import native
+    from oracle.restate import Kernel
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c4(20000)
+    p = np.random.default_rng(9).normal(0, 1e-3, w.q.shape)
+    for spec in (gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha)),
+                 gs.SystemSpec(kernel=gs.KernelSpec(family="gaussian", alpha=0.004), sigma2=0.1)):
+        qv, pv, _ = _evolve(gs, spec, w.q, p, 3)
+        k = Kernel(0 if spec.kernel.family.value == "conical" else 1, spec.kernel.alpha, True)
+        oq, op = native.evolve(k, spec.sigma2, w.q, p, 3 / 20, 3, cutoff=gs.support_radius(spec.kernel))
+        assert rel(qv, oq) <= 1e-10 and rel(pv, op) <= 1e-10
+
+
+def test_list_buffer_overflow_is_redone_with_a_larger_buffer(cuda):
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c5(32768)
+    p = 0.05 * (w.target - w.q)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    qa, pa, (b_ok, _) = _evolve(gs, spec, w.q, p, 4)
+    # a buffer sized at 30 % of the first build overflows on the first in-graph build
+    qb, pb, (b_small, _) = _evolve(gs, spec, w.q, p, 4, GS_B200_VERLET_SLACK=-0.7)
+    assert np.array_equal(qa, qb) and np.array_equal(pa, pb)  # the redo is the same computation
+    assert b_small > b_ok
+
+
+def test_coincident_interacting_pair_through_the_lists(cuda):
+    import paper_1510_03816_b200 as gs
+
+    rng = np.random.default_rng(4)
+    n = 20000
+    q = rng.uniform(0, 1, (n, 2))
+    q[17001] = q[256]
+    p = rng.normal(0, 0.01, (n, 2))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.02 / gs.LAMBDA))
+    with pytest.raises(gs.DegenerateConfigurationError,
+                       match=r"particles 256 and 17001 coincide with interacting momenta.*during step 1"):
+        _evolve(gs, spec, q, p, 2)
+    p[17001] = 0.0  # an inert coincident pair is fine (particles.py:92-98: p_i . p_j == 0)
+    qv, pv, _ = _evolve(gs, spec, q, p, 2)
+    qs, ps, _ = _evolve(gs, spec, q, p, 2, GS_B200_VERLET=0)
+    assert rel(qv, qs) <= TOL and rel(pv, ps) <= TOL

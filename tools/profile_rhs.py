@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--path", default="auto")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--save", default="", help="write dq, dp of the last RHS to this .npz")
+    ap.add_argument("--evolve", type=int, default=0, help="time an evolve of this many RK4 steps instead")
     a = ap.parse_args()
     import torch
 
@@ -34,10 +35,14 @@ def main():
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for k in range(a.reps):
         s.record()
-        dq, dp = device.rhs(spec, q_d, p_d)
+        if a.evolve:
+            dq, dp, _ = device.evolve(spec, q_d, p_d, a.evolve * w.t_final / w.steps, a.evolve)
+        else:
+            dq, dp = device.rhs(spec, q_d, p_d)
         e.record()
         torch.cuda.synchronize()
-        print(f"{a.config} {a.path} rhs {s.elapsed_time(e):.3f} ms", flush=True)
+        what = f"evolve {a.evolve} steps" if a.evolve else "rhs"
+        print(f"{a.config} {a.path} {what} {s.elapsed_time(e):.3f} ms", flush=True)
 
     if a.save:
         np.savez(a.save, dq=dq.cpu().numpy(), dp=dp.cpu().numpy())
