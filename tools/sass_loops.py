@@ -4,6 +4,7 @@
 
 For each backward branch: address range, instruction count, FP64 (DFMA/DMUL/DADD), MUFU,
 UMOV/IMAD.MOV (re-materialised constants), loads — to compare A/B builds before spending GPU time.
+`fp64_per_pair()` is what bench.py reports as the implemented FP64-pipe work per ordered pair.
 """
 
 import re
@@ -11,11 +12,11 @@ import subprocess
 import sys
 
 
-def main():
-    obj, pat = sys.argv[1], sys.argv[2]
+def loops(obj: str, pat: str) -> list:
+    """[{kernel, start, end, instr, fp64, mufu, umov, imad_mov, ldg, lds, shfl}] of every loop."""
     out = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
-    funcs = re.split(r"\n\s+Function : ", out)
-    for f in funcs[1:]:
+    res = []
+    for f in re.split(r"\n\s+Function : ", out)[1:]:
         name = f.split("\n", 1)[0].strip()
         if not re.search(pat, name):
             continue
@@ -25,7 +26,6 @@ def main():
             if m:
                 ins.append((int(m.group(1), 16), m.group(2).strip()))
         addr = {a: k for k, (a, _) in enumerate(ins)}
-        print(name[:110])
         for k, (a, t) in enumerate(ins):
             m = re.search(r"BRA (0x[0-9a-f]+)", t)
             if not m or int(m.group(1), 16) >= a:
@@ -35,11 +35,36 @@ def main():
                 continue
             body = [x for _, x in ins[s:k + 1]]
             ops = [re.sub(r"^@!?U?P\w+\s+", "", x).split()[0] for x in body]
-            fp64 = sum(o.split(".")[0] in ("DFMA", "DMUL", "DADD") for o in ops)
-            cnt = lambda p: sum(o.startswith(p) for o in ops)
-            print(f"  loop {ins[s][0]:#07x}-{a:#07x}: {len(body):4d} instr, fp64 {fp64:3d}, mufu {cnt('MUFU'):2d}, "
-                  f"umov {cnt('UMOV'):2d}, imad.mov {cnt('IMAD.MOV'):2d}, ldg {cnt('LDG'):2d}, lds {cnt('LDS'):2d}, "
-                  f"shfl {cnt('SHFL'):2d}")
+            cnt = lambda p: sum(o.startswith(p) for o in ops)  # noqa: E731
+            res.append(dict(kernel=name, start=ins[s][0], end=a, instr=len(body),
+                            fp64=sum(o.split(".")[0] in ("DFMA", "DMUL", "DADD") for o in ops),
+                            mufu=cnt("MUFU"), umov=cnt("UMOV"), imad_mov=cnt("IMAD.MOV"), ldg=cnt("LDG"),
+                            lds=cnt("LDS"), shfl=cnt("SHFL")))
+    return res
+
+
+def fp64_per_pair(obj: str, pat: str, symmetric: bool):
+    """FP64-pipe instructions per ORDERED pair in the hottest loop of the kernel: the loop with the
+    most FP64 instructions; every conical pair evaluation issues one MUFU.RSQ64H, so the loop's
+    pair count is its MUFU count (an unordered pair feeds two ordered pairs in the symmetric
+    kernel).  Returns (fp64 per ordered pair, loop dict) or (None, None)."""
+    ls = [x for x in loops(obj, pat) if x["mufu"] > 0]
+    if not ls:
+        return None, None
+    best = max(ls, key=lambda x: x["fp64"])
+    return best["fp64"] / (best["mufu"] * (2 if symmetric else 1)), best
+
+
+def main():
+    obj, pat = sys.argv[1], sys.argv[2]
+    last = None
+    for x in loops(obj, pat):
+        if x["kernel"] != last:
+            print(x["kernel"][:110])
+            last = x["kernel"]
+        print(f"  loop {x['start']:#07x}-{x['end']:#07x}: {x['instr']:4d} instr, fp64 {x['fp64']:3d}, "
+              f"mufu {x['mufu']:2d}, umov {x['umov']:2d}, imad.mov {x['imad_mov']:2d}, ldg {x['ldg']:2d}, "
+              f"lds {x['lds']:2d}, shfl {x['shfl']:2d}")
 
 
 if __name__ == "__main__":
