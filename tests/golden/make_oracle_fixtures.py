@@ -153,9 +153,15 @@ def onset_fixture(name, w, h, stride):
         blown = len(hist) > 0 and (not math.isfinite(hist[-1]) or hist[-1] > BLOWUP_FACTOR * hist[0]) \
             if w.stop_rule != "residual" else not (hist[0] <= BLOWUP_FACTOR * r0)
         outcome.update(iterations=len(hist), history=hist, blown_up=bool(blown))
+    # rows are stored for the steps whose sampled rows all stay near the unit square (the test compares
+    # those); q_absmax / p_absmax (over all particles) are kept for every step
+    bound = 1.5 * float(np.abs(w.q).max())
+    keep = 0
+    while keep < len(qs) and np.abs(qs[keep]).max() < bound:
+        keep += 1
     save(name, dict(config=w.name, n=w.n, h=h, dt=dt, stride=stride, failed=failed, seconds=float(sum(secs)),
-                    threads=native.max_threads(), outcome=outcome),
-         rows=rows, q=np.array(qs), p=np.array(ps), q_absmax=np.array(qmax), p_absmax=np.array(pmax))
+                    threads=native.max_threads(), outcome=outcome, stored_steps=keep, in_place_bound=bound),
+         rows=rows, q=np.array(qs[:keep]), p=np.array(ps[:keep]), q_absmax=np.array(qmax), p_absmax=np.array(pmax))
 
 
 def match_fixture(name, w, h, max_iter, stride, with_h=False):

@@ -154,8 +154,13 @@ def test_full_size_matches_run_all_iterations(cuda, name):
 @pytest.mark.parametrize("name", ["C4", "C5"])
 def test_survey_gains_blow_up_like_the_oracle(cuda, name):
     """The survey's gains (C4 h = 0.1, C5 h = 0.4): the first shoot, step by step, equals the oracle's
-    until the cloud is flung apart; the match then ends as "step too large" after the same number of
-    iterations (shooting.py:287-291)."""
+    up to the onset of the blow-up, and the match ends as "step too large" after the same number of
+    iterations (shooting.py:287-291).
+
+    Compared steps: those whose sampled rows all stay near the unit square in the oracle (the
+    fixture stores exactly these).  Steps before the onset (every particle still in place) are held
+    to 1e-8; the onset step itself — where some particle is already flung away and rounding starts
+    to be amplified without bound (C4: step 2, C5: step 1) — to 1e-6."""
     import paper_1510_03816_b200 as gs
     from paper_1510_03816_b200 import configs, device
 
@@ -163,19 +168,15 @@ def test_survey_gains_blow_up_like_the_oracle(cuda, name):
     w = configs.CONFIGS[name]()
     spec = _spec(gs, w)
     rows = z["rows"]
-    extent = float(np.abs(w.q).max())
     q, p = w.q.copy(), meta["h"] * (w.target - w.q)
-    compared = 0
+    assert meta["stored_steps"] >= 1
     with _Path("auto"):
-        for k in range(len(z["q_absmax"])):
-            if z["q_absmax"][k] > 1.5 * extent:
-                break  # onset: from here on rounding differences are amplified without bound
+        for k in range(meta["stored_steps"]):
             qd, pd, _ = device.evolve(spec, q, p, meta["dt"], 1)
             q, p = qd.cpu().numpy(), pd.cpu().numpy()
-            assert rel(q[rows], z["q"][k]) <= TOL, f"step {k + 1}"
-            assert rel(p[rows], z["p"][k]) <= TOL, f"step {k + 1}"
-            compared += 1
-        assert compared >= 1
+            tol = TOL if z["q_absmax"][k] < meta["in_place_bound"] else 1e-6
+            assert rel(q[rows], z["q"][k]) <= tol, f"step {k + 1}"
+            assert rel(p[rows], z["p"][k]) <= tol, f"step {k + 1}"
         r = _match(gs, w, meta["h"], w.max_iter)
     out = meta["outcome"]
     assert r["diagnosis"] == "step too large" and out["blown_up"]

@@ -125,8 +125,14 @@ def test_match_matches_reference(cuda, name):
     # eigvalsh vs SVD agree to many digits but not to the printed 4 for a near-singular K
     assert bool(res.warnings) == bool(m.get("warnings"))
     if res.warnings:
+        # ill-conditioned K: the momenta carry the factorisation error (cond x 1e-16), so p0 is not
+        # compared; the loop's outcome, its iteration count and H still are
         assert res.warnings[0].startswith("Gram matrix condition number")
-        return  # ill-conditioned K: the momenta carry the factorisation error (cond x 1e-16)
+        assert res.converged == m["converged"] and res.iterations == m["iterations"]
+        assert res.diagnosis == m["diagnosis"]
+        assert res.hamiltonian == pytest.approx(m["hamiltonian"], rel=MATCH_TOL)
+        assert np.abs(res.final_template.points - c["endpoint"]).max() <= 1e-6 * max(1.0, np.abs(c["endpoint"]).max())
+        return
     assert res.converged == m["converged"]
     assert len(res.residual_history) == res.iterations
     assert res.final_template.label == m["final_label"]
