@@ -739,7 +739,11 @@ int pairs_sym_impl(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_
 // ======================================================================================
 extern "C" {
 
+#ifdef GS_CHECKED
+const char* gs_version(void) { return "geoshoot-b200 0.1.0 (sm_100a, fp64, checked)"; }
+#else
 const char* gs_version(void) { return "geoshoot-b200 0.1.0 (sm_100a, fp64)"; }
+#endif
 int gs_abi_version(void) { return GS_ABI_VERSION; }
 const char* gs_last_error(void) { return g_last_error.c_str(); }
 

@@ -158,9 +158,10 @@ __device__ __forceinline__ int cell_coord(double v, double v0, double inv_h, int
 __device__ __forceinline__ double cell_coordf(double v, double v0, double inv_h) { return floor((v - v0) * inv_h); }
 
 __device__ __forceinline__ unsigned cell_hash(double cx, double cy, int ncells) {
-    unsigned long long h = (unsigned long long)__double_as_longlong(cx + 0.0) * 0x9E3779B97F4A7C15ull ^
-                           (unsigned long long)__double_as_longlong(cy + 0.0) * 0xC2B2AE3D27D4EB4Full;
-    h ^= h >> 31;
+    // splitmix64 finalizer of each coordinate's bits (the low bits of small integral doubles are all
+    // zero: a plain multiply would put most cells into a few buckets)
+    const unsigned long long h = mix64((unsigned long long)__double_as_longlong(cx + 0.0)) ^
+                                 mix64((unsigned long long)__double_as_longlong(cy + 0.0) ^ 0xC2B2AE3D27D4EB4Full);
     return (unsigned)h & (unsigned)(ncells - 1);
 }
 
@@ -280,8 +281,10 @@ __global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, c
     const GridParams g = *gp;
     const long long prev = (k == 0) ? -1 : (long long)keys_sorted[k - 1];
     const long long cur = (k == n) ? (long long)g.ncells : (long long)keys_sorted[k];
+    GS_ASSERT(cur <= (long long)g.ncells);
     for (long long c = prev + 1; c <= cur; ++c) start[c] = (int)k;
     if (k < n) {
+        GS_ASSERT(perm[k] < (unsigned)n);
         const double4 v = S[perm[k]];
         Ss[k] = v;
         Sf[k] = make_float2((float)(v.x - g.x0), (float)(v.y - g.y0));
@@ -350,6 +353,7 @@ __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* 
                     if (u + 1 < cnt) s_nx = Ss[s_list[u + 1][threadIdx.x]];
 #else
                     const int j = s_list[u][threadIdx.x];
+                    GS_ASSERT(j >= 0 && j < n);
                     const double4 s = Ss[j];
 #endif
                     const double dx = me.x - s.x, dy = me.y - s.y;

@@ -16,6 +16,13 @@ namespace gsb {
 // target then visits 2 sub + 1 stencil rows, each trimmed to the x-range of cells its disk
 // of radius rc reaches — fewer fp32 candidates per accepted pair (C5: 9 -> ~5 sigma^2).
 constexpr int kCellSubMax = 4;
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {  // splitmix64 finalizer
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
 struct GridParams {
     double x0, y0, inv_h;
     double h, rc;        // cell edge; filter radius (double) = sqrt(rc2f) before fp32 rounding

@@ -284,6 +284,7 @@ __device__ __forceinline__ bool finish_reduce(const FinishArgs& a, int64_t& li, 
     const bool valid = li < a.nrows;
     const int64_t ps = a.pstride ? a.pstride : a.nrows;
     double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+    GS_ASSERT(a.nchunks >= 1 && (a.pstride == 0 || a.pstride >= a.nrows));
     if (valid)
         for (int c = w; c < a.nchunks; c += groups) {
             const double4 v = a.part[(int64_t)c * ps + li];

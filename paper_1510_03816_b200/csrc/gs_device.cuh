@@ -20,6 +20,24 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked builds (-DGS_CHECKED, tools/checked_build.sh): device-side bounds and protocol asserts in
+// every kernel family.  compute-sanitizer is not available on the GPU pool this was built on, so
+// the checked library running the whole GPU test suite is the memory-safety evidence.
+#ifdef GS_CHECKED
+#include <cstdio>
+#define GS_ASSERT(c)                                                                   \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            printf("GS_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define GS_ASSERT(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace gsb {
 
 constexpr int kFamConical = 0;

@@ -326,6 +326,8 @@ __device__ unsigned long long small_evolve(Ctx& c, const SysConst& sc, double4& 
                 const int nb = cur ^ 1;
                 unsigned long long* bar = &s_mbar[nb];
                 if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(c.n * 32 + Ctx::C * 12));
+                GS_ASSERT(!c.act || (c.tgt >= 0 && c.tgt < c.n));
+                GS_ASSERT(c.rank >= 0 && c.rank < Ctx::C && nb >= 0 && nb < 2);
                 if (c.act)
                     for (int r = c.sub; r < Ctx::C; r += c.split)
                         st_async_rec(mapa_u32(smem_u32(&Sn[c.tgt]), r), nxt, mapa_u32(smem_u32(bar), r));

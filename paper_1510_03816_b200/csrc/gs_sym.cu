@@ -125,6 +125,7 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
     while (row_start(SI + 1) <= t) ++SI;
     const long long SJ = SI + (t - row_start(SI));
     const bool diag = SI == SJ;
+    GS_ASSERT(SI >= 0 && SI <= SJ && SJ < nsb);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int r0 = w * 64 + lane, r1 = r0 + 32;  // this thread's two rows inside a block
@@ -221,6 +222,7 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
             add_to(&s_acc[ib * kDB + r0], a0);
             add_to(&s_acc[ib * kDB + r1], a1);
         } else {
+            GS_ASSERT(I * kDB + kDB <= pstride);
             if (i0 < n) part[SJ * pstride + i0] = make_double4(a0.qx, a0.qy, a0.px, a0.py);
             if (i1 < n) part[SJ * pstride + i1] = make_double4(a1.qx, a1.qy, a1.px, a1.py);
         }

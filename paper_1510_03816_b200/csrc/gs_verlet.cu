@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     long long e = beg + 2 * sub;
     auto ldl = [&](long long x) { return x < end ? __ldg(reinterpret_cast<const int2*>(list + x)) : sent; };
     int2 j = ldl(e);
+    GS_ASSERT(!valid || (beg >= 0 && (end - beg) % (2 * TPL) == 0));
+    GS_ASSERT(j.x >= 0 && j.x <= n && j.y >= 0 && j.y <= n);
     double4 a0 = Ss[j.x], a1 = Ss[j.y];
     j = ldl(e + step);
     double4 b0 = Ss[j.x], b1 = Ss[j.y];
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     while (true) {
         if (e >= end) break;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(list + e + GS_VERLET_PF * step));
+        GS_ASSERT(jc.x >= 0 && jc.x <= n && jc.y >= 0 && jc.y <= n);
         c0 = Ss[jc.x]; c1 = Ss[jc.y];
         jc = ldl(e + 3 * step);
 #pragma unroll
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
             const int64_t k = c * kVM + m;
             if (k >= n) continue;
             const int64_t i = (int64_t)perm[k];
+            GS_ASSERT(i >= 0 && i < n);
             if (nz[m] > 1) {  // rare: a coincident particle among the list (reference error, particles.py:92-98)
                 for (long long e = beg; e < end; ++e) {
                     const int j = list[e];
@@ -228,9 +232,10 @@ __device__ __forceinline__ int vcell(double v, double v0, double inv_h, int nmax
 __device__ __forceinline__ double vcellf(double v, double v0, double inv_h) { return floor((v - v0) * inv_h); }
 
 __device__ __forceinline__ unsigned vhash(double cx, double cy, int ncells) {
-    unsigned long long h = (unsigned long long)__double_as_longlong(cx + 0.0) * 0x9E3779B97F4A7C15ull ^
-                           (unsigned long long)__double_as_longlong(cy + 0.0) * 0xC2B2AE3D27D4EB4Full;
-    h ^= h >> 31;
+    // splitmix64 finalizer of each coordinate's bits (the low bits of small integral doubles are all
+    // zero: a plain multiply would put most cells into a few buckets)
+    const unsigned long long h = mix64((unsigned long long)__double_as_longlong(cx + 0.0)) ^
+                                 mix64((unsigned long long)__double_as_longlong(cy + 0.0) ^ 0xC2B2AE3D27D4EB4Full);
     return (unsigned)h & (unsigned)(ncells - 1);
 }
 
@@ -378,11 +383,14 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__
                 acc = !(d2 >= rc2f);  // NaN radius (filter off): keep
             }
             const unsigned bal = __ballot_sync(kFull, acc);
-            if (acc) list[obase + count + __popc(bal & ((1u << sub) - 1))] = pos;
+            const int64_t widx = obase + count + __popc(bal & ((1u << sub) - 1));
+            GS_ASSERT(!acc || (pos >= 0 && pos < n && widx < ofs[c + 1]));
+            if (acc) list[widx] = pos;
             count += __popc(bal);
         }
     });
     const int padded = (count + pad - 1) / pad * pad;
+    GS_ASSERT(obase + padded <= ofs[c + 1] && ofs[c + 1] <= cap);
     for (int e = count + sub; e < padded; e += kTplB) list[obase + e] = (int)n;  // padding: sentinel
     if (sub == 0) len[c] = padded;
 }

@@ -1,0 +1,84 @@
+"""Race evidence by repetition: every kernel family sums in a fixed order (no fp64 atomics on the
+hot path), so repeated runs must be bitwise identical.  A data race on the shared-memory
+accumulators of k_dense_sym, the DSMEM st.async + mbarrier stage exchange of the small-N cluster
+kernel, the cluster Verlet lists or the batched items would show up as run-to-run differences.
+(compute-sanitizer is closed on the GPU pool; see profiles/r02_sanitizer.md for the checked build.)"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(runs):
+    first = runs[0]
+    return all(all(np.array_equal(a, b) for a, b in zip(first, r)) for r in runs[1:])
+
+
+def test_cluster_match_is_bitwise_repeatable(cuda):
+    from paper_1510_03816_b200 import configs, device
+    import paper_1510_03816_b200 as gs
+
+    w = configs.c1()  # N = 64: one 8-CTA cluster, DSMEM exchange every stage
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
+    runs = []
+    for _ in range(20):
+        r = device.match(spec, w.q, w.target, w.h, w.epsilon, w.max_iter, "residual", "max", 1.0, w.steps)
+        runs.append((r["p0"].cpu().numpy(), r["endpoint"].cpu().numpy(), np.array(r["residual_history"])))
+    assert _same(runs)
+
+
+def test_symmetric_dense_rhs_is_bitwise_repeatable(cuda):
+    import paper_1510_03816_b200 as gs
+
+    rng = np.random.default_rng(2)
+    n = 8192
+    q, p = rng.uniform(0, 1, (n, 2)), rng.normal(0, 0.01, (n, 2))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.05 / gs.LAMBDA))
+    prev = gs.get_path()
+    gs.set_path("dense")
+    try:
+        runs = [gs.rhs(spec, gs.ParticleState(q, p)) for _ in range(10)]
+    finally:
+        gs.set_path(prev)
+    assert _same(runs)
+
+
+def test_verlet_evolve_is_bitwise_repeatable(cuda):
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c5(65536)
+    p = 0.05 * (w.target - w.q)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    prev = gs.get_path()
+    gs.set_path("cell")
+    try:
+        runs = []
+        for _ in range(4):
+            out = gs.evolve(spec, gs.ParticleState(w.q, p), gs.EvolveConfig(t_final=0.4, steps=8))
+            runs.append((out.final.q, out.final.p))
+    finally:
+        gs.set_path(prev)
+    assert _same(runs)
+
+
+def test_batched_sweep_is_bitwise_repeatable(cuda):
+    import paper_1510_03816_b200 as gs
+
+    a, b = gs.circle(1.0, n=48), gs.ellipse_rot_shift(1.2, 0.8, 0.0, n=48)
+    grid = gs.SweepGrid((0.2, 0.4, 0.8), (0.2, 0.4), n_landmarks=48, max_iter=30)
+    runs = [(gs.convergence_sweep(a, b, grid),) for _ in range(5)]
+    assert _same(runs)
+
+
+def test_loaded_library_reports_its_build(cuda):
+    """GS_B200_LIB may point at the checked build (tools/checked_build.sh); the version says which."""
+    from paper_1510_03816_b200 import _native as N
+
+    v = N.load().gs_version().decode()
+    assert v.startswith("geoshoot-b200")
+    if os.environ.get("GS_B200_LIB", "").endswith("_checked.so"):
+        assert "checked" in v
