@@ -160,9 +160,13 @@ def check(rc: int, what: str) -> None:
 
 
 class Context:
-    """One gs_context per (process, device); owns the library's device workspaces."""
+    """One gs_context per (thread, device): the library's device workspaces and graph caches.
 
-    _by_device: dict = {}
+    The reference's calls are pure and may run concurrently; the C ABI asks
+    for one context per concurrent caller (include/geoshoot_b200.h), so each Python thread gets
+    its own context per device on first use."""
+
+    _tls = threading.local()
 
     def __init__(self, device: int):
         import torch
@@ -177,6 +181,21 @@ class Context:
         self.handle = h
 
     @classmethod
+    def _contexts(cls) -> dict:
+        d = getattr(cls._tls, "by_device", None)
+        if d is None:
+            d = cls._tls.by_device = {}
+        return d
+
+    @classmethod
+    def swap(cls, contexts: dict | None = None) -> dict:
+        """Replace this thread's contexts (None: none yet, so the next call creates a fresh one —
+        e.g. after changing a GS_B200_* environment knob read at gs_create); returns the old ones."""
+        old = cls._contexts()
+        cls._tls.by_device = {} if contexts is None else contexts
+        return old
+
+    @classmethod
     def get(cls, device: int | None = None) -> "Context":
         import torch
 
@@ -184,10 +203,11 @@ class Context:
             if not torch.cuda.is_available():
                 raise NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
             device = torch.cuda.current_device()
-        ctx = cls._by_device.get(device)
+        by_device = cls._contexts()
+        ctx = by_device.get(device)
         if ctx is None:
             ctx = cls(device)
-            cls._by_device[device] = ctx
+            by_device[device] = ctx
         return ctx
 
     def __del__(self):

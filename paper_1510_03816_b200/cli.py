@@ -36,7 +36,7 @@ def gpu_facts() -> dict:
 
         if torch.cuda.is_available():
             facts["device"] = torch.cuda.get_device_name(torch.cuda.current_device())
-            if N.Context._by_device:
+            if N.Context._contexts():
                 import ctypes
 
                 ctx = N.Context.get()

@@ -603,6 +603,7 @@ int run_evolve(gs_context* ctx, const SysConst& sc, double t_final, int steps, i
         GS_CUDA(cudaMemcpyAsync(frames, ctx->B.ptr, nrows * sizeof(double4), cudaMemcpyDeviceToDevice, stream));
     if (capture_every > 0) f = 1;
     for (int step = 1; step <= steps; ++step) {
+        NvtxScope nvtx_step("RK4 step");
         for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, stream);
         if (capture_every > 0 && (step % capture_every == 0 || step == steps)) {
             if (frames)
@@ -853,11 +854,13 @@ static int rhs_impl(gs_context* ctx, const gs_system_t* sys, int64_t n, const do
 
 int gs_rhs_rows(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p, int64_t row0,
                 int64_t row1, double* dq, double* dp, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_rhs_rows");
     return rhs_impl(ctx, sys, n, q, p, row0, row1, dq, dp, (cudaStream_t)stream);
 }
 
 int gs_rhs(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p, double* dq,
            double* dp, gs_status_t* status, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_rhs");
     int rc = rhs_impl(ctx, sys, n, q, p, 0, n, dq, dp, (cudaStream_t)stream);
     if (rc) return rc;
     gs_status_t st;
@@ -869,6 +872,7 @@ int gs_rhs(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, 
 
 int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
                    double* h_out, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_hamiltonian");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !h_out) return fail(GS_ERR_INVALID, "NULL argument");
     int rc = check_system(sys);
@@ -905,6 +909,7 @@ int gs_hamiltonian(gs_context* ctx, const gs_system_t* sys, int64_t n, const dou
 
 int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final, int32_t steps,
               int32_t capture_every, double* q, double* p, double* frames, gs_status_t* status, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_evolve");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx) return fail(GS_ERR_INVALID, "ctx is NULL");
     int rc = check_system(sys);
@@ -1057,6 +1062,7 @@ int match_device_loop(gs_context* ctx, const SysConst& sc, const gs_match_config
 int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* cfg, int64_t n, const double* q0,
              const double* target, double* p0_out, double* endpoint_out, double* history_out,
              gs_match_result_t* result, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_match");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !cfg || !result || !history_out) return fail(GS_ERR_INVALID, "NULL argument");
     int rc = check_match(sys, cfg);
@@ -1144,6 +1150,7 @@ int gs_match(gs_context* ctx, const gs_system_t* sys, const gs_match_config_t* c
         }
         if (!done) {
             for (int it = 0; it < cfg->max_iter; ++it) {
+                NvtxScope nvtx_it("feedback iteration");
                 const double delta = cfg->h * nrm;
                 k_match_begin<<<nblk(n), 256, 0, s>>>(ctx->q0.ptr, ctx->p.ptr, ctx->resid.ptr, cfg->h, n, ctx->S.ptr,
                                                       ctx->B.ptr);
@@ -1221,6 +1228,7 @@ int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stre
 // ---- stage API ------------------------------------------------------------------------
 int gs_stage_begin(gs_context* ctx, int64_t n, const double* q, const double* p, int64_t row0, int64_t row1,
                    void* stream) {
+    gsapi::NvtxScope nvtx_("gs_stage_begin");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !q || !p || n < 1 || row0 < 0 || row1 > n || row0 > row1) return fail(GS_ERR_INVALID, "bad stage args");
     GS_CUDA(cudaSetDevice(ctx->device));
@@ -1236,6 +1244,7 @@ int gs_stage_begin(gs_context* ctx, int64_t n, const double* q, const double* p,
 }
 
 int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_stage_run");
     if (!ctx || ctx->n < 1) return fail(GS_ERR_INVALID, "no stage session");
     int rc = check_system(sys);
     if (rc) return rc;
@@ -1249,6 +1258,7 @@ int gs_stage_run(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
 double* gs_stage_state(gs_context* ctx) { return ctx ? reinterpret_cast<double*>(ctx->S.ptr) : nullptr; }
 
 int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_stage_end");
     if (!ctx || !q_rows) return fail(GS_ERR_INVALID, "bad stage args");
     const int64_t nrows = ctx->row1 - ctx->row0;
     if (nrows > 0) k_unpack<<<nblk(nrows), 256, 0, (cudaStream_t)stream>>>(ctx->B.ptr, nrows, q_rows, p_rows);
@@ -1258,6 +1268,7 @@ int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream) 
 
 int gs_gram(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, double* K, int64_t* bad_i,
             int64_t* bad_j, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_gram");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !q || !K || !bad_i || !bad_j || n < 1) return fail(GS_ERR_INVALID, "bad gram args");
     int rc = check_system(sys);
@@ -1278,6 +1289,7 @@ int gs_gram(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q,
 
 int gs_velocity_field(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, const double* p,
                       int64_t m, const double* x, double* u, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_velocity_field");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !q || !p || !x || !u || n < 1 || m < 0) return fail(GS_ERR_INVALID, "bad velocity-field args");
     int rc = check_system(sys);
@@ -1310,11 +1322,13 @@ int64_t gs_sym_parts(int64_t n) {
 
 int gs_stage_pairs_sym(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
                        int64_t part_end, double* R, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_stage_pairs_sym");
     return pairs_sym_impl(ctx, sys, step, stg, part_begin, part_end, R, stream);
 }
 
 int gs_stage_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt,
                     const double* R_rows, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_stage_finish");
     if (!ctx || ctx->n < 1) return fail(GS_ERR_INVALID, "no stage session");
     int rc = check_system(sys);
     if (rc) return rc;

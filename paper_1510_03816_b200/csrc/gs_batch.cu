@@ -29,6 +29,7 @@ int gs_match_batch(gs_context* ctx, const gs_batch_item_t* items, int64_t batch,
                    int64_t q0_stride, const double* target, int64_t target_stride, const double* gram_factor,
                    int64_t factor_stride, double* p0_out, double* endpoint_out, double* history_out,
                    int64_t history_stride, gs_match_result_t* results, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_match_batch");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !items || !results || !history_out) return fail(GS_ERR_INVALID, "NULL argument");
     if (batch < 1) return fail(GS_ERR_INVALID, "batch must be >= 1");
@@ -109,6 +110,7 @@ int gs_match_batch(gs_context* ctx, const gs_batch_item_t* items, int64_t batch,
 int gs_evolve_batch(gs_context* ctx, const gs_system_t* sys, int64_t batch, int64_t n, double t_final, int32_t steps,
                     const double* q_in, int64_t q_stride, double* q_out, double* p_io, gs_status_t* status,
                     void* stream) {
+    gsapi::NvtxScope nvtx_("gs_evolve_batch");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !status) return fail(GS_ERR_INVALID, "NULL argument");
     int rc = check_system(sys);

@@ -10,11 +10,23 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/geoshoot_b200.h"
 #include "gs_cell.cuh"
 #include "gs_kernels.cuh"
 
 namespace gsapi {
+
+// NVTX range for the lifetime of a scope (every C-ABI call, every host-driven feedback iteration
+// and RK stage): visible in nsys / ncu timelines, free when no tool is attached (nvtx3 is
+// header-only and loads a tool only through NVTX_INJECTION64_PATH).
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+    NvtxScope(const NvtxScope&) = delete;
+    NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 extern thread_local std::string g_last_error;
 int fail(int code, const std::string& msg);

@@ -102,6 +102,7 @@ int gs_p2p_import(gs_context* ctx, int world, int rank, const void* handles_all)
 
 int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, int64_t part_begin,
                  int64_t part_end, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_p2p_pairs");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers (gs_p2p_import / gs_p2p_set_peers)");
     GS_CUDA(cudaSetDevice(ctx->device));
@@ -123,6 +124,7 @@ int gs_p2p_pairs(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t 
 }
 
 int gs_p2p_finish(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stg, double dt, void* stream) {
+    gsapi::NvtxScope nvtx_("gs_p2p_finish");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || ctx->p2p.world < 1) return fail(GS_ERR_INVALID, "no peers (gs_p2p_import / gs_p2p_set_peers)");
     int rc = check_system(sys);

@@ -181,6 +181,20 @@ def _event_key(st) -> tuple:
     return (st.step * 8 + st.event, st.i, st.j)
 
 
+def _nvtx(name: str):
+    """An NVTX range on the CUDA timeline (no-op without CUDA / a profiler)."""
+    import contextlib
+
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.nvtx.range(name)
+    except Exception:
+        pass
+    return contextlib.nullcontext()
+
+
 class ShardedSolver:
     """Row-sharded evolve / match across the ranks of ``group`` (default: the world)."""
 
@@ -272,13 +286,14 @@ class ShardedSolver:
                 return self._evolve_p2p(q, p, t_final, steps, n, c, b, e, S, r0, r1)
         for step in range(1, steps + 1):
             for s in range(4):
-                if sym:
-                    self.backend.pairs_sym(step, s, b, e, R)
-                    self._reduce_scatter_rows(R_rows, R, c)
-                    self.backend.finish(step, s, dt, R_rows)
-                else:
-                    self.backend.run(step, s, dt)
-                self._allgather_rows(S, r0, c)
+                with _nvtx(f"stage {step}.{s}"):
+                    if sym:
+                        self.backend.pairs_sym(step, s, b, e, R)
+                        self._reduce_scatter_rows(R_rows, R, c)
+                        self.backend.finish(step, s, dt, R_rows)
+                    else:
+                        self.backend.run(step, s, dt)
+                    self._allgather_rows(S, r0, c)
         self._raise_first_failure(t_final, steps)
         return S[:n, 0:2].clone(), S[:n, 2:4].clone()
 
@@ -384,11 +399,12 @@ class ShardedSolver:
             converged = True
         else:
             diagnosis = "iteration cap reached before the stopping rule"
-            for _ in range(max_iter):
+            for it in range(max_iter):
                 delta = h * nrm
                 p = p + h * residual
                 try:
-                    qT, _ = self.evolve(q0, p, t_final, steps)
+                    with _nvtx(f"feedback iteration {it + 1}"):
+                        qT, _ = self.evolve(q0, p, t_final, steps)
                 except (_errors.DivergenceError, _errors.DegenerateConfigurationError) as exc:
                     diagnosis = f"step too large ({exc})"
                     break

@@ -82,3 +82,38 @@ def test_loaded_library_reports_its_build(cuda):
     assert v.startswith("geoshoot-b200")
     if os.environ.get("GS_B200_LIB", "").endswith("_checked.so"):
         assert "checked" in v
+
+
+def test_concurrent_threads_get_their_own_contexts(cuda):
+    """Independent matches from two Python threads at once (the reference allows concurrent
+    trajectories): each thread has its own library context, and the results equal
+    the same matches run one after the other."""
+    import threading
+
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import _native as N
+    from paper_1510_03816_b200 import configs, device
+
+    w = configs.c4(4096)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha))
+    hs = (0.0005, 0.001)
+
+    def run(h):
+        r = device.match(spec, w.q, w.target, h, 1e-6, 6, "residual", "max", 1.0, 20)
+        return r["p0"].cpu().numpy(), np.array(r["residual_history"])
+
+    serial = [run(h) for h in hs]
+    out, ctxs = [None, None], [None, None]
+
+    def worker(k):
+        out[k] = run(hs[k])
+        ctxs[k] = N.Context.get().handle.value
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert ctxs[0] != ctxs[1] and ctxs[0] != N.Context.get().handle.value
+    for k in range(2):
+        assert np.array_equal(out[k][0], serial[k][0]) and np.array_equal(out[k][1], serial[k][1])

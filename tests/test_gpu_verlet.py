@@ -30,8 +30,7 @@ class _Env:
         self.N = N
         self.saved = {k: os.environ.get(k) for k in self.env}
         os.environ.update({k: str(v) for k, v in self.env.items()})
-        self.ctxs = N.Context._by_device
-        N.Context._by_device = {}
+        self.ctxs = N.Context.swap()
         return N
 
     def __exit__(self, *exc):
@@ -40,7 +39,7 @@ class _Env:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-        self.N.Context._by_device = self.ctxs
+        self.N.Context.swap(self.ctxs)
 
 
 def _stats(N):

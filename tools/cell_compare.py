@@ -41,7 +41,7 @@ def main():
 
     def run(w, p, steps, tf, verlet):
         os.environ["GS_B200_VERLET"] = "1" if verlet else "0"
-        N.Context._by_device = {}  # noqa: SLF001  (fresh context: reads the env at gs_create)
+        N.Context.swap()  # fresh context: reads the env at gs_create
         spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
         qd = torch.from_numpy(w.q).cuda()
         pd = torch.from_numpy(p).cuda()
