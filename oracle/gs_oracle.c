@@ -84,13 +84,21 @@ typedef struct {
     double* ps;    /* n x 2, p in bucket order */
 } go_grid;
 
+static inline unsigned long long mix64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 static unsigned long cell_bucket(double cx, double cy, unsigned long nb) {
     double ax = cx + 0.0, ay = cy + 0.0;   /* -0.0 -> +0.0 */
     unsigned long long bx, by;
     memcpy(&bx, &ax, 8);
     memcpy(&by, &ay, 8);
-    unsigned long long h = bx * 0x9E3779B97F4A7C15ull ^ by * 0xC2B2AE3D27D4EB4Full;
-    h ^= h >> 31;
+    /* splitmix64 finalizer of each coordinate's bits: the low bits of small integral doubles are
+     * all zero, so a plain multiply would put most cells into a few buckets */
+    unsigned long long h = mix64(bx) ^ mix64(by ^ 0xC2B2AE3D27D4EB4Full);
     return (unsigned long)(h & (nb - 1));
 }
 
