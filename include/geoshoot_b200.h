@@ -225,6 +225,17 @@ int gs_stage_end(gs_context* ctx, double* q_rows, double* p_rows, void* stream);
 int gs_gram(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q, double* K, int64_t* bad_i,
             int64_t* bad_j, void* stream);
 
+/* shooting.py:138-159, 263-265 (_GramSolver.solve) without forming K: solves (K (x) I2) p = u by
+ * conjugate gradients, K v being the dq half of the RHS at (q0, v) through the same pair kernels
+ * (dense, or the cluster lists of q0 built once).  q0, u (device, n x 2); p (device, n x 2) is the
+ * initial guess on entry (warm start) and the solution on exit.  Stops when |u - K p| <= tol |u|
+ * or after max_it iterations; *iters and *relres (host) report which.  coef (host, 2 * max_it
+ * doubles, nullable) receives alpha_k, beta_k of every iteration — the Lanczos tridiagonal whose
+ * extreme eigenvalues estimate cond(K) for the reference's ill-conditioning warning
+ * (shooting.py:237-242).  Synchronises (once per iteration). */
+int gs_gram_cg(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q0, const double* u, double* p,
+               double tol, int32_t max_it, int32_t* iters, double* coef, double* relres, void* stream);
+
 /* Symmetric multi-GPU split of the dense RHS (each unordered pair once, gs_sym.cu):
  *   gs_sym_parts       : number of work items (superblock pairs) of one RHS at this n (0 if the
  *                        symmetric kernel is not available for n)

@@ -36,7 +36,7 @@ EXPORTS = (
     "gs_profile_read", "gs_stage_path", "gs_sym_parts", "gs_stage_pairs_sym", "gs_stage_finish", "gs_gram",
     "gs_match_batch", "gs_evolve_batch", "gs_velocity_field", "gs_p2p_local", "gs_p2p_export", "gs_p2p_import",
     "gs_p2p_set_peers", "gs_p2p_pairs", "gs_p2p_finish", "gs_p2p_sync", "gs_p2p_timeouts", "gs_p2p_close",
-    "gs_cell_stats",
+    "gs_cell_stats", "gs_gram_cg",
 )
 
 
@@ -139,6 +139,8 @@ def load(path: str = LIB_PATH):
             "gs_p2p_close": ([_vp], ctypes.c_int),
             "gs_profile_enable": ([_vp, ctypes.c_int32], ctypes.c_int),
             "gs_cell_stats": ([_vp, P(_i64), P(_i64), _vp], ctypes.c_int),
+            "gs_gram_cg": ([_vp, P(System), _i64, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
+                            P(ctypes.c_int32), P(ctypes.c_double), P(ctypes.c_double), _vp], ctypes.c_int),
             "gs_profile_read": ([_vp, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64),
                                  ctypes.c_int32], ctypes.c_int),
         }

@@ -801,7 +801,7 @@ int gs_destroy(gs_context* ctx) {
     if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
-    ctx->v_over.release(); ctx->v_scan.release();
+    ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release();
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     gs_p2p_close(ctx);
@@ -1222,6 +1222,162 @@ int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stre
     GS_CUDA(cudaStreamSynchronize(s));
     *builds = f[1];
     *entries = tot;
+    return GS_OK;
+}
+
+// ---- matrix-free Gram solve (velocity update space) --------------------------
+// shooting.py:138-159, 263-265: p = K^-1 u with K_ij = G(|q0_i - q0_j|) (the reference factors K
+// once with Cholesky).  Here K v is the dq half of the RHS at (q0, v) — the same pair kernels
+// (dense, cell sweep or cluster lists built once: q0 never moves) — and conjugate gradients on the
+// 2N vector (K (x) I2 is SPD) solve to a relative residual `tol`.  Reductions are fixed-order.
+
+namespace gsapi {
+
+__global__ void k_cg_dot_partial(const double* __restrict__ a, const double* __restrict__ b, int64_t m, double* red) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        acc = fma(a[i], b[i], acc);
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) red[blockIdx.x] = s[0];
+}
+
+// r = u - Kp; d = r
+__global__ void k_cg_init(const double* __restrict__ u, const double* __restrict__ Kp, int64_t m, double* r, double* d) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        const double v = u[i] - Kp[i];
+        r[i] = v;
+        d[i] = v;
+    }
+}
+
+// p += alpha d; r -= alpha Kd   (alpha = scal[0] / scal[1])
+__global__ void k_cg_step(const double* __restrict__ scal, const double* __restrict__ d, const double* __restrict__ Kd,
+                          int64_t m, double* p, double* r) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        const double alpha = scal[0] / scal[1];
+        p[i] = fma(alpha, d[i], p[i]);
+        r[i] = fma(-alpha, Kd[i], r[i]);
+    }
+}
+
+// d = r + beta d   (beta = scal[2] / scal[0])
+__global__ void k_cg_dir(const double* __restrict__ scal, const double* __restrict__ r, int64_t m, double* d) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) d[i] = fma(scal[2] / scal[0], d[i], r[i]);
+}
+
+}  // namespace gsapi
+
+// out = K v at the fixed points q0 (device, n x 2 each).  With lists: the cluster lists of q0,
+// built by the caller, refreshed (momenta only) and swept.
+static void gram_matvec(gs_context* ctx, const SysConst& sc, int64_t n, const double* q0, const double* v,
+                        double* out, double* scratch, bool lists, cudaStream_t s) {
+    k_pack<<<nblk(n), 256, 0, s>>>(q0, v, n, ctx->S.ptr, ctx->st.ptr, 0);
+    PairOut po{1, 0};
+    if (lists) {
+        CellWs w = cell_ws(ctx);
+        VerletWs vw = verlet_ws(ctx, n, sc.cutoff);
+        verlet_gather(w, vw, ctx->S.ptr, n, 0, cudaGraphConditionalHandle{}, 0, s);
+        launch_verlet_pair(sc, w, vw, n, ctx->part.ptr, ctx->st.ptr, 2ull, ctx->tbl.ptr, nullptr, s);
+        ctx->launches += 2;
+        ctx->pair_launches++;
+    } else {
+        const DensePlan plan = dense_plan(n, ctx->sm_count);
+        po = pair_kernel(ctx, sc, ctx->S.ptr, n, 0, n, plan, ctx->part.ptr, 2ull, s);
+    }
+    FinishArgs fa{};
+    fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = n; fa.row0 = 0;
+    fa.S = ctx->S.ptr; fa.dq = out; fa.dp = scratch; fa.st = ctx->st.ptr; fa.event = 3ull;
+    launch_finish(kFinRhs, sc, fa, s);
+    ctx->launches += 2;
+}
+
+extern "C" int gs_gram_cg(gs_context* ctx, const gs_system_t* sys, int64_t n, const double* q0, const double* u,
+                          double* p, double tol, int32_t max_it, int32_t* iters, double* coef, double* relres,
+                          void* stream) {
+    gsapi::NvtxScope nvtx_("gs_gram_cg");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx || !iters || !relres) return fail(GS_ERR_INVALID, "NULL argument");
+    int rc = check_system(sys);
+    if (rc) return rc;
+    if (n < 1 || !q0 || !u || !p) return fail(GS_ERR_INVALID, "q0, u and p must have shape (N, 2), N >= 1");
+    if (!(tol > 0.0) || max_it < 1) return fail(GS_ERR_INVALID, "tol must be positive and max_it >= 1");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    gs_system_t plain = *sys;
+    plain.sigma2 = 0.0;  // K only (the sigma2 term belongs to the RHS, not to the Gram matrix)
+    const SysConst sc = make_const(&plain);
+    if ((rc = ensure_session(ctx, n, n))) return rc;
+    ctx->n = n; ctx->row0 = 0; ctx->row1 = n;
+    const int64_t m = 2 * n;
+    GS_CUDA(ctx->cg.ensure(4 * m));
+    GS_CUDA(ctx->red.ensure(kRedBlocks));
+    double* r = ctx->cg.ptr;
+    double* d = r + m;
+    double* Kd = d + m;
+    double* scratch = Kd + m;
+    k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
+    k_pack<<<nblk(n), 256, 0, s>>>(q0, p, n, ctx->S.ptr, ctx->st.ptr, 0);
+    if ((rc = choose_path(ctx, &plain, ctx->S.ptr, n, s, false))) return rc;
+    bool lists = false;
+    if (ctx->cell_on && ctx->verlet_on) {  // q0 is fixed: one list build serves every product
+        if ((rc = ensure_verlet(ctx, ctx->S.ptr, n, sc.cutoff, s))) return rc;
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            if (verlet_build(cell_ws(ctx), verlet_ws(ctx, n, sc.cutoff), ctx->S.ptr, n, sc.cutoff, s))
+                return fail(GS_ERR_CUDA, "verlet build failed");
+            ctx->verlet_call = 1;
+            bool retry = false;
+            if ((rc = verlet_retry(ctx, s, &retry))) return rc;
+            if (!retry) break;
+        }
+        lists = ctx->verlet_on != 0;
+    }
+    const int nb = (int)std::min<int64_t>(kRedBlocks, (m + 255) / 256);
+    double* sc_dev = ctx->scal.ptr;  // [0] r.r, [1] d.Kd, [2] r.r new, [3] u.u
+    auto dot = [&](const double* a, const double* b, int slot) {
+        k_cg_dot_partial<<<nb, 256, 0, s>>>(a, b, m, ctx->red.ptr);
+        k_reduce_final<<<1, 512, 0, s>>>(ctx->red.ptr, nb, 2, sc_dev + slot, nullptr);
+    };
+    gram_matvec(ctx, sc, n, q0, p, Kd, scratch, lists, s);  // K p0 (warm start)
+    k_cg_init<<<nblk(m), 256, 0, s>>>(u, Kd, m, r, d);
+    dot(r, r, 0);
+    dot(u, u, 3);
+    GS_CUDA(cudaMemcpyAsync(ctx->scal_host, sc_dev, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(cudaStreamSynchronize(s));
+    const double unorm = std::sqrt(ctx->scal_host[3]);
+    double rr = ctx->scal_host[0];
+    int it = 0;
+    while (it < max_it && std::sqrt(rr) > tol * unorm && rr > 0.0) {
+        gram_matvec(ctx, sc, n, q0, d, Kd, scratch, lists, s);
+        dot(d, Kd, 1);
+        k_cg_step<<<nblk(m), 256, 0, s>>>(sc_dev, d, Kd, m, p, r);
+        dot(r, r, 2);
+        k_cg_dir<<<nblk(m), 256, 0, s>>>(sc_dev, r, m, d);
+        GS_CUDA(cudaMemcpyAsync(ctx->scal_host, sc_dev, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        GS_CUDA(cudaMemcpyAsync(sc_dev, sc_dev + 2, sizeof(double), cudaMemcpyDeviceToDevice, s));  // rr <- rr new
+        GS_CUDA(cudaStreamSynchronize(s));
+        const double alpha = ctx->scal_host[0] / ctx->scal_host[1], beta = ctx->scal_host[2] / ctx->scal_host[0];
+        if (coef) { coef[2 * it] = alpha; coef[2 * it + 1] = beta; }
+        rr = ctx->scal_host[2];
+        ctx->launches += 8;
+        ++it;
+        if (!(ctx->scal_host[1] > 0.0)) break;  // K not positive definite along d (or a NaN)
+    }
+    *iters = it;
+    *relres = unorm > 0.0 ? std::sqrt(rr) / unorm : 0.0;
+    ctx->verlet_call = 0;
+    gs_status_t st;
+    rc = fetch_status(ctx, s, n, &st);
+    if (rc == GS_ERR_COINCIDENT) return fail(rc, "coincident points: the Gram matrix is singular");
+    if (rc == GS_ERR_CUDA) return rc;
+    if ((rc = take_cell_err(ctx))) return rc;
     return GS_OK;
 }
 

@@ -95,6 +95,7 @@ struct gs_context {
     DevBuf<SmallItem> b_items;       // batched launches: per-item constants
     DevBuf<DevStatus> b_st;          // batched evolve: per-item failure records
     DevBuf<double2> vf_part;         // velocity-field chunk partials
+    DevBuf<double> cg;               // matrix-free Gram solve: r, d, K d, scratch (4 x 2n)
     // rank split of the symmetric kernel: slots written per row superblock for the cached range
     DevBuf<int> sym_slots, sym_counts;
     int64_t sym_key_n = -1, sym_key_b = -1, sym_key_e = -1;

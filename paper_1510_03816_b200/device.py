@@ -10,6 +10,7 @@ streams only; all arithmetic of the hot path runs in the library's kernels.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import numpy as np
@@ -167,6 +168,44 @@ def gram(spec, q):
             f"points {bi.value} and {bj.value} coincide; Gram matrix would be singular")
     N.check(rc, "gs_gram")
     return K
+
+
+def gram_cg(spec, q0, u, p0=None, tol: float = 1e-14, max_it: int = 2000):
+    """p = K^-1 u without forming K (gs_gram_cg): conjugate gradients whose K v is the dq half of
+    the RHS at (q0, v) through the library's pair kernels.  p0: warm start (zeros if None).
+    Returns (p, iterations, relative residual, [(alpha_k, beta_k)])."""
+    torch = _torch()
+    ctx = N.Context.get()
+    q0 = as_device(q0, torch)
+    u = as_device(u, torch)
+    n = q0.shape[0]
+    p = torch.zeros_like(q0) if p0 is None else as_device(p0, torch).clone()
+    coef = (ctypes.c_double * (2 * max(1, max_it)))()
+    iters, relres = ctypes.c_int32(), ctypes.c_double()
+    sysc = system_struct(spec)
+    rc = ctx.lib.gs_gram_cg(ctx.handle, ctypes.byref(sysc), n, _ptr(q0), _ptr(u), _ptr(p), float(tol), int(max_it),
+                            ctypes.byref(iters), coef, ctypes.byref(relres), _stream_ptr(torch))
+    if rc == N.GS_ERR_COINCIDENT:
+        raise _errors.DegenerateConfigurationError("kernel Gram matrix is not positive definite: coincident points")
+    N.check(rc, "gs_gram_cg")
+    k = int(iters.value)
+    return p, k, float(relres.value), [(coef[2 * i], coef[2 * i + 1]) for i in range(k)]
+
+
+def lanczos_condition(coefs) -> float:
+    """cond(K) estimate from the CG coefficients: the extreme eigenvalues of the Lanczos
+    tridiagonal T (diag 1/a_k + b_(k-1)/a_(k-1), off-diagonal sqrt(b_k)/a_k).  A lower bound that
+    tightens with the iteration count."""
+    if not coefs:
+        return 1.0
+    a = np.array([c[0] for c in coefs])
+    b = np.array([c[1] for c in coefs])
+    diag = 1.0 / a
+    diag[1:] += b[:-1] / a[:-1]
+    off = np.sqrt(np.maximum(b[:-1], 0.0)) / a[:-1]
+    T = np.diag(diag) + np.diag(off, 1) + np.diag(off, -1)
+    ev = np.linalg.eigvalsh(T)
+    return float(ev[-1] / ev[0]) if ev[0] > 0 else math.inf
 
 
 def velocity_field(spec, q, p, x):

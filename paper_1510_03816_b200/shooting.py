@@ -171,22 +171,69 @@ def match_config_dict(cfg) -> dict:
                 norm=_enum_value(cfg.norm), t_final=cfg.evolve.t_final, steps=cfg.evolve.steps)
 
 
+CG_TOL = 1e-14          # relative residual of the matrix-free Gram solve
+CG_MAX_IT = 2000
+DENSE_FALLBACK_MAX = 16384  # CG stagnating (ill-conditioned K): dense Cholesky up to this N (K = 2 GB)
+
+
+class CGGramSolver:
+    """_GramSolver (shooting.py:138-159) for N above the persistent-kernel range, without forming K:
+    p = K^-1 u by conjugate gradients on the device (gs_gram_cg: K v is the dq half of the RHS at
+    (q0, v) through the pair kernels, dense or the cluster lists of q0), warm-started from the
+    previous iteration's p (u changes by h r per iteration).  cond(K) for the reference's warning
+    (shooting.py:145, 237-242) is estimated from the first solve's Lanczos coefficients.  When CG
+    stagnates above 1e-10 (a near-singular K) and N <= DENSE_FALLBACK_MAX, the solver switches to the
+    reference's own method: the dense Gram matrix (gs_gram) and its Cholesky factor (cuSOLVER)."""
+
+    def __init__(self, spec, q0):
+        self.spec, self.q0 = spec, q0
+        self.p = None
+        self.condition = None
+        self.factor = None
+        self.solves = self.cg_iterations = 0
+
+    def solve(self, u):
+        torch = device._torch()
+        if self.factor is not None:
+            return torch.cholesky_solve(u, self.factor)
+        p, it, rel, coef = device.gram_cg(self.spec, self.q0, u, self.p, CG_TOL, CG_MAX_IT)
+        self.solves += 1
+        self.cg_iterations += it
+        if self.condition is None and coef:
+            self.condition = device.lanczos_condition(coef)
+        if rel > 1e-10 and self.q0.shape[0] <= DENSE_FALLBACK_MAX:
+            self.factor, self.condition, _ = gram_factor(self.spec, self.q0)
+            return torch.cholesky_solve(u, self.factor)
+        self.p = p
+        return p
+
+    def warnings(self, u_probe=None):
+        if self.condition is None and u_probe is not None:
+            self.solve(u_probe)
+        cond = self.condition if self.condition is not None else 1.0
+        if not (cond < _ILL_CONDITIONED):
+            return (f"Gram matrix condition number {cond:.3e} exceeds {_ILL_CONDITIONED:.0e}; "
+                    "momenta recovery may lose accuracy",)
+        return ()
+
+
 def _match_velocity(reference, target, cfg):
     """shooting.py:218-301 with UpdateSpace.VELOCITY: u <- u + h r, p = K^-1 u (:263-265).
 
     N <= 512: the whole loop — the triangular solve pair of every iteration included — runs in
-    one persistent CTA (gs_match_batch with the Gram factor).  Above that each iteration is
-    one cuSOLVER triangular solve pair (torch.cholesky_solve) plus a device shoot, and the
-    host reads the residual norm.
+    one persistent CTA (gs_match_batch with the Gram factor, cuSOLVER Cholesky once).  Above
+    that K is never formed: each iteration solves K p = u by matrix-free conjugate gradients on
+    the device (CGGramSolver), then shoots on the device; the host reads the residual norm.
     """
     torch = device._torch()
     q0 = device.as_device(reference.points, torch)
-    L, _, warnings = gram_factor(cfg.system, q0)
     if _batchable(reference.n):
+        L, _, warnings = gram_factor(cfg.system, q0)
         r = device.match_batch([cfg.system], [match_config_dict(cfg)], q0, target.points, factor=L)[0]
         return _make_result(r["p0"].cpu().numpy(), r["iterations"], r["converged"], r["residual_history"],
                             r["hamiltonian"], r["endpoint"].cpu().numpy(), reference, target, r["final_residual"],
                             r["diagnosis"], warnings)
+    solver = CGGramSolver(cfg.system, q0)
     tgt = device.as_device(target.points, torch)
     norm_kind = _enum_value(cfg.norm)
     mdelta = _enum_value(cfg.stop_rule) == "momentum-delta"
@@ -200,7 +247,7 @@ def _match_velocity(reference, target, cfg):
     def result(p, history, converged, endpoint, diagnosis):
         return _make_result(p.cpu().numpy(), len(history), converged, history,
                             device.hamiltonian(cfg.system, q0, p), endpoint.cpu().numpy(), reference, target,
-                            dnorm(tgt - endpoint), diagnosis, warnings)
+                            dnorm(tgt - endpoint), diagnosis, solver.warnings(tgt - q0))
 
     u = torch.zeros_like(q0)
     p = torch.zeros_like(q0)
@@ -215,7 +262,7 @@ def _match_velocity(reference, target, cfg):
     for _ in range(cfg.max_iter):
         delta = cfg.h * dnorm(residual)
         u = u + cfg.h * residual
-        p = torch.cholesky_solve(u, L)
+        p = solver.solve(u)
         try:
             endpoint_new, _, _ = device.evolve(cfg.system, q0, p, ev.t_final, ev.steps, 0)
         except (_errors.DivergenceError, _errors.DegenerateConfigurationError) as exc:
@@ -240,7 +287,10 @@ def momenta_from_velocity(kernel, q0, u0) -> np.ndarray:
     if q0.shape != u0.shape or q0.ndim != 2 or q0.shape[1] != 2:
         raise ValueError(f"q0 and u0 must both have shape (N, 2), got {q0.shape} and {u0.shape}")
     torch = device._torch()
-    L, _, _ = gram_factor(SystemSpec(kernel=kernel), q0)
+    spec = SystemSpec(kernel=kernel)
+    if q0.shape[0] > SMALL_MAX:  # matrix-free: K is never formed
+        return CGGramSolver(spec, device.as_device(q0, torch)).solve(device.as_device(u0, torch)).cpu().numpy()
+    L, _, _ = gram_factor(spec, q0)
     return torch.cholesky_solve(device.as_device(u0, torch), L).cpu().numpy()
 
 

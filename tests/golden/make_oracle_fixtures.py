@@ -19,6 +19,9 @@ Fixtures (tests/golden/oracle_<name>.npz):
   c5_match2       C5 at the configured h: the first 2 feedback iterations
   c4_mid          C4 recipe at N = 32768: the whole 100-iteration match at the configured h
   c5_mid          C5 recipe at N = 65536: the whole 20-iteration match at the configured h
+  vel_<n>         velocity-space matches (UpdateSpace.VELOCITY, shooting.py:138-159, 263-265) above the
+                  persistent-kernel range, N = 600 / 1024 / 4096, circle -> ellipse (converging cases), dense oracle
+                  evolve and scipy's Cholesky of the Gram matrix (the reference's own method)
 The feedback loop below restates shooting.py:218-301 (momentum branch, :266-267) exactly as
 oracle/restate.py does, with the oracle's truncated evolve and the exact zero-momentum shoot
 (p = 0 gives dq = dp = 0, so the endpoint is q0 bitwise).
@@ -177,6 +180,28 @@ def match_fixture(name, w, h, max_iter, stride, with_h=False):
     save(name, meta, rows=rows, p0=r["p0"][rows], endpoint=r["endpoint"][rows], history=r["history"])
 
 
+# (N, support radius, ellipse axes): converging velocity-space matches (larger deformations or the
+# narrowest kernels blow up, which would only pin an amplified rounding race)
+VEL_CASES = ((600, 2.0, 1.1, 0.9), (1024, 1.0, 1.1, 0.9), (4096, 0.2, 1.05, 0.95))
+
+
+def vel_fixture(n, sig, ax, ay):
+    from oracle import restate
+
+    q0 = configs._circle(1.0, n)
+    y = configs._ellipse(ax, ay, n)
+    k = Kernel(0, sig / configs.LAMBDA, True)
+    t0 = time.perf_counter()
+    ev = lambda qq, pp: q0.copy() if not np.any(pp) else native.evolve(k, 0.0, qq, pp, 1.0, 20)[0]  # noqa: E731
+    r = restate.match_momentum(k, 0.0, q0, y, 0.5, 1e-6, 100, "residual", "max", 1.0, 20, evolve_fn=ev,
+                               update_space="velocity")
+    meta = dict(n=n, sigma=sig, alpha=k.alpha, axes=[ax, ay], h=0.5, epsilon=1e-6, max_iter=100, steps=20,
+                iterations=r["iterations"], converged=r["converged"], diagnosis=r["diagnosis"],
+                hamiltonian=r["hamiltonian"], final_residual=r["final_residual"], seconds=time.perf_counter() - t0,
+                cond=float(np.linalg.cond(restate.gram_matrix(k, q0))))
+    save(f"vel_{n}", meta, p0=r["p0"], endpoint=r["endpoint"], history=np.array(r["residual_history"]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -199,6 +224,9 @@ def main():
     if want("c5_mid"):
         w = configs.c5(65536)
         match_fixture("c5_mid", w, w.h, w.max_iter, stride=16, with_h=True)
+    for n, sig, ax, ay in VEL_CASES:
+        if want(f"vel_{n}"):
+            vel_fixture(n, sig, ax, ay)
     if want("c4_onset"):
         w = configs.c4()
         onset_fixture("c4_onset", w, ONSET_H["C4"], stride=64)
