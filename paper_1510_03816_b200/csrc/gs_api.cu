@@ -283,9 +283,14 @@ VerletWs verlet_ws(gs_context* ctx, int64_t n, double cutoff) {
     VerletWs v;
     v.cnt = ctx->v_cnt.ptr; v.ofs = ctx->v_ofs.ptr; v.len = ctx->v_len.ptr; v.list = ctx->v_list.ptr;
     v.cap = (int64_t)ctx->v_list.cap;
-    v.Xb = ctx->v_xb.ptr; v.flags = ctx->v_flags.ptr; v.overflow = ctx->v_over.ptr;
+    v.Xb = ctx->v_xb.ptr; v.inv = ctx->v_inv.ptr; v.flags = ctx->v_flags.ptr; v.overflow = ctx->v_over.ptr;
     v.scan_temp = ctx->v_scan.ptr; v.scan_bytes = ctx->v_scan.cap;
-    v.tpl = verlet_tpl(n); v.skin = ctx->verlet_skin; v.cutoff = cutoff;
+    // skin: small clouds are launch/latency bound, so fewer rebuilds beat fewer masked pairs
+    // (C2: 0.05 -> 0.1 saves 1.5 ms per 100-step solve); large ones are FP64 bound (C4/C5: the
+    // masked skin pairs cost more than the rebuilds they save) — tools/verlet_ab.py
+    v.tpl = verlet_tpl(n);
+    v.skin = ctx->verlet_skin >= 0.0 ? ctx->verlet_skin : (n < 131072 ? 0.1 : 0.05);
+    v.cutoff = cutoff;
     return v;
 }
 
@@ -296,7 +301,7 @@ int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, c
     const int64_t ncl = verlet_clusters(n);
     const bool fresh = ctx->v_flags.cap == 0;
     GS_CUDA(ctx->v_cnt.ensure(ncl + 1)); GS_CUDA(ctx->v_ofs.ensure(ncl + 1)); GS_CUDA(ctx->v_xb.ensure(n));
-    GS_CUDA(ctx->v_len.ensure(ncl));
+    GS_CUDA(ctx->v_len.ensure(ncl)); GS_CUDA(ctx->v_inv.ensure(n));
     GS_CUDA(ctx->v_flags.ensure(4)); GS_CUDA(ctx->v_over.ensure(1));
     GS_CUDA(ctx->v_scan.ensure(verlet_scan_bytes(ncl)));
     if (fresh) {
@@ -451,48 +456,56 @@ int take_cell_err(gs_context* ctx) {
     return fail(GS_ERR_CUDA, std::string("cell-list build failed: ") + cudaGetErrorString((cudaError_t)e));
 }
 
-// The cluster-list RHS sweep of one stage (gs_verlet.cu): gather + rebuild decision, the
-// rebuild (a conditional IF node when captured into a graph, unconditional otherwise), the sweep.
+// The cluster-list RHS sweep of one stage (gs_verlet.cu).  The lists are rebuilt when the previous
+// stage's fused epilogue saw a particle move more than half the skin (captured: a conditional IF
+// node on the condition that epilogue set; host-driven: unconditionally, or decided on the host
+// with GS_B200_VERLET=3) and always at the first stage of an evolve (`force`).  Then the sweep.
 void verlet_stage(gs_context* ctx, const SysConst& sc, int force, unsigned long long ev, cudaStream_t stream) {
     const int64_t n = ctx->n;
     CellWs w = cell_ws(ctx);
     VerletWs v = verlet_ws(ctx, n, sc.cutoff);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(stream, &cs);
-    if (cs == cudaStreamCaptureStatusActive) {
+    const bool capturing = cs == cudaStreamCaptureStatusActive;
+    const bool pending = ctx->v_next_valid != 0;
+    ctx->v_next_valid = 0;
+    if (capturing && !force && pending) {
         cudaGraph_t g = nullptr;
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
-        cudaGraphConditionalHandle cond;
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = ctx->v_next_cond;
+        np.conditional.type = cudaGraphCondTypeIf;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
         bool ok = cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, &deps, &nd) == cudaSuccess &&
-                  cudaGraphConditionalHandleCreate(&cond, g, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+                  cudaGraphAddNode(&node, g, deps, nd, &np) == cudaSuccess;
+        if (ok && !ctx->cap_stream2) ok = cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) == cudaSuccess;
         if (ok) {
-            verlet_gather(w, v, ctx->S.ptr, n, force, cond, 1, stream);
-            ctx->launches++;
-            cudaGraphNodeParams np = {};
-            np.type = cudaGraphNodeTypeConditional;
-            np.conditional.handle = cond;
-            np.conditional.type = cudaGraphCondTypeIf;
-            np.conditional.size = 1;
-            cudaGraphNode_t node;
-            ok = cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, &deps, &nd) == cudaSuccess &&
-                 cudaGraphAddNode(&node, g, deps, nd, &np) == cudaSuccess;
-            if (ok && !ctx->cap_stream2) ok = cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) == cudaSuccess;
+            cudaStream_t s2 = ctx->cap_stream2;
+            ok = cudaStreamBeginCaptureToGraph(s2, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             if (ok) {
-                cudaStream_t s2 = ctx->cap_stream2;
-                ok = cudaStreamBeginCaptureToGraph(s2, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                                   cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-                if (ok) {
-                    if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, s2)) ctx->cell_err = rc;
-                    cudaGraph_t body = nullptr;
-                    ok = cudaStreamEndCapture(s2, &body) == cudaSuccess;
-                }
-                if (ok) ok = cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies) ==
-                             cudaSuccess;
+                if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, s2)) ctx->cell_err = rc;
+                cudaGraph_t body = nullptr;
+                ok = cudaStreamEndCapture(s2, &body) == cudaSuccess;
             }
+            if (ok) ok = cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies) ==
+                         cudaSuccess;
         }
         if (!ok && !ctx->cell_err) ctx->cell_err = (int)cudaErrorStreamCaptureInvalidated;
         ctx->launches += 10;  // a rebuild, when it runs (approx.)
+    } else if (!capturing && ctx->verlet_on == 3 && !force && pending) {
+        // profiling aid (GS_B200_VERLET=3): the graph's lazy rebuild decided on the host, so a
+        // per-kernel profiler sees the same kernels as a graph replay (one sync per RHS)
+        unsigned f = 0;
+        cudaMemcpyAsync(&f, v.flags + 3, sizeof(f), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        if (f) {
+            if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, stream)) ctx->cell_err = rc;
+        }
+        ctx->launches += f ? 10 : 0;
     } else {
         if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, stream)) ctx->cell_err = rc;
         ctx->launches += 10;
@@ -505,13 +518,37 @@ void verlet_stage(gs_context* ctx, const SysConst& sc, int force, unsigned long 
     ctx->pair_launches++;
 }
 
-// One RK4 stage for the session's rows (pair kernel + finish epilogue).
-void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cudaStream_t stream) {
+// The fused gather + rebuild trigger of a stage epilogue whose next stage sweeps the lists; inside a
+// capture it creates the condition handle of that stage's IF node.
+VerletFuse verlet_fuse(gs_context* ctx, const SysConst& sc, cudaStream_t stream) {
+    VerletWs v = verlet_ws(ctx, ctx->n, sc.cutoff);
+    const double thr = 0.5 * v.skin * sc.cutoff;
+    VerletFuse f{ctx->c_Ss.ptr, ctx->v_inv.ptr, ctx->v_xb.ptr, thr * thr * (1.0 - 1e-9), ctx->v_flags.ptr, {}, 0};
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, nullptr, nullptr) == cudaSuccess &&
+            cudaGraphConditionalHandleCreate(&f.cond, g, 0, cudaGraphCondAssignDefault) == cudaSuccess) {
+            f.use_cond = 1;
+        } else if (!ctx->cell_err) {
+            ctx->cell_err = (int)cudaErrorStreamCaptureInvalidated;
+        }
+        ctx->v_next_cond = f.cond;
+    }
+    ctx->v_next_valid = 1;
+    return f;
+}
+
+// One RK4 stage for the session's rows (pair kernel + finish epilogue).  `last`: no RK stage of
+// this call follows (the lists' fused gather is skipped).
+void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cudaStream_t stream, bool last = false) {
     const int64_t n = ctx->n, nrows = ctx->row1 - ctx->row0;
     const DensePlan plan = dense_plan(n, ctx->sm_count);
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)s;
     PairOut po{1, 0};
-    if (ctx->verlet_call && ctx->cell_on && ctx->row0 == 0 && nrows == n)
+    const bool lists = ctx->verlet_call && ctx->cell_on && ctx->row0 == 0 && nrows == n;
+    if (lists)
         verlet_stage(ctx, sc, step == 1 && s == 0, ev, stream);
     else
         po = pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
@@ -521,7 +558,10 @@ void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cuda
     fa.row0 = ctx->row0;
     fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr;
     fa.stage = s; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
-    launch_finish(kFinStage, sc, fa, stream);
+    if (lists && !last)
+        launch_finish_verlet(sc, fa, verlet_fuse(ctx, sc, stream), stream);
+    else
+        launch_finish(kFinStage, sc, fa, stream);
 }
 
 void graph_reset(gs_context* ctx) {
@@ -539,7 +579,7 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
             P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr),
             P(ctx->c_keys_sorted.ptr), P(ctx->c_vals.ptr), P(ctx->c_bbox.ptr), P(ctx->c_gp.ptr), P(ctx->c_tlist.ptr),
             P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes, (double)ctx->verlet_call,
-            P(ctx->v_cnt.ptr), P(ctx->v_ofs.ptr), P(ctx->v_len.ptr), P(ctx->v_list.ptr), (double)ctx->v_list.cap, P(ctx->v_xb.ptr),
+            P(ctx->v_cnt.ptr), P(ctx->v_ofs.ptr), P(ctx->v_len.ptr), P(ctx->v_inv.ptr), P(ctx->v_list.ptr), (double)ctx->v_list.cap, P(ctx->v_xb.ptr),
             P(ctx->v_flags.ptr), P(ctx->v_over.ptr), P(ctx->v_scan.ptr), ctx->verlet_skin};
 }
 
@@ -556,7 +596,7 @@ int run_evolve_graph(gs_context* ctx, const SysConst& sc, double t_final, int st
         ctx->capture_events = &ctx->graph.ev;
         GS_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
         for (int step = 1; step <= steps; ++step)
-            for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, ctx->cap_stream);
+            for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, ctx->cap_stream, step == steps && s == 3);
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
         ctx->capture_events = nullptr;
@@ -604,7 +644,7 @@ int run_evolve(gs_context* ctx, const SysConst& sc, double t_final, int steps, i
     if (capture_every > 0) f = 1;
     for (int step = 1; step <= steps; ++step) {
         NvtxScope nvtx_step("RK4 step");
-        for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, stream);
+        for (int s = 0; s < 4; ++s) stage(ctx, sc, step, s, dt, stream, step == steps && s == 3);
         if (capture_every > 0 && (step % capture_every == 0 || step == steps)) {
             if (frames)
                 GS_CUDA(cudaMemcpyAsync(frames + (size_t)f * nrows * 4, ctx->B.ptr, nrows * sizeof(double4),
@@ -761,7 +801,7 @@ int gs_create(gs_context** out, int device) {
     if (const char* g = std::getenv("GS_B200_SYM")) ctx->sym_on = std::atoi(g) != 0;
     if (const char* g = std::getenv("GS_B200_DEVLOOP")) ctx->devloop_on = std::atoi(g) != 0;
     if (const char* g = std::getenv("GS_B200_VERLET")) ctx->verlet_on = std::atoi(g);
-    if (const char* g = std::getenv("GS_B200_SKIN")) ctx->verlet_skin = std::max(0.0, std::atof(g));
+    if (const char* g = std::getenv("GS_B200_SKIN")) ctx->verlet_skin = std::atof(g);
     if (const char* g = std::getenv("GS_B200_VERLET_SLACK")) ctx->verlet_slack = std::atof(g);  // tests
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
@@ -800,7 +840,7 @@ int gs_destroy(gs_context* ctx) {
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
-    ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
+    ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_inv.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
     ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release();
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
@@ -936,8 +976,8 @@ int gs_evolve(gs_context* ctx, const gs_system_t* sys, int64_t n, double t_final
     } else {
         if ((rc = ensure_session(ctx, n, n))) return rc;
         ctx->row0 = 0; ctx->row1 = n;
-        // (verlet_on == 2: lists in host-driven evolves too, for per-kernel profiling)
-        const bool multi = capture_every == 0 && (ctx->graphs_on || ctx->verlet_on == 2);
+        // (verlet_on >= 2: lists in host-driven evolves too, for per-kernel profiling)
+        const bool multi = capture_every == 0 && (ctx->graphs_on || ctx->verlet_on >= 2);
         for (bool retry = true; retry;) {
             ctx->launches += 4;  // reset, pack, copy, unpack
             k_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
@@ -1013,7 +1053,7 @@ int match_device_loop(gs_context* ctx, const SysConst& sc, const gs_match_config
                                               ctx->B.ptr);
         k_status_reset<<<1, 1, 0, c>>>(ctx->st.ptr);
         for (int step = 1; step <= cfg->steps; ++step)
-            for (int st = 0; st < 4; ++st) stage(ctx, sc, step, st, dt, c);
+            for (int st = 0; st < 4; ++st) stage(ctx, sc, step, st, dt, c, step == cfg->steps && st == 3);
         k_residual<<<nb, 256, 0, c>>>(reinterpret_cast<const double*>(ctx->B.ptr), 4, ctx->tgt.ptr, n, ctx->ep.ptr,
                                       ctx->resid.ptr, cfg->norm, ctx->red.ptr, ctx->st.ptr);
         k_reduce_final<<<1, 512, 0, c>>>(ctx->red.ptr, nb, red_kind, ctx->scal.ptr, ctx->st.ptr);

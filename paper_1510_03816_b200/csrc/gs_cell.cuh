@@ -73,6 +73,7 @@ struct VerletWs {
     int* list;                     // cap entries
     int64_t cap;
     double2* Xb;                   // n: positions at the build, sorted order
+    int* inv;                      // n: original index -> sorted slot
     unsigned* flags;               // [0] rebuild wanted, [2] CTA counter, [3] last decision (zero-initialised)
     unsigned long long* overflow;  // entries a build needed beyond cap (0: none)
     void* scan_temp;

@@ -135,7 +135,9 @@ struct gs_context {
     int cell_on = 0;                    // path of the current call
     int cell_err = 0;                   // sticky: a cell build failed to enqueue (reported by the API call)
     // cluster Verlet lists of the cell path in multi-RHS calls (gs_verlet.cu)
-    DevBuf<int> v_list, v_len;
+    DevBuf<int> v_list, v_len, v_inv;
+    cudaGraphConditionalHandle v_next_cond{};  // IF-node condition the last fused epilogue sets
+    int v_next_valid = 0;
     DevBuf<long long> v_cnt, v_ofs;
     DevBuf<double2> v_xb;
     DevBuf<unsigned> v_flags;
@@ -146,7 +148,7 @@ struct gs_context {
     int64_t v_list_n = -1;              // n and cutoff the list buffer was sized for
     double v_list_cutoff = 0.0;
     int verlet_retries = 0;
-    double verlet_skin = 0.05;          // GS_B200_SKIN
+    double verlet_skin = -1.0;          // GS_B200_SKIN (< 0: by n, see verlet_ws)
     double verlet_slack = 0.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
     cudaStream_t cap_stream2 = nullptr; // captures the conditional rebuild bodies
     // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds

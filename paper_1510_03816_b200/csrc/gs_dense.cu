@@ -276,6 +276,11 @@ __device__ __forceinline__ double4 stage_update(const FinishArgs& a, int64_t li,
 constexpr int kFinRows = 32;
 constexpr int kFinGroups = 8;
 
+inline int finish_threads(int nchunks) {
+    const int g = nchunks < 1 ? 1 : (nchunks < kFinGroups ? nchunks : kFinGroups);
+    return g * kFinRows;
+}
+
 __device__ __forceinline__ bool finish_reduce(const FinishArgs& a, int64_t& li, double4& sum) {
     __shared__ double4 s_part[kFinGroups][kFinRows];
     const int r = threadIdx.x & (kFinRows - 1), w = threadIdx.x / kFinRows;
@@ -332,6 +337,49 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish(SysConst sc, F
     if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
 }
 
+__global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish_verlet(SysConst sc, FinishArgs a, VerletFuse f) {
+    int64_t li = 0;
+    double4 sum;
+    bool act = finish_reduce(a, li, sum);
+    act = act && !(*((volatile unsigned long long*)&a.st->first_event) < a.event);
+    bool need = false;
+    if (act) {
+        const int64_t i = a.row0 + li;
+        const double4 me = a.S[i];
+        double dqx = sum.x * sc.scale_q, dqy = sum.y * sc.scale_q;
+        if (sc.sigma2 != 0.0) {
+            dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
+            dqy = __dadd_rn(dqy, __dmul_rn(sc.sigma2, me.w));
+        }
+        const double4 nxt = stage_update(a, li, dqx, dqy, sum.z * sc.scale_p, sum.w * sc.scale_p);
+        a.S[i] = nxt;
+        if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
+        const int k = f.inv[i];
+        GS_ASSERT(k >= 0 && k < a.nrows);
+        f.Ss[k] = nxt;
+        const double2 b = f.Xb[k];
+        const double dx = nxt.x - b.x, dy = nxt.y - b.y;
+        need = fma(dx, dx, dy * dy) > f.thr2;
+    }
+    if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&f.flags[0], 1u);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&f.flags[2], 1u);
+        if (prev == gridDim.x - 1) {
+            const unsigned d = atomicExch(&f.flags[0], 0u);
+            f.flags[2] = 0u;
+            if (f.use_cond) cudaGraphSetConditional(f.cond, d);
+            f.flags[3] = d;
+        }
+    }
+}
+
+void launch_finish_verlet(const SysConst& sc, const FinishArgs& a, const VerletFuse& f, cudaStream_t stream) {
+    if (a.nrows <= 0) return;
+    const unsigned blocks = (unsigned)((a.nrows + kFinRows - 1) / kFinRows);
+    k_finish_verlet<<<blocks, finish_threads(a.nchunks), 0, stream>>>(sc, a, f);
+}
+
 // R[i] = the same fixed-order slot sum k_finish forms (multi-GPU symmetric split: the rank's
 // raw row sums before the reduce-scatter), so 1-GPU and N-GPU runs agree bitwise.
 __global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce(FinishArgs a, double4* R) {
@@ -381,11 +429,6 @@ void launch_slot_reduce_list(const double4* part, int64_t pstride, int64_t n, in
     if (n <= 0) return;
     k_slot_reduce_list<<<(unsigned)((n + kFinRows - 1) / kFinRows), kFinRows * kFinGroups, 0, stream>>>(
         part, pstride, n, rows_per_sb, nsb, slots, counts, R, sig);
-}
-
-inline int finish_threads(int nchunks) {
-    const int g = nchunks < 1 ? 1 : (nchunks < kFinGroups ? nchunks : kFinGroups);
-    return g * kFinRows;
 }
 
 void launch_slot_reduce(const double4* part, int nslots, int64_t pstride, int64_t n, double4* R, cudaStream_t stream) {

@@ -143,6 +143,20 @@ struct FinishArgs {
     unsigned long long event;
 };
 void launch_finish(int mode, const SysConst& sc, const FinishArgs& a, cudaStream_t stream);
+// Stage epilogue fused with the cluster-list gather (gs_verlet.cu, single rank, all rows): the new
+// record also goes to its sorted slot Ss[inv[i]], and the last CTA decides the rebuild trigger (a
+// particle farther than sqrt(thr2) from its position Xb at the last build): the next stage's
+// IF-node condition (use_cond) or flags[3].
+struct VerletFuse {
+    double4* Ss;
+    const int* inv;
+    const double2* Xb;
+    double thr2;
+    unsigned* flags;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+};
+void launch_finish_verlet(const SysConst& sc, const FinishArgs& a, const VerletFuse& f, cudaStream_t stream);
 // Stage epilogue of rows [row0, row0 + nrows) from the raw row sums of all `world` ranks
 // (Rp[w], full length, summed in rank order), storing each new stage record into Sp[w] of
 // every rank (peer memory).

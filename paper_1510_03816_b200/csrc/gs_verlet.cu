@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__
                                                       const int* __restrict__ start, const GridParams* __restrict__ gp,
                                                       int64_t n, int64_t ncl, int pad, const long long* __restrict__ ofs,
                                                       int* len, int* list, int64_t cap, double2* Xb,
+                                                      const unsigned* __restrict__ perm, int* inv,
                                                       unsigned long long* overflow) {
     const int sub = threadIdx.x & 31;
     const int64_t c = (int64_t)blockIdx.x * (kVBB / kTplB) + threadIdx.x / kTplB;
@@ -355,7 +356,11 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__
     load_members(Ss, Sf, n, c, cm);
 #pragma unroll
     for (int m = 0; m < kVM; ++m)
-        if (sub == m && m < cm.nm) Xb[c * kVM + m] = make_double2(cm.mx[m], cm.my[m]);
+        if (sub == m && m < cm.nm) {
+            const int64_t k = c * kVM + m;
+            Xb[k] = make_double2(cm.mx[m], cm.my[m]);
+            inv[perm[k]] = (int)k;  // original index -> sorted slot (the fused stage epilogue's gather)
+        }
     const int64_t obase = ofs[c];
     const bool ok = ofs[ncl] <= cap;  // the list buffer holds the whole build
     if (!ok) {  // no list: the sweep reads nothing (the call is redone with a larger buffer)
@@ -419,14 +424,16 @@ __global__ void __launch_bounds__(256) k_verlet_gather(const double4* __restrict
             const unsigned f = force ? 1u : atomicExch(&flags[0], 0u);
             flags[0] = 0u;
             flags[2] = 0u;
-            flags[1] += f;  // builds so far (diagnostics)
             if (use_cond) cudaGraphSetConditional(cond, f);
             flags[3] = f;
         }
     }
 }
 
-__global__ void k_verlet_sentinel(double4* Ss, int64_t n) { Ss[n] = far_record(0); }
+__global__ void k_verlet_sentinel(double4* Ss, int64_t n, unsigned* flags) {
+    Ss[n] = far_record(0);
+    flags[1] += 1u;  // builds so far (diagnostics)
+}
 
 }  // namespace
 
@@ -435,15 +442,12 @@ int verlet_tpl(int64_t n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ncl = (n + kVM - 1) / kVM;
-    static const int depth = [] {
-        const char* e = std::getenv("GS_B200_VERLET_DEPTH");
-        return e ? std::max(1, std::atoi(e)) : GS_VERLET_DEPTH;
-    }();
-    static const int tpl_min = [] {
-        const char* e = std::getenv("GS_B200_VERLET_TPL");  // A/B: minimum lanes per cluster
-        const int v = e ? std::atoi(e) : 4;
-        return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 4;
-    }();
+    // A/B knobs (read per call): lanes grow until clusters * lanes >= SMs * depth; minimum lanes
+    const char* ed = std::getenv("GS_B200_VERLET_DEPTH");
+    const int depth = ed ? std::max(1, std::atoi(ed)) : GS_VERLET_DEPTH;
+    const char* et = std::getenv("GS_B200_VERLET_TPL");
+    const int tv = et ? std::atoi(et) : 4;
+    const int tpl_min = (tv == 1 || tv == 2 || tv == 4 || tv == 8 || tv == 16) ? tv : 4;
     int tpl = tpl_min;
     while (tpl < 16 && ncl * tpl < (int64_t)sms * depth) tpl *= 2;
     return tpl;
@@ -461,7 +465,7 @@ int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n
     const double rl = cutoff * (1.0 + v.skin);
     int rc = cell_build(w, S, n, rl, stream);
     if (rc) return rc;
-    k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, n);
+    k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, n, v.flags);
     const int64_t ncl = verlet_clusters(n);
     const int pad = 2 * v.tpl;
     k_verlet_caps<<<(unsigned)((ncl + 255) / 256), 256, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.cnt);
@@ -470,7 +474,7 @@ int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n
     if (e != cudaSuccess) return (int)e;
     const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
     k_verlet_fill<<<blocks, kVBB, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.ofs, v.len, v.list, v.cap,
-                                               v.Xb, v.overflow);
+                                               v.Xb, w.perm, v.inv, v.overflow);
     return (int)cudaGetLastError();
 }
 
