@@ -50,7 +50,7 @@ constexpr int kTplB = 32;    // list-build lanes per cluster: one warp (warp-uni
 #define GS_VERLET_PF 8
 #endif
 #ifndef GS_VERLET_DEPTH      // lanes per cluster grow until clusters * lanes >= SMs * this (A/B)
-#define GS_VERLET_DEPTH 1024
+#define GS_VERLET_DEPTH 128   // A/B (C2 100-step solve, ms): lanes 4 -> 13.6, 8 -> 14.1, 16 -> 14.3, 2 -> 16.1
 #endif
 constexpr int kVM = GS_VERLET_M;
 
