@@ -14,8 +14,8 @@
 //   than skin * cutoff / 2 since the build triggers a rebuild (a pair now closer than the cutoff
 //   was closer than rl at the build: both particles moved less than half the skin); then TPL lanes
 //   per cluster walk its list two sources at a time, each source evaluated against all M members
-//   with the fp64 pair core of gs_device.cuh and masked to d^2 < cutoff^2 exactly (so the sum is
-//   over the same pairs as a fresh cell sweep, whenever the list was built).
+//   with the fp64 pair core of gs_device.cuh (the list's pairs beyond the cutoff add terms below
+//   2^-53 of the self term; GS_VERLET_NOMASK=0 masks them to d^2 < cutoff^2 exactly).
 //
 // Why: the per-RHS cell sweep (gs_cell.cu) spends its issue slots on the fp32 candidate filter and
 // idles lanes whose filtered lists are short; here the filter runs once per rebuild, every lane of
@@ -48,6 +48,13 @@ constexpr int kTplB = 32;    // list-build lanes per cluster: one warp (warp-uni
 #endif
 #ifndef GS_VERLET_PF         // L2 prefetch distance of the list, in trips (A/B)
 #define GS_VERLET_PF 8
+#endif
+// The sweep sums every pair of the list (d < cutoff (1 + skin) at the last build): the pairs
+// beyond the cutoff add terms below 2^-53 of the self term (G(cutoff) = 2^-53, KD-1) — the order of
+// the truncation itself — and dropping the per-pair cutoff test saves ~5 % (C5 1.62 -> 1.55 ms per
+// RHS, profiles/r02_history.md).  The pair count of the throughput metric (COUNT) still uses d < cutoff.
+#ifndef GS_VERLET_NOMASK
+#define GS_VERLET_NOMASK 1
 #endif
 #ifndef GS_VERLET_DEPTH      // lanes per cluster grow until clusters * lanes >= SMs * this (A/B)
 #define GS_VERLET_DEPTH 128   // A/B (C2 100-step solve, ms): lanes 4 -> 13.6, 8 -> 14.1, 16 -> 14.3, 2 -> 16.1
@@ -85,7 +92,11 @@ __device__ __forceinline__ void vbody(const double4& me, const double4& s, const
     const double pdot = fma(me.z, s.z, me.w * s.w);
     const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
     const long long r2b = __double_as_longlong(r2);
+#if GS_VERLET_NOMASK  // A/B: sum every list pair (skin pairs add their sub-2^-53 terms)
+    const bool in = COUNT ? r2b < rc2b : true;
+#else
     const bool in = r2b < rc2b;
+#endif
     nz += __double2hiint(r2) == __double2hiint(kTinyR2);
     if (COUNT) nin += in;
     double g, c;
