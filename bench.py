@@ -347,6 +347,10 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for k in range(a.steps):
+            # ~1 ms device sleep ahead of the flush: the host enqueues the whole step (clones,
+            # graph launch) while the GPU still sleeps, so the events time the GPU work only,
+            # not the host's submission latency (the solve syncs at its end to read the status)
+            torch.cuda._sleep(2_000_000)
             flush.zero_()  # outside the events
             starts[k].record()
             solve()

@@ -96,19 +96,49 @@ __device__ __forceinline__ double rsqrt_refined(double x) {
 // where the low word would wrap) without an extra FP64 instruction.
 constexpr double kRoundMagicK = 6755399441055744.0 + 1073741824.0;
 constexpr int kMagicHi = 0x43380000;
+// The integer side is written for the fewest instructions: `tb` is the
+// 32-bit shared-memory byte address of this lane's table copy (lane_table_addr), so a lookup is
+// one AND + one shift-add; the range test is two compares on the words of s; the exponent goes
+// into the table value's high word as ((lo(s) >> 6) << 20) (lo(s) = k + 2^30 and 2^30 / 64 << 20
+// vanishes mod 2^32).  (Zeroing only the high word on the out-of-range side was tried: for the
+// far padding records u = y - kd is huge and the polynomial overflows to inf, inf * 0 = NaN.)
+constexpr unsigned kLoMin = (1u << 30) + (unsigned)kKMin;  // lo(s) >= kLoMin <=> k >= kKMin
+__device__ __forceinline__ double exp2_tbl_fast(double y, unsigned tb) {
+    const double s = y + gs_cb[kCbMagicK];
+    const double kd = s - gs_cb[kCbMagicK];
+    const double u = y - kd;
+    const unsigned lo = (unsigned)__double2loint(s), hi = (unsigned)__double2hiint(s);
+    // the integer side in PTX, so that ptxas keeps the two-instruction forms: table address
+    // (and + mad), exponent ((lo >> 6) << 20 added to the table value's high word: shr + mad),
+    // range test (two chained compares: one predicate)
+    unsigned addr, sh;
+    asm("{\n\t.reg .b32 x;\n\tand.b32 x, %1, 63;\n\tmad.lo.u32 %0, x, 128, %2;\n\t}" : "=r"(addr) : "r"(lo), "r"(tb));
+    asm("shr.u32 %0, %1, 6;" : "=r"(sh) : "r"(lo));
+    double t;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(t) : "r"(addr));
+    unsigned th;
+    asm("mad.lo.u32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(sh), "r"((unsigned)__double2hiint(t)));
+    const double e1 = u * fma(fma(fma(fma(gs_cb[kCbC5], u, gs_cb[kCbC4]), u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u,
+                              gs_cb[kCbC1]);
+    const double tn = __hiloint2double((int)th, __double2loint(t));
+    const double g = fma(tn, e1, tn);
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %1, %2;\n\tsetp.eq.and.u32 p, %3, %4, p;\n\t"
+        "selp.f64 %0, %5, 0d0000000000000000, p;\n\t}"
+        : "=d"(r) : "r"(lo), "n"(kLoMin), "r"(hi), "n"(kMagicHi), "d"(g));
+    return r;
+}
+static_assert(kTblRep * 8 == 128, "lane copies interleave in 128-byte rows (exp2_tbl_fast)");
+
+// The table exp every kernel calls: `tbl` is the lane's copy in shared memory (lane_table); its
+// 32-bit shared address is loop-invariant and hoisted out of the hot loops.
 __device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ tbl) {
-    double s = y + gs_cb[kCbMagicK];
-    double kd = s - gs_cb[kCbMagicK];
-    double u = y - kd;
-    const int k = __double2loint(s) - (1 << 30);
-    const bool ok = ((__double2hiint(s) ^ kMagicHi) | ((k - kKMin) >> 31)) == 0;  // one predicate
-    double t = tbl[(k & (kTbl - 1)) * kTblRep];
-    int n = k >> kTblBits;
-    double tn = __hiloint2double(__double2hiint(t) + (n << 20), __double2loint(t));
-    double e1 = u * fma(fma(fma(fma(gs_cb[kCbC5], u, gs_cb[kCbC4]), u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u,
-                        gs_cb[kCbC1]);
-    double g = fma(tn, e1, tn);
-    return ok ? g : 0.0;
+    return exp2_tbl_fast(y, (unsigned)__cvta_generic_to_shared(tbl));
+}
+
+// 32-bit shared address of this lane's table copy (exp2_tbl_fast).
+__device__ __forceinline__ unsigned lane_table_addr(const double* s_tbl) {
+    return (unsigned)__cvta_generic_to_shared(s_tbl + (threadIdx.x & (kTblRep - 1)));
 }
 
 // This thread's copy of the replicated table in shared memory.
@@ -137,6 +167,25 @@ __device__ __forceinline__ void pair_core(double dx, double dy, double pdot, con
         c = (pdot * g) * rs;
     } else {
         g = exp2_tbl(r2 * k1, tbl);
+        c = pdot * g;
+    }
+}
+
+// pair_core for the symmetric kernel's off-diagonal tiles (no self pairs there): instead of a
+// d == 0 flag per pair it hands back the high word of d^2 (the caller keeps the minimum, one
+// integer op per pair); a minimum <= hi(1e-200) means a pair with d^2 within 2^-20 of the offset
+// (d < ~1e-103, in practice d == 0) and triggers the exact re-scan.
+template <int FAM>
+__device__ __forceinline__ void pair_core_hi(double dx, double dy, double pdot, unsigned tb, double k1, double& g,
+                                             double& c, int& r2hi) {
+    const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
+    r2hi = __double2hiint(r2);
+    if (FAM == kFamConical) {
+        const double rs = rsqrt_refined(r2);
+        g = exp2_tbl_fast((r2 * rs) * k1, tb);
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl_fast(r2 * k1, tb);
         c = pdot * g;
     }
 }

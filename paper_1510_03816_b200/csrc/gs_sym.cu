@@ -71,14 +71,25 @@ __device__ __forceinline__ void one_sided(const double4& me, const double4& s, c
     nz += z;
 }
 
+#ifndef GS_SYM_ZMIN      // coincidence detection by the minimum high word of d^2 (1 op per pair, A/B)
+#define GS_SYM_ZMIN 1
+#endif
+
 template <int FAM>
-__device__ __forceinline__ void two_sided(const double4& me, const double4& s, const double* tbl, double k1, Acc& a,
-                                          Acc& j, int& nz) {
+__device__ __forceinline__ void two_sided(const double4& me, const double4& s, const double* tbl, unsigned tb,
+                                          double k1, Acc& a, Acc& j, int& nz) {
     const double dx = me.x - s.x, dy = me.y - s.y;
     const double pdot = fma(me.z, s.z, me.w * s.w);
     double g, c;
+#if GS_SYM_ZMIN
+    int h;
+    pair_core_hi<FAM>(dx, dy, pdot, tb, k1, g, c, h);
+    nz = min(nz, h);  // nz: the minimum high word of d^2 (see pair_core_hi)
+#else
     int z;
     pair_core<FAM>(dx, dy, pdot, tbl, k1, g, c, z);
+    nz += z;
+#endif
     a.qx = fma(g, s.z, a.qx);
     a.qy = fma(g, s.w, a.qy);
     a.px = fma(c, dx, a.px);
@@ -87,7 +98,6 @@ __device__ __forceinline__ void two_sided(const double4& me, const double4& s, c
     j.qy = fma(g, me.w, j.qy);
     j.px = fma(-c, dx, j.px);
     j.py = fma(-c, dy, j.py);
-    nz += z;
 }
 
 __device__ __forceinline__ void add_to(double4* dst, const Acc& a) {
@@ -115,6 +125,7 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
     block_wait(wait);  // multi-GPU peer exchange: every rank's records of the previous stage are in S
     for (int t = threadIdx.x; t < kTblWords; t += kST) s_tbl[t] = tbl_g[t];
     const double* tbl = lane_table(s_tbl);
+    const unsigned tb = lane_table_addr(s_tbl);
 
     // CTA -> superblock pair (SI, SJ), SI <= SJ, row-major over the upper triangle
     const long long t = cta0 + blockIdx.x;
@@ -162,6 +173,9 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                 if (nz1 > 1 && i1 < n) record_coincident(S, n, i1, me1, J * kDB, J * kDB + kDB, st, event);
                 continue;
             }
+#if GS_SYM_ZMIN
+            nz0 = nz1 = 0x7fffffff;
+#endif
             double4* jacc = s_acc + jb * kDB;
             for (int ph = 0; ph < 4; ++ph) {
                 const int b = (2 * w + ph) & 3;
@@ -175,10 +189,10 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                 for (int step = 0; step < 32; step += 2) {
                     const double4 sa = rot[step];
                     const double4 sb = rot[step + 1];
-                    two_sided<FAM>(me0, sa, tbl, k1, a0, j, nz0);
-                    two_sided<FAM>(me1, sa, tbl, k1, a1, j, nz1);
-                    two_sided<FAM>(me0, sb, tbl, k1, a0, jb2, nz0);
-                    two_sided<FAM>(me1, sb, tbl, k1, a1, jb2, nz1);
+                    two_sided<FAM>(me0, sa, tbl, tb, k1, a0, j, nz0);
+                    two_sided<FAM>(me1, sa, tbl, tb, k1, a1, j, nz1);
+                    two_sided<FAM>(me0, sb, tbl, tb, k1, a0, jb2, nz0);
+                    two_sided<FAM>(me1, sb, tbl, tb, k1, a1, jb2, nz1);
                     const int src = (lane + 2) & 31;
                     j.qx = __shfl_sync(kFull, j.qx, src);
                     j.qy = __shfl_sync(kFull, j.qy, src);
@@ -200,8 +214,8 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
 #pragma unroll 4
                 for (int step = 0; step < 32; ++step) {
                     const double4 s = rot[step];
-                    two_sided<FAM>(me0, s, tbl, k1, a0, j, nz0);
-                    two_sided<FAM>(me1, s, tbl, k1, a1, j, nz1);
+                    two_sided<FAM>(me0, s, tbl, tb, k1, a0, j, nz0);
+                    two_sided<FAM>(me1, s, tbl, tb, k1, a1, j, nz1);
                     const int src = (lane + 1) & 31;
                     j.qx = __shfl_sync(kFull, j.qx, src);
                     j.qy = __shfl_sync(kFull, j.qy, src);
@@ -212,6 +226,11 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                 add_to(&jacc[b * 32 + lane], j);
                 __syncthreads();
             }
+#if GS_SYM_ZMIN
+            constexpr int kTinyHi = 0x16687e92;  // high word of kTinyR2 = 1e-200
+            nz0 = nz0 <= kTinyHi;
+            nz1 = nz1 <= kTinyHi;
+#endif
             if (nz0 > 0 && i0 < n) record_coincident(S, n, i0, me0, J * kDB, J * kDB + kDB, st, event);  // rare
             if (nz1 > 0 && i1 < n) record_coincident(S, n, i1, me1, J * kDB, J * kDB + kDB, st, event);
         }

@@ -65,29 +65,28 @@ struct Acc {
     double qx, qy, px, py;
 };
 
-// exp2_tbl with an extra acceptance predicate (the cutoff mask): G = 0 outside.
-__device__ __forceinline__ double exp2_tbl_in(double y, const double* __restrict__ tbl, bool in) {
-    double s = y + gs_cb[kCbMagicK];
-    double kd = s - gs_cb[kCbMagicK];
-    double u = y - kd;
-    const int k = __double2loint(s) - (1 << 30);
-    const bool ok = ((__double2hiint(s) ^ kMagicHi) | ((k - kKMin) >> 31)) == 0;
-    double t = tbl[(k & (kTbl - 1)) * kTblRep];
-    int nn = k >> kTblBits;
-    double tn = __hiloint2double(__double2hiint(t) + (nn << 20), __double2loint(t));
-    double e1 = u * fma(fma(fma(fma(gs_cb[kCbC5], u, gs_cb[kCbC4]), u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u,
-                        gs_cb[kCbC1]);
-    double g = fma(tn, e1, tn);
-    return (ok && in) ? g : 0.0;
+// exp2_tbl with an extra acceptance predicate (the cutoff mask, GS_VERLET_NOMASK=0): G = 0 outside.
+__device__ __forceinline__ double exp2_tbl_in(double y, unsigned tb, bool in) {
+    const double g = exp2_tbl_fast(y, tb);
+    return in ? g : 0.0;
 }
 
 // One ordered pair (target me <- source s), masked to d^2 < cutoff^2 (rc2b = bits of cutoff^2:
 // non-negative doubles order like their bit patterns, so the test is one 64-bit integer compare).
 // nz counts pairs whose d^2 has the high word of the 1e-200 offset (d == 0: the self pair and any
 // coincident particle; a superset, the rare re-scan decides exactly).
+template <int FAM>
+__device__ __forceinline__ double vexp(double y, unsigned tb, bool in) {
+#if GS_VERLET_NOMASK
+    return exp2_tbl_fast(y, tb);  // `in` only counts pairs here
+#else
+    return exp2_tbl_in(y, tb, in);
+#endif
+}
+
 template <int FAM, bool COUNT>
-__device__ __forceinline__ void vbody(const double4& me, const double4& s, const double* __restrict__ tbl, double k1,
-                                      long long rc2b, Acc& a, int& nz, int& nin) {
+__device__ __forceinline__ void vbody(const double4& me, const double4& s, const double* __restrict__ tbl, unsigned tb,
+                                      double k1, long long rc2b, Acc& a, int& nz, int& nin) {
     const double dx = me.x - s.x, dy = me.y - s.y;
     const double pdot = fma(me.z, s.z, me.w * s.w);
     const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
@@ -102,10 +101,10 @@ __device__ __forceinline__ void vbody(const double4& me, const double4& s, const
     double g, c;
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
-        g = exp2_tbl_in((r2 * rs) * k1, tbl, in);
+        g = vexp<FAM>((r2 * rs) * k1, tb, in);
         c = (pdot * g) * rs;
     } else {
-        g = exp2_tbl_in(r2 * k1, tbl, in);
+        g = vexp<FAM>(r2 * k1, tb, in);
         c = pdot * g;
     }
     a.qx = fma(g, s.z, a.qx);
@@ -128,6 +127,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     if (threadIdx.x == 0) s_acc_count = 0;
     __syncthreads();
     const double* tbl = lane_table(s_tbl);
+    const unsigned tb = lane_table_addr(s_tbl);
 
     const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
     const int64_t c = cl0 + (int64_t)blockIdx.x * (kVB / TPL) + threadIdx.x / TPL;
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         jc = ldl(e + 3 * step);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            vbody<FAM, COUNT>(me[m], a0, tbl, k1, rc2b, a[m], nz[m], nin);
-            vbody<FAM, COUNT>(me[m], a1, tbl, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], a0, tbl, tb, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], a1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
         }
         e += step;
         if (e >= end) break;
@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         jc = ldl(e + 3 * step);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            vbody<FAM, COUNT>(me[m], b0, tbl, k1, rc2b, a[m], nz[m], nin);
-            vbody<FAM, COUNT>(me[m], b1, tbl, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], b0, tbl, tb, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], b1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
         }
         e += step;
         if (e >= end) break;
@@ -186,8 +186,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         jc = ldl(e + 3 * step);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            vbody<FAM, COUNT>(me[m], c0, tbl, k1, rc2b, a[m], nz[m], nin);
-            vbody<FAM, COUNT>(me[m], c1, tbl, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], c0, tbl, tb, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], c1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
         }
         e += step;
     }

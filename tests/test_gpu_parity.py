@@ -211,6 +211,31 @@ def test_errors_on_the_general_path(cuda):
         gs.evolve(gs.SystemSpec(), gs.ParticleState(q, p), gs.EvolveConfig(steps=4))
 
 
+def test_errors_on_the_symmetric_path(cuda):
+    """Coincidence detection of the symmetric dense kernel (N >= 3072): off-diagonal tiles flag a
+    pair by the minimum high word of d^2, diagonal tiles by count; the row-major-first pair wins
+    and an inert coincident pair (p_i . p_j == 0) is tolerated (particles.py:92-98)."""
+    import paper_1510_03816_b200 as gs
+
+    rng = np.random.default_rng(6)
+    n = 8192
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=0.05))
+    for (a, b) in ((17, 6000), (200, 230), (5000, 8191)):  # other block / same block / last row
+        q = rng.uniform(0, 1, (n, 2))
+        p = rng.normal(0, 0.1, (n, 2))
+        q[b] = q[a]
+        with pytest.raises(gs.DegenerateConfigurationError, match=f"particles {a} and {b} coincide"):
+            gs.rhs(spec, gs.ParticleState(q, p))
+        p[b] = 0.0
+        dq, dp = gs.rhs(spec, gs.ParticleState(q, p))
+        assert np.isfinite(dq).all() and np.isfinite(dp).all()
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 0.1, (n, 2))
+    q[7000], q[4000], q[100] = q[3000], q[50], q[50]  # the row-major-first pair is (50, 100)
+    with pytest.raises(gs.DegenerateConfigurationError, match="particles 50 and 100 coincide"):
+        gs.rhs(spec, gs.ParticleState(q, p))
+
+
 def test_zero_momentum_is_a_fixed_point_bitwise(cuda):
     import paper_1510_03816_b200 as gs
 
