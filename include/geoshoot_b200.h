@@ -294,6 +294,52 @@ int gs_profile_read(gs_context* ctx, double* pair_ms, int64_t* pair_launches, in
  * build.  Synchronises. */
 int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stream);
 
+/* ---- slab decomposition of the cell path across ranks (multi-GPU) -----------
+ * Replaces "every rank all-gathers all N stage records and rebuilds the whole grid" for the
+ * compactly supported kernel (particles.py:109-117 truncated at the support radius, KD-1): each
+ * rank owns the particles of a contiguous band of cell rows of the global grid (balanced by an
+ * all-reduced row histogram) and holds `sub` halo rows on each side, all in global sorted order.
+ * The host driver (paper_1510_03816_b200/slab.py) issues the collectives; per list build:
+ *   gs_slab_bbox   : (min x, min y, -max x, -max y) of the own particles into b4 (device, 4
+ *                    doubles) -> elementwise MIN all-reduce over the ranks
+ *   gs_slab_grid   : the one-rank build's grid for list radius cutoff (1 + skin) from the reduced
+ *                    b4 (the same on every rank); synchronises
+ *   gs_slab_rows   : own particles per cell row into hist (device, ny int64) -> SUM all-reduce
+ *   gs_slab_pack   : every own particle (S, RK4 base B and accumulator A, global index: 13
+ *                    doubles) into send (device, n_own x 13) grouped by the owner of its row
+ *                    (owner: device, ny int32); counts[world] (host); synchronises
+ *                    -> all-to-all -> gs_slab_unpack (the rank's new own particles)
+ *   gs_slab_layout : own particles sorted by (cell, global index) into local positions
+ *                    [own_begin, own_begin + n_own) of the n_loc local records (rows
+ *                    [y_loc0, y_loc1) = own rows [y_own0, y_own1) + halo rows)
+ *                    -> the halo slices of S and of the global indices (gs_slab_views) are
+ *                    copied in from the neighbours' own blocks
+ *   gs_slab_lists  : cell starts, own clusters (pairs restarting at every cell row) and their
+ *                    lists over the local particles; synchronises
+ * per RK4 stage: gs_slab_stage (sweep + epilogue of the own rows, rebuild flag = some own
+ * particle moved more than skin * cutoff / 2 since the build, *flag of gs_slab_views) -> the
+ * halo slices of S -> MAX all-reduce of the flags: rebuild before the next stage.
+ * Rows are bitwise independent of the number of ranks.  gs_slab_begin sets the own particles
+ * (q, p: device (n_own, 2); gidx: device int32 global indices) and resets the status;
+ * gs_slab_status decodes it with global indices (synchronises). */
+typedef struct gs_slab_grid {
+    double x0, y0, h;          /* grid origin and cell edge (= cutoff (1 + skin) / sub) */
+    int32_t nx, ny, sub, hashed;
+} gs_slab_grid_t;
+int gs_slab_begin(gs_context* ctx, const gs_system_t* sys, int64_t n_glob, int64_t n_own, const double* q,
+                  const double* p, const int32_t* gidx, void* stream);
+int gs_slab_bbox(gs_context* ctx, double* b4, void* stream);
+int gs_slab_grid(gs_context* ctx, const double* b4, gs_slab_grid_t* grid, void* stream);
+int gs_slab_rows(gs_context* ctx, int64_t* hist, void* stream);
+int gs_slab_pack(gs_context* ctx, const int32_t* owner, int32_t world, double* send, int64_t* counts, void* stream);
+int gs_slab_unpack(gs_context* ctx, int64_t n_own, const double* recv, void* stream);
+int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_loc0, int32_t y_loc1, int64_t own_begin,
+                   int64_t n_loc, void* stream);
+int gs_slab_views(gs_context* ctx, double** S, int32_t** gidx, int32_t** flag);
+int gs_slab_lists(gs_context* ctx, void* stream);
+int gs_slab_stage(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt, void* stream);
+int gs_slab_status(gs_context* ctx, gs_status_t* status, void* stream);
+
 /* micro-benchmark used by bench.py for the FP64 roofline denominator: `iters` dependent
  * DFMA chains per thread on a full grid; returns the device time in *ms (host). */
 int gs_fp64_peak_probe(gs_context* ctx, int32_t iters, double* ms, double* flops, void* stream);

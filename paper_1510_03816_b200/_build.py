@@ -19,7 +19,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libgs_b200.so")
-SOURCES = ["gs_dense.cu", "gs_sym.cu", "gs_small.cu", "gs_cell.cu", "gs_verlet.cu", "gs_api.cu", "gs_batch.cu", "gs_p2p.cu"]
+SOURCES = ["gs_dense.cu", "gs_sym.cu", "gs_small.cu", "gs_cell.cu", "gs_verlet.cu", "gs_api.cu", "gs_batch.cu", "gs_p2p.cu", "gs_slab.cu"]
 HEADERS = ["gs_device.cuh", "gs_kernels.cuh", "gs_cell.cuh", "gs_context.cuh",
            os.path.join("..", "..", "include", "geoshoot_b200.h")]
 

@@ -36,7 +36,8 @@ EXPORTS = (
     "gs_profile_read", "gs_stage_path", "gs_sym_parts", "gs_stage_pairs_sym", "gs_stage_finish", "gs_gram",
     "gs_match_batch", "gs_evolve_batch", "gs_velocity_field", "gs_p2p_local", "gs_p2p_export", "gs_p2p_import",
     "gs_p2p_set_peers", "gs_p2p_pairs", "gs_p2p_finish", "gs_p2p_sync", "gs_p2p_timeouts", "gs_p2p_close",
-    "gs_cell_stats", "gs_gram_cg",
+    "gs_cell_stats", "gs_gram_cg", "gs_slab_begin", "gs_slab_bbox", "gs_slab_grid", "gs_slab_rows", "gs_slab_pack",
+    "gs_slab_unpack", "gs_slab_layout", "gs_slab_views", "gs_slab_lists", "gs_slab_stage", "gs_slab_status",
 )
 
 
@@ -59,6 +60,11 @@ class System(ctypes.Structure):
 class Status(ctypes.Structure):
     _fields_ = [("code", ctypes.c_int32), ("step", ctypes.c_int32), ("i", ctypes.c_int64), ("j", ctypes.c_int64),
                 ("iteration", ctypes.c_int32), ("event", ctypes.c_int32)]
+
+
+class SlabGrid(ctypes.Structure):
+    _fields_ = [("x0", ctypes.c_double), ("y0", ctypes.c_double), ("h", ctypes.c_double), ("nx", ctypes.c_int32),
+                ("ny", ctypes.c_int32), ("sub", ctypes.c_int32), ("hashed", ctypes.c_int32)]
 
 
 class MatchConfig(ctypes.Structure):
@@ -141,6 +147,18 @@ def load(path: str = LIB_PATH):
             "gs_cell_stats": ([_vp, P(_i64), P(_i64), _vp], ctypes.c_int),
             "gs_gram_cg": ([_vp, P(System), _i64, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
                             P(ctypes.c_int32), P(ctypes.c_double), P(ctypes.c_double), _vp], ctypes.c_int),
+            "gs_slab_begin": ([_vp, P(System), _i64, _i64, _dp, _dp, _dp, _vp], ctypes.c_int),
+            "gs_slab_bbox": ([_vp, _dp, _vp], ctypes.c_int),
+            "gs_slab_grid": ([_vp, _dp, P(SlabGrid), _vp], ctypes.c_int),
+            "gs_slab_rows": ([_vp, _dp, _vp], ctypes.c_int),
+            "gs_slab_pack": ([_vp, _dp, ctypes.c_int32, _dp, P(_i64), _vp], ctypes.c_int),
+            "gs_slab_unpack": ([_vp, _i64, _dp, _vp], ctypes.c_int),
+            "gs_slab_layout": ([_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i64, _i64, _vp],
+                               ctypes.c_int),
+            "gs_slab_views": ([_vp, P(_vp), P(_vp), P(_vp)], ctypes.c_int),
+            "gs_slab_lists": ([_vp, _vp], ctypes.c_int),
+            "gs_slab_stage": ([_vp, P(System), ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _vp], ctypes.c_int),
+            "gs_slab_status": ([_vp, P(Status), _vp], ctypes.c_int),
             "gs_profile_read": ([_vp, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64),
                                  ctypes.c_int32], ctypes.c_int),
         }

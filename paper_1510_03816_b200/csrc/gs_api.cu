@@ -848,6 +848,15 @@ int gs_destroy(gs_context* ctx) {
     ctx->p2p.R.release(); ctx->p2p.flags.release(); ctx->p2p.done.release(); ctx->p2p.Rp.release(); ctx->p2p.Sp.release(); ctx->p2p.Fp.release();
     ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release(); ctx->sym_slots.release();
     ctx->sym_counts.release();
+    {
+        auto& L = ctx->slab;
+        L.S.release(); L.gidx.release(); L.B.release(); L.A.release(); L.part.release(); L.Xb.release();
+        L.Su.release(); L.Bu.release(); L.Au.release(); L.gu.release(); L.skey.release(); L.skey2.release();
+        L.sval.release(); L.sval2.release(); L.cub.release(); L.keys.release(); L.start.release();
+        L.cfirst.release(); L.head.release(); L.len.release(); L.list.release(); L.Sf.release(); L.gp.release();
+        L.cnt.release(); L.ofs.release(); L.red.release(); L.b4.release(); L.dest.release(); L.dcount.release();
+        L.flags.release(); L.over.release();
+    }
     delete ctx;
     return GS_OK;
 }

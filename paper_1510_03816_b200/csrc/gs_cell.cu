@@ -84,32 +84,11 @@ __global__ void k_bbox_partial(const double4* __restrict__ S, int64_t n, double*
     if (threadIdx.x < 4) red[4 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
 }
 
-__global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, int sub_max,
-                              GridParams* gp) {
-    __shared__ double s[4][kBB];
-    __shared__ int s_bad;
-    if (threadIdx.x == 0) s_bad = 0;
-    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
-    bool badl = false;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        badl |= red[4 * b] != red[4 * b];
-        mnx = fmin(mnx, red[4 * b]); mny = fmin(mny, red[4 * b + 1]);
-        mxx = fmax(mxx, red[4 * b + 2]); mxy = fmax(mxy, red[4 * b + 3]);
-    }
-    s[0][threadIdx.x] = mnx; s[1][threadIdx.x] = mny; s[2][threadIdx.x] = mxx; s[3][threadIdx.x] = mxy;
-    __syncthreads();
-    if (badl) s_bad = 1;
-    for (int w = blockDim.x / 2; w; w >>= 1) {
-        if (threadIdx.x < w) {
-            const int o = threadIdx.x + w;
-            s[0][threadIdx.x] = fmin(s[0][threadIdx.x], s[0][o]); s[1][threadIdx.x] = fmin(s[1][threadIdx.x], s[1][o]);
-            s[2][threadIdx.x] = fmax(s[2][threadIdx.x], s[2][o]); s[3][threadIdx.x] = fmax(s[3][threadIdx.x], s[3][o]);
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x != 0) return;
-    const bool bad = s_bad != 0;
-    mnx = s[0][0]; mny = s[1][0]; mxx = s[2][0]; mxy = s[3][0];
+// Grid of the bounding box [mnx, mxx] x [mny, mxy] (bad: a non-finite position was seen).  One
+// function for the whole-cloud build and the slab build (gs_slab.cu), so that every rank of a
+// slab decomposition derives bitwise the grid of the one-GPU build from the all-reduced box.
+__device__ GridParams grid_params_of(double mnx, double mny, double mxx, double mxy, bool bad, double cutoff,
+                                     int64_t cap, int sub_max) {
     GridParams g;
     // fp32 filter radius: positions are stored as float(x - x0); each carries an error of at
     // most 2^-24 * extent, so a pair's distance in fp32 is off by <= 4 * 2^-24 * extent.
@@ -144,7 +123,36 @@ __global__ void k_grid_params(const double* __restrict__ red, int nb, double cut
             g.nx = 0; g.ny = 0; g.ncells = (int)cap; g.hashed = 1;
         }
     }
-    *gp = g;
+    g.ylo = 0;
+    g.yhi = g.ny;
+    return g;
+}
+
+__global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, int sub_max,
+                              GridParams* gp) {
+    __shared__ double s[4][kBB];
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    bool badl = false;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        badl |= red[4 * b] != red[4 * b];
+        mnx = fmin(mnx, red[4 * b]); mny = fmin(mny, red[4 * b + 1]);
+        mxx = fmax(mxx, red[4 * b + 2]); mxy = fmax(mxy, red[4 * b + 3]);
+    }
+    s[0][threadIdx.x] = mnx; s[1][threadIdx.x] = mny; s[2][threadIdx.x] = mxx; s[3][threadIdx.x] = mxy;
+    __syncthreads();
+    if (badl) s_bad = 1;
+    for (int w = blockDim.x / 2; w; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            s[0][threadIdx.x] = fmin(s[0][threadIdx.x], s[0][o]); s[1][threadIdx.x] = fmin(s[1][threadIdx.x], s[1][o]);
+            s[2][threadIdx.x] = fmax(s[2][threadIdx.x], s[2][o]); s[3][threadIdx.x] = fmax(s[3][threadIdx.x], s[3][o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    *gp = grid_params_of(s[0][0], s[1][0], s[2][0], s[3][0], s_bad != 0, cutoff, cap, sub_max);
 }
 
 __device__ __forceinline__ int cell_coord(double v, double v0, double inv_h, int nmax) {
@@ -421,15 +429,53 @@ int64_t cell_cap(int64_t n) {
     return cap;
 }
 
+namespace {
+int cell_sub_max() {
+    static const int v = [] {
+        const char* e = std::getenv("GS_B200_CELL_SUB");  // A/B: cells per cutoff (1 = classic 3x3 stencil)
+        return e ? std::min(std::max(std::atoi(e), 1), kCellSubMax) : 2;
+    }();
+    return v;
+}
+
+// Slab decomposition (gs_slab.cu): the bounding box of a rank's particles as (min x, min y,
+// -max x, -max y), so that ONE elementwise MIN all-reduce over the ranks gives the global box.
+__global__ void k_bbox4(const double* __restrict__ red, int nb, double* b4) {
+    if (threadIdx.x != 0) return;
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    bool bad = false;
+    for (int b = 0; b < nb; ++b) {
+        bad |= red[4 * b] != red[4 * b];
+        mnx = fmin(mnx, red[4 * b]); mny = fmin(mny, red[4 * b + 1]);
+        mxx = fmax(mxx, red[4 * b + 2]); mxy = fmax(mxy, red[4 * b + 3]);
+    }
+    b4[0] = bad ? -INFINITY : mnx;  // a non-finite position poisons the global box (-> one cell)
+    b4[1] = mny; b4[2] = -mxx; b4[3] = -mxy;
+}
+
+__global__ void k_grid_from_b4(const double* __restrict__ b4, double cutoff, int64_t cap, int sub_max, GridParams* gp) {
+    const double mnx = b4[0], mny = b4[1], mxx = -b4[2], mxy = -b4[3];
+    const bool empty = mnx > mxx;  // no particles at all
+    *gp = grid_params_of(empty ? 0.0 : mnx, empty ? 0.0 : mny, empty ? 0.0 : mxx, empty ? 0.0 : mxy,
+                         mnx == -INFINITY, cutoff, cap, sub_max);
+}
+}  // namespace
+
+void slab_bbox(const double4* S, int64_t n, double* red, double* b4, cudaStream_t stream) {
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB));
+    k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, red);
+    k_bbox4<<<1, 32, 0, stream>>>(red, nb, b4);
+}
+
+void slab_grid(const double* b4, double cutoff, int64_t n_glob, GridParams* gp, cudaStream_t stream) {
+    k_grid_from_b4<<<1, 1, 0, stream>>>(b4, cutoff, cell_cap(n_glob), cell_sub_max(), gp);
+}
+
 int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream) {
     const int nb = (int)std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB);
     k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, w.bbox_red);
     const int64_t cap = cell_cap(n);
-    static const int sub_max = [] {
-        const char* e = std::getenv("GS_B200_CELL_SUB");  // A/B: cells per cutoff (1 = classic 3x3 stencil)
-        return e ? std::min(std::max(std::atoi(e), 1), kCellSubMax) : 2;
-    }();
-    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, sub_max, w.gp);
+    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, cell_sub_max(), w.gp);
     const unsigned blocks = (unsigned)((n + 255) / 256);
     k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
     int end_bit = 1;

@@ -30,6 +30,7 @@ struct GridParams {
     float rc2f;          // fp32 candidate-filter radius^2: cutoff^2 grown by the fp32 position error
     int hashed;
     int sub;             // cells per cutoff (row-major grid; 1 when hashed or degenerate)
+    int ylo, yhi;        // row-major: `start` covers cell rows [ylo, yhi) (0, ny except on a slab)
 };
 
 constexpr int kCellBboxBlocks = 296;
@@ -94,5 +95,35 @@ void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t
 void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
                         DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
                         cudaStream_t stream);
+
+// ---- slab decomposition (gs_slab.cu): a rank's cell rows + halo rows -------------------------
+// Bounding box of n records as (min x, min y, -max x, -max y) into b4 (red: kCellBboxBlocks x 4 scratch).
+void slab_bbox(const double4* S, int64_t n, double* red, double* b4, cudaStream_t stream);
+// The grid of the one-rank build for list radius `cutoff` from an all-reduced b4 (n_glob particles).
+void slab_grid(const double* b4, double cutoff, int64_t n_glob, GridParams* gp, cudaStream_t stream);
+
+struct SlabLists {
+    const double4* S;      // n_loc + 1 local records in global sorted order (S[n_loc]: sentinel)
+    const float2* Sf;      // n_loc
+    const int* start;      // local cells + 1 (rows [gp->ylo, gp->yhi))
+    const GridParams* gp;
+    const int* cfirst;     // ncl + 1: first local position of each own cluster
+    long long* cnt;        // ncl + 1 (cnt[ncl] = 0)
+    long long* ofs;        // ncl + 1
+    int* len;              // ncl
+    int* list;             // cap entries
+    int64_t cap;
+    double2* Xb;           // own particles: positions at the build
+    unsigned long long* overflow;
+    void* scan_temp;
+    size_t scan_bytes;
+};
+// capacities + their exclusive scan (ofs[ncl] = entries); then the lists themselves
+int slab_list_caps(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, cudaStream_t stream);
+void slab_list_fill(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, int64_t own_begin, cudaStream_t stream);
+// raw pair sums of the own clusters -> part[k - own_begin] (local sorted order)
+void slab_sweep(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
+                int64_t own_begin, int64_t n_glob, double4* part, DevStatus* st, unsigned long long event,
+                const double* tbl_dev, unsigned long long* accepted, cudaStream_t stream);
 
 }  // namespace gsb

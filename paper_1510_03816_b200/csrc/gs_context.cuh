@@ -151,6 +151,34 @@ struct gs_context {
     double verlet_skin = -1.0;          // GS_B200_SKIN (< 0: by n, see verlet_ws)
     double verlet_slack = 0.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
     cudaStream_t cap_stream2 = nullptr; // captures the conditional rebuild bodies
+    // slab decomposition of the cell path across ranks (gs_slab.cu): this rank's own particles
+    // (contiguous cell rows of the global grid) + the halo rows, all in global sorted order
+    struct Slab {
+        int64_t n_glob = 0, n_own = 0, n_loc = 0, own_begin = 0, ncl = 0;
+        int tpl = 4;
+        double skin = 0.05, cutoff = 0.0, rl = 0.0;
+        int own_sorted = 0;                 // own particles live in the local layout (else in the *_u arrays)
+        GridParams g{};                     // host copy of the last grid
+        int y_own0 = 0, y_own1 = 0, y_loc0 = 0, y_loc1 = 0;
+        DevBuf<double4> S;                  // n_loc + 1 local records (S[n_loc]: sentinel far record)
+        DevBuf<unsigned> gidx;              // n_loc: global index of each local particle
+        DevBuf<double4> B, A, part;         // own particles, local sorted order
+        DevBuf<double2> Xb;                 // own particles: positions at the last build
+        DevBuf<double4> Su, Bu, Au;         // own particles in arrival order (begin / after a migration)
+        DevBuf<unsigned> gu;
+        DevBuf<unsigned long long> skey, skey2;  // (cell, global index) sort keys of the own particles
+        DevBuf<unsigned> sval, sval2;
+        DevBuf<unsigned char> cub;
+        DevBuf<unsigned> keys;              // n_loc local cell keys
+        DevBuf<int> start, cfirst, head, len, list;
+        DevBuf<float2> Sf;
+        DevBuf<GridParams> gp;
+        DevBuf<long long> cnt, ofs;
+        DevBuf<double> red, b4;
+        DevBuf<int> dest, dcount;
+        DevBuf<unsigned> flags;             // [0] rebuild wanted, [2] CTA counter, [3] decision of the last stage
+        DevBuf<unsigned long long> over;
+    } slab;
     // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds
     struct Graph {
         cudaGraphExec_t exec = nullptr;
@@ -184,6 +212,7 @@ int check_system(const gs_system_t* sys);
 int check_match(const gs_system_t* sys, const gs_match_config_t* cfg);
 SysConst make_const(const gs_system_t* sys);
 void decode_status(const DevStatus& d, int64_t n, gs_status_t* out);
+int fetch_status(gs_context* ctx, cudaStream_t s, int64_t n, gs_status_t* out);
 cudaEvent_t prof_event(gs_context* ctx);
 void prof_mark(gs_context* ctx, cudaStream_t stream);
 // small-N cluster kernel: CTAs per item, launch setup, eligibility, per-item constants, result

@@ -354,9 +354,9 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish_verlet(SysCons
         const double4 nxt = stage_update(a, li, dqx, dqy, sum.z * sc.scale_p, sum.w * sc.scale_p);
         a.S[i] = nxt;
         if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
-        const int k = f.inv[i];
+        const int64_t k = f.inv ? (int64_t)f.inv[i] : li;  // slab path (gs_slab.cu): rows already in sorted order
         GS_ASSERT(k >= 0 && k < a.nrows);
-        f.Ss[k] = nxt;
+        if (f.Ss) f.Ss[k] = nxt;
         const double2 b = f.Xb[k];
         const double dx = nxt.x - b.x, dy = nxt.y - b.y;
         need = fma(dx, dx, dy * dy) > f.thr2;

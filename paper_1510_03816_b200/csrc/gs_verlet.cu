@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
                   const int* __restrict__ len,
                   const unsigned* __restrict__ perm, int64_t n, int64_t cl0, int64_t cl1, double k1, long long rc2b,
                   double4* __restrict__ part, int64_t row0, DevStatus* st, unsigned long long event,
-                  const double* __restrict__ tbl_g, unsigned long long* accepted) {
+                  const double* __restrict__ tbl_g, unsigned long long* accepted, const int* __restrict__ cfirst,
+                  int64_t n_ev) {
     __shared__ double s_tbl[kTblWords];
     __shared__ unsigned long long s_acc_count;
     if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
@@ -132,13 +133,23 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
     const int64_t c = cl0 + (int64_t)blockIdx.x * (kVB / TPL) + threadIdx.x / TPL;
     const bool valid = c < cl1;
+    // members: sorted positions first .. first + cnt - 1 (slab: clusters restart at every cell row,
+    // cfirst[c]; otherwise c * M)
+    int64_t first = c * kVM;
+    int cnt = kVM;
+    if (cfirst) {
+        first = valid ? cfirst[c] : 0;
+        cnt = valid ? cfirst[c + 1] - (int)first : 0;
+    } else if (first + kVM > n) {
+        cnt = (int)(n - first);
+    }
     double4 me[kVM];
     Acc a[kVM];
     int nz[kVM];
 #pragma unroll
     for (int m = 0; m < kVM; ++m) {
-        const int64_t k = c * kVM + m;
-        me[m] = (valid && k < n) ? Ss[k] : far_record(m);
+        const int64_t k = first + m;
+        me[m] = (valid && m < cnt) ? Ss[k] : far_record(m);
         a[m] = Acc{0.0, 0.0, 0.0, 0.0};
         nz[m] = 0;
     }
@@ -204,10 +215,10 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     if (valid && sub == 0) {
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            const int64_t k = c * kVM + m;
-            if (k >= n) continue;
+            if (m >= cnt) continue;
+            const int64_t k = first + m;
             const int64_t i = (int64_t)perm[k];
-            GS_ASSERT(i >= 0 && i < n);
+            GS_ASSERT(i >= 0 && i < n_ev);
             if (nz[m] > 1) {  // rare: a coincident particle among the list (reference error, particles.py:92-98)
                 for (long long e = beg; e < end; ++e) {
                     const int j = list[e];
@@ -218,10 +229,11 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
                     const double dx = me[m].x - s.x, dy = me[m].y - s.y;
                     if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) != 0.0) continue;
                     if (fma(me[m].z, s.z, me[m].w * s.w) != 0.0)
-                        record_event(st, event, (unsigned long long)(i * n + jo));
+                        record_event(st, event, (unsigned long long)(i * n_ev + jo));
                 }
             }
-            part[i - row0] = make_double4(a[m].qx, a[m].qy, a[m].px, a[m].py);
+            // slab: part in sorted order of the rank's own particles; else at the original index
+            part[(cfirst ? k : i) - row0] = make_double4(a[m].qx, a[m].qy, a[m].px, a[m].py);
         }
     }
     if (COUNT) {
@@ -275,7 +287,7 @@ __device__ __forceinline__ void for_each_range(const GridParams& g, const int* _
             if (m < cm.nm) { lo = min(lo, cy[m]); hi = max(hi, cy[m]); }
         }
         const double rc2 = g.rc * g.rc;
-        for (int yy = max(lo - sub, 0); yy <= min(hi + sub, g.ny - 1); ++yy) {
+        for (int yy = max(lo - sub, g.ylo); yy <= min(hi + sub, g.yhi - 1); ++yy) {
             int xa = g.nx, xb = -1;
 #pragma unroll
             for (int m = 0; m < kVM; ++m) {
@@ -297,7 +309,8 @@ __device__ __forceinline__ void for_each_range(const GridParams& g, const int* _
                 xa = min(xa, a);
                 xb = max(xb, b);
             }
-            if (xb >= xa) f(start[yy * g.nx + xa], start[yy * g.nx + xb + 1]);
+            const int r0 = (yy - g.ylo) * g.nx;  // `start` covers rows [ylo, yhi)
+            if (xb >= xa) f(start[r0 + xa], start[r0 + xb + 1]);
         }
         return;
     }
@@ -316,13 +329,19 @@ __device__ __forceinline__ void for_each_range(const GridParams& g, const int* _
     }
 }
 
+__device__ __forceinline__ int64_t cluster_first(const int* __restrict__ cfirst, int64_t c) {
+    return cfirst ? (int64_t)cfirst[c] : c * kVM;
+}
+
 __device__ __forceinline__ void load_members(const double4* __restrict__ Ss, const float2* __restrict__ Sf, int64_t n,
-                                             int64_t c, ClusterMembers& cm) {
+                                             int64_t c, const int* __restrict__ cfirst, ClusterMembers& cm) {
     cm.nm = 0;
+    const int64_t first = cluster_first(cfirst, c);
+    const int64_t end = cfirst ? (int64_t)cfirst[c + 1] : n;
 #pragma unroll
     for (int m = 0; m < kVM; ++m) {
-        const int64_t k = c * kVM + m;
-        if (k < n) {
+        const int64_t k = first + m;
+        if (k < end) {
             const double4 v = Ss[k];
             cm.mx[m] = v.x; cm.my[m] = v.y;
             const float2 f = Sf[k];
@@ -339,12 +358,13 @@ __device__ __forceinline__ void load_members(const double4* __restrict__ Ss, con
 // upper bound of the filtered list, found without touching a candidate (one thread per cluster).
 __global__ void __launch_bounds__(256) k_verlet_caps(const float2* __restrict__ Sf, const double4* __restrict__ Ss,
                                                      const int* __restrict__ start, const GridParams* __restrict__ gp,
-                                                     int64_t n, int64_t ncl, int pad, long long* cap) {
+                                                     int64_t n, int64_t ncl, int pad, long long* cap,
+                                                     const int* __restrict__ cfirst) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncl) return;
     const GridParams g = *gp;
     ClusterMembers cm;
-    load_members(Ss, Sf, n, c, cm);
+    load_members(Ss, Sf, n, c, cfirst, cm);
     long long total = 0;
     for_each_range(g, start, cm, [&](int a, int b) { total += b - a; });
     cap[c] = (total + pad - 1) / pad * pad;
@@ -358,19 +378,20 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__
                                                       int64_t n, int64_t ncl, int pad, const long long* __restrict__ ofs,
                                                       int* len, int* list, int64_t cap, double2* Xb,
                                                       const unsigned* __restrict__ perm, int* inv,
-                                                      unsigned long long* overflow) {
+                                                      unsigned long long* overflow, const int* __restrict__ cfirst,
+                                                      int64_t xb_base) {
     const int sub = threadIdx.x & 31;
     const int64_t c = (int64_t)blockIdx.x * (kVBB / kTplB) + threadIdx.x / kTplB;
     if (c >= ncl) return;  // warp-uniform
     const GridParams g = *gp;
     ClusterMembers cm;
-    load_members(Ss, Sf, n, c, cm);
+    load_members(Ss, Sf, n, c, cfirst, cm);
 #pragma unroll
     for (int m = 0; m < kVM; ++m)
         if (sub == m && m < cm.nm) {
-            const int64_t k = c * kVM + m;
-            Xb[k] = make_double2(cm.mx[m], cm.my[m]);
-            inv[perm[k]] = (int)k;  // original index -> sorted slot (the fused stage epilogue's gather)
+            const int64_t k = cluster_first(cfirst, c) + m;
+            Xb[k - xb_base] = make_double2(cm.mx[m], cm.my[m]);
+            if (inv) inv[perm[k]] = (int)k;  // original index -> sorted slot (the fused stage epilogue's gather)
         }
     const int64_t obase = ofs[c];
     const bool ok = ofs[ncl] <= cap;  // the list buffer holds the whole build
@@ -479,13 +500,14 @@ int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n
     k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, n, v.flags);
     const int64_t ncl = verlet_clusters(n);
     const int pad = 2 * v.tpl;
-    k_verlet_caps<<<(unsigned)((ncl + 255) / 256), 256, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.cnt);
+    k_verlet_caps<<<(unsigned)((ncl + 255) / 256), 256, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.cnt,
+                                                                     nullptr);
     size_t bytes = v.scan_bytes;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(v.scan_temp, bytes, v.cnt, v.ofs, (int)(ncl + 1), stream);
     if (e != cudaSuccess) return (int)e;
     const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
     k_verlet_fill<<<blocks, kVBB, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.ofs, v.len, v.list, v.cap,
-                                               v.Xb, w.perm, v.inv, v.overflow);
+                                               v.Xb, w.perm, v.inv, v.overflow, nullptr, 0);
     return (int)cudaGetLastError();
 }
 
@@ -496,22 +518,23 @@ void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t
                                                                      v.flags, force, cond, use_cond);
 }
 
-void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
-                        DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
-                        cudaStream_t stream) {
-    const int64_t ncl = verlet_clusters(n);
+namespace {
+void sweep(const SysConst& sc, const double4* Ss, const int* list, const long long* ofs, const int* len,
+           const unsigned* perm, int64_t n, int64_t ncl, int tpl, double4* part, int64_t row0, DevStatus* st,
+           unsigned long long event, const double* tbl_dev, unsigned long long* accepted, const int* cfirst,
+           int64_t n_ev, cudaStream_t stream) {
+    if (ncl <= 0) return;
     const double rc2 = sc.cutoff * sc.cutoff;
     long long rc2b;
     memcpy(&rc2b, &rc2, sizeof(rc2b));
-    const int tpl = v.tpl;
     const unsigned blocks = (unsigned)((ncl * tpl + kVB - 1) / kVB);
 #define GS_V_LAUNCH(F, T)                                                                                  \
     if (accepted)                                                                                          \
-        k_verlet_pair<F, T, true><<<blocks, kVB, 0, stream>>>(w.Ss, v.list, v.ofs, v.len, w.perm, n, 0, ncl, sc.k1,  \
-                                                              rc2b, part, 0, st, event, tbl_dev, accepted);  \
+        k_verlet_pair<F, T, true><<<blocks, kVB, 0, stream>>>(Ss, list, ofs, len, perm, n, 0, ncl, sc.k1, rc2b, part, \
+                                                              row0, st, event, tbl_dev, accepted, cfirst, n_ev);   \
     else                                                                                                   \
-        k_verlet_pair<F, T, false><<<blocks, kVB, 0, stream>>>(w.Ss, v.list, v.ofs, v.len, w.perm, n, 0, ncl, sc.k1, \
-                                                               rc2b, part, 0, st, event, tbl_dev, accepted)
+        k_verlet_pair<F, T, false><<<blocks, kVB, 0, stream>>>(Ss, list, ofs, len, perm, n, 0, ncl, sc.k1, rc2b, part,\
+                                                               row0, st, event, tbl_dev, accepted, cfirst, n_ev)
 #define GS_V_FAM(F)                           \
     switch (tpl) {                            \
         case 1: GS_V_LAUNCH(F, 1); break;     \
@@ -524,6 +547,42 @@ void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, 
     else { GS_V_FAM(kFamGaussian) }
 #undef GS_V_FAM
 #undef GS_V_LAUNCH
+}
+}  // namespace
+
+void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
+                        DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                        cudaStream_t stream) {
+    sweep(sc, w.Ss, v.list, v.ofs, v.len, w.perm, n, verlet_clusters(n), v.tpl, part, 0, st, event, tbl_dev, accepted,
+          nullptr, n, stream);
+}
+
+// ---- slab decomposition (gs_slab.cu) ---------------------------------------------------------
+// The same list build and sweep over a rank's local particles (its own cell rows + the halo rows,
+// in global sorted order), clusters given by cfirst (they restart at every cell row, so a rank
+// forms exactly the clusters of the one-rank build), output in the rank's own sorted order.
+
+int slab_list_caps(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, cudaStream_t stream) {
+    if (ncl > 0)
+        k_verlet_caps<<<(unsigned)((ncl + 255) / 256), 256, 0, stream>>>(L.Sf, L.S, L.start, L.gp, n_loc, ncl,
+                                                                         2 * tpl, L.cnt, L.cfirst);
+    size_t bytes = L.scan_bytes;
+    const cudaError_t e = cub::DeviceScan::ExclusiveSum(L.scan_temp, bytes, L.cnt, L.ofs, (int)(ncl + 1), stream);
+    return (int)e;
+}
+
+void slab_list_fill(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, int64_t own_begin, cudaStream_t stream) {
+    if (ncl <= 0) return;
+    const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
+    k_verlet_fill<<<blocks, kVBB, 0, stream>>>(L.Sf, L.S, L.start, L.gp, n_loc, ncl, 2 * tpl, L.ofs, L.len, L.list,
+                                               L.cap, L.Xb, nullptr, nullptr, L.overflow, L.cfirst, own_begin);
+}
+
+void slab_sweep(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
+                int64_t own_begin, int64_t n_glob, double4* part, DevStatus* st, unsigned long long event,
+                const double* tbl_dev, unsigned long long* accepted, cudaStream_t stream) {
+    sweep(sc, L.S, L.list, L.ofs, L.len, gidx, n_loc, ncl, tpl, part, own_begin, st, event, tbl_dev, accepted,
+          L.cfirst, n_glob, stream);
 }
 
 }  // namespace gsb

@@ -68,6 +68,7 @@ class DeviceStageBackend:
 
         self.torch = torch
         self.ctx = ctx or N.Context.get()
+        self.spec = spec
         self.sysc = device.system_struct(spec)
         self.n = 0
 
@@ -96,6 +97,13 @@ class DeviceStageBackend:
 
     # -- symmetric split (dense path, world > 1) -------------------------------------------
     supports_sym = True
+    # -- slab decomposition (cell path, world > 1): slab.py over gs_slab_* ------------------
+    supports_slab = True
+
+    def slab_backend(self):
+        from . import slab
+
+        return slab.DeviceSlabBackend(self.spec, ctx=self.ctx)
 
     def path(self) -> str:
         rc = self.ctx.lib.gs_stage_path(self.ctx.handle, ctypes.byref(self.sysc), self._s())
@@ -221,6 +229,8 @@ class ShardedSolver:
             p2p = env == "1" or (env != "0" and self.world > 1)
         self.p2p = bool(p2p) and getattr(self.backend, "supports_p2p", False)
         self._p2p_key = None
+        # cell path across ranks: slab decomposition (GS_B200_SLAB=0: all-gather of every record)
+        self.slab = os.environ.get("GS_B200_SLAB", "1") != "0"
 
     # -- collectives (plumbing) -------------------------------------------------------------
     def _allgather_rows(self, S, r0: int, c: int):
@@ -266,12 +276,25 @@ class ShardedSolver:
         Dense path with world > 1: the symmetric split — rank r evaluates its share of the
         unordered pairs (each pair once, both rows fed), the raw row sums are reduce-scattered
         to the row owners (NCCL), the owners run the stage epilogue and the stage records are
-        all-gathered.  Otherwise every rank evaluates its own rows one-sided (cell list or
-        dense) and only the all-gather is needed."""
+        all-gathered.  Cell path with world > 1: the slab decomposition (slab.py: each rank
+        owns a band of cell rows + a halo, exchanges only the halo per stage).  Otherwise (a
+        cloud spread beyond a row-major grid) every rank evaluates its own rows one-sided and
+        the stage records are all-gathered."""
         n = q.shape[0]
         W = self.world
         r0, r1, c = row_split(n, W, self.rank)
         self.backend.begin(q, p, r0, r1)
+        if self.split and self.slab and getattr(self.backend, "supports_slab", False) and \
+                self.backend.path() == "cell":
+            from . import slab
+
+            torch = _torch_of(self.backend)
+            try:
+                solver = slab.SlabSolver(self.spec, [self.backend.slab_backend()], slab.DistComm(self.group))
+                return solver.evolve(device.as_device(q, torch), device.as_device(p, torch), t_final, steps)
+            except slab.SlabUnavailable:
+                self.slab = False  # hashed grid: the all-gather path below (the same on every rank)
+                self.backend.begin(q, p, r0, r1)
         S = self.backend.state(c * W)
         dt = t_final / steps
         sym = False

@@ -52,6 +52,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(N.MatchConfig) == 40
     assert ctypes.sizeof(N.MatchResultC) == 64
     assert ctypes.sizeof(N.BatchItem) == 80
+    assert ctypes.sizeof(N.SlabGrid) == 40
 
 
 def test_no_device_means_loud_failure():
