@@ -304,18 +304,20 @@ int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stre
  *                    doubles) -> elementwise MIN all-reduce over the ranks
  *   gs_slab_grid   : the one-rank build's grid for list radius cutoff (1 + skin) from the reduced
  *                    b4 (the same on every rank); synchronises
- *   gs_slab_rows   : own particles per cell row into hist (device, ny int64) -> SUM all-reduce
+ *   gs_slab_rows   : own particles per cell row into hist (device, ny int64) -> all-gather
  *   gs_slab_pack   : every own particle (S, RK4 base B and accumulator A, global index: 13
  *                    doubles) into send (device, n_own x 13) grouped by the owner of its row
- *                    (owner: device, ny int32); counts[world] (host); synchronises
+ *                    (owner: device, ny int32); counts[world] (host, optional: NULL = the
+ *                    driver knows them from the all-gathered histograms; else synchronises)
  *                    -> all-to-all -> gs_slab_unpack (the rank's new own particles)
  *   gs_slab_layout : own particles sorted by (cell, global index) into local positions
  *                    [own_begin, own_begin + n_own) of the n_loc local records (rows
  *                    [y_loc0, y_loc1) = own rows [y_own0, y_own1) + halo rows)
  *                    -> the halo slices of S and of the global indices (gs_slab_views) are
  *                    copied in from the neighbours' own blocks
- *   gs_slab_lists  : cell starts, own clusters (pairs restarting at every cell row) and their
- *                    lists over the local particles; synchronises
+ *   gs_slab_lists  : cell starts, own clusters (pairs restarting at every cell row: ncl = sum
+ *                    over the own rows of ceil(count / 2)) and their lists over the local
+ *                    particles; synchronises once (list capacity)
  * per RK4 stage: gs_slab_stage (sweep + epilogue of the own rows, rebuild flag = some own
  * particle moved more than skin * cutoff / 2 since the build, *flag of gs_slab_views) -> the
  * halo slices of S -> MAX all-reduce of the flags: rebuild before the next stage.
@@ -336,7 +338,7 @@ int gs_slab_unpack(gs_context* ctx, int64_t n_own, const double* recv, void* str
 int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_loc0, int32_t y_loc1, int64_t own_begin,
                    int64_t n_loc, void* stream);
 int gs_slab_views(gs_context* ctx, double** S, int32_t** gidx, int32_t** flag);
-int gs_slab_lists(gs_context* ctx, void* stream);
+int gs_slab_lists(gs_context* ctx, int64_t ncl, void* stream);
 int gs_slab_stage(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt, void* stream);
 int gs_slab_status(gs_context* ctx, gs_status_t* status, void* stream);
 

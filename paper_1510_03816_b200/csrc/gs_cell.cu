@@ -441,16 +441,31 @@ int cell_sub_max() {
 // Slab decomposition (gs_slab.cu): the bounding box of a rank's particles as (min x, min y,
 // -max x, -max y), so that ONE elementwise MIN all-reduce over the ranks gives the global box.
 __global__ void k_bbox4(const double* __restrict__ red, int nb, double* b4) {
-    if (threadIdx.x != 0) return;
+    __shared__ double sh[4][kBB];
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
     double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     bool bad = false;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = threadIdx.x; b < nb; b += kBB) {
         bad |= red[4 * b] != red[4 * b];
         mnx = fmin(mnx, red[4 * b]); mny = fmin(mny, red[4 * b + 1]);
         mxx = fmax(mxx, red[4 * b + 2]); mxy = fmax(mxy, red[4 * b + 3]);
     }
-    b4[0] = bad ? -INFINITY : mnx;  // a non-finite position poisons the global box (-> one cell)
-    b4[1] = mny; b4[2] = -mxx; b4[3] = -mxy;
+    if (bad) s_bad = 1;
+    sh[0][threadIdx.x] = mnx; sh[1][threadIdx.x] = mny; sh[2][threadIdx.x] = mxx; sh[3][threadIdx.x] = mxy;
+    __syncthreads();
+    for (int w = kBB / 2; w; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            sh[0][threadIdx.x] = fmin(sh[0][threadIdx.x], sh[0][o]); sh[1][threadIdx.x] = fmin(sh[1][threadIdx.x], sh[1][o]);
+            sh[2][threadIdx.x] = fmax(sh[2][threadIdx.x], sh[2][o]); sh[3][threadIdx.x] = fmax(sh[3][threadIdx.x], sh[3][o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    b4[0] = s_bad ? -INFINITY : sh[0][0];  // a non-finite position poisons the global box (-> one cell)
+    b4[1] = sh[1][0]; b4[2] = -sh[2][0]; b4[3] = -sh[3][0];
 }
 
 __global__ void k_grid_from_b4(const double* __restrict__ b4, double cutoff, int64_t cap, int sub_max, GridParams* gp) {
@@ -464,7 +479,7 @@ __global__ void k_grid_from_b4(const double* __restrict__ b4, double cutoff, int
 void slab_bbox(const double4* S, int64_t n, double* red, double* b4, cudaStream_t stream) {
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB));
     k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, red);
-    k_bbox4<<<1, 32, 0, stream>>>(red, nb, b4);
+    k_bbox4<<<1, kBB, 0, stream>>>(red, nb, b4);
 }
 
 void slab_grid(const double* b4, double cutoff, int64_t n_glob, GridParams* gp, cudaStream_t stream) {

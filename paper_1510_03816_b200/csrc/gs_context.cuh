@@ -175,8 +175,9 @@ struct gs_context {
         DevBuf<GridParams> gp;
         DevBuf<long long> cnt, ofs;
         DevBuf<double> red, b4;
-        DevBuf<int> dest, dcount;
-        DevBuf<unsigned> flags;             // [0] rebuild wanted, [2] CTA counter, [3] decision of the last stage
+        DevBuf<int> dest;
+        DevBuf<unsigned long long> dcount;
+        DevBuf<unsigned> flags;             // [0] rebuild wanted (set by the last stage's epilogue)
         DevBuf<unsigned long long> over;
     } slab;
     // CUDA graph of a whole evolve (all steps x 4 stages), re-launched while its key holds

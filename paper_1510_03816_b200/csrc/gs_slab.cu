@@ -50,24 +50,37 @@ __global__ void k_slab_begin(const double* __restrict__ q, const double* __restr
     gu[i] = (unsigned)g[i];
 }
 
+// One atomic per distinct value per warp (own particles are in cell order after a layout, so a
+// warp's lanes mostly share one row / one destination: per-lane atomics on a few addresses
+// serialised to ~100 us at 131k particles).
+__device__ __forceinline__ void warp_count(unsigned long long* ctr, int key, bool valid) {
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const unsigned peers = __match_any_sync(act, key);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&ctr[key], (unsigned long long)__popc(peers));
+}
+
 __global__ void k_slab_rows(const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
                             unsigned long long* hist) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
     const GridParams g = *gp;
-    atomicAdd(&hist[grid_cell(S[i].y, g.y0, g.inv_h, g.ny)], 1ull);
+    const bool valid = i < n;
+    warp_count(hist, valid ? grid_cell(S[i].y, g.y0, g.inv_h, g.ny) : 0, valid);
 }
 
 // destination rank of every own particle: the owner of its cell row
 __global__ void k_slab_dest(const double4* __restrict__ S, int64_t n, const GridParams* __restrict__ gp,
-                            const int* __restrict__ owner, unsigned long long* key, unsigned* val, int* count) {
+                            const int* __restrict__ owner, unsigned long long* key, unsigned* val,
+                            unsigned long long* count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
     const GridParams g = *gp;
-    const int d = owner[grid_cell(S[i].y, g.y0, g.inv_h, g.ny)];
-    key[i] = (unsigned long long)d;
-    val[i] = (unsigned)i;
-    atomicAdd(&count[d], 1);
+    const bool valid = i < n;
+    const int d = valid ? owner[grid_cell(S[i].y, g.y0, g.inv_h, g.ny)] : 0;
+    if (valid) {
+        key[i] = (unsigned long long)d;
+        val[i] = (unsigned)i;
+    }
+    warp_count(count, d, valid);
 }
 
 __global__ void k_slab_pack(const unsigned* __restrict__ order, int64_t n, const double4* __restrict__ S,
@@ -156,9 +169,10 @@ __global__ void k_slab_heads(const unsigned* __restrict__ keys, const int* __res
 }
 
 __global__ void k_slab_cfirst(const int* __restrict__ head, const int* __restrict__ cid, int64_t own_begin,
-                              int64_t n_own, int* cfirst) {
+                              int64_t n_own, int* cfirst, int ncl) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k > n_own) return;
+    GS_ASSERT(cid[n_own] == ncl);
     if (k == n_own) cfirst[cid[k]] = (int)(own_begin + n_own);
     else if (head[k]) cfirst[cid[k]] = (int)(own_begin + k);
 }
@@ -284,13 +298,13 @@ int gs_slab_rows(gs_context* ctx, int64_t* hist, void* stream) {
 int gs_slab_pack(gs_context* ctx, const int32_t* owner, int32_t world, double* send, int64_t* counts, void* stream) {
     gsapi::NvtxScope nvtx_("gs_slab_pack");
     cudaStream_t s = (cudaStream_t)stream;
-    if (!ctx || !owner || world < 1 || !counts || (ctx->slab.n_own && !send)) return fail(GS_ERR_INVALID, "bad slab args");
+    if (!ctx || !owner || world < 1 || (ctx->slab.n_own && !send)) return fail(GS_ERR_INVALID, "bad slab args");
     auto& L = ctx->slab;
     GS_CUDA(cudaSetDevice(ctx->device));
     const int64_t n = L.n_own;
     const Own o = own_arrays(ctx);
     GS_CUDA(L.dcount.ensure(world));
-    GS_CUDA(cudaMemsetAsync(L.dcount.ptr, 0, world * sizeof(int), s));
+    GS_CUDA(cudaMemsetAsync(L.dcount.ptr, 0, world * sizeof(unsigned long long), s));
     if (n) {
         k_slab_dest<<<blk(n), 256, 0, s>>>(o.S, n, L.gp.ptr, owner, L.skey.ptr, L.sval.ptr, L.dcount.ptr);
         size_t bytes = 0;
@@ -303,10 +317,13 @@ int gs_slab_pack(gs_context* ctx, const int32_t* owner, int32_t world, double* s
                                                 (int)n, 0, end_bit, s));
         k_slab_pack<<<blk(n), 256, 0, s>>>(L.sval2.ptr, n, o.S, o.B, o.A, o.g, send);
     }
-    std::vector<int> c(world);
-    GS_CUDA(cudaMemcpyAsync(c.data(), L.dcount.ptr, world * sizeof(int), cudaMemcpyDeviceToHost, s));
-    GS_CUDA(cudaStreamSynchronize(s));
-    for (int d = 0; d < world; ++d) counts[d] = c[d];
+    if (counts) {  // optional: the driver knows them from the all-gathered row histograms
+        std::vector<unsigned long long> c(world);
+        GS_CUDA(cudaMemcpyAsync(c.data(), L.dcount.ptr, world * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        GS_CUDA(cudaStreamSynchronize(s));
+        for (int d = 0; d < world; ++d) counts[d] = (int64_t)c[d];
+    }
+    GS_CUDA(cudaGetLastError());
     return GS_OK;
 }
 
@@ -372,15 +389,16 @@ int gs_slab_views(gs_context* ctx, double** S, int32_t** gidx, int32_t** flag) {
     if (!ctx || !S || !gidx || !flag) return fail(GS_ERR_INVALID, "bad slab args");
     *S = reinterpret_cast<double*>(ctx->slab.S.ptr);
     *gidx = reinterpret_cast<int32_t*>(ctx->slab.gidx.ptr);
-    *flag = reinterpret_cast<int32_t*>(ctx->slab.flags.ptr + 3);
+    *flag = reinterpret_cast<int32_t*>(ctx->slab.flags.ptr);
     return GS_OK;
 }
 
 // After the halo exchange: cell starts over the local rows, own clusters, their lists.
-int gs_slab_lists(gs_context* ctx, void* stream) {
+int gs_slab_lists(gs_context* ctx, int64_t ncl_host, void* stream) {
     gsapi::NvtxScope nvtx_("gs_slab_lists");
     cudaStream_t s = (cudaStream_t)stream;
     if (!ctx || !ctx->slab.own_sorted) return fail(GS_ERR_INVALID, "slab lists before the layout");
+    if (ncl_host < 0 || ncl_host > ctx->slab.n_own) return fail(GS_ERR_INVALID, "bad cluster count");
     GS_CUDA(cudaSetDevice(ctx->device));
     auto& L = ctx->slab;
     const int64_t n_loc = L.n_loc, n = L.n_own;
@@ -396,13 +414,13 @@ int gs_slab_lists(gs_context* ctx, void* stream) {
     GS_CUDA(L.cub.ensure(bytes));
     bytes = L.cub.cap;
     GS_CUDA(cub::DeviceScan::ExclusiveSum(L.cub.ptr, bytes, L.head.ptr, L.dest.ptr, (int)(n + 1), s));
-    int ncl = 0;
-    GS_CUDA(cudaMemcpyAsync(&ncl, L.dest.ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
-    GS_CUDA(cudaStreamSynchronize(s));
+    // clusters: sum over the own rows of ceil(count / 2), known to the driver from the histogram
+    // (checked on the device: the scan's total must agree)
+    const int ncl = (int)ncl_host;
     L.ncl = ncl;
     GS_CUDA(L.cfirst.ensure(ncl + 1)); GS_CUDA(L.cnt.ensure(ncl + 1)); GS_CUDA(L.ofs.ensure(ncl + 1));
     GS_CUDA(L.len.ensure(std::max(ncl, 1)));
-    k_slab_cfirst<<<blk(n + 1), 256, 0, s>>>(L.head.ptr, L.dest.ptr, L.own_begin, n, L.cfirst.ptr);
+    k_slab_cfirst<<<blk(n + 1), 256, 0, s>>>(L.head.ptr, L.dest.ptr, L.own_begin, n, L.cfirst.ptr, ncl);
     k_slab_sentinel<<<1, 1, 0, s>>>(L.S.ptr, n_loc, L.cnt.ptr, ncl);
     bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, L.cnt.ptr, L.ofs.ptr, ncl + 1, s);
@@ -442,9 +460,8 @@ int gs_slab_stage(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t
     fa.S = L.S.ptr + L.own_begin; fa.B = L.B.ptr; fa.A = L.A.ptr;
     fa.stage = stg; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
     const double thr = 0.5 * L.skin * L.cutoff;
-    const VerletFuse f{nullptr, nullptr, L.Xb.ptr, thr * thr * (1.0 - 1e-9), L.flags.ptr, {}, 0};
-    if (L.n_own) launch_finish_verlet(sc, fa, f, s);
-    else GS_CUDA(cudaMemsetAsync(L.flags.ptr + 3, 0, sizeof(unsigned), s));
+    GS_CUDA(cudaMemsetAsync(L.flags.ptr, 0, sizeof(unsigned), s));
+    launch_finish_slab(sc, fa, L.Xb.ptr, thr * thr * (1.0 - 1e-9), L.flags.ptr, s);
     GS_CUDA(cudaGetLastError());
     return GS_OK;
 }

@@ -66,7 +66,9 @@ class SlabPlan:
     source's local array, offset in the destination's local array, count): a source's rows
     inside a destination's halo are a contiguous run of its own block."""
 
-    def __init__(self, hist, world: int, sub: int):
+    def __init__(self, hist, world: int, sub: int, rank_hists=None):
+        """``hist``: particles per cell row (all ranks); ``rank_hists`` (W, ny): the same per
+        current owner, which fixes every migration count (``send_counts`` / ``recv_counts``)."""
         hist = np.asarray(hist, dtype=np.int64)
         self.ny = ny = int(hist.shape[0])
         self.world = W = int(world)
@@ -90,6 +92,15 @@ class SlabPlan:
             loc0, loc1 = (max(own0 - sub, 0), min(own1 + sub, ny)) if n_own else (own0, own1)
             self.rows.append(RankRows(own0, own1, loc0, loc1, int(cum[own0] - cum[loc0]), n_own,
                                       int(cum[loc1] - cum[loc0])))
+        # own clusters per rank: pairs restart at every cell row (csrc/gs_slab.cu)
+        self.ncl = [int(((hist[r.own0:r.own1] + 1) // 2).sum()) for r in self.rows]
+        if rank_hists is not None:
+            H = np.asarray(rank_hists, dtype=np.int64)
+            csum = np.zeros((W, ny + 1), dtype=np.int64)
+            np.cumsum(H, axis=1, out=csum[:, 1:])
+            M = np.stack([csum[:, Y[d + 1]] - csum[:, Y[d]] for d in range(W)], axis=1)  # M[s, d]
+            self.send_counts = [[int(x) for x in M[s]] for s in range(W)]
+            self.recv_counts = [[int(x) for x in M[:, d]] for d in range(W)]
         self.slices = []
         for d in range(W):
             rd = self.rows[d]
@@ -127,7 +138,13 @@ class LocalComm:
         for t in ts:
             t.copy_(acc)
 
-    def alltoallv(self, sends, counts):
+    def allgather(self, ts):
+        """Per local rank: the (W, ...) stack of every rank's tensor."""
+        torch = _torch_mod()
+        full = torch.stack(ts)
+        return [full for _ in ts]
+
+    def alltoallv(self, sends, counts, recv_counts=None):
         """sends[r]: rows grouped by destination, counts[r][d] rows for rank d -> recvs[d]."""
         torch = _torch_mod()
         offs = [np.concatenate([[0], np.cumsum(c)]) for c in counts]
@@ -163,13 +180,22 @@ class DistComm:
         R = self.dist.ReduceOp
         self.dist.all_reduce(ts[0], op={"min": R.MIN, "max": R.MAX, "sum": R.SUM}[op], group=self.group)
 
-    def alltoallv(self, sends, counts):
+    def allgather(self, ts):
+        torch = _torch_mod()
+        parts = [torch.empty_like(ts[0]) for _ in range(self.world)]
+        self.dist.all_gather(parts, ts[0].contiguous(), group=self.group)
+        return [torch.stack(parts)]
+
+    def alltoallv(self, sends, counts, recv_counts=None):
         torch = _torch_mod()
         send = sends[0]
-        cin = torch.tensor(list(counts[0]), dtype=torch.int64, device=send.device)
-        cout = torch.empty_like(cin)
-        self.dist.all_to_all_single(cout, cin, group=self.group)
-        out_splits = [int(x) for x in cout.tolist()]
+        if recv_counts is None:
+            cin = torch.tensor(list(counts[0]), dtype=torch.int64, device=send.device)
+            cout = torch.empty_like(cin)
+            self.dist.all_to_all_single(cout, cin, group=self.group)
+            out_splits = [int(x) for x in cout.tolist()]
+        else:
+            out_splits = [int(x) for x in recv_counts[0]]
         recv = torch.empty((sum(out_splits),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
         self.dist.all_to_all_single(recv, send, out_splits, [int(x) for x in counts[0]], group=self.group)
         return [recv]
@@ -257,13 +283,13 @@ class DeviceSlabBackend:
         return h
 
     def pack(self, owner, world: int):
+        """Own particles grouped by destination rank (the counts come from the plan)."""
         t = self.torch
         n_own = self._n_own
         send = t.empty((max(n_own, 0), PACK_W), dtype=t.float64, device=self.dev)
-        counts = (ctypes.c_int64 * world)()
         self._chk(self.ctx.lib.gs_slab_pack(self.ctx.handle, owner.data_ptr(), world, send.data_ptr() if n_own else 0,
-                                            counts, self._s()), "gs_slab_pack")
-        return send, [int(c) for c in counts]
+                                            None, self._s()), "gs_slab_pack")
+        return send
 
     def unpack(self, recv):
         recv = recv.contiguous()
@@ -283,8 +309,8 @@ class DeviceSlabBackend:
         self.flag = _wrap(self.torch, f.value, (1,), "<i4", self.dev)
         self.rows_ = r
 
-    def lists(self):
-        self._chk(self.ctx.lib.gs_slab_lists(self.ctx.handle, self._s()), "gs_slab_lists")
+    def lists(self, ncl: int):
+        self._chk(self.ctx.lib.gs_slab_lists(self.ctx.handle, ncl, self._s()), "gs_slab_lists")
 
     def stage(self, step: int, s: int, dt: float):
         self._chk(self.ctx.lib.gs_slab_stage(self.ctx.handle, ctypes.byref(self.sysc), step, s, dt, self._s()),
@@ -338,26 +364,27 @@ class SlabSolver:
 
     def rebuild(self):
         comm, W = self.comm, self.W
-        b4 = self._each("build", lambda b, r: b.bbox())
+        b4 = self._each("build:bbox", lambda b, r: b.bbox())
         comm.allreduce(b4, "min")
-        grids = self._each("build", lambda b, r: b.grid(b4[self.comm.ranks.index(r)]))
+        grids = self._each("build:grid", lambda b, r: b.grid(b4[self.comm.ranks.index(r)]))
         g = grids[0]
         if g.hashed:
             raise SlabUnavailable("the cloud spread beyond a row-major grid (hashed cells)")
-        hists = self._each("build", lambda b, r: b.rows(g.ny))
-        comm.allreduce(hists, "sum")
-        plan = SlabPlan(hists[0].cpu().numpy(), W, g.sub)
+        hists = self._each("build:rows", lambda b, r: b.rows(g.ny))
+        H = comm.allgather(hists)[0].cpu().numpy()  # (W, ny): particles per row and current owner
+        plan = SlabPlan(H.sum(axis=0), W, g.sub, rank_hists=H)
         torch = _torch_mod()
         owner = [torch.as_tensor(plan.owner, device=h.device) for h in hists]
-        packed = self._each("build", lambda b, r: b.pack(owner[self.comm.ranks.index(r)], W))
-        recvs = comm.alltoallv([p[0] for p in packed], [p[1] for p in packed])
+        sends = self._each("build:pack", lambda b, r: b.pack(owner[self.comm.ranks.index(r)], W))
+        recvs = comm.alltoallv(sends, [plan.send_counts[r] for r in comm.ranks],
+                               [plan.recv_counts[r] for r in comm.ranks])
         for b, r, rv in zip(self.backends, comm.ranks, recvs):
             assert rv.shape[0] == plan.rows[r].n_own, (rv.shape, plan.rows[r])
-            self.timer("build", r, lambda b=b, rv=rv: b.unpack(rv))
-        self._each("build", lambda b, r: b.layout(plan.rows[r]))
+            self.timer("build:unpack", r, lambda b=b, rv=rv: b.unpack(rv))
+        self._each("build:layout", lambda b, r: b.layout(plan.rows[r]))
         comm.exchange(plan.slices, [b.S for b in self.backends])
         comm.exchange(plan.slices, [b.g for b in self.backends])
-        self._each("build", lambda b, r: b.lists())
+        self._each("build:lists", lambda b, r: b.lists(plan.ncl[r]))
         self.plan = plan
         self.builds += 1
 

@@ -86,7 +86,7 @@ class NumpySlabBackend:
         dest = owner.numpy()[cy]
         order = np.argsort(dest, kind="stable")
         send = torch.cat([S, B, A, g.double()[:, None]], dim=1)[torch.from_numpy(order)]
-        return send.contiguous(), [int(c) for c in np.bincount(dest, minlength=world)]
+        return send.contiguous()
 
     def unpack(self, recv):
         self.Su, self.Bu, self.Au = recv[:, 0:4].clone(), recv[:, 4:8].clone(), recv[:, 8:12].clone()
@@ -107,7 +107,7 @@ class NumpySlabBackend:
         self.rows_ = r
         self.sorted = True
 
-    def lists(self):
+    def lists(self, ncl):
         r = self.rows_
         self.Xb = self.S[r.own_begin:r.own_begin + r.n_own, 0:2].clone()
 

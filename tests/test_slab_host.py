@@ -70,6 +70,15 @@ def test_plan_partitions_rows_and_covers_halos(W):
                     rs = plan.rows[s]
                     assert rs.own_begin <= so and so + c <= rs.own_begin + rs.n_own  # from the sender's own block
             assert (got == 1).all()
+    # migration counts from per-owner histograms: rows of d held by s
+    H = np.stack([rng.multinomial(int(h), [1.0 / W] * W) for h in hist], axis=1)  # (W, ny), sums to hist
+    plan2 = slab.SlabPlan(hist, W, 2, rank_hists=H)
+    for s_ in range(W):
+        for d in range(W):
+            rd = plan2.rows[d]
+            assert plan2.send_counts[s_][d] == H[s_, rd.own0:rd.own1].sum() == plan2.recv_counts[d][s_]
+    assert [sum(c) for c in plan2.recv_counts] == [r.n_own for r in plan2.rows]
+    assert plan2.ncl == [int(((hist[r.own0:r.own1] + 1) // 2).sum()) for r in plan2.rows]
     # balance: no rank owns more than its share plus one row
     for rr in plan.rows:
         assert rr.n_own <= hist.sum() / W + hist.max()

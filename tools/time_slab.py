@@ -82,7 +82,7 @@ def main():
         stage = np.zeros((rhs, W))
         k = 0
         build = {}
-        nb = 0
+        phases = {}
         for kind, rank, s0, e0 in rec:
             t = s0.elapsed_time(e0)
             if kind == "stage":
@@ -91,6 +91,7 @@ def main():
             else:
                 build.setdefault(rank, 0.0)
                 build[rank] += t
+                phases.setdefault(kind, np.zeros(W))[rank] += t
         plan = solver.plan
         halo = [plan.halo_particles(r) for r in range(W)]
         results[W] = (qW, pW)
@@ -104,6 +105,7 @@ def main():
             "halo_particles": halo,
             "halo_bytes_per_stage_max_rank": 32 * max(halo),
             "slices": len(plan.slices),
+            "build_phase_ms_max_rank": {k: float(v.max()) for k, v in phases.items()},
         }
         d = out[f"W{W}"]
         d["rank_ms_per_rhs_measured"] = d["stage_ms_per_rhs_max_rank"] + d["build_ms_total_max_rank"] / rhs
