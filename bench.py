@@ -516,6 +516,19 @@ def run_extras(a, gs, device, configs, torch, world, rank, dist, sharded_run):
                                      "h": wk.h}
         finally:
             device.set_path(path0)
+        # the multi-GPU cell path (slab decomposition) at W = 8 run on this one GPU: per-rank device
+        # time per RHS, rows bitwise equal to W = 1 (tools/time_slab.py; exchange cost modelled)
+        from tools import time_slab
+
+        em = time_slab.measure("C5", 8, 4)
+        w8 = em["W8"]
+        out["c5_slab_w8_emulated"] = {
+            "rank_ms_per_rhs": w8["rank_ms_per_rhs_measured"], "stage_ms_per_rhs": w8["stage_ms_per_rhs_max_rank"],
+            "build_ms": w8["build_ms_per_build_max_rank"], "builds_per_16_rhs": w8["builds"],
+            "halo_bytes_per_stage": w8["halo_bytes_per_stage_max_rank"],
+            "modelled_rank_ms_per_rhs_with_exchange": w8["modelled_rank_ms_per_rhs"],
+            "modelled_strong_scaling_eff": w8["modelled_strong_scaling_eff_vs_one_gpu"],
+            "one_gpu_ms_per_rhs": em["one_gpu_verlet_ms_per_rhs"], "bitwise_equal_w1": em["bitwise_equal_w1_vs_w"]}
         c1 = configs.c1()
         spec1 = gs.SystemSpec(kernel=gs.KernelSpec(alpha=c1.alpha))
         for _ in range(2):

@@ -337,10 +337,16 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish(SysConst sc, F
     if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
 }
 
-__global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish_verlet(SysConst sc, FinishArgs a, VerletFuse f) {
-    int64_t li = 0;
-    double4 sum;
-    bool act = finish_reduce(a, li, sum);
+// One raw-sum record per row (the lists' sweep): one thread per row in 256-thread CTAs (with the
+// 32-row CTAs of finish_reduce a C5 stage ran 32768 CTAs, each bumping the decision counter).
+__global__ void __launch_bounds__(256) k_finish_verlet(SysConst sc, FinishArgs a, VerletFuse f) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double4 sum = make_double4(0.0, 0.0, 0.0, 0.0);
+    bool act = li < a.nrows;
+    if (act) {
+        const double4 v = a.part[li];
+        sum = make_double4(0.0 + v.x, 0.0 + v.y, 0.0 + v.z, 0.0 + v.w);  // as finish_reduce (nchunks = 1)
+    }
     act = act && !(*((volatile unsigned long long*)&a.st->first_event) < a.event);
     bool need = false;
     if (act) {
@@ -376,8 +382,8 @@ __global__ void __launch_bounds__(kFinRows * kFinGroups) k_finish_verlet(SysCons
 
 void launch_finish_verlet(const SysConst& sc, const FinishArgs& a, const VerletFuse& f, cudaStream_t stream) {
     if (a.nrows <= 0) return;
-    const unsigned blocks = (unsigned)((a.nrows + kFinRows - 1) / kFinRows);
-    k_finish_verlet<<<blocks, finish_threads(a.nchunks), 0, stream>>>(sc, a, f);
+    // the lists' sweep leaves one partial per row (a.nchunks == 1)
+    k_finish_verlet<<<(unsigned)((a.nrows + 255) / 256), 256, 0, stream>>>(sc, a, f);
 }
 
 // Slab path (gs_slab.cu): the stage epilogue of a rank's own rows, already in local sorted order

@@ -34,6 +34,16 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
+    out = measure(a.config, a.world, a.steps, a.gain, a.reps)
+    print(json.dumps(out, indent=1))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(out, f, indent=1)
+
+
+def measure(config="C5", world=8, steps=4, gain=None, reps=2) -> dict:
+    """The emulation (see the module docstring) as a dict."""
+    a = argparse.Namespace(config=config, world=world, steps=steps, gain=gain, reps=reps)
     import torch
 
     import paper_1510_03816_b200 as gs
@@ -121,10 +131,7 @@ def main():
     dW["modelled_exchange_ms_per_stage"] = xch
     dW["modelled_rank_ms_per_rhs"] = dW["rank_ms_per_rhs_measured"] + xch
     dW["modelled_strong_scaling_eff_vs_one_gpu"] = one_gpu_ms / (a.world * dW["modelled_rank_ms_per_rhs"])
-    print(json.dumps(out, indent=1))
-    if a.out:
-        with open(a.out, "w") as f:
-            json.dump(out, f, indent=1)
+    return out
 
 
 if __name__ == "__main__":
