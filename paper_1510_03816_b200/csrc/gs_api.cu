@@ -291,6 +291,8 @@ VerletWs verlet_ws(gs_context* ctx, int64_t n, double cutoff) {
     v.tpl = verlet_tpl(n);
     v.skin = ctx->verlet_skin >= 0.0 ? ctx->verlet_skin : (n < 131072 ? 0.1 : 0.05);
     v.cutoff = cutoff;
+    v.Ss_pair[0] = ctx->c_Ss.ptr;
+    v.Ss_pair[1] = ctx->c_Ss2.cap >= (size_t)(n + 1) ? ctx->c_Ss2.ptr : nullptr;
     return v;
 }
 
@@ -304,6 +306,8 @@ int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, c
     GS_CUDA(ctx->v_len.ensure(ncl)); GS_CUDA(ctx->v_inv.ensure(n));
     GS_CUDA(ctx->v_flags.ensure(4)); GS_CUDA(ctx->v_over.ensure(1));
     GS_CUDA(ctx->v_scan.ensure(verlet_scan_bytes(ncl)));
+    GS_CUDA(ctx->c_Ss2.ensure(n + 1));  // the ping-pong half of the sorted records (fused epilogue);
+                                        // every list build writes the sentinel record [n] into both halves
     if (fresh) {
         GS_CUDA(cudaMemsetAsync(ctx->v_flags.ptr, 0, 4 * sizeof(unsigned), s));
         GS_CUDA(cudaMemsetAsync(ctx->v_over.ptr, 0, sizeof(unsigned long long), s));
@@ -460,9 +464,11 @@ int take_cell_err(gs_context* ctx) {
 // stage's fused epilogue saw a particle move more than half the skin (captured: a conditional IF
 // node on the condition that epilogue set; host-driven: unconditionally, or decided on the host
 // with GS_B200_VERLET=3) and always at the first stage of an evolve (`force`).  Then the sweep.
-void verlet_stage(gs_context* ctx, const SysConst& sc, int force, unsigned long long ev, cudaStream_t stream) {
+// Returns the cell workspace of the stage (its sorted records: c_Ss or c_Ss2 by `parity`).
+CellWs verlet_prepare(gs_context* ctx, const SysConst& sc, int force, cudaStream_t stream, int parity) {
     const int64_t n = ctx->n;
     CellWs w = cell_ws(ctx);
+    if (parity) w.Ss = ctx->c_Ss2.ptr;  // the stage's sorted records: ping-pong with the fused epilogue
     VerletWs v = verlet_ws(ctx, n, sc.cutoff);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(stream, &cs);
@@ -510,9 +516,17 @@ void verlet_stage(gs_context* ctx, const SysConst& sc, int force, unsigned long 
         if (int rc = verlet_build(w, v, ctx->S.ptr, n, sc.cutoff, stream)) ctx->cell_err = rc;
         ctx->launches += 10;
     }
+    return w;
+}
+
+// The stage's list sweep with the RK4 stage epilogue fused in.
+void verlet_sweep(gs_context* ctx, const SysConst& sc, const CellWs& w, unsigned long long ev, const VerletEpi& epi,
+                  cudaStream_t stream) {
+    const int64_t n = ctx->n;
+    VerletWs v = verlet_ws(ctx, n, sc.cutoff);
     if (ctx->prof_on) prof_mark(ctx, stream);
-    launch_verlet_pair(sc, w, v, n, ctx->part.ptr, ctx->st.ptr, ev, ctx->tbl.ptr,
-                       ctx->prof_on ? ctx->c_acc.ptr : nullptr, stream);
+    launch_verlet_pair_epi(sc, w, v, n, epi, ctx->st.ptr, ev, ctx->tbl.ptr, ctx->prof_on ? ctx->c_acc.ptr : nullptr,
+                           stream);
     if (ctx->prof_on) prof_mark(ctx, stream);
     ctx->launches++;
     ctx->pair_launches++;
@@ -548,20 +562,48 @@ void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cuda
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)s;
     PairOut po{1, 0};
     const bool lists = ctx->verlet_call && ctx->cell_on && ctx->row0 == 0 && nrows == n;
-    if (lists)
-        verlet_stage(ctx, sc, step == 1 && s == 0, ev, stream);
-    else
-        po = pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
-    ctx->launches++;  // finish
     FinishArgs fa{};
     fa.part = ctx->part.ptr; fa.nchunks = po.nchunks; fa.pstride = po.pstride; fa.nrows = nrows;
     fa.row0 = ctx->row0;
     fa.S = ctx->S.ptr; fa.B = ctx->B.ptr; fa.A = ctx->A.ptr;
     fa.stage = s; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
-    if (lists && !last)
-        launch_finish_verlet(sc, fa, verlet_fuse(ctx, sc, stream), stream);
-    else
-        launch_finish(kFinStage, sc, fa, stream);
+    if (lists && ctx->verlet_fuse_max_n > n) {
+        // small clouds (launch/latency bound): the sweep carries the stage epilogue, one kernel per
+        // stage plus the conditional rebuild (C2 100-step solve 13.3 -> 12.3 ms); sorted records
+        // ping-pong between c_Ss and c_Ss2 by the stage's parity within the evolve.  Large clouds
+        // keep the separate epilogue: its rows are coalesced in original order, where the fused
+        // lanes would touch S / B / A scattered by the sort (C5 evolve 23.2 -> 23.7 ms fused).
+        const int parity = ((step - 1) * 4 + s) & 1;
+        // the rebuild first: its IF node reads the condition the previous stage's sweep set
+        const CellWs w = verlet_prepare(ctx, sc, step == 1 && s == 0, stream, parity);
+        VerletEpi e{};
+        e.a = fa;
+        e.scale_q = sc.scale_q; e.scale_p = sc.scale_p; e.sigma2 = sc.sigma2;
+        if (!last) {  // this sweep sets the condition of the next stage's IF node
+            const VerletFuse f = verlet_fuse(ctx, sc, stream);
+            e.Ss_next = parity ? ctx->c_Ss.ptr : ctx->c_Ss2.ptr;
+            e.Xb = f.Xb; e.thr2 = f.thr2; e.flags = f.flags; e.cond = f.cond; e.use_cond = f.use_cond;
+        }
+        verlet_sweep(ctx, sc, w, ev, e, stream);
+        return;
+    }
+    if (lists) {
+        const CellWs w = verlet_prepare(ctx, sc, step == 1 && s == 0, stream, 0);
+        const VerletWs v = verlet_ws(ctx, n, sc.cutoff);
+        if (ctx->prof_on) prof_mark(ctx, stream);
+        launch_verlet_pair(sc, w, v, n, ctx->part.ptr, ctx->st.ptr, ev, ctx->tbl.ptr,
+                           ctx->prof_on ? ctx->c_acc.ptr : nullptr, stream);
+        if (ctx->prof_on) prof_mark(ctx, stream);
+        ctx->launches += 2;
+        ctx->pair_launches++;
+        if (!last) launch_finish_verlet(sc, fa, verlet_fuse(ctx, sc, stream), stream);
+        else launch_finish(kFinStage, sc, fa, stream);
+        return;
+    }
+    po = pair_kernel(ctx, sc, ctx->S.ptr, n, ctx->row0, nrows, plan, ctx->part.ptr, ev, stream);
+    fa.nchunks = po.nchunks; fa.pstride = po.pstride;
+    ctx->launches++;  // finish
+    launch_finish(kFinStage, sc, fa, stream);
 }
 
 void graph_reset(gs_context* ctx) {
@@ -575,12 +617,12 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
     auto P = [](const void* p) { return (double)(uintptr_t)p; };
     return {(double)ctx->n, (double)ctx->row0, (double)ctx->row1, (double)steps, dt, (double)ctx->cell_on,
             (double)ctx->prof_on, (double)sc.fam, sc.k1, sc.scale_q, sc.scale_p, sc.sigma2, sc.cutoff,
-            P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr), P(ctx->c_Sf.ptr),
+            P(ctx->S.ptr), P(ctx->B.ptr), P(ctx->A.ptr), P(ctx->part.ptr), P(ctx->st.ptr), P(ctx->c_Ss.ptr), P(ctx->c_Ss2.ptr), P(ctx->c_Sf.ptr),
             P(ctx->c_cub.ptr), P(ctx->c_start.ptr), P(ctx->c_keys.ptr), P(ctx->c_perm.ptr), P(ctx->c_acc.ptr),
             P(ctx->c_keys_sorted.ptr), P(ctx->c_vals.ptr), P(ctx->c_bbox.ptr), P(ctx->c_gp.ptr), P(ctx->c_tlist.ptr),
             P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes, (double)ctx->verlet_call,
             P(ctx->v_cnt.ptr), P(ctx->v_ofs.ptr), P(ctx->v_len.ptr), P(ctx->v_inv.ptr), P(ctx->v_list.ptr), (double)ctx->v_list.cap, P(ctx->v_xb.ptr),
-            P(ctx->v_flags.ptr), P(ctx->v_over.ptr), P(ctx->v_scan.ptr), ctx->verlet_skin};
+            P(ctx->v_flags.ptr), P(ctx->v_over.ptr), P(ctx->v_scan.ptr), ctx->verlet_skin, (double)ctx->verlet_fuse_max_n};
 }
 
 // integrator.py:95-119 as one CUDA graph (4 x steps stages, ~2 kernels per dense stage and
@@ -802,6 +844,7 @@ int gs_create(gs_context** out, int device) {
     if (const char* g = std::getenv("GS_B200_DEVLOOP")) ctx->devloop_on = std::atoi(g) != 0;
     if (const char* g = std::getenv("GS_B200_VERLET")) ctx->verlet_on = std::atoi(g);
     if (const char* g = std::getenv("GS_B200_SKIN")) ctx->verlet_skin = std::atof(g);
+    if (const char* g = std::getenv("GS_B200_VERLET_FUSE_MAX_N")) ctx->verlet_fuse_max_n = std::atoll(g);
     if (const char* g = std::getenv("GS_B200_VERLET_SLACK")) ctx->verlet_slack = std::atof(g);  // tests
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
@@ -843,7 +886,7 @@ int gs_destroy(gs_context* ctx) {
     ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_inv.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
     ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release();
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
-    ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
+    ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Ss2.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     gs_p2p_close(ctx);
     ctx->p2p.R.release(); ctx->p2p.flags.release(); ctx->p2p.done.release(); ctx->p2p.Rp.release(); ctx->p2p.Sp.release(); ctx->p2p.Fp.release();
     ctx->c_acc.release(); ctx->gram_bad.release(); ctx->b_items.release(); ctx->b_st.release(); ctx->vf_part.release(); ctx->sym_slots.release();

@@ -82,11 +82,28 @@ struct VerletWs {
     int tpl;                       // pair-sweep lanes per cluster (lists padded to 2 tpl)
     double skin;                   // list radius = cutoff (1 + skin); rebuild at skin * cutoff / 2
     double cutoff;
+    double4* Ss_pair[2];           // both halves of the sorted-record ping-pong: the sentinel goes into each
+};
+// The stage epilogue fused into the list sweep (single rank, all rows): the lane that reduced a
+// member's sums applies scales, sigma2 and the RK4 stage update (stage_update) to its row of
+// a.S / a.B / a.A (original order), stores the new record into the next stage's sorted buffer
+// (Ss_next, the other half of a ping-pong pair; nullptr on the call's last stage) and the last
+// CTA decides the next stage's rebuild (flags[3] / the IF-node condition), as k_finish_verlet.
+struct VerletEpi {
+    FinishArgs a;                  // S, B, A, stage, dt, st, event (= the sweep's event + 1)
+    double scale_q, scale_p, sigma2;
+    double4* Ss_next;
+    const double2* Xb;
+    double thr2;
+    unsigned* flags;               // [0] rebuild wanted, [2] CTA counter, [3] decision
+    cudaGraphConditionalHandle cond;
+    int use_cond;
 };
 int64_t verlet_clusters(int64_t n);
 int verlet_tpl(int64_t n);
 size_t verlet_scan_bytes(int64_t ncl);
-// Grid + lists for the records of S (cell workspace w is rebuilt; Ss[n] becomes the sentinel).
+// Grid + lists for the records of S (cell workspace w is rebuilt; Ss[n] becomes the sentinel;
+// the decision counter flags[2] is reset).
 int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, double cutoff, cudaStream_t stream);
 // Ss <- S in sorted order and the rebuild decision (force: no gather, rebuild) -> IF condition / flags[3].
 void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, int force,
@@ -95,6 +112,10 @@ void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t
 void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
                         DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
                         cudaStream_t stream);
+// The same sweep with the stage epilogue fused in (no partials): e.a.S gets the new records.
+void launch_verlet_pair_epi(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, const VerletEpi& e,
+                            DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                            cudaStream_t stream);
 
 // ---- slab decomposition (gs_slab.cu): a rank's cell rows + halo rows -------------------------
 // Bounding box of n records as (min x, min y, -max x, -max y) into b4 (red: kCellBboxBlocks x 4 scratch).

@@ -123,7 +123,7 @@ struct gs_context {
     // cell list (gs_cell.cu)
     DevBuf<unsigned> c_keys, c_keys_sorted, c_vals, c_perm;
     DevBuf<int> c_start;
-    DevBuf<double4> c_Ss;
+    DevBuf<double4> c_Ss, c_Ss2;        // sorted records; c_Ss2: ping-pong half for the fused list epilogue
     DevBuf<float2> c_Sf;
     DevBuf<double> c_bbox;
     DevBuf<GridParams> c_gp;
@@ -149,6 +149,7 @@ struct gs_context {
     double v_list_cutoff = 0.0;
     int verlet_retries = 0;
     double verlet_skin = -1.0;          // GS_B200_SKIN (< 0: by n, see verlet_ws)
+    int64_t verlet_fuse_max_n = 131072; // lists: epilogue fused into the sweep below this n (GS_B200_VERLET_FUSE_MAX_N)
     double verlet_slack = 0.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
     cudaStream_t cap_stream2 = nullptr; // captures the conditional rebuild bodies
     // slab decomposition of the cell path across ranks (gs_slab.cu): this rank's own particles

@@ -233,42 +233,7 @@ void launch_velocity_field(const SysConst& sc, const double4* S, int64_t n, cons
 
 // ---------------------------------------------------------------------------------------
 // Finish: chunk reduction (fixed order) + scale + sigma2 + mode-specific epilogue.
-// RK4 stage epilogue of row li in the reference's evaluation order (integrator.py:98-114):
-//   stage inputs q + (0.5 dt) k_s, q + dt k_3; combine q + (dt/6) (((k1 + 2k2) + 2k3) + k4).
-// Updates the row's accumulator / base records and returns the next stage input.
-__device__ __forceinline__ double4 stage_update(const FinishArgs& a, int64_t li, double dqx, double dqy, double dpx,
-                                                double dpy) {
-    double4 b = a.B[li];
-    double4 acc;
-    double4 nxt;
-    if (a.stage == 0) {
-        acc = make_double4(dqx, dqy, dpx, dpy);
-    } else {
-        acc = a.A[li];
-        const double w = (a.stage == 3) ? 1.0 : 2.0;
-        acc.x = __dadd_rn(acc.x, __dmul_rn(w, dqx));
-        acc.y = __dadd_rn(acc.y, __dmul_rn(w, dqy));
-        acc.z = __dadd_rn(acc.z, __dmul_rn(w, dpx));
-        acc.w = __dadd_rn(acc.w, __dmul_rn(w, dpy));
-    }
-    if (a.stage < 3) {
-        const double c = (a.stage == 2) ? a.dt : 0.5 * a.dt;
-        nxt.x = __dadd_rn(b.x, __dmul_rn(c, dqx));
-        nxt.y = __dadd_rn(b.y, __dmul_rn(c, dqy));
-        nxt.z = __dadd_rn(b.z, __dmul_rn(c, dpx));
-        nxt.w = __dadd_rn(b.w, __dmul_rn(c, dpy));
-        a.A[li] = acc;
-    } else {
-        const double c = a.dt / 6.0;
-        nxt.x = __dadd_rn(b.x, __dmul_rn(c, acc.x));
-        nxt.y = __dadd_rn(b.y, __dmul_rn(c, acc.y));
-        nxt.z = __dadd_rn(b.z, __dmul_rn(c, acc.z));
-        nxt.w = __dadd_rn(b.w, __dmul_rn(c, acc.w));
-        a.B[li] = nxt;
-    }
-    return nxt;
-}
-
+// (the RK4 stage epilogue itself, stage_update, is in gs_kernels.cuh)
 // Partial sums are reduced by kFinGroups warps per 32 rows: warp w sums slots w, w + 8, ...
 // (coalesced over the rows), warp 0 adds the group sums in group order — a fixed order, and
 // 8x the parallelism of one thread per row walking all slots (the symmetric kernel leaves

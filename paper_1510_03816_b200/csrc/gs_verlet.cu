@@ -113,17 +113,36 @@ __device__ __forceinline__ void vbody(const double4& me, const double4& s, const
     a.py = fma(c, dy, a.py);
 }
 
-template <int FAM, int TPL, bool COUNT>
+// The last CTA of a fused sweep (EPI) turns the CTAs' "rebuild wanted" into the decision: flags[3]
+// and, inside a graph, the next stage's IF-node condition (k_finish_verlet's protocol).
+__device__ __forceinline__ void epi_decide(const VerletEpi& e, bool need) {
+    if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&e.flags[0], 1u);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&e.flags[2], 1u);
+        if (prev == gridDim.x - 1) {
+            const unsigned d = atomicExch(&e.flags[0], 0u);
+            e.flags[2] = 0u;
+            if (e.use_cond) cudaGraphSetConditional(e.cond, d);
+            e.flags[3] = d;
+        }
+    }
+}
+
+template <int FAM, int TPL, bool COUNT, bool EPI>
 __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     k_verlet_pair(const double4* __restrict__ Ss, const int* __restrict__ list, const long long* __restrict__ ofs,
                   const int* __restrict__ len,
                   const unsigned* __restrict__ perm, int64_t n, int64_t cl0, int64_t cl1, double k1, long long rc2b,
                   double4* __restrict__ part, int64_t row0, DevStatus* st, unsigned long long event,
                   const double* __restrict__ tbl_g, unsigned long long* accepted, const int* __restrict__ cfirst,
-                  int64_t n_ev) {
+                  int64_t n_ev, VerletEpi epi) {
     __shared__ double s_tbl[kTblWords];
     __shared__ unsigned long long s_acc_count;
-    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
+        if (EPI && epi.Ss_next) epi_decide(epi, false);  // every CTA counts towards the decision
+        return;
+    }
     for (int t = threadIdx.x; t < kTblWords; t += kVB) s_tbl[t] = tbl_g[t];
     if (threadIdx.x == 0) s_acc_count = 0;
     __syncthreads();
@@ -212,6 +231,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
             a[m].py += __shfl_xor_sync(kFull, a[m].py, off);
         }
     }
+    bool need = false;
     if (valid && sub == 0) {
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
@@ -232,10 +252,29 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
                         record_event(st, event, (unsigned long long)(i * n_ev + jo));
                 }
             }
-            // slab: part in sorted order of the rank's own particles; else at the original index
-            part[(cfirst ? k : i) - row0] = make_double4(a[m].qx, a[m].qy, a[m].px, a[m].py);
+            if (EPI) {  // k_finish_verlet's arithmetic (the sum as finish_reduce forms it: 0 + v)
+                const double sx = 0.0 + a[m].qx, sy = 0.0 + a[m].qy, sz = 0.0 + a[m].px, sw = 0.0 + a[m].py;
+                double dqx = sx * epi.scale_q, dqy = sy * epi.scale_q;
+                if (epi.sigma2 != 0.0) {
+                    dqx = __dadd_rn(dqx, __dmul_rn(epi.sigma2, me[m].z));
+                    dqy = __dadd_rn(dqy, __dmul_rn(epi.sigma2, me[m].w));
+                }
+                const double4 nxt = stage_update(epi.a, i, dqx, dqy, sz * epi.scale_p, sw * epi.scale_p);
+                epi.a.S[i] = nxt;
+                if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(epi.a.st, epi.a.event, kNoEvent);
+                if (epi.Ss_next) {
+                    epi.Ss_next[k] = nxt;
+                    const double2 b = epi.Xb[k];
+                    const double dx = nxt.x - b.x, dy = nxt.y - b.y;
+                    need |= fma(dx, dx, dy * dy) > epi.thr2;
+                }
+            } else {
+                // slab: part in sorted order of the rank's own particles; else at the original index
+                part[(cfirst ? k : i) - row0] = make_double4(a[m].qx, a[m].qy, a[m].px, a[m].py);
+            }
         }
     }
+    if (EPI && epi.Ss_next) epi_decide(epi, need);
     if (COUNT) {
         unsigned long long v = (unsigned long long)nin;
         for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
@@ -462,9 +501,12 @@ __global__ void __launch_bounds__(256) k_verlet_gather(const double4* __restrict
     }
 }
 
-__global__ void k_verlet_sentinel(double4* Ss, int64_t n, unsigned* flags) {
+__global__ void k_verlet_sentinel(double4* Ss, double4* Ss0, double4* Ss1, int64_t n, unsigned* flags) {
     Ss[n] = far_record(0);
+    if (Ss0) Ss0[n] = far_record(0);  // the ping-pong halves (a buffer sized for a larger n holds a stale record at n)
+    if (Ss1) Ss1[n] = far_record(0);
     flags[1] += 1u;  // builds so far (diagnostics)
+    flags[2] = 0u;   // decision counter (a failed evolve may have left CTAs uncounted)
 }
 
 }  // namespace
@@ -497,7 +539,7 @@ int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n
     const double rl = cutoff * (1.0 + v.skin);
     int rc = cell_build(w, S, n, rl, stream);
     if (rc) return rc;
-    k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, n, v.flags);
+    k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, v.Ss_pair[0], v.Ss_pair[1], n, v.flags);
     const int64_t ncl = verlet_clusters(n);
     const int pad = 2 * v.tpl;
     k_verlet_caps<<<(unsigned)((ncl + 255) / 256), 256, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.cnt,
@@ -519,10 +561,11 @@ void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t
 }
 
 namespace {
+template <bool EPI>
 void sweep(const SysConst& sc, const double4* Ss, const int* list, const long long* ofs, const int* len,
            const unsigned* perm, int64_t n, int64_t ncl, int tpl, double4* part, int64_t row0, DevStatus* st,
            unsigned long long event, const double* tbl_dev, unsigned long long* accepted, const int* cfirst,
-           int64_t n_ev, cudaStream_t stream) {
+           int64_t n_ev, const VerletEpi& e, cudaStream_t stream) {
     if (ncl <= 0) return;
     const double rc2 = sc.cutoff * sc.cutoff;
     long long rc2b;
@@ -530,11 +573,11 @@ void sweep(const SysConst& sc, const double4* Ss, const int* list, const long lo
     const unsigned blocks = (unsigned)((ncl * tpl + kVB - 1) / kVB);
 #define GS_V_LAUNCH(F, T)                                                                                  \
     if (accepted)                                                                                          \
-        k_verlet_pair<F, T, true><<<blocks, kVB, 0, stream>>>(Ss, list, ofs, len, perm, n, 0, ncl, sc.k1, rc2b, part, \
-                                                              row0, st, event, tbl_dev, accepted, cfirst, n_ev);   \
+        k_verlet_pair<F, T, true, EPI><<<blocks, kVB, 0, stream>>>(Ss, list, ofs, len, perm, n, 0, ncl, sc.k1, rc2b,   \
+                                                              part, row0, st, event, tbl_dev, accepted, cfirst, n_ev, e); \
     else                                                                                                   \
-        k_verlet_pair<F, T, false><<<blocks, kVB, 0, stream>>>(Ss, list, ofs, len, perm, n, 0, ncl, sc.k1, rc2b, part,\
-                                                               row0, st, event, tbl_dev, accepted, cfirst, n_ev)
+        k_verlet_pair<F, T, false, EPI><<<blocks, kVB, 0, stream>>>(Ss, list, ofs, len, perm, n, 0, ncl, sc.k1, rc2b,  \
+                                                               part, row0, st, event, tbl_dev, accepted, cfirst, n_ev, e)
 #define GS_V_FAM(F)                           \
     switch (tpl) {                            \
         case 1: GS_V_LAUNCH(F, 1); break;     \
@@ -553,8 +596,15 @@ void sweep(const SysConst& sc, const double4* Ss, const int* list, const long lo
 void launch_verlet_pair(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, double4* part,
                         DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
                         cudaStream_t stream) {
-    sweep(sc, w.Ss, v.list, v.ofs, v.len, w.perm, n, verlet_clusters(n), v.tpl, part, 0, st, event, tbl_dev, accepted,
-          nullptr, n, stream);
+    sweep<false>(sc, w.Ss, v.list, v.ofs, v.len, w.perm, n, verlet_clusters(n), v.tpl, part, 0, st, event, tbl_dev,
+                 accepted, nullptr, n, VerletEpi{}, stream);
+}
+
+void launch_verlet_pair_epi(const SysConst& sc, const CellWs& w, const VerletWs& v, int64_t n, const VerletEpi& e,
+                            DevStatus* st, unsigned long long event, const double* tbl_dev, unsigned long long* accepted,
+                            cudaStream_t stream) {
+    sweep<true>(sc, w.Ss, v.list, v.ofs, v.len, w.perm, n, verlet_clusters(n), v.tpl, nullptr, 0, st, event, tbl_dev,
+                accepted, nullptr, n, e, stream);
 }
 
 // ---- slab decomposition (gs_slab.cu) ---------------------------------------------------------
@@ -581,8 +631,8 @@ void slab_list_fill(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, int
 void slab_sweep(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
                 int64_t own_begin, int64_t n_glob, double4* part, DevStatus* st, unsigned long long event,
                 const double* tbl_dev, unsigned long long* accepted, cudaStream_t stream) {
-    sweep(sc, L.S, L.list, L.ofs, L.len, gidx, n_loc, ncl, tpl, part, own_begin, st, event, tbl_dev, accepted,
-          L.cfirst, n_glob, stream);
+    sweep<false>(sc, L.S, L.list, L.ofs, L.len, gidx, n_loc, ncl, tpl, part, own_begin, st, event, tbl_dev, accepted,
+                 L.cfirst, n_glob, VerletEpi{}, stream);
 }
 
 }  // namespace gsb

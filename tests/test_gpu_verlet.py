@@ -122,3 +122,22 @@ def test_coincident_interacting_pair_through_the_lists(cuda):
     qv, pv, _ = _evolve(gs, spec, q, p, 2)
     qs, ps, _ = _evolve(gs, spec, q, p, 2, GS_B200_VERLET=0)
     assert rel(qv, qs) <= TOL and rel(pv, ps) <= TOL
+
+
+def test_fused_epilogue_equals_the_separate_epilogue(cuda):
+    """Below GS_B200_VERLET_FUSE_MAX_N the list sweep carries the RK4 stage epilogue and the sorted
+    records ping-pong between two buffers; the arithmetic is k_finish_verlet's, so the evolve is
+    bitwise the one with the separate epilogue, rebuilds included — also after a larger cloud left
+    a stale record in the second buffer (the lists' sentinel slot)."""
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs
+
+    w = configs.c5(65536)
+    p = 0.05 * (w.target - w.q)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    for n in (65536, 20000):
+        q0, p0 = w.q[:n], p[:n]
+        qf, pf, (bf, _) = _evolve(gs, spec, q0, p0, 6)
+        qs, ps, (bs, _) = _evolve(gs, spec, q0, p0, 6, GS_B200_VERLET_FUSE_MAX_N=0)
+        assert np.array_equal(qf, qs) and np.array_equal(pf, ps), n
+        assert bf == bs and bf >= 3
