@@ -173,10 +173,27 @@ __device__ __forceinline__ unsigned cell_hash(double cx, double cy, int ncells) 
     return (unsigned)h & (unsigned)(ncells - 1);
 }
 
+// Row-major keys carry a 4 x 4 sub-cell index (Morton order) below the cell index: the cells stay
+// contiguous and x-ordered in a row (the stencil ranges are unchanged), and inside a cell the
+// sorted order walks the sub-cells, so consecutive sorted particles — the lists' clusters — are
+// close together: the union of a cluster's two neighbourhoods, i.e. its list, shrinks.
+#ifndef GS_CELL_SUBKEY          // sub-cell key bits (A/B builds: 0 = index order inside a cell)
+#define GS_CELL_SUBKEY 4
+#endif
 __device__ __forceinline__ unsigned cell_key(const GridParams& g, double x, double y) {
     if (g.hashed) return cell_hash(cell_coordf(x, g.x0, g.inv_h), cell_coordf(y, g.y0, g.inv_h), g.ncells);
     const int cx = cell_coord(x, g.x0, g.inv_h, g.nx), cy = cell_coord(y, g.y0, g.inv_h, g.ny);
+#if GS_CELL_SUBKEY
+    constexpr int kB = GS_CELL_SUBKEY / 2, kS = 1 << kB;  // bits / sub-cells per axis
+    const double fx = (x - g.x0) * g.inv_h - (double)cx, fy = (y - g.y0) * g.inv_h - (double)cy;
+    const unsigned sx = (unsigned)min(max((int)(fx * kS), 0), kS - 1), sy = (unsigned)min(max((int)(fy * kS), 0), kS - 1);
+    unsigned sub = 0;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) sub |= (((sx >> b) & 1u) << (2 * b)) | (((sy >> b) & 1u) << (2 * b + 1));
+    return ((unsigned)(cy * g.nx + cx) << GS_CELL_SUBKEY) | sub;
+#else
     return (unsigned)(cy * g.nx + cx);
+#endif
 }
 
 // The candidate ranges of a target at (x, y): 3 contiguous stencil rows of the row-major grid,
@@ -287,8 +304,9 @@ __global__ void k_cell_start_permute(const unsigned* __restrict__ keys_sorted, c
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k > n) return;
     const GridParams g = *gp;
-    const long long prev = (k == 0) ? -1 : (long long)keys_sorted[k - 1];
-    const long long cur = (k == n) ? (long long)g.ncells : (long long)keys_sorted[k];
+    const int sh = g.hashed ? 0 : GS_CELL_SUBKEY;  // row-major keys: cell index above the sub-cell bits
+    const long long prev = (k == 0) ? -1 : (long long)(keys_sorted[k - 1] >> sh);
+    const long long cur = (k == n) ? (long long)g.ncells : (long long)(keys_sorted[k] >> sh);
     GS_ASSERT(cur <= (long long)g.ncells);
     for (long long c = prev + 1; c <= cur; ++c) start[c] = (int)k;
     if (k < n) {
@@ -495,6 +513,7 @@ int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cuda
     k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
     int end_bit = 1;
     while ((1ll << end_bit) < cap) ++end_bit;
+    end_bit += GS_CELL_SUBKEY;
     static const int64_t small_max = [] {
         const char* e = std::getenv("GS_B200_SORT_SMALL_MAX");  // A/B: 0 = always the device-wide sort
         return e ? std::min<int64_t>(std::atoll(e), kSortSmallMax) : kSortSmallMax;
