@@ -173,27 +173,11 @@ __device__ __forceinline__ unsigned cell_hash(double cx, double cy, int ncells) 
     return (unsigned)h & (unsigned)(ncells - 1);
 }
 
-// Row-major keys carry a 4 x 4 sub-cell index (Morton order) below the cell index: the cells stay
-// contiguous and x-ordered in a row (the stencil ranges are unchanged), and inside a cell the
-// sorted order walks the sub-cells, so consecutive sorted particles — the lists' clusters — are
-// close together: the union of a cluster's two neighbourhoods, i.e. its list, shrinks.
-#ifndef GS_CELL_SUBKEY          // sub-cell key bits (A/B builds: 0 = index order inside a cell)
-#define GS_CELL_SUBKEY 4
-#endif
 __device__ __forceinline__ unsigned cell_key(const GridParams& g, double x, double y) {
     if (g.hashed) return cell_hash(cell_coordf(x, g.x0, g.inv_h), cell_coordf(y, g.y0, g.inv_h), g.ncells);
     const int cx = cell_coord(x, g.x0, g.inv_h, g.nx), cy = cell_coord(y, g.y0, g.inv_h, g.ny);
-#if GS_CELL_SUBKEY
-    constexpr int kB = GS_CELL_SUBKEY / 2, kS = 1 << kB;  // bits / sub-cells per axis
     const double fx = (x - g.x0) * g.inv_h - (double)cx, fy = (y - g.y0) * g.inv_h - (double)cy;
-    const unsigned sx = (unsigned)min(max((int)(fx * kS), 0), kS - 1), sy = (unsigned)min(max((int)(fy * kS), 0), kS - 1);
-    unsigned sub = 0;
-#pragma unroll
-    for (int b = 0; b < kB; ++b) sub |= (((sx >> b) & 1u) << (2 * b)) | (((sy >> b) & 1u) << (2 * b + 1));
-    return ((unsigned)(cy * g.nx + cx) << GS_CELL_SUBKEY) | sub;
-#else
-    return (unsigned)(cy * g.nx + cx);
-#endif
+    return ((unsigned)(cy * g.nx + cx) << GS_CELL_SUBKEY) | cell_subkey(fx, fy);
 }
 
 // The candidate ranges of a target at (x, y): 3 contiguous stencil rows of the row-major grid,

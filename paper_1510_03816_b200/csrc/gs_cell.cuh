@@ -23,6 +23,28 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {  // 
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
+// Row-major cell keys carry a sub-cell index (Morton order over 2^(GS_CELL_SUBKEY/2) sub-cells per
+// axis) below the cell index: cells stay contiguous and x-ordered in a row (the stencil ranges are
+// unchanged), and inside a cell the sorted order walks the sub-cells, so consecutive sorted
+// particles — the lists' clusters — sit close together and a cluster's list (the union of its
+// members' neighbourhoods) shrinks (C4 RHS 1.96 -> 1.71 ms, C5 1.46 -> 1.36 ms).
+#ifndef GS_CELL_SUBKEY          // sub-cell key bits (A/B builds: 0 = index order inside a cell)
+#define GS_CELL_SUBKEY 4
+#endif
+// fx, fy: the position inside its cell in cell units (clamped to the sub-cell range)
+__device__ __forceinline__ unsigned cell_subkey(double fx, double fy) {
+#if GS_CELL_SUBKEY
+    constexpr int kB = GS_CELL_SUBKEY / 2, kS = 1 << kB;  // bits / sub-cells per axis
+    const unsigned sx = (unsigned)min(max((int)(fx * kS), 0), kS - 1), sy = (unsigned)min(max((int)(fy * kS), 0), kS - 1);
+    unsigned sub = 0;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) sub |= (((sx >> b) & 1u) << (2 * b)) | (((sy >> b) & 1u) << (2 * b + 1));
+    return sub;
+#else
+    return 0u;
+#endif
+}
+
 struct GridParams {
     double x0, y0, inv_h;
     double h, rc;        // cell edge; filter radius (double) = sqrt(rc2f) before fp32 rounding

@@ -118,7 +118,9 @@ __global__ void k_slab_own_keys(const double4* __restrict__ S, const unsigned* _
     const double4 v = S[i];
     const int cy = grid_cell(v.y, G.y0, G.inv_h, G.ny), cx = grid_cell(v.x, G.x0, G.inv_h, G.nx);
     GS_ASSERT(cy >= y_own0);
-    key[i] = ((unsigned long long)((int64_t)(cy - y_own0) * G.nx + cx) << gbits) | (unsigned long long)g[i];
+    const unsigned sub = cell_subkey((v.x - G.x0) * G.inv_h - (double)cx, (v.y - G.y0) * G.inv_h - (double)cy);
+    const unsigned long long cell = ((unsigned long long)((int64_t)(cy - y_own0) * G.nx + cx) << GS_CELL_SUBKEY) | sub;
+    key[i] = (cell << gbits) | (unsigned long long)g[i];
     val[i] = (unsigned)i;
 }
 
@@ -143,16 +145,17 @@ __global__ void k_slab_local_keys(const double4* __restrict__ S, int64_t n, cons
     const double4 v = S[k];
     const int cy = grid_cell(v.y, G.y0, G.inv_h, G.ny), cx = grid_cell(v.x, G.x0, G.inv_h, G.nx);
     GS_ASSERT(cy >= G.ylo && cy < G.yhi);
-    keys[k] = (unsigned)((cy - G.ylo) * G.nx + cx);
+    const unsigned sub = cell_subkey((v.x - G.x0) * G.inv_h - (double)cx, (v.y - G.y0) * G.inv_h - (double)cy);
+    keys[k] = ((unsigned)((cy - G.ylo) * G.nx + cx) << GS_CELL_SUBKEY) | sub;
     Sf[k] = make_float2((float)(v.x - G.x0), (float)(v.y - G.y0));
 }
 
-// start[c] = first local position with key >= c, c in [0, ncells]
+// start[c] = first local position with cell >= c, c in [0, ncells] (cell = key above the sub-cell bits)
 __global__ void k_slab_start(const unsigned* __restrict__ keys, int64_t n, int64_t ncells, int* start) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k > n) return;
-    const long long prev = (k == 0) ? -1 : (long long)keys[k - 1];
-    const long long cur = (k == n) ? ncells : (long long)keys[k];
+    const long long prev = (k == 0) ? -1 : (long long)(keys[k - 1] >> GS_CELL_SUBKEY);
+    const long long cur = (k == n) ? ncells : (long long)(keys[k] >> GS_CELL_SUBKEY);
     GS_ASSERT(cur >= prev && cur <= ncells);
     for (long long c = prev + 1; c <= cur; ++c) start[c] = (int)k;
 }
@@ -164,7 +167,7 @@ __global__ void k_slab_heads(const unsigned* __restrict__ keys, const int* __res
     if (k > n_own) return;
     if (k == n_own) { head[k] = 0; return; }
     const int64_t pos = own_begin + k;
-    const int row = (int)(keys[pos] / (unsigned)nx);
+    const int row = (int)((keys[pos] >> GS_CELL_SUBKEY) / (unsigned)nx);
     head[k] = ((pos - start[(int64_t)row * nx]) % 2) == 0 ? 1 : 0;
 }
 
@@ -367,7 +370,7 @@ int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_lo
     if (n) {
         const int gbits = bits_for(L.n_glob - 1 > 0 ? L.n_glob - 1 : 1);
         const int64_t cells = (int64_t)(y_own1 - y_own0) * L.g.nx;
-        const int end_bit = gbits + bits_for(cells);
+        const int end_bit = gbits + bits_for(cells) + GS_CELL_SUBKEY;
         if (end_bit > 64) return fail(GS_ERR_UNSUPPORTED, "slab sort key exceeds 64 bits");
         k_slab_own_keys<<<blk(n), 256, 0, s>>>(L.Su.ptr, L.gu.ptr, n, L.gp.ptr, y_own0, gbits, L.skey.ptr, L.sval.ptr);
         size_t bytes = 0;
