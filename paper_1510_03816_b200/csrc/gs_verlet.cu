@@ -471,6 +471,202 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__
     if (sub == 0) len[c] = padded;
 }
 
+// The same lists for kVQ consecutive clusters per warp (row-major grid): per stencil row the warp
+// sweeps the union of the clusters' ranges once, each candidate is tested against every member
+// (fp32) and appended to each cluster whose own range holds it and whose members it is near —
+// exactly the lists of k_verlet_fill (same candidates, same order), at a third of its loads,
+// ballots and loop overhead (consecutive clusters share most of their stencil).  The members'
+// x-ranges are computed one member per lane.  Hashed grids: the per-cluster loop.
+#ifndef GS_VERLET_FILL_Q        // clusters per warp in the grouped list build (A/B)
+#define GS_VERLET_FILL_Q 4
+#endif
+constexpr int kVQ = GS_VERLET_FILL_Q;
+constexpr int kVQM = kVQ * kVM;  // members per warp (<= 32)
+static_assert(kVQM <= 32, "one lane per member");
+
+__global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restrict__ Sf, const double4* __restrict__ Ss,
+                                                          const int* __restrict__ start,
+                                                          const GridParams* __restrict__ gp, int64_t n, int64_t ncl,
+                                                          int pad, const long long* __restrict__ ofs, int* len,
+                                                          int* list, int64_t cap, double2* Xb,
+                                                          const unsigned* __restrict__ perm, int* inv,
+                                                          unsigned long long* overflow, const int* __restrict__ cfirst,
+                                                          int64_t xb_base) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = ((int64_t)blockIdx.x * (kVBB / 32) + threadIdx.x / 32) * kVQ;
+    if (c0 >= ncl) return;  // warp-uniform
+    const GridParams g = *gp;
+    const int nq = (int)min((int64_t)kVQ, ncl - c0);
+    const bool ok = ofs[ncl] <= cap;
+    // lane t < kVQM: member t % kVM of cluster c0 + t / kVM
+    const int tq = lane / kVM, tm = lane % kVM;
+    bool mv = false;
+    double mx = 0.0, my = 0.0;
+    float fx = 0.0f, fy = 0.0f;
+    if (lane < kVQM && tq < nq) {
+        const int64_t c = c0 + tq;
+        const int64_t k = cluster_first(cfirst, c) + tm;
+        const int64_t end = cfirst ? (int64_t)cfirst[c + 1] : n;
+        if (k < end) {
+            mv = true;
+            const double4 v = Ss[k];
+            mx = v.x; my = v.y;
+            const float2 f = Sf[k];
+            fx = f.x; fy = f.y;
+            Xb[k - xb_base] = make_double2(mx, my);
+            if (inv) inv[perm[k]] = (int)k;  // original index -> sorted slot
+        }
+    }
+    if (!ok) {  // no list: the sweep reads nothing (the call is redone with a larger buffer)
+        if (lane < nq) {
+            atomicMax(overflow, (unsigned long long)ofs[ncl]);
+            len[c0 + lane] = 0;
+        }
+        return;
+    }
+    if (g.hashed) {  // flung-apart clouds: the per-cluster candidate walk of k_verlet_fill
+        for (int q = 0; q < nq; ++q) {
+            const int64_t c = c0 + q;
+            ClusterMembers cm;
+            load_members(Ss, Sf, n, c, cfirst, cm);
+            const int64_t obase = ofs[c];
+            int count = 0;
+            for_each_range(g, start, cm, [&](int a, int b) {
+                for (int base = a; base < b; base += 32) {
+                    const int pos = base + lane;
+                    bool acc = false;
+                    if (pos < b) {
+                        const float2 f = Sf[pos];
+                        float d2 = INFINITY;
+#pragma unroll
+                        for (int m = 0; m < kVM; ++m) {
+                            const float dx = cm.fx[m] - f.x, dy = cm.fy[m] - f.y;
+                            const float dm = fmaf(dx, dx, dy * dy);
+                            d2 = m < cm.nm ? fminf(d2, dm) : d2;
+                        }
+                        acc = !(d2 >= g.rc2f);
+                    }
+                    const unsigned bal = __ballot_sync(kFull, acc);
+                    if (acc) list[obase + count + __popc(bal & ((1u << lane) - 1))] = pos;
+                    count += __popc(bal);
+                }
+            });
+            const int padded = (count + pad - 1) / pad * pad;
+            for (int e = count + lane; e < padded; e += 32) list[obase + e] = (int)n;
+            if (lane == 0) len[c] = padded;
+        }
+        return;
+    }
+    // every lane holds every member's fp32 position (the filter) and validity
+    float qfx[kVQM], qfy[kVQM];
+    unsigned valid = __ballot_sync(kFull, mv);
+#pragma unroll
+    for (int t = 0; t < kVQM; ++t) {
+        qfx[t] = __shfl_sync(kFull, fx, t);
+        qfy[t] = __shfl_sync(kFull, fy, t);
+    }
+    long long obase[kVQ];
+    int count[kVQ];
+#pragma unroll
+    for (int q = 0; q < kVQ; ++q) {
+        obase[q] = q < nq ? ofs[c0 + q] : 0;
+        count[q] = 0;
+    }
+    const int sub = g.sub;
+    const int cy = mv ? vcell(my, g.y0, g.inv_h, g.ny) : 0;
+    int lo = __reduce_min_sync(kFull, mv ? cy : g.ny), hi = __reduce_max_sync(kFull, mv ? cy : -1);
+    const double rc2 = g.rc * g.rc;
+    const float rc2f = g.rc2f;
+    for (int yy = max(lo - sub, g.ylo); yy <= min(hi + sub, g.yhi - 1); ++yy) {
+        // this lane's member: its trimmed x-range of cells in row yy (as for_each_range)
+        int a = g.nx, b = -1;
+        if (mv && yy >= cy - sub && yy <= cy + sub) {
+            if (sub > 1) {
+                const double ylo = fma((double)yy, g.h, g.y0), yhi = ylo + g.h;
+                const double gap = fmax(0.0, fmax(ylo - my, my - yhi));
+                const double xr2 = fma(-gap, gap, rc2);
+                if (xr2 > 0.0) {
+                    const double xr = sqrt(xr2);
+                    a = vcell(mx - xr, g.x0, g.inv_h, g.nx);
+                    b = vcell(mx + xr, g.x0, g.inv_h, g.nx);
+                }
+            } else {
+                const int cx = vcell(mx, g.x0, g.inv_h, g.nx);
+                a = max(cx - 1, 0);
+                b = min(cx + 1, g.nx - 1);
+            }
+        }
+        const int r0 = (yy - g.ylo) * g.nx;
+        int pa[kVQ], pb[kVQ];
+        int A = 0x7fffffff, B = -1;
+#pragma unroll
+        for (int q = 0; q < kVQ; ++q) {
+            int xa = g.nx, xb = -1;
+#pragma unroll
+            for (int m = 0; m < kVM; ++m) {
+                xa = min(xa, __shfl_sync(kFull, a, q * kVM + m));
+                xb = max(xb, __shfl_sync(kFull, b, q * kVM + m));
+            }
+            pa[q] = 0; pb[q] = 0;
+            if (xb >= xa) {
+                pa[q] = start[r0 + xa];
+                pb[q] = start[r0 + xb + 1];
+                A = min(A, pa[q]);
+                B = max(B, pb[q]);
+            }
+        }
+        for (int base = A; base < B; base += 32) {
+            const int pos = base + lane;
+            float2 f = make_float2(0.0f, 0.0f);
+            if (pos < B) f = Sf[pos];
+#pragma unroll
+            for (int q = 0; q < kVQ; ++q) {
+                float d2 = INFINITY;
+#pragma unroll
+                for (int m = 0; m < kVM; ++m) {
+                    const int t = q * kVM + m;
+                    const float dx = qfx[t] - f.x, dy = qfy[t] - f.y;
+                    const float dm = fmaf(dx, dx, dy * dy);
+                    d2 = (valid >> t) & 1u ? fminf(d2, dm) : d2;
+                }
+                const bool acc = pos >= pa[q] && pos < pb[q] && !(d2 >= rc2f);  // NaN radius: keep
+                const unsigned bal = __ballot_sync(kFull, acc);
+                GS_ASSERT(!acc || (pos < n && obase[q] + count[q] + __popc(bal) <= ofs[c0 + q + 1]));
+                if (acc) list[obase[q] + count[q] + __popc(bal & ((1u << lane) - 1))] = pos;
+                count[q] += __popc(bal);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kVQ; ++q) {
+        if (q >= nq) break;
+        const int padded = (count[q] + pad - 1) / pad * pad;
+        GS_ASSERT(obase[q] + padded <= ofs[c0 + q + 1]);
+        for (int e = count[q] + lane; e < padded; e += 32) list[obase[q] + e] = (int)n;  // padding: sentinel
+        if (lane == 0) len[c0 + q] = padded;
+    }
+}
+
+#ifndef GS_VERLET_FILL_GRP   // A/B: 0 = one warp per cluster (k_verlet_fill)
+#define GS_VERLET_FILL_GRP 1
+#endif
+
+void launch_fill(const float2* Sf, const double4* Ss, const int* start, const GridParams* gp, int64_t n, int64_t ncl,
+                 int pad, const long long* ofs, int* len, int* list, int64_t cap, double2* Xb, const unsigned* perm,
+                 int* inv, unsigned long long* overflow, const int* cfirst, int64_t xb_base, cudaStream_t stream) {
+    if (ncl <= 0) return;
+#if GS_VERLET_FILL_GRP
+    const int64_t warps = (ncl + kVQ - 1) / kVQ;
+    const unsigned blocks = (unsigned)((warps * 32 + kVBB - 1) / kVBB);
+    k_verlet_fill_grp<<<blocks, kVBB, 0, stream>>>(Sf, Ss, start, gp, n, ncl, pad, ofs, len, list, cap, Xb, perm, inv,
+                                                   overflow, cfirst, xb_base);
+#else
+    const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
+    k_verlet_fill<<<blocks, kVBB, 0, stream>>>(Sf, Ss, start, gp, n, ncl, pad, ofs, len, list, cap, Xb, perm, inv,
+                                               overflow, cfirst, xb_base);
+#endif
+}
+
 // Gather of the stage records into sorted order + the rebuild trigger.  The last CTA decides:
 // rebuild if forced or any particle moved more than half the skin since the build; in a graph
 // it sets the IF node's condition, otherwise flags[3] (host-driven paths always rebuild).
@@ -547,9 +743,8 @@ int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n
     size_t bytes = v.scan_bytes;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(v.scan_temp, bytes, v.cnt, v.ofs, (int)(ncl + 1), stream);
     if (e != cudaSuccess) return (int)e;
-    const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
-    k_verlet_fill<<<blocks, kVBB, 0, stream>>>(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.ofs, v.len, v.list, v.cap,
-                                               v.Xb, w.perm, v.inv, v.overflow, nullptr, 0);
+    launch_fill(w.Sf, w.Ss, w.start, w.gp, n, ncl, pad, v.ofs, v.len, v.list, v.cap, v.Xb, w.perm, v.inv, v.overflow,
+                nullptr, 0, stream);
     return (int)cudaGetLastError();
 }
 
@@ -622,10 +817,8 @@ int slab_list_caps(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, cuda
 }
 
 void slab_list_fill(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, int64_t own_begin, cudaStream_t stream) {
-    if (ncl <= 0) return;
-    const unsigned blocks = (unsigned)((ncl * kTplB + kVBB - 1) / kVBB);
-    k_verlet_fill<<<blocks, kVBB, 0, stream>>>(L.Sf, L.S, L.start, L.gp, n_loc, ncl, 2 * tpl, L.ofs, L.len, L.list,
-                                               L.cap, L.Xb, nullptr, nullptr, L.overflow, L.cfirst, own_begin);
+    launch_fill(L.Sf, L.S, L.start, L.gp, n_loc, ncl, 2 * tpl, L.ofs, L.len, L.list, L.cap, L.Xb, nullptr, nullptr,
+                L.overflow, L.cfirst, own_begin, stream);
 }
 
 void slab_sweep(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
