@@ -140,3 +140,28 @@ def test_sharded_solver_takes_the_slab_path_in_an_nccl_world(cuda):
         gs.set_path("auto")
     assert calls, "the slab path was not taken"
     assert torch.equal(qT, ref_q) and torch.equal(pT, ref_p)
+
+
+def test_full_size_c5_slab_ranks_match_the_one_gpu_lists(cuda):
+    """C5 at full size (N = 2^20) on 8 slab ranks (one GPU, LocalComm) at the configured gain: one RK4
+    step equals the one-GPU cluster-list evolve to rounding (the C oracle pins that one,
+    tests/test_gpu_fullsize.py), and every rank holds a balanced share."""
+    torch = cuda
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs, device
+
+    w = configs.c5()
+    p = np.ascontiguousarray(w.h * (w.target - w.q))
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    q_d, p_d = torch.from_numpy(w.q).cuda(), torch.from_numpy(p).cuda()
+    s = _solver(torch, spec, 8)
+    qT, pT = s.evolve(q_d, p_d, w.t_final / w.steps, 1)
+    device.set_path("cell")
+    try:
+        q1, p1, _ = device.evolve(spec, q_d, p_d, w.t_final / w.steps, 1)
+    finally:
+        device.set_path("auto")
+    assert float((qT - q1).abs().max() / q1.abs().max()) <= 1e-13
+    assert float((pT - p1).abs().max() / p1.abs().max()) <= 1e-11
+    own = [r.n_own for r in s.plan.rows]
+    assert sum(own) == w.n and max(own) <= 1.05 * w.n / 8
