@@ -137,8 +137,8 @@ __global__ void k_gram(const double* __restrict__ q, int64_t n, double k1, doubl
     const double dx = q[2 * i] - q[2 * j], dy = q[2 * i + 1] - q[2 * j + 1];
     const double r2 = fma(dx, dx, fma(dy, dy, kTinyR2));
     double g;
-    if (FAM == kFamConical) g = exp2_tbl((r2 * rsqrt_refined(r2)) * k1, tbl);
-    else g = exp2_tbl(r2 * k1, tbl);
+    if (FAM == kFamConical) g = exp2_tbl(r2 * rsqrt_refined(r2), k1, tbl);
+    else g = exp2_tbl(r2, k1, tbl);
     K[i * n + j] = g * scale;
     if (i != j && __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) == 0.0)
         atomicMin(bad, (unsigned long long)(i * n + j));

@@ -89,7 +89,7 @@ __device__ __forceinline__ double rsqrt_refined(double x) {
     return fma(ye, t, y0);
 }
 
-// 2^(y / kTbl) for y <= 0 (y = -r/alpha * kTbl/ln2); 0 below 2^-1020.
+// 2^(y / kTbl) for y = x k <= 0 (x = r, k = -kTbl/(alpha ln2)); 0 below 2^-1020.
 // Rounding trick with a biased magic 1.5*2^52 + 2^30: for y in [-2^30, 0] the high word of
 // s = y + magic is exactly kMagicHi and its low word is rint(y) + 2^30, so one integer
 // compare on each word rejects both the underflow range and far-away pairs (|y| > 2^30,
@@ -103,10 +103,13 @@ constexpr int kMagicHi = 0x43380000;
 // vanishes mod 2^32).  (Zeroing only the high word on the out-of-range side was tried: for the
 // far padding records u = y - kd is huge and the polynomial overflows to inf, inf * 0 = NaN.)
 constexpr unsigned kLoMin = (1u << 30) + (unsigned)kKMin;  // lo(s) >= kLoMin <=> k >= kKMin
-__device__ __forceinline__ double exp2_tbl_fast(double y, unsigned tb) {
-    const double s = y + gs_cb[kCbMagicK];
+// The argument is y = x k, never rounded on its own: the exact product enters the magic-constant
+// rounding and the reduced argument u = x k - rint(x k) through fused multiply-adds (what nvcc's
+// contraction made of the y + M / y - kd form anyway; written out so the rounding is explicit).
+__device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb) {
+    const double s = fma(x, k, gs_cb[kCbMagicK]);
     const double kd = s - gs_cb[kCbMagicK];
-    const double u = y - kd;
+    const double u = fma(x, k, -kd);
     const unsigned lo = (unsigned)__double2loint(s), hi = (unsigned)__double2hiint(s);
     // the integer side in PTX, so that ptxas keeps the two-instruction forms: table address
     // (and + mad), exponent ((lo >> 6) << 20 added to the table value's high word: shr + mad),
@@ -132,8 +135,8 @@ static_assert(kTblRep * 8 == 128, "lane copies interleave in 128-byte rows (exp2
 
 // The table exp every kernel calls: `tbl` is the lane's copy in shared memory (lane_table); its
 // 32-bit shared address is loop-invariant and hoisted out of the hot loops.
-__device__ __forceinline__ double exp2_tbl(double y, const double* __restrict__ tbl) {
-    return exp2_tbl_fast(y, (unsigned)__cvta_generic_to_shared(tbl));
+__device__ __forceinline__ double exp2_tbl(double x, double k, const double* __restrict__ tbl) {
+    return exp2_tbl_fast(x, k, (unsigned)__cvta_generic_to_shared(tbl));
 }
 
 // 32-bit shared address of this lane's table copy (exp2_tbl_fast).
@@ -163,10 +166,10 @@ __device__ __forceinline__ void pair_core(double dx, double dy, double pdot, con
     z = ((__double2hiint(r2) ^ __double2hiint(kTinyR2)) | (__double2loint(r2) ^ __double2loint(kTinyR2))) == 0;
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
-        g = exp2_tbl((r2 * rs) * k1, tbl);
+        g = exp2_tbl(r2 * rs, k1, tbl);
         c = (pdot * g) * rs;
     } else {
-        g = exp2_tbl(r2 * k1, tbl);
+        g = exp2_tbl(r2, k1, tbl);
         c = pdot * g;
     }
 }
@@ -182,10 +185,10 @@ __device__ __forceinline__ void pair_core_hi(double dx, double dy, double pdot, 
     r2hi = __double2hiint(r2);
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
-        g = exp2_tbl_fast((r2 * rs) * k1, tb);
+        g = exp2_tbl_fast(r2 * rs, k1, tb);
         c = (pdot * g) * rs;
     } else {
-        g = exp2_tbl_fast(r2 * k1, tb);
+        g = exp2_tbl_fast(r2, k1, tb);
         c = pdot * g;
     }
 }
@@ -209,11 +212,11 @@ __device__ __forceinline__ bool pair_accum(double xi, double yi, double pxi, dou
         double r2s = z ? 1.0 : r2;
         double rs = rsqrt_refined(r2s);
         double r = r2s * rs;
-        g = exp2_tbl(r * k1, tbl);
+        g = exp2_tbl(r, k1, tbl);
         g = z ? 1.0 : g;
         c = (pdot * g) * rs;
     } else {
-        g = exp2_tbl(r2 * k1, tbl);   // exactly 1 at r2 == 0
+        g = exp2_tbl(r2, k1, tbl);   // exactly 1 at r2 == 0
         c = pdot * g;
     }
     c = z ? 0.0 : c;
@@ -242,11 +245,11 @@ __device__ __forceinline__ bool pair_sym(double xi, double yi, double pxi, doubl
         double r2s = z ? 1.0 : r2;
         double rs = rsqrt_refined(r2s);
         double r = r2s * rs;
-        g = exp2_tbl(r * k1, tbl);
+        g = exp2_tbl(r, k1, tbl);
         g = z ? 1.0 : g;
         c = (pdot * g) * rs;
     } else {
-        g = exp2_tbl(r2 * k1, tbl);
+        g = exp2_tbl(r2, k1, tbl);
         c = pdot * g;
     }
     c = z ? 0.0 : c;

@@ -66,8 +66,8 @@ struct Acc {
 };
 
 // exp2_tbl with an extra acceptance predicate (the cutoff mask, GS_VERLET_NOMASK=0): G = 0 outside.
-__device__ __forceinline__ double exp2_tbl_in(double y, unsigned tb, bool in) {
-    const double g = exp2_tbl_fast(y, tb);
+__device__ __forceinline__ double exp2_tbl_in(double x, double k, unsigned tb, bool in) {
+    const double g = exp2_tbl_fast(x, k, tb);
     return in ? g : 0.0;
 }
 
@@ -76,11 +76,11 @@ __device__ __forceinline__ double exp2_tbl_in(double y, unsigned tb, bool in) {
 // nz counts pairs whose d^2 has the high word of the 1e-200 offset (d == 0: the self pair and any
 // coincident particle; a superset, the rare re-scan decides exactly).
 template <int FAM>
-__device__ __forceinline__ double vexp(double y, unsigned tb, bool in) {
+__device__ __forceinline__ double vexp(double x, double k, unsigned tb, bool in) {
 #if GS_VERLET_NOMASK
-    return exp2_tbl_fast(y, tb);  // `in` only counts pairs here
+    return exp2_tbl_fast(x, k, tb);  // `in` only counts pairs here
 #else
-    return exp2_tbl_in(y, tb, in);
+    return exp2_tbl_in(x, k, tb, in);
 #endif
 }
 
@@ -101,10 +101,10 @@ __device__ __forceinline__ void vbody(const double4& me, const double4& s, const
     double g, c;
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
-        g = vexp<FAM>((r2 * rs) * k1, tb, in);
+        g = vexp<FAM>(r2 * rs, k1, tb, in);
         c = (pdot * g) * rs;
     } else {
-        g = vexp<FAM>(r2 * k1, tb, in);
+        g = vexp<FAM>(r2, k1, tb, in);
         c = pdot * g;
     }
     a.qx = fma(g, s.z, a.qx);
