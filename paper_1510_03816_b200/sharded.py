@@ -231,6 +231,12 @@ class ShardedSolver:
         self._p2p_key = None
         # cell path across ranks: slab decomposition (GS_B200_SLAB=0: all-gather of every record)
         self.slab = os.environ.get("GS_B200_SLAB", "1") != "0"
+        # dense split over NCCL: the whole evolve (pair share, reduce-scatter, finish, all-gather per
+        # stage) captured once as a CUDA graph and replayed (GS_B200_SHARDED_GRAPHS=0: host loop)
+        self.graphs = os.environ.get("GS_B200_SHARDED_GRAPHS", "1") != "0"
+        self._graph = None
+        self._graph_key = None
+        self._bufs = {}
 
     # -- collectives (plumbing) -------------------------------------------------------------
     def _allgather_rows(self, S, r0: int, c: int):
@@ -303,22 +309,61 @@ class ShardedSolver:
             sym = total > 0
         if sym:
             b, e = self.rank * total // W, (self.rank + 1) * total // W
-            R = self.backend.new_partials(c * W)
-            R_rows = self.backend.new_partials(c)
+            R, R_rows = self._partials(c)
             if self.p2p and self._p2p_ready(q, p, n, c, r0, r1, b, e, S, R, R_rows, dt):
                 return self._evolve_p2p(q, p, t_final, steps, n, c, b, e, S, r0, r1)
-        for step in range(1, steps + 1):
-            for s in range(4):
-                with _nvtx(f"stage {step}.{s}"):
-                    if sym:
-                        self.backend.pairs_sym(step, s, b, e, R)
-                        self._reduce_scatter_rows(R_rows, R, c)
-                        self.backend.finish(step, s, dt, R_rows)
-                    else:
-                        self.backend.run(step, s, dt)
-                    self._allgather_rows(S, r0, c)
+        def stage(step, s):
+            with _nvtx(f"stage {step}.{s}"):
+                if sym:
+                    self.backend.pairs_sym(step, s, b, e, R)
+                    self._reduce_scatter_rows(R_rows, R, c)
+                    self.backend.finish(step, s, dt, R_rows)
+                else:
+                    self.backend.run(step, s, dt)
+                self._allgather_rows(S, r0, c)
+
+        if sym and self._graphable():
+            key = (n, c, steps, dt, b, e, int(S.data_ptr()), int(R.data_ptr()), int(R_rows.data_ptr()))
+            if self._graph_key != key:
+                torch = _torch_of(self.backend)
+                # outside the capture: the first stage builds the slot lists and workspaces and
+                # initialises the NCCL communicator; then the state is rewound
+                stage(1, 0)
+                torch.cuda.synchronize()
+                self.backend.begin(q, p, r0, r1)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for step in range(1, steps + 1):
+                        for s in range(4):
+                            stage(step, s)
+                self._graph, self._graph_key = g, key
+            self._graph.replay()
+        else:
+            for step in range(1, steps + 1):
+                for s in range(4):
+                    stage(step, s)
         self._raise_first_failure(t_final, steps)
         return S[:n, 0:2].clone(), S[:n, 2:4].clone()
+
+    def _partials(self, c: int):
+        """The split's raw row sums (all rows) and this rank's reduced rows, kept across evolves
+        (a captured graph bakes their addresses in)."""
+        key = ("partials", c, self.world)
+        if key not in self._bufs:
+            self._bufs[key] = (self.backend.new_partials(c * self.world), self.backend.new_partials(c))
+        return self._bufs[key]
+
+    def _graphable(self) -> bool:
+        """The dense split's stage loop can be captured: the device backend over NCCL (or a world of
+        one), torch CUDA graphs available."""
+        if not self.graphs or not isinstance(self.backend, DeviceStageBackend):
+            return False
+        if self.world > 1 or self.split:
+            try:
+                return self.dist.get_backend(self.group) == "nccl"
+            except Exception:
+                return False
+        return True
 
     def _agree(self, ok: bool) -> bool:
         """All ranks' verdict (MIN over ranks)."""

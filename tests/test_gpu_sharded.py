@@ -309,3 +309,31 @@ def test_cell_rows_of_a_rank_equal_the_full_cell_rhs(cuda):
         gs.set_path("auto")
     np.testing.assert_array_equal(np.concatenate([a.cpu().numpy() for a, _ in parts]), dq.cpu().numpy())
     np.testing.assert_array_equal(np.concatenate([b.cpu().numpy() for _, b in parts]), dp.cpu().numpy())
+
+
+def test_sharded_dense_evolve_is_one_graph_replay(cuda, monkeypatch):
+    """The dense split's stage loop (pair share, NCCL reduce-scatter, finish, NCCL all-gather) is
+    captured once per configuration and replayed: bitwise the host-driven loop, the second evolve
+    reuses the graph, and a coincidence inside the replayed stages is still raised."""
+    import torch
+
+    from paper_1510_03816_b200 import sharded
+
+    _nccl_world1()
+    gs, q, p, spec = _setup(n=5000)
+    host = sharded.ShardedSolver(spec, force_split=True)
+    host.graphs = False
+    qh, ph = host.evolve(q, p, 1.0, 4)
+    solver = sharded.ShardedSolver(spec, force_split=True)
+    qg, pg = solver.evolve(q, p, 1.0, 4)
+    assert solver._graph is not None
+    assert torch.equal(qg, qh) and torch.equal(pg, ph)
+    g0 = solver._graph
+    q2, p2 = solver.evolve(q, p, 1.0, 4)
+    assert solver._graph is g0 and torch.equal(q2, qh)
+    qc = q.copy()
+    qc[7] = qc[3]
+    with pytest.raises(gs.DegenerateConfigurationError, match="particles 3 and 7 coincide"):
+        solver.evolve(qc, p, 1.0, 4)
+    q3, _ = solver.evolve(q, p, 1.0, 4)  # the status is reset by the next evolve
+    assert torch.equal(q3, qh)
