@@ -165,3 +165,37 @@ def test_full_size_c5_slab_ranks_match_the_one_gpu_lists(cuda):
     assert float((pT - p1).abs().max() / p1.abs().max()) <= 1e-11
     own = [r.n_own for r in s.plan.rows]
     assert sum(own) == w.n and max(own) <= 1.05 * w.n / 8
+
+
+def test_hashed_grid_falls_back_to_the_all_gather_path(cuda):
+    """A cloud that needs the hashed grid (a far outlier: the row-major grid would exceed the cell
+    cap) has no row slabs: ShardedSolver's cell path falls back to own rows + all-gather, and the
+    result is the one-GPU cell path's."""
+    torch = cuda
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import device, sharded
+
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    w, p = _workload(20000, 0.01)
+    q = w.q.copy()
+    q[123] = (3.0e3, -2.0e3)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    gs.set_path("cell")
+    try:
+        solver = sharded.ShardedSolver(spec, force_split=True)
+        qT, pT = solver.evolve(q, p, 0.1, 2)
+        q1, p1, _ = device.evolve(spec, q, p, 0.1, 2)
+    finally:
+        gs.set_path("auto")
+    assert solver.slab is False  # took the fallback
+    assert float((qT - q1).abs().max() / q1.abs().max()) <= 1e-13
