@@ -557,21 +557,19 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
         }
         return;
     }
-    // every lane holds every member's fp32 position (the filter) and validity
+    // every lane holds every member's fp32 position (the filter); a missing member sits at 3e38,
+    // whose squared distance overflows to +inf and never passes (with the filter off — a NaN radius
+    // — acceptance only follows the cluster's own ranges, which skip missing members)
     float qfx[kVQM], qfy[kVQM];
-    unsigned valid = __ballot_sync(kFull, mv);
 #pragma unroll
     for (int t = 0; t < kVQM; ++t) {
-        qfx[t] = __shfl_sync(kFull, fx, t);
-        qfy[t] = __shfl_sync(kFull, fy, t);
+        qfx[t] = __shfl_sync(kFull, mv ? fx : 3e38f, t);
+        qfy[t] = __shfl_sync(kFull, mv ? fy : 3e38f, t);
     }
-    long long obase[kVQ];
-    int count[kVQ];
+    int wpos[kVQ];  // each cluster's next list slot (32-bit: a build never exceeds 2^31 entries)
 #pragma unroll
-    for (int q = 0; q < kVQ; ++q) {
-        obase[q] = q < nq ? ofs[c0 + q] : 0;
-        count[q] = 0;
-    }
+    for (int q = 0; q < kVQ; ++q) wpos[q] = q < nq ? (int)ofs[c0 + q] : 0;
+    const unsigned lt = (1u << lane) - 1u;  // lanes below this one
     const int sub = g.sub;
     const int cy = mv ? vcell(my, g.y0, g.inv_h, g.ny) : 0;
     int lo = __reduce_min_sync(kFull, mv ? cy : g.ny), hi = __reduce_max_sync(kFull, mv ? cy : -1);
@@ -626,23 +624,24 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
                 for (int m = 0; m < kVM; ++m) {
                     const int t = q * kVM + m;
                     const float dx = qfx[t] - f.x, dy = qfy[t] - f.y;
-                    const float dm = fmaf(dx, dx, dy * dy);
-                    d2 = (valid >> t) & 1u ? fminf(d2, dm) : d2;
+                    d2 = fminf(d2, fmaf(dx, dx, dy * dy));
                 }
-                const bool acc = pos >= pa[q] && pos < pb[q] && !(d2 >= rc2f);  // NaN radius: keep
+                const bool acc = (pos >= pa[q]) & (pos < pb[q]) & !(d2 >= rc2f);  // NaN radius: keep
                 const unsigned bal = __ballot_sync(kFull, acc);
-                GS_ASSERT(!acc || (pos < n && obase[q] + count[q] + __popc(bal) <= ofs[c0 + q + 1]));
-                if (acc) list[obase[q] + count[q] + __popc(bal & ((1u << lane) - 1))] = pos;
-                count[q] += __popc(bal);
+                GS_ASSERT(!acc || (pos < n && wpos[q] + __popc(bal) <= ofs[c0 + q + 1]));
+                const int at = wpos[q] + __popc(bal & lt);
+                if (acc) list[at] = pos;
+                wpos[q] += __popc(bal);
             }
         }
     }
 #pragma unroll
     for (int q = 0; q < kVQ; ++q) {
         if (q >= nq) break;
-        const int padded = (count[q] + pad - 1) / pad * pad;
-        GS_ASSERT(obase[q] + padded <= ofs[c0 + q + 1]);
-        for (int e = count[q] + lane; e < padded; e += 32) list[obase[q] + e] = (int)n;  // padding: sentinel
+        const int base = (int)ofs[c0 + q], count = wpos[q] - base;
+        const int padded = (count + pad - 1) / pad * pad;
+        GS_ASSERT(base + padded <= ofs[c0 + q + 1]);
+        for (int e = count + lane; e < padded; e += 32) list[base + e] = (int)n;  // padding: sentinel
         if (lane == 0) len[c0 + q] = padded;
     }
 }
