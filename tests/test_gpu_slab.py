@@ -199,3 +199,28 @@ def test_hashed_grid_falls_back_to_the_all_gather_path(cuda):
         gs.set_path("auto")
     assert solver.slab is False  # took the fallback
     assert float((qT - q1).abs().max() / q1.abs().max()) <= 1e-13
+
+
+def test_slab_gaussian_family(cuda):
+    """The gaussian family through the slab path (support radius alpha sqrt(2 Lambda)): W = 3 ranks
+    bitwise W = 1, and the one-GPU cluster-list evolve to rounding."""
+    torch = cuda
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import device
+
+    rng = np.random.default_rng(12)
+    n = 30000
+    q = rng.uniform(0, 1, (n, 2))
+    p = rng.normal(0, 1e-3, (n, 2))  # a gentle flow: particles move less than alpha (no chaotic amplification)
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(family="gaussian", alpha=0.002), sigma2=0.05)
+    q_d, p_d = torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()
+    q1s, p1s = _solver(torch, spec, 1).evolve(q_d, p_d, 0.2, 3)
+    q3s, p3s = _solver(torch, spec, 3).evolve(q_d, p_d, 0.2, 3)
+    assert torch.equal(q1s, q3s) and torch.equal(p1s, p3s)
+    device.set_path("cell")
+    try:
+        q1, p1, _ = device.evolve(spec, q_d, p_d, 0.2, 3)
+    finally:
+        device.set_path("auto")
+    assert float((q1s - q1).abs().max() / q1.abs().max()) <= 1e-13
+    assert float((p1s - p1).abs().max() / p1.abs().max()) <= 1e-11
