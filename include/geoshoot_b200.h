@@ -318,9 +318,12 @@ int gs_cell_stats(gs_context* ctx, int64_t* builds, int64_t* entries, void* stre
  *   gs_slab_lists  : cell starts, own clusters (pairs restarting at every cell row: ncl = sum
  *                    over the own rows of ceil(count / 2)) and their lists over the local
  *                    particles; synchronises once (list capacity)
- * per RK4 stage: gs_slab_stage (sweep + epilogue of the own rows, rebuild flag = some own
- * particle moved more than skin * cutoff / 2 since the build, *flag of gs_slab_views) -> the
- * halo slices of S -> MAX all-reduce of the flags: rebuild before the next stage.
+ * per RK4 stage: gs_slab_stage (the list sweep with the RK4 stage epilogue of the own rows fused
+ * in; rebuild flag = some own particle moved more than skin * cutoff / 2 since the build, *flag of
+ * gs_slab_views) -> the halo slices of S -> MAX all-reduce of the flags: rebuild before the next
+ * stage.  The local records ping-pong between two buffers: a stage reads the current one (S of
+ * gs_slab_views after the layout) and writes the own rows' next records into the other (S_alt),
+ * which is current for the next stage — the halo slices go there.
  * Rows are bitwise independent of the number of ranks.  gs_slab_begin sets the own particles
  * (q, p: device (n_own, 2); gidx: device int32 global indices) and resets the status;
  * gs_slab_status decodes it with global indices (synchronises). */
@@ -337,7 +340,7 @@ int gs_slab_pack(gs_context* ctx, const int32_t* owner, int32_t world, double* s
 int gs_slab_unpack(gs_context* ctx, int64_t n_own, const double* recv, void* stream);
 int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_loc0, int32_t y_loc1, int64_t own_begin,
                    int64_t n_loc, void* stream);
-int gs_slab_views(gs_context* ctx, double** S, int32_t** gidx, int32_t** flag);
+int gs_slab_views(gs_context* ctx, double** S, double** S_alt, int32_t** gidx, int32_t** flag);
 int gs_slab_lists(gs_context* ctx, int64_t ncl, void* stream);
 int gs_slab_stage(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t stage, double dt, void* stream);
 int gs_slab_status(gs_context* ctx, gs_status_t* status, void* stream);

@@ -155,7 +155,7 @@ def load(path: str = LIB_PATH):
             "gs_slab_unpack": ([_vp, _i64, _dp, _vp], ctypes.c_int),
             "gs_slab_layout": ([_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i64, _i64, _vp],
                                ctypes.c_int),
-            "gs_slab_views": ([_vp, P(_vp), P(_vp), P(_vp)], ctypes.c_int),
+            "gs_slab_views": ([_vp, P(_vp), P(_vp), P(_vp), P(_vp)], ctypes.c_int),
             "gs_slab_lists": ([_vp, _i64, _vp], ctypes.c_int),
             "gs_slab_stage": ([_vp, P(System), ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _vp], ctypes.c_int),
             "gs_slab_status": ([_vp, P(Status), _vp], ctypes.c_int),

@@ -583,6 +583,7 @@ void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cuda
             const VerletFuse f = verlet_fuse(ctx, sc, stream);
             e.Ss_next = parity ? ctx->c_Ss.ptr : ctx->c_Ss2.ptr;
             e.Xb = f.Xb; e.thr2 = f.thr2; e.flags = f.flags; e.cond = f.cond; e.use_cond = f.use_cond;
+            e.decide = 1;
         }
         verlet_sweep(ctx, sc, w, ev, e, stream);
         return;
@@ -893,7 +894,7 @@ int gs_destroy(gs_context* ctx) {
     ctx->sym_counts.release();
     {
         auto& L = ctx->slab;
-        L.S.release(); L.gidx.release(); L.B.release(); L.A.release(); L.part.release(); L.Xb.release();
+        L.S.release(); L.S2.release(); L.gidx.release(); L.B.release(); L.A.release(); L.Xb.release();
         L.Su.release(); L.Bu.release(); L.Au.release(); L.gu.release(); L.skey.release(); L.skey2.release();
         L.sval.release(); L.sval2.release(); L.cub.release(); L.keys.release(); L.start.release();
         L.cfirst.release(); L.head.release(); L.len.release(); L.list.release(); L.Sf.release(); L.gp.release();

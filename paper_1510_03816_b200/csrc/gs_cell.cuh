@@ -114,12 +114,15 @@ struct VerletWs {
 struct VerletEpi {
     FinishArgs a;                  // S, B, A, stage, dt, st, event (= the sweep's event + 1)
     double scale_q, scale_p, sigma2;
-    double4* Ss_next;
-    const double2* Xb;
+    double4* Ss_next;              // the next stage's sorted copy (nullptr: none)
+    const double2* Xb;             // positions at the build (nullptr: no rebuild check, last stage)
     double thr2;
     unsigned* flags;               // [0] rebuild wanted, [2] CTA counter, [3] decision
     cudaGraphConditionalHandle cond;
     int use_cond;
+    int decide;                    // 1: the last CTA decides (flags[3] / IF condition); 0: OR into flags[0]
+    int local;                     // rows of S / B / A / Xb by sorted position k - rbase (the slab
+    int64_t rbase;                 // layout) instead of by original index (single GPU)
 };
 int64_t verlet_clusters(int64_t n);
 int verlet_tpl(int64_t n);
@@ -168,5 +171,10 @@ void slab_list_fill(const SlabLists& L, int64_t n_loc, int64_t ncl, int tpl, int
 void slab_sweep(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
                 int64_t own_begin, int64_t n_glob, double4* part, DevStatus* st, unsigned long long event,
                 const double* tbl_dev, unsigned long long* accepted, cudaStream_t stream);
+// The same sweep with the RK4 stage epilogue fused in (e.local: rows by local position), reading
+// L.S and writing the new own records through e.a.S (the other half of the slab's ping-pong pair).
+void slab_sweep_epi(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
+                    int64_t n_glob, const VerletEpi& e, DevStatus* st, unsigned long long event, const double* tbl_dev,
+                    cudaStream_t stream);
 
 }  // namespace gsb

@@ -161,9 +161,10 @@ struct gs_context {
         int own_sorted = 0;                 // own particles live in the local layout (else in the *_u arrays)
         GridParams g{};                     // host copy of the last grid
         int y_own0 = 0, y_own1 = 0, y_loc0 = 0, y_loc1 = 0;
-        DevBuf<double4> S;                  // n_loc + 1 local records (S[n_loc]: sentinel far record)
+        DevBuf<double4> S, S2;              // n_loc + 1 local records (S[n_loc]: sentinel far record), ping-pong:
+        int par = 0;                        // the stage reads buffer `par` and writes its own rows into the other
         DevBuf<unsigned> gidx;              // n_loc: global index of each local particle
-        DevBuf<double4> B, A, part;         // own particles, local sorted order
+        DevBuf<double4> B, A;               // own particles, local sorted order
         DevBuf<double2> Xb;                 // own particles: positions at the last build
         DevBuf<double4> Su, Bu, Au;         // own particles in arrival order (begin / after a migration)
         DevBuf<unsigned> gu;

@@ -351,38 +351,6 @@ void launch_finish_verlet(const SysConst& sc, const FinishArgs& a, const VerletF
     k_finish_verlet<<<(unsigned)((a.nrows + 255) / 256), 256, 0, stream>>>(sc, a, f);
 }
 
-// Slab path (gs_slab.cu): the stage epilogue of a rank's own rows, already in local sorted order
-// (one raw-sum record per row, one thread per row); "rebuild wanted" -> *flag (one atomic per warp
-// that saw a particle move more than half the skin; the host clears it before every stage).
-__global__ void __launch_bounds__(256) k_finish_slab(SysConst sc, FinishArgs a, const double2* __restrict__ Xb,
-                                                     double thr2, unsigned* flag) {
-    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool need = false;
-    if (li < a.nrows && !(*((volatile unsigned long long*)&a.st->first_event) < a.event)) {
-        const double4 v = a.part[li];
-        const double4 sum = make_double4(0.0 + v.x, 0.0 + v.y, 0.0 + v.z, 0.0 + v.w);  // as finish_reduce
-        const double4 me = a.S[li];
-        double dqx = sum.x * sc.scale_q, dqy = sum.y * sc.scale_q;
-        if (sc.sigma2 != 0.0) {
-            dqx = __dadd_rn(dqx, __dmul_rn(sc.sigma2, me.z));
-            dqy = __dadd_rn(dqy, __dmul_rn(sc.sigma2, me.w));
-        }
-        const double4 nxt = stage_update(a, li, dqx, dqy, sum.z * sc.scale_p, sum.w * sc.scale_p);
-        a.S[li] = nxt;
-        if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(a.st, a.event, kNoEvent);
-        const double2 b = Xb[li];
-        const double dx = nxt.x - b.x, dy = nxt.y - b.y;
-        need = fma(dx, dx, dy * dy) > thr2;
-    }
-    if (__any_sync(0xffffffffu, need) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
-}
-
-void launch_finish_slab(const SysConst& sc, const FinishArgs& a, const double2* Xb, double thr2, unsigned* flag,
-                        cudaStream_t stream) {
-    if (a.nrows <= 0) return;
-    k_finish_slab<<<(unsigned)((a.nrows + 255) / 256), 256, 0, stream>>>(sc, a, Xb, thr2, flag);
-}
-
 // R[i] = the same fixed-order slot sum k_finish forms (multi-GPU symmetric split: the rank's
 // raw row sums before the reduce-scatter), so 1-GPU and N-GPU runs agree bitwise.
 __global__ void __launch_bounds__(kFinRows * kFinGroups) k_slot_reduce(FinishArgs a, double4* R) {

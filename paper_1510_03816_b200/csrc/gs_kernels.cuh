@@ -194,10 +194,6 @@ struct VerletFuse {
     int use_cond;
 };
 void launch_finish_verlet(const SysConst& sc, const FinishArgs& a, const VerletFuse& f, cudaStream_t stream);
-// Stage epilogue of the slab path (gs_slab.cu): rows [0, nrows) of a.S / a.B / a.A / a.part in the
-// rank's local order; *flag |= 1 when a particle moved farther than sqrt(thr2) from Xb.
-void launch_finish_slab(const SysConst& sc, const FinishArgs& a, const double2* Xb, double thr2, unsigned* flag,
-                        cudaStream_t stream);
 // Stage epilogue of rows [row0, row0 + nrows) from the raw row sums of all `world` ranks
 // (Rp[w], full length, summed in rank order), storing each new stage record into Sp[w] of
 // every rank (peer memory).

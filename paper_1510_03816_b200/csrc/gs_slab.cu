@@ -180,8 +180,9 @@ __global__ void k_slab_cfirst(const int* __restrict__ head, const int* __restric
     else if (head[k]) cfirst[cid[k]] = (int)(own_begin + k);
 }
 
-__global__ void k_slab_sentinel(double4* S, int64_t n_loc, long long* cnt, int64_t ncl) {
+__global__ void k_slab_sentinel(double4* S, double4* S2, int64_t n_loc, long long* cnt, int64_t ncl) {
     S[n_loc] = far_record(0);
+    S2[n_loc] = far_record(0);
     cnt[ncl] = 0;
 }
 
@@ -198,10 +199,12 @@ int bits_for(int64_t v) {  // smallest b with 2^b > v
     return b;
 }
 
+double4* slab_cur(gs_context* ctx) { return ctx->slab.par ? ctx->slab.S2.ptr : ctx->slab.S.ptr; }
+
 SlabLists slab_lists(gs_context* ctx) {
     auto& L = ctx->slab;
     SlabLists s;
-    s.S = L.S.ptr; s.Sf = L.Sf.ptr; s.start = L.start.ptr; s.gp = L.gp.ptr; s.cfirst = L.cfirst.ptr;
+    s.S = slab_cur(ctx); s.Sf = L.Sf.ptr; s.start = L.start.ptr; s.gp = L.gp.ptr; s.cfirst = L.cfirst.ptr;
     s.cnt = L.cnt.ptr; s.ofs = L.ofs.ptr; s.len = L.len.ptr; s.list = L.list.ptr; s.cap = (int64_t)L.list.cap;
     s.Xb = L.Xb.ptr; s.overflow = L.over.ptr; s.scan_temp = L.cub.ptr; s.scan_bytes = L.cub.cap;
     return s;
@@ -214,7 +217,7 @@ struct Own {
 };
 Own own_arrays(gs_context* ctx) {
     auto& L = ctx->slab;
-    if (L.own_sorted) return Own{L.S.ptr + L.own_begin, L.B.ptr, L.A.ptr, L.gidx.ptr + L.own_begin};
+    if (L.own_sorted) return Own{slab_cur(ctx) + L.own_begin, L.B.ptr, L.A.ptr, L.gidx.ptr + L.own_begin};
     return Own{L.Su.ptr, L.Bu.ptr, L.Au.ptr, L.gu.ptr};
 }
 
@@ -360,9 +363,10 @@ int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_lo
     L.own_begin = own_begin;
     L.n_loc = n_loc;
     const int64_t n = L.n_own;
-    GS_CUDA(L.S.ensure(n_loc + 1)); GS_CUDA(L.gidx.ensure(std::max<int64_t>(n_loc, 1)));
+    GS_CUDA(L.S.ensure(n_loc + 1)); GS_CUDA(L.S2.ensure(n_loc + 1)); GS_CUDA(L.gidx.ensure(std::max<int64_t>(n_loc, 1)));
+    L.par = 0;
     GS_CUDA(L.B.ensure(std::max<int64_t>(n, 1))); GS_CUDA(L.A.ensure(std::max<int64_t>(n, 1)));
-    GS_CUDA(L.part.ensure(std::max<int64_t>(n, 1))); GS_CUDA(L.Xb.ensure(std::max<int64_t>(n, 1)));
+    GS_CUDA(L.Xb.ensure(std::max<int64_t>(n, 1)));
     // the device grid covers the local rows from now on
     L.g.ylo = y_loc0;
     L.g.yhi = y_loc1;
@@ -388,9 +392,10 @@ int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_lo
     return GS_OK;
 }
 
-int gs_slab_views(gs_context* ctx, double** S, int32_t** gidx, int32_t** flag) {
-    if (!ctx || !S || !gidx || !flag) return fail(GS_ERR_INVALID, "bad slab args");
-    *S = reinterpret_cast<double*>(ctx->slab.S.ptr);
+int gs_slab_views(gs_context* ctx, double** S, double** S_alt, int32_t** gidx, int32_t** flag) {
+    if (!ctx || !S || !S_alt || !gidx || !flag) return fail(GS_ERR_INVALID, "bad slab args");
+    *S = reinterpret_cast<double*>(slab_cur(ctx));
+    *S_alt = reinterpret_cast<double*>(ctx->slab.par ? ctx->slab.S.ptr : ctx->slab.S2.ptr);
     *gidx = reinterpret_cast<int32_t*>(ctx->slab.gidx.ptr);
     *flag = reinterpret_cast<int32_t*>(ctx->slab.flags.ptr);
     return GS_OK;
@@ -409,7 +414,7 @@ int gs_slab_lists(gs_context* ctx, int64_t ncl_host, void* stream) {
     GS_CUDA(L.keys.ensure(std::max<int64_t>(n_loc, 1))); GS_CUDA(L.Sf.ensure(std::max<int64_t>(n_loc, 1)));
     GS_CUDA(L.start.ensure(ncells + 1));
     GS_CUDA(L.head.ensure(n + 1)); GS_CUDA(L.dest.ensure(n + 1));
-    if (n_loc) k_slab_local_keys<<<blk(n_loc), 256, 0, s>>>(L.S.ptr, n_loc, L.gp.ptr, L.keys.ptr, L.Sf.ptr);
+    if (n_loc) k_slab_local_keys<<<blk(n_loc), 256, 0, s>>>(slab_cur(ctx), n_loc, L.gp.ptr, L.keys.ptr, L.Sf.ptr);
     k_slab_start<<<blk(n_loc + 1), 256, 0, s>>>(L.keys.ptr, n_loc, ncells, L.start.ptr);
     k_slab_heads<<<blk(n + 1), 256, 0, s>>>(L.keys.ptr, L.start.ptr, L.own_begin, n, L.g.nx, L.head.ptr);
     size_t bytes = 0;
@@ -424,7 +429,7 @@ int gs_slab_lists(gs_context* ctx, int64_t ncl_host, void* stream) {
     GS_CUDA(L.cfirst.ensure(ncl + 1)); GS_CUDA(L.cnt.ensure(ncl + 1)); GS_CUDA(L.ofs.ensure(ncl + 1));
     GS_CUDA(L.len.ensure(std::max(ncl, 1)));
     k_slab_cfirst<<<blk(n + 1), 256, 0, s>>>(L.head.ptr, L.dest.ptr, L.own_begin, n, L.cfirst.ptr, ncl);
-    k_slab_sentinel<<<1, 1, 0, s>>>(L.S.ptr, n_loc, L.cnt.ptr, ncl);
+    k_slab_sentinel<<<1, 1, 0, s>>>(L.S.ptr, L.S2.ptr, n_loc, L.cnt.ptr, ncl);
     bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, L.cnt.ptr, L.ofs.ptr, ncl + 1, s);
     GS_CUDA(L.cub.ensure(bytes));
@@ -452,19 +457,23 @@ int gs_slab_stage(gs_context* ctx, const gs_system_t* sys, int32_t step, int32_t
     auto& L = ctx->slab;
     const SysConst sc = make_const(sys);
     const unsigned long long ev = (unsigned long long)step * 8ull + 2ull * (unsigned long long)stg;
-    if (ctx->prof_on) prof_mark(ctx, s);
-    slab_sweep(sc, slab_lists(ctx), L.gidx.ptr, L.n_loc, L.ncl, L.tpl, L.own_begin, L.n_glob, L.part.ptr, ctx->st.ptr,
-               ev, ctx->tbl.ptr, nullptr, s);
-    if (ctx->prof_on) prof_mark(ctx, s);
-    ctx->launches += 2;
-    ctx->pair_launches++;
-    FinishArgs fa{};
-    fa.part = L.part.ptr; fa.nchunks = 1; fa.pstride = 0; fa.nrows = L.n_own; fa.row0 = 0;
-    fa.S = L.S.ptr + L.own_begin; fa.B = L.B.ptr; fa.A = L.A.ptr;
-    fa.stage = stg; fa.dt = dt; fa.st = ctx->st.ptr; fa.event = ev + 1;
+    // the sweep carries the RK4 stage epilogue (rows in local order: coalesced): it reads the
+    // current buffer and writes the own rows' next records into the other one, which becomes current
+    double4* next = L.par ? L.S.ptr : L.S2.ptr;
     const double thr = 0.5 * L.skin * L.cutoff;
+    VerletEpi e{};
+    e.a.S = next + L.own_begin; e.a.B = L.B.ptr; e.a.A = L.A.ptr;
+    e.a.nrows = L.n_own; e.a.stage = stg; e.a.dt = dt; e.a.st = ctx->st.ptr; e.a.event = ev + 1;
+    e.scale_q = sc.scale_q; e.scale_p = sc.scale_p; e.sigma2 = sc.sigma2;
+    e.Xb = L.Xb.ptr; e.thr2 = thr * thr * (1.0 - 1e-9); e.flags = L.flags.ptr;
+    e.decide = 0; e.local = 1; e.rbase = L.own_begin;
     GS_CUDA(cudaMemsetAsync(L.flags.ptr, 0, sizeof(unsigned), s));
-    launch_finish_slab(sc, fa, L.Xb.ptr, thr * thr * (1.0 - 1e-9), L.flags.ptr, s);
+    if (ctx->prof_on) prof_mark(ctx, s);
+    slab_sweep_epi(sc, slab_lists(ctx), L.gidx.ptr, L.n_loc, L.ncl, L.tpl, L.n_glob, e, ctx->st.ptr, ev, ctx->tbl.ptr, s);
+    if (ctx->prof_on) prof_mark(ctx, s);
+    ctx->launches += 1;
+    ctx->pair_launches++;
+    L.par ^= 1;
     GS_CUDA(cudaGetLastError());
     return GS_OK;
 }

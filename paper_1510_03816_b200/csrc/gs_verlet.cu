@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     __shared__ double s_tbl[kTblWords];
     __shared__ unsigned long long s_acc_count;
     if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
-        if (EPI && epi.Ss_next) epi_decide(epi, false);  // every CTA counts towards the decision
+        if (EPI && epi.Xb && epi.decide) epi_decide(epi, false);  // every CTA counts towards the decision
         return;
     }
     for (int t = threadIdx.x; t < kTblWords; t += kVB) s_tbl[t] = tbl_g[t];
@@ -259,12 +259,13 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
                     dqx = __dadd_rn(dqx, __dmul_rn(epi.sigma2, me[m].z));
                     dqy = __dadd_rn(dqy, __dmul_rn(epi.sigma2, me[m].w));
                 }
-                const double4 nxt = stage_update(epi.a, i, dqx, dqy, sz * epi.scale_p, sw * epi.scale_p);
-                epi.a.S[i] = nxt;
+                const int64_t ri = epi.local ? k - epi.rbase : i;  // row of S / B / A
+                const double4 nxt = stage_update(epi.a, ri, dqx, dqy, sz * epi.scale_p, sw * epi.scale_p);
+                epi.a.S[ri] = nxt;
                 if (!finite4(nxt.x, nxt.y, nxt.z, nxt.w)) record_event(epi.a.st, epi.a.event, kNoEvent);
-                if (epi.Ss_next) {
-                    epi.Ss_next[k] = nxt;
-                    const double2 b = epi.Xb[k];
+                if (epi.Ss_next) epi.Ss_next[k] = nxt;
+                if (epi.Xb) {
+                    const double2 b = epi.Xb[epi.local ? ri : k];
                     const double dx = nxt.x - b.x, dy = nxt.y - b.y;
                     need |= fma(dx, dx, dy * dy) > epi.thr2;
                 }
@@ -274,7 +275,10 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
             }
         }
     }
-    if (EPI && epi.Ss_next) epi_decide(epi, need);
+    if (EPI && epi.Xb) {
+        if (epi.decide) epi_decide(epi, need);
+        else if (__any_sync(kFull, need) && (threadIdx.x & 31) == 0) atomicOr(&epi.flags[0], 1u);
+    }
     if (COUNT) {
         unsigned long long v = (unsigned long long)nin;
         for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
@@ -825,6 +829,13 @@ void slab_sweep(const SysConst& sc, const SlabLists& L, const unsigned* gidx, in
                 const double* tbl_dev, unsigned long long* accepted, cudaStream_t stream) {
     sweep<false>(sc, L.S, L.list, L.ofs, L.len, gidx, n_loc, ncl, tpl, part, own_begin, st, event, tbl_dev, accepted,
                  L.cfirst, n_glob, VerletEpi{}, stream);
+}
+
+void slab_sweep_epi(const SysConst& sc, const SlabLists& L, const unsigned* gidx, int64_t n_loc, int64_t ncl, int tpl,
+                    int64_t n_glob, const VerletEpi& e, DevStatus* st, unsigned long long event, const double* tbl_dev,
+                    cudaStream_t stream) {
+    sweep<true>(sc, L.S, L.list, L.ofs, L.len, gidx, n_loc, ncl, tpl, nullptr, 0, st, event, tbl_dev, nullptr,
+                L.cfirst, n_glob, e, stream);
 }
 
 }  // namespace gsb

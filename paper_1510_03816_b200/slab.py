@@ -301,10 +301,13 @@ class DeviceSlabBackend:
     def layout(self, r: RankRows):
         self._chk(self.ctx.lib.gs_slab_layout(self.ctx.handle, r.own0, r.own1, r.loc0, r.loc1, r.own_begin, r.n_loc,
                                               self._s()), "gs_slab_layout")
-        S, g, f = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
-        self._chk(self.ctx.lib.gs_slab_views(self.ctx.handle, ctypes.byref(S), ctypes.byref(g), ctypes.byref(f)),
-                  "gs_slab_views")
-        self.S = _wrap(self.torch, S.value, (r.n_loc + 1, 4), "<f8", self.dev)
+        S, S2, g, f = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        self._chk(self.ctx.lib.gs_slab_views(self.ctx.handle, ctypes.byref(S), ctypes.byref(S2), ctypes.byref(g),
+                                             ctypes.byref(f)), "gs_slab_views")
+        # the stage ping-pongs the local records: buffer 0 is current after the layout
+        self._S = (_wrap(self.torch, S.value, (r.n_loc + 1, 4), "<f8", self.dev),
+                   _wrap(self.torch, S2.value, (r.n_loc + 1, 4), "<f8", self.dev))
+        self._par = 0
         self.g = _wrap(self.torch, g.value, (max(r.n_loc, 1),), "<i4", self.dev)[:r.n_loc]
         self.flag = _wrap(self.torch, f.value, (1,), "<i4", self.dev)
         self.rows_ = r
@@ -312,9 +315,15 @@ class DeviceSlabBackend:
     def lists(self, ncl: int):
         self._chk(self.ctx.lib.gs_slab_lists(self.ctx.handle, ncl, self._s()), "gs_slab_lists")
 
+    @property
+    def S(self):
+        """(n_loc + 1, 4) view of the current local records (the halo slices go here)."""
+        return self._S[self._par]
+
     def stage(self, step: int, s: int, dt: float):
         self._chk(self.ctx.lib.gs_slab_stage(self.ctx.handle, ctypes.byref(self.sysc), step, s, dt, self._s()),
                   "gs_slab_stage")
+        self._par ^= 1
 
     def own(self):
         """(records (n_own, 4), global indices) of the own particles (views)."""
