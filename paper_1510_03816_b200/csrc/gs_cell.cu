@@ -313,12 +313,16 @@ __global__ void __launch_bounds__(kCB, GS_CELL_MINB) k_cell_pair(const double4* 
                                                       double4* __restrict__ part, DevStatus* st,
                                                       unsigned long long event, const double* __restrict__ tbl_g,
                                                       unsigned long long* accepted) {
-    __shared__ double s_tbl[kTblWords];
+    __shared__ __align__(128) double s_tbl[kTblWords];
     __shared__ int s_list[kCL][kCB];
-    __shared__ unsigned long long s_acc_count;
+    __shared__ unsigned long long s_acc_count, s_tbar;
+    table_bulk_issue(s_tbl, tbl_g, &s_tbar);
     // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
-    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
-    for (int t = threadIdx.x; t < kTblWords; t += kCB) s_tbl[t] = tbl_g[t];
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
+        table_bulk_wait(&s_tbar);
+        return;
+    }
+    table_bulk_wait(&s_tbar);
     const double* tbl = lane_table(s_tbl);
     if (threadIdx.x == 0) s_acc_count = 0;
     __syncthreads();

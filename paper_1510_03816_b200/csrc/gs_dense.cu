@@ -67,11 +67,16 @@ __global__ void __launch_bounds__(kDPT, 12) k_dense_partial(const double4* __res
                                                             int64_t nrows, int64_t chunk, double k1,
                                                             double4* __restrict__ part, DevStatus* st,
                                                             unsigned long long event, const double* __restrict__ tbl_g) {
-    __shared__ double s_tbl[kTblWords];
+    __shared__ __align__(128) double s_tbl[kTblWords];
     __shared__ double4 s_src[kDT];
+    __shared__ unsigned long long s_tbar;
+    table_bulk_issue(s_tbl, tbl_g, &s_tbar);
     // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
-    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
-    for (int t = threadIdx.x; t < kTblWords; t += kDPT) s_tbl[t] = tbl_g[t];
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
+        table_bulk_wait(&s_tbar);
+        return;
+    }
+    table_bulk_wait(&s_tbar);
     const double* tbl = lane_table(s_tbl);
 
     const int64_t li0 = (int64_t)blockIdx.x * kDB + threadIdx.x, li1 = li0 + kDPT;

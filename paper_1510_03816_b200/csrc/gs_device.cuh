@@ -133,6 +133,30 @@ __device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb)
 }
 static_assert(kTblRep * 8 == 128, "lane copies interleave in 128-byte rows (exp2_tbl_fast)");
 
+// The exp table into shared memory by one bulk copy (TMA engine, cp.async.bulk): thread 0 arms an
+// mbarrier with the table's byte count and issues the copy; the CTA synchronises (the barrier's
+// init is then visible) and every thread waits on the barrier before its first lookup.  Replaces
+// 16 loads + stores per thread of a 64-thread CTA in the prologue of every tile-pair CTA (7 % of
+// k_dense_sym's stall samples sat there at C2).
+__device__ __forceinline__ void table_bulk_issue(double* s_tbl, const double* tbl_g, unsigned long long* bar) {
+    if (threadIdx.x != 0) return;
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    const unsigned d = (unsigned)__cvta_generic_to_shared(s_tbl);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kTblWords * 8) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(tbl_g), "r"(kTblWords * 8), "r"(b) : "memory");
+}
+
+__device__ __forceinline__ void table_bulk_wait(unsigned long long* bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(b) : "memory");
+}
+
 // The table exp every kernel calls: `tbl` is the lane's copy in shared memory (lane_table); its
 // 32-bit shared address is loop-invariant and hoisted out of the hot loops.
 __device__ __forceinline__ double exp2_tbl(double x, double k, const double* __restrict__ tbl) {

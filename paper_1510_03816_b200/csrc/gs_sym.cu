@@ -117,13 +117,17 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                                                        int nsb, long long cta0, double k1, double4* __restrict__ part,
                                                        int64_t pstride, DevStatus* st, unsigned long long event,
                                                        const double* __restrict__ tbl_g, PeerWait wait) {
-    __shared__ double s_tbl[kTblWords];
+    __shared__ __align__(128) double s_tbl[kTblWords];
     __shared__ double4 s_rot[4][64];     // sub-block b of J twice: s_rot[b][k] = record 32 b + (k & 31)
+    __shared__ unsigned long long s_tbar;
     extern __shared__ double4 s_acc[];   // G * kDB records
+    table_bulk_issue(s_tbl, tbl_g, &s_tbar);  // lands while the CTA sets up its first tile
     // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
-    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) return;
+    if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
+        table_bulk_wait(&s_tbar);  // no copy in flight into a retiring CTA
+        return;
+    }
     block_wait(wait);  // multi-GPU peer exchange: every rank's records of the previous stage are in S
-    for (int t = threadIdx.x; t < kTblWords; t += kST) s_tbl[t] = tbl_g[t];
     const double* tbl = lane_table(s_tbl);
     const unsigned tb = lane_table_addr(s_tbl);
 
@@ -142,6 +146,7 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
     const int r0 = w * 64 + lane, r1 = r0 + 32;  // this thread's two rows inside a block
     const double4 zero4 = make_double4(0.0, 0.0, 0.0, 0.0);
     for (int k = threadIdx.x; k < G * kDB; k += kST) s_acc[k] = zero4;
+    table_bulk_wait(&s_tbar);
 
     for (int ib = 0; ib < G; ++ib) {
         const long long I = SI * G + ib;

@@ -137,13 +137,14 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
                   double4* __restrict__ part, int64_t row0, DevStatus* st, unsigned long long event,
                   const double* __restrict__ tbl_g, unsigned long long* accepted, const int* __restrict__ cfirst,
                   int64_t n_ev, VerletEpi epi) {
-    __shared__ double s_tbl[kTblWords];
-    __shared__ unsigned long long s_acc_count;
+    __shared__ __align__(128) double s_tbl[kTblWords];
+    __shared__ unsigned long long s_acc_count, s_tbar;
+    table_bulk_issue(s_tbl, tbl_g, &s_tbar);  // lands while the lanes load their members and first records
     if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
+        table_bulk_wait(&s_tbar);
         if (EPI && epi.Xb && epi.decide) epi_decide(epi, false);  // every CTA counts towards the decision
         return;
     }
-    for (int t = threadIdx.x; t < kTblWords; t += kVB) s_tbl[t] = tbl_g[t];
     if (threadIdx.x == 0) s_acc_count = 0;
     __syncthreads();
     const double* tbl = lane_table(s_tbl);
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     double4 b0 = Ss[j.x], b1 = Ss[j.y];
     int2 jc = ldl(e + 2 * step);
     double4 c0, c1;
+    table_bulk_wait(&s_tbar);
     while (true) {
         if (e >= end) break;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(list + e + GS_VERLET_PF * step));
