@@ -30,6 +30,8 @@
 // over superblock SI goes to slot SI (in a diagonal superblock both land in one shared
 // accumulator, slot SI).  Every row receives exactly nsb partials, part[slot * pstride + row],
 // summed in slot order by k_finish — deterministic.
+#include <atomic>
+
 #include "gs_kernels.cuh"
 
 namespace gsb {
@@ -100,6 +102,37 @@ __device__ __forceinline__ void two_sided(const double4& me, const double4& s, c
     j.py = fma(-c, dy, j.py);
 }
 
+// The J tile into s_rot by 8 bulk copies (each 32-record sub-block twice, the rotation's doubled
+// layout) on the tile mbarrier — one thread, no registers, overlapping the CTA's setup for the
+// first tile.  Full tiles only (a partial last tile takes the thread loop and its far records).
+__device__ __forceinline__ void tile_bar_init(unsigned long long* bar) {
+    if (threadIdx.x != 0) return;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void tile_bulk_issue(double4 (*rot)[64], const double4* __restrict__ src,
+                                                unsigned long long* bar) {
+    if (threadIdx.x != 0) return;
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the previous tile's reads are done (barrier)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kDB * 64) : "memory");
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(&rot[k >> 1][(k & 1) * 32]);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 1024, [%2];"
+                     ::"r"(d), "l"(src + 32 * (k >> 1)), "r"(b) : "memory");
+    }
+}
+
+__device__ __forceinline__ void tile_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(b), "r"(parity) : "memory");
+}
+
 __device__ __forceinline__ void add_to(double4* dst, const Acc& a) {
     double4 v = *dst;
     v.x += a.qx; v.y += a.qy; v.z += a.px; v.w += a.py;
@@ -118,10 +151,11 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                                                        int64_t pstride, DevStatus* st, unsigned long long event,
                                                        const double* __restrict__ tbl_g, PeerWait wait) {
     __shared__ __align__(128) double s_tbl[kTblWords];
-    __shared__ double4 s_rot[4][64];     // sub-block b of J twice: s_rot[b][k] = record 32 b + (k & 31)
-    __shared__ unsigned long long s_tbar;
+    __shared__ __align__(128) double4 s_rot[4][64];  // sub-block b of J twice: s_rot[b][k] = record 32 b + (k & 31)
+    __shared__ unsigned long long s_tbar, s_rbar;
     extern __shared__ double4 s_acc[];   // G * kDB records
     table_bulk_issue(s_tbl, tbl_g, &s_tbar);  // lands while the CTA sets up its first tile
+    tile_bar_init(&s_rbar);
     // an earlier failure: skip (one decision per CTA, the status may change while CTAs start)
     if (__syncthreads_or(*((volatile unsigned long long*)&st->first_event) < event)) {
         table_bulk_wait(&s_tbar);  // no copy in flight into a retiring CTA
@@ -142,6 +176,13 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
     const bool diag = SI == SJ;
     GS_ASSERT(SI >= 0 && SI <= SJ && SJ < nsb);
 
+    // the first tile (SJ G, full) goes in flight now
+    const long long J0 = SJ * G;
+    const bool pre = (J0 + 1) * kDB <= n;
+    if (pre) tile_bulk_issue(s_rot, S + J0 * kDB, &s_rbar);
+    unsigned rph = 0;
+    bool first = true;
+
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int r0 = w * 64 + lane, r1 = r0 + 32;  // this thread's two rows inside a block
     const double4 zero4 = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -159,13 +200,21 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
             const long long J = SJ * G + jb;
             if (J >= nb) break;
             __syncthreads();  // previous tile done with s_rot / s_acc
-            for (int r = threadIdx.x; r < kDB; r += kST) {
-                const int64_t js = J * kDB + r;
-                const double4 rec = (js < n) ? S[js] : far_record(kDB + r);
-                s_rot[r >> 5][r & 31] = rec;
-                s_rot[r >> 5][(r & 31) + 32] = rec;
+            const bool full = (J + 1) * kDB <= n;
+            if (full) {
+                if (!(first && pre)) tile_bulk_issue(s_rot, S + J * kDB, &s_rbar);
+                tile_wait(&s_rbar, rph);
+                rph ^= 1u;
+            } else {
+                for (int r = threadIdx.x; r < kDB; r += kST) {
+                    const int64_t js = J * kDB + r;
+                    const double4 rec = (js < n) ? S[js] : far_record(kDB + r);
+                    s_rot[r >> 5][r & 31] = rec;
+                    s_rot[r >> 5][(r & 31) + 32] = rec;
+                }
+                __syncthreads();
             }
-            __syncthreads();
+            first = false;
             int nz0 = 0, nz1 = 0;
             if (I == J) {
 #pragma unroll 4
@@ -300,6 +349,20 @@ void launch_dense_sym(const SysConst& sc, const double4* S, int64_t n, double4* 
     if (cta1 <= cta0) return;
     const unsigned ctas = (unsigned)(cta1 - cta0);
     const size_t smem = (size_t)p.G * kDB * sizeof(double4);
+    {   // static (table, s_rot, barriers) + dynamic (G blocks of J-side sums) exceeds the 48 KB default
+        // at G = 8: opt in to more dynamic shared memory, once per device (the attribute is per device)
+        static std::atomic<signed char> done[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && done[dev].load() == 0) {
+            const int max_dyn = kSymMaxG * kDB * (int)sizeof(double4);
+            const bool ok = cudaFuncSetAttribute(k_dense_sym<kFamConical>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 max_dyn) == cudaSuccess &&
+                            cudaFuncSetAttribute(k_dense_sym<kFamGaussian>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 max_dyn) == cudaSuccess;
+            done[dev] = ok ? 1 : -1;
+        }
+    }
     if (sc.fam == kFamConical)
         k_dense_sym<kFamConical><<<ctas, kST, smem, stream>>>(S, n, p.nb, p.G, p.nsb, cta0, sc.k1, part, pstride, st,
                                                               event, tbl_dev, wait);
