@@ -47,7 +47,8 @@ constexpr int kST = 64;  // threads per CTA
 #define GS_SYM_SB 128  // A/B on C2 (ms per 100-step solve): 128 -> 152.8, 64 -> 165.4, 32 -> 178.7
 #endif
 #ifndef GS_SYM_UNROLL     // unroll of the two-source rotation loop (16 trips)
-#define GS_SYM_UNROLL 2  // A/B on C2 (ms per RHS): 2 -> 0.365, 4 -> 0.375, 8 -> 0.420 (fewer moves, slower)
+#define GS_SYM_UNROLL 4  // A/B on C2 (ms per 100-step solve, bulk-copy prologue, 152-160 regs): 1 -> 138.1,
+                         // 2 -> 139.5, 4 -> 137.1, 8 -> 150.6 (spills), 16 -> 164.9 (round 1, 160 regs: 2 best)
 #endif
 constexpr int kSymUnroll = GS_SYM_UNROLL;
 #ifndef GS_SYM_SRC2      // two sources per rotation step: 4 independent pair chains per lane

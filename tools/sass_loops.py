@@ -27,7 +27,8 @@ def loops(obj: str, pat: str) -> list:
                 ins.append((int(m.group(1), 16), m.group(2).strip()))
         addr = {a: k for k, (a, _) in enumerate(ins)}
         for k, (a, t) in enumerate(ins):
-            m = re.search(r"BRA (0x[0-9a-f]+)", t)
+            # BRA 0x.., @P0 BRA 0x.., BRA.U UP0, 0x.. (uniform-predicate back edges of unrolled loops)
+            m = re.search(r"BRA\S*\s+(?:!?U?P\w+,\s*)?(0x[0-9a-f]+)", t)
             if not m or int(m.group(1), 16) >= a:
                 continue
             s = addr.get(int(m.group(1), 16))
@@ -49,6 +50,10 @@ def fp64_per_pair(obj: str, pat: str, symmetric: bool):
     pair count is its MUFU count (an unordered pair feeds two ordered pairs in the symmetric
     kernel).  Returns (fp64 per ordered pair, loop dict) or (None, None)."""
     ls = [x for x in loops(obj, pat) if x["mufu"] > 0]
+    # innermost pair loops only: a loop around another loop with MUFU (phase / tile loops) mixes in
+    # the diagonal one-sided tiles and the setup code
+    ls = [x for x in ls if not any(y is not x and y["kernel"] == x["kernel"] and x["start"] <= y["start"]
+                                   and y["end"] <= x["end"] for y in ls)]
     if not ls:
         return None, None
     best = max(ls, key=lambda x: x["fp64"])
