@@ -321,8 +321,11 @@ int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, c
     GS_CUDA(cudaMemcpyAsync(&total, ctx->v_ofs.ptr + ncl, sizeof(total), cudaMemcpyDeviceToHost, s));
     GS_CUDA(cudaMemsetAsync(ctx->v_over.ptr, 0, sizeof(unsigned long long), s));
     GS_CUDA(cudaStreamSynchronize(s));
-    const double slack = ctx->verlet_slack;  // spare capacity as a fraction of the sizing build
-    const long long want = slack >= 0.5 ? std::max<long long>(total + total / 2, total + (1 << 20))
+    // spare capacity as a fraction of the sizing build: a build that outgrows the buffer makes the
+    // whole call (a 100-iteration match: seconds) run again, and lists grow when a deforming cloud
+    // packs tighter (C4's late iterations outgrew 1.5x), so room is generous — HBM is plentiful
+    const double slack = ctx->verlet_slack;
+    const long long want = slack >= 0.5 ? std::max<long long>((long long)((1.0 + slack) * (double)total), total + (1 << 20))
                                         : std::max<long long>(1, (long long)((1.0 + slack) * (double)total));
     ctx->v_list.release();
     GS_CUDA(ctx->v_list.ensure((size_t)want));

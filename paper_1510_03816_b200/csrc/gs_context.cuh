@@ -150,7 +150,7 @@ struct gs_context {
     int verlet_retries = 0;
     double verlet_skin = -1.0;          // GS_B200_SKIN (< 0: by n, see verlet_ws)
     int64_t verlet_fuse_max_n = 131072; // lists: epilogue fused into the sweep below this n (GS_B200_VERLET_FUSE_MAX_N)
-    double verlet_slack = 0.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
+    double verlet_slack = 1.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
     cudaStream_t cap_stream2 = nullptr; // captures the conditional rebuild bodies
     // slab decomposition of the cell path across ranks (gs_slab.cu): this rank's own particles
     // (contiguous cell rows of the global grid) + the halo rows, all in global sorted order
