@@ -477,6 +477,43 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill(const float2* __restrict__
     if (sub == 0) len[c] = padded;
 }
 
+// Packed FP32 pairs (sm_100: FADD2 / FMUL2 / FFMA2 on {lo, hi} = two members).
+#ifndef GS_VERLET_FILL_F32X2   // A/B: 0 = one member at a time
+#define GS_VERLET_FILL_F32X2 1
+#endif
+__device__ __forceinline__ unsigned long long f32x2_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f32x2_splat(float v) { return f32x2_pack(v, v); }
+__device__ __forceinline__ float f32x2_lo(unsigned long long v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo;
+}
+__device__ __forceinline__ float f32x2_hi(unsigned long long v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return hi;
+}
+__device__ __forceinline__ unsigned long long f32x2_sub(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f32x2_mul(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f32x2_fma(unsigned long long a, unsigned long long b,
+                                                        unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // The same lists for kVQ consecutive clusters per warp (row-major grid): per stencil row the warp
 // sweeps the union of the clusters' ranges once, each candidate is tested against every member
 // (fp32) and appended to each cluster whose own range holds it and whose members it is near —
@@ -572,6 +609,15 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
         qfx[t] = __shfl_sync(kFull, mv ? fx : 3e38f, t);
         qfy[t] = __shfl_sync(kFull, mv ? fy : 3e38f, t);
     }
+#if GS_VERLET_FILL_F32X2
+    static_assert(kVM == 2, "packed member pairs");
+    unsigned long long qx2[kVQ], qy2[kVQ];
+#pragma unroll
+    for (int q = 0; q < kVQ; ++q) {
+        qx2[q] = f32x2_pack(qfx[2 * q], qfx[2 * q + 1]);
+        qy2[q] = f32x2_pack(qfy[2 * q], qfy[2 * q + 1]);
+    }
+#endif
     int wpos[kVQ];  // each cluster's next list slot (32-bit: a build never exceeds 2^31 entries)
 #pragma unroll
     for (int q = 0; q < kVQ; ++q) wpos[q] = q < nq ? (int)ofs[c0 + q] : 0;
@@ -623,8 +669,18 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
             const int pos = base + lane;
             float2 f = make_float2(0.0f, 0.0f);
             if (pos < B) f = Sf[pos];
+#if GS_VERLET_FILL_F32X2
+            const unsigned long long fxx = f32x2_splat(f.x), fyy = f32x2_splat(f.y);
+#endif
 #pragma unroll
             for (int q = 0; q < kVQ; ++q) {
+#if GS_VERLET_FILL_F32X2
+                // both members at once on the packed FP32 pipe (FADD2 / FMUL2 / FFMA2): the same
+                // roundings as fmaf(dx, dx, dy * dy) per member
+                const unsigned long long dx2 = f32x2_sub(qx2[q], fxx), dy2 = f32x2_sub(qy2[q], fyy);
+                const unsigned long long d22 = f32x2_fma(dx2, dx2, f32x2_mul(dy2, dy2));
+                const float d2 = fminf(fminf(INFINITY, f32x2_lo(d22)), f32x2_hi(d22));
+#else
                 float d2 = INFINITY;
 #pragma unroll
                 for (int m = 0; m < kVM; ++m) {
@@ -632,6 +688,7 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
                     const float dx = qfx[t] - f.x, dy = qfy[t] - f.y;
                     d2 = fminf(d2, fmaf(dx, dx, dy * dy));
                 }
+#endif
                 const bool acc = (pos >= pa[q]) & (pos < pb[q]) & !(d2 >= rc2f);  // NaN radius: keep
                 const unsigned bal = __ballot_sync(kFull, acc);
                 GS_ASSERT(!acc || (pos < n && wpos[q] + __popc(bal) <= ofs[c0 + q + 1]));
