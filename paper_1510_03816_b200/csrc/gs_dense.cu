@@ -335,8 +335,10 @@ __global__ void __launch_bounds__(256) k_finish_verlet(SysConst sc, FinishArgs a
         if (f.Ss) f.Ss[k] = nxt;
         const double2 b = f.Xb[k];
         const double dx = nxt.x - b.x, dy = nxt.y - b.y;
-        need = fma(dx, dx, dy * dy) > f.thr2;
+        if (f.dX) f.dX[k] = make_double2(dx, dy);
+        else need = fma(dx, dx, dy * dy) > f.thr2;
     }
+    if (f.dX) return;  // the trigger kernel decides
     if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&f.flags[0], 1u);
     if (threadIdx.x == 0) {
         __threadfence();

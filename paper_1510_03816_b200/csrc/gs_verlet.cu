@@ -817,6 +817,146 @@ void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t
                                                                      v.flags, force, cond, use_cond);
 }
 
+// ---- the rebuild trigger of large clouds: relative displacement of neighbours ----------------
+// A list built with radius rl = cutoff (1 + skin) stays exact while no pair that was >= rl apart at
+// the build has come closer than the cutoff.  Blanket rule (the fused epilogue, small clouds):
+// rebuild when any particle moved skin cutoff / 2.  Here, with Delta_i = x_i(t) - x_i(build):
+// coarse cells of edge L = 2 rl (by the build positions) get the bounding box B_C of their
+// particles' Delta; a pair in the same or adjacent coarse cells has |Delta_i - Delta_j| <=
+// diam(B_C u B_C'), a pair in non-adjacent cells started >= L apart.  So the lists hold while
+//   diam(B_C u B_C') < skin cutoff for every adjacent / same pair of cells, and
+//   max |Delta| < (L - cutoff) / 2.
+// In a smooth flow neighbours move together and rebuilds get rarer.  Boxes are kept as
+// order-preserving 32-bit keys of the displacements rounded outwards to float (a valid, slightly
+// wider box): one warp reduction (REDUX) per run of a coarse cell, then 4 atomics.
+namespace {
+__device__ __forceinline__ unsigned fkey(float v) {  // monotone float -> unsigned
+    const unsigned u = __float_as_uint(v);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+constexpr unsigned kBoxEmptyMin = 0xffffffffu, kBoxEmptyMax = 0u;
+
+struct TriggerArgs {
+    const double2* dX;
+    const unsigned* keys;      // the build's sorted cell keys (cell above GS_CELL_SUBKEY bits)
+    const GridParams* gp;
+    int64_t n;
+    unsigned* box;             // 4 per coarse cell: min x, max x, min y, max y (keys); capacity `cap`
+    int64_t cap;
+    double lim2;               // (skin cutoff)^2, slightly reduced
+    double mlim2;              // ((L - cutoff) / 2)^2, slightly reduced
+    double thr2;               // blanket rule (hashed grid): (skin cutoff / 2)^2
+    unsigned* flags;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+};
+
+__global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
+    const GridParams g = *t.gp;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = k < t.n;
+    const int fct = 2 * max(g.sub, 1);  // fine cells per coarse cell: L = fct h = 2 rl
+    const int ncx = g.hashed ? 1 : (g.nx + fct - 1) / fct, ncy = g.hashed ? 1 : (g.ny + fct - 1) / fct;
+    const bool coarse = !g.hashed && (int64_t)ncx * ncy * 4 <= t.cap;
+    bool need = false;
+    double2 d = make_double2(0.0, 0.0);
+    if (valid) d = t.dX[k];
+    if (!coarse) {
+        need = valid && fma(d.x, d.x, d.y * d.y) > t.thr2;
+    } else {
+        int cc = -1;
+        if (valid) {
+            const unsigned cell = t.keys[k] >> GS_CELL_SUBKEY;
+            const int cy = (int)(cell / (unsigned)g.nx), cx = (int)(cell % (unsigned)g.nx);
+            cc = (cy / fct) * ncx + cx / fct;
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(act, cc);
+            const unsigned mnx = __reduce_min_sync(peers, fkey(__double2float_rd(d.x)));
+            const unsigned mxx = __reduce_max_sync(peers, fkey(__double2float_ru(d.x)));
+            const unsigned mny = __reduce_min_sync(peers, fkey(__double2float_rd(d.y)));
+            const unsigned mxy = __reduce_max_sync(peers, fkey(__double2float_ru(d.y)));
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) {
+                unsigned* b = t.box + 4 * (int64_t)cc;
+                atomicMin(&b[0], mnx); atomicMax(&b[1], mxx); atomicMin(&b[2], mny); atomicMax(&b[3], mxy);
+            }
+        }
+    }
+    if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&t.flags[0], 1u);
+    __shared__ unsigned s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&t.flags[2], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // the last CTA: every box is in; check the neighbour pairs, reset the boxes, decide
+    __threadfence();
+    bool bad = false;
+    if (coarse) {
+        const int ncell = ncx * ncy;
+        for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+            volatile unsigned* b = t.box + 4 * (int64_t)c;
+            if (b[0] == kBoxEmptyMin) continue;
+            const float ax0 = funkey(b[0]), ax1 = funkey(b[1]), ay0 = funkey(b[2]), ay1 = funkey(b[3]);
+            const double mx = fmax(fabs((double)ax0), fabs((double)ax1)), my = fmax(fabs((double)ay0), fabs((double)ay1));
+            bad |= fma(mx, mx, my * my) >= t.mlim2;
+            const int cx = c % ncx, cy = c / ncx;
+            const int nb[5][2] = {{0, 0}, {1, 0}, {-1, 1}, {0, 1}, {1, 1}};
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const int ex = cx + nb[q][0], ey = cy + nb[q][1];
+                if (ex < 0 || ex >= ncx || ey >= ncy) continue;
+                volatile unsigned* e = t.box + 4 * ((int64_t)ey * ncx + ex);
+                if (e[0] == kBoxEmptyMin) continue;
+                const double wx = (double)fmaxf(ax1, funkey(e[1])) - (double)fminf(ax0, funkey(e[0]));
+                const double wy = (double)fmaxf(ay1, funkey(e[3])) - (double)fminf(ay0, funkey(e[2]));
+                bad |= fma(wx, wx, wy * wy) >= t.lim2;
+            }
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+            unsigned* b = t.box + 4 * (int64_t)c;
+            b[0] = kBoxEmptyMin; b[1] = kBoxEmptyMax; b[2] = kBoxEmptyMin; b[3] = kBoxEmptyMax;
+        }
+    }
+    const bool any = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        const unsigned dflag = (atomicExch(&t.flags[0], 0u) != 0u || any) ? 1u : 0u;
+        t.flags[2] = 0u;
+        if (t.use_cond) cudaGraphSetConditional(t.cond, dflag);
+        t.flags[3] = dflag;
+    }
+}
+
+__global__ void k_box_reset(unsigned* box, int64_t cells) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    box[4 * c] = kBoxEmptyMin; box[4 * c + 1] = kBoxEmptyMax; box[4 * c + 2] = kBoxEmptyMin; box[4 * c + 3] = kBoxEmptyMax;
+}
+}  // namespace
+
+void verlet_box_reset(unsigned* box, int64_t cells, cudaStream_t stream) {
+    if (cells > 0) k_box_reset<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(box, cells);
+}
+
+void launch_verlet_trigger(const CellWs& w, const VerletWs& v, int64_t n, const double2* dX, unsigned* box,
+                           int64_t box_cap, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream) {
+    TriggerArgs t;
+    t.dX = dX; t.keys = w.keys_sorted; t.gp = w.gp; t.n = n; t.box = box; t.cap = box_cap;
+    const double lim = v.skin * v.cutoff, rl = v.cutoff * (1.0 + v.skin), mlim = 0.5 * (2.0 * rl - v.cutoff);
+    t.lim2 = lim * lim * (1.0 - 1e-6);
+    t.mlim2 = mlim * mlim * (1.0 - 1e-6);
+    const double thr = 0.5 * v.skin * v.cutoff;
+    t.thr2 = thr * thr * (1.0 - 1e-9);
+    t.flags = v.flags; t.cond = cond; t.use_cond = use_cond;
+    k_verlet_trigger<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(t);
+}
+
 namespace {
 template <bool EPI>
 void sweep(const SysConst& sc, const double4* Ss, const int* list, const long long* ofs, const int* len,
