@@ -513,9 +513,13 @@ def run_extras(a, gs, device, configs, torch, world, rank, dist, sharded_run):
                 device.set_path("auto")
                 steps = 4
                 tf = steps * wk.t_final / wk.steps
-                device.evolve(sp, qk, pk, tf, steps)
-                _, ms = _timed(torch, lambda: device.evolve(sp, qk, pk, tf, steps), 2)
+                # the first calls of a new size allocate the multi-GB list buffer and capture the graphs
+                for _ in range(2):
+                    device.evolve(sp, qk, pk, tf, steps)
+                _, ms = _timed(torch, lambda: device.evolve(sp, qk, pk, tf, steps), 3)
                 _, acc, pair_ms = _accepted_pairs(lambda: device.evolve(sp, qk, pk, tf, steps), torch)
+                # the match loop's conditional graph is captured on its first call: warm it up
+                device.match(sp, wk.q, wk.target, wk.h, wk.epsilon, 1, wk.stop_rule, "max", wk.t_final, wk.steps)
                 r = device.match(sp, wk.q, wk.target, wk.h, wk.epsilon, 2, wk.stop_rule, "max", wk.t_final, wk.steps)
                 out[name.lower()] = {"n": wk.n, "rhs_ms_in_evolve": ms / (4 * steps), "pair_kernel_ms": pair_ms,
                                      "accepted_pairs_per_rhs": acc / (4 * steps),
