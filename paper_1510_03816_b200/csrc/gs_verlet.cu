@@ -627,8 +627,9 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
     int lo = __reduce_min_sync(kFull, mv ? cy : g.ny), hi = __reduce_max_sync(kFull, mv ? cy : -1);
     const double rc2 = g.rc * g.rc;
     const float rc2f = g.rc2f;
-    for (int yy = max(lo - sub, g.ylo); yy <= min(hi + sub, g.yhi - 1); ++yy) {
-        // this lane's member: its trimmed x-range of cells in row yy (as for_each_range)
+    // a row's candidate ranges: this lane's member's trimmed x-range of cells in row yy (as
+    // for_each_range), the clusters' unions by shuffles, their sorted-position ranges from `start`
+    auto row_ranges = [&](int yy, int* pa, int* pb, int& A, int& B) {
         int a = g.nx, b = -1;
         if (mv && yy >= cy - sub && yy <= cy + sub) {
             if (sub > 1) {
@@ -647,8 +648,8 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
             }
         }
         const int r0 = (yy - g.ylo) * g.nx;
-        int pa[kVQ], pb[kVQ];
-        int A = 0x7fffffff, B = -1;
+        A = 0x7fffffff;
+        B = -1;
 #pragma unroll
         for (int q = 0; q < kVQ; ++q) {
             int xa = g.nx, xb = -1;
@@ -661,10 +662,23 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
             if (xb >= xa) {
                 pa[q] = start[r0 + xa];
                 pb[q] = start[r0 + xb + 1];
-                A = min(A, pa[q]);
-                B = max(B, pb[q]);
             }
         }
+    };
+    const int y_first = max(lo - sub, g.ylo), y_last = min(hi + sub, g.yhi - 1);
+    // software pipeline over the rows: the next row's `start` loads are in flight while this
+    // row's candidates are filtered
+    int na[kVQ], nb[kVQ], nA = 0, nB = -1;
+    if (y_first <= y_last) row_ranges(y_first, na, nb, nA, nB);
+    for (int yy = y_first; yy <= y_last; ++yy) {
+        int pa[kVQ], pb[kVQ];
+#pragma unroll
+        for (int q = 0; q < kVQ; ++q) { pa[q] = na[q]; pb[q] = nb[q]; }
+        if (yy < y_last) row_ranges(yy + 1, na, nb, nA, nB);
+        int A = 0x7fffffff, B = -1;
+#pragma unroll
+        for (int q = 0; q < kVQ; ++q)
+            if (pb[q] > pa[q] || pa[q] != 0) { A = min(A, pa[q]); B = max(B, pb[q]); }
         for (int base = A; base < B; base += 32) {
             const int pos = base + lane;
             float2 f = make_float2(0.0f, 0.0f);
