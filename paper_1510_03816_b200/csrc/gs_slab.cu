@@ -33,6 +33,14 @@ namespace {
 
 constexpr int kPackW = 13;  // doubles per migrating particle: S (4), B (4), A (4), global index
 
+// Per-build buffers grow with 25 % headroom: counts change by a few per cent at every build
+// (migration, halo, list length), and an exact-size reallocation costs a device-wide
+// cudaFree + cudaMalloc inside the build.
+template <typename T>
+cudaError_t grow(DevBuf<T>& b, size_t n) {
+    return n <= b.cap ? cudaSuccess : b.ensure(n + n / 4 + 256);
+}
+
 __device__ __forceinline__ int grid_cell(double v, double v0, double inv_h, int nmax) {
     // the cell coordinate of gs_cell.cu / gs_verlet.cu (floor, clamped to the grid)
     const int c = (int)floor((v - v0) * inv_h);
@@ -223,8 +231,8 @@ Own own_arrays(gs_context* ctx) {
 
 int ensure_own(gs_context* ctx, int64_t n) {
     auto& L = ctx->slab;
-    GS_CUDA(L.Su.ensure(n)); GS_CUDA(L.Bu.ensure(n)); GS_CUDA(L.Au.ensure(n)); GS_CUDA(L.gu.ensure(n));
-    GS_CUDA(L.skey.ensure(n)); GS_CUDA(L.skey2.ensure(n)); GS_CUDA(L.sval.ensure(n)); GS_CUDA(L.sval2.ensure(n));
+    GS_CUDA(grow(L.Su, n)); GS_CUDA(grow(L.Bu, n)); GS_CUDA(grow(L.Au, n)); GS_CUDA(grow(L.gu, n));
+    GS_CUDA(grow(L.skey, n)); GS_CUDA(grow(L.skey2, n)); GS_CUDA(grow(L.sval, n)); GS_CUDA(grow(L.sval2, n));
     return GS_OK;
 }
 
@@ -254,8 +262,8 @@ int gs_slab_begin(gs_context* ctx, const gs_system_t* sys, int64_t n_glob, int64
     L.rl = sys->cutoff * (1.0 + L.skin);
     L.tpl = verlet_tpl(n_glob);
     if ((rc = ensure_own(ctx, std::max<int64_t>(n_own, 1)))) return rc;
-    GS_CUDA(L.red.ensure(4 * kCellBboxBlocks)); GS_CUDA(L.b4.ensure(4)); GS_CUDA(L.gp.ensure(1));
-    GS_CUDA(L.flags.ensure(4)); GS_CUDA(L.over.ensure(1));
+    GS_CUDA(grow(L.red, 4 * kCellBboxBlocks)); GS_CUDA(grow(L.b4, 4)); GS_CUDA(grow(L.gp, 1));
+    GS_CUDA(grow(L.flags, 4)); GS_CUDA(grow(L.over, 1));
     GS_CUDA(cudaMemsetAsync(L.flags.ptr, 0, 4 * sizeof(unsigned), s));
     GS_CUDA(cudaMemsetAsync(L.over.ptr, 0, sizeof(unsigned long long), s));
     k_slab_status_reset<<<1, 1, 0, s>>>(ctx->st.ptr);
@@ -309,7 +317,7 @@ int gs_slab_pack(gs_context* ctx, const int32_t* owner, int32_t world, double* s
     GS_CUDA(cudaSetDevice(ctx->device));
     const int64_t n = L.n_own;
     const Own o = own_arrays(ctx);
-    GS_CUDA(L.dcount.ensure(world));
+    GS_CUDA(grow(L.dcount, world));
     GS_CUDA(cudaMemsetAsync(L.dcount.ptr, 0, world * sizeof(unsigned long long), s));
     if (n) {
         k_slab_dest<<<blk(n), 256, 0, s>>>(o.S, n, L.gp.ptr, owner, L.skey.ptr, L.sval.ptr, L.dcount.ptr);
@@ -317,7 +325,7 @@ int gs_slab_pack(gs_context* ctx, const int32_t* owner, int32_t world, double* s
         const int end_bit = std::max(1, bits_for(world));
         cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.skey.ptr, L.skey2.ptr, L.sval.ptr, L.sval2.ptr, (int)n, 0,
                                         end_bit, s);
-        GS_CUDA(L.cub.ensure(bytes));
+        GS_CUDA(grow(L.cub, bytes));
         bytes = L.cub.cap;
         GS_CUDA(cub::DeviceRadixSort::SortPairs(L.cub.ptr, bytes, L.skey.ptr, L.skey2.ptr, L.sval.ptr, L.sval2.ptr,
                                                 (int)n, 0, end_bit, s));
@@ -363,10 +371,10 @@ int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_lo
     L.own_begin = own_begin;
     L.n_loc = n_loc;
     const int64_t n = L.n_own;
-    GS_CUDA(L.S.ensure(n_loc + 1)); GS_CUDA(L.S2.ensure(n_loc + 1)); GS_CUDA(L.gidx.ensure(std::max<int64_t>(n_loc, 1)));
+    GS_CUDA(grow(L.S, n_loc + 1)); GS_CUDA(grow(L.S2, n_loc + 1)); GS_CUDA(grow(L.gidx, std::max<int64_t>(n_loc, 1)));
     L.par = 0;
-    GS_CUDA(L.B.ensure(std::max<int64_t>(n, 1))); GS_CUDA(L.A.ensure(std::max<int64_t>(n, 1)));
-    GS_CUDA(L.Xb.ensure(std::max<int64_t>(n, 1)));
+    GS_CUDA(grow(L.B, std::max<int64_t>(n, 1))); GS_CUDA(grow(L.A, std::max<int64_t>(n, 1)));
+    GS_CUDA(grow(L.Xb, std::max<int64_t>(n, 1)));
     // the device grid covers the local rows from now on
     L.g.ylo = y_loc0;
     L.g.yhi = y_loc1;
@@ -380,7 +388,7 @@ int gs_slab_layout(gs_context* ctx, int32_t y_own0, int32_t y_own1, int32_t y_lo
         size_t bytes = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.skey.ptr, L.skey2.ptr, L.sval.ptr, L.sval2.ptr, (int)n, 0,
                                         end_bit, s);
-        GS_CUDA(L.cub.ensure(bytes));
+        GS_CUDA(grow(L.cub, bytes));
         bytes = L.cub.cap;
         GS_CUDA(cub::DeviceRadixSort::SortPairs(L.cub.ptr, bytes, L.skey.ptr, L.skey2.ptr, L.sval.ptr, L.sval2.ptr,
                                                 (int)n, 0, end_bit, s));
@@ -411,35 +419,35 @@ int gs_slab_lists(gs_context* ctx, int64_t ncl_host, void* stream) {
     auto& L = ctx->slab;
     const int64_t n_loc = L.n_loc, n = L.n_own;
     const int64_t ncells = (int64_t)(L.y_loc1 - L.y_loc0) * L.g.nx;
-    GS_CUDA(L.keys.ensure(std::max<int64_t>(n_loc, 1))); GS_CUDA(L.Sf.ensure(std::max<int64_t>(n_loc, 1)));
-    GS_CUDA(L.start.ensure(ncells + 1));
-    GS_CUDA(L.head.ensure(n + 1)); GS_CUDA(L.dest.ensure(n + 1));
+    GS_CUDA(grow(L.keys, std::max<int64_t>(n_loc, 1))); GS_CUDA(grow(L.Sf, std::max<int64_t>(n_loc, 1)));
+    GS_CUDA(grow(L.start, ncells + 1));
+    GS_CUDA(grow(L.head, n + 1)); GS_CUDA(grow(L.dest, n + 1));
     if (n_loc) k_slab_local_keys<<<blk(n_loc), 256, 0, s>>>(slab_cur(ctx), n_loc, L.gp.ptr, L.keys.ptr, L.Sf.ptr);
     k_slab_start<<<blk(n_loc + 1), 256, 0, s>>>(L.keys.ptr, n_loc, ncells, L.start.ptr);
     k_slab_heads<<<blk(n + 1), 256, 0, s>>>(L.keys.ptr, L.start.ptr, L.own_begin, n, L.g.nx, L.head.ptr);
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, L.head.ptr, L.dest.ptr, (int)(n + 1), s);
-    GS_CUDA(L.cub.ensure(bytes));
+    GS_CUDA(grow(L.cub, bytes));
     bytes = L.cub.cap;
     GS_CUDA(cub::DeviceScan::ExclusiveSum(L.cub.ptr, bytes, L.head.ptr, L.dest.ptr, (int)(n + 1), s));
     // clusters: sum over the own rows of ceil(count / 2), known to the driver from the histogram
     // (checked on the device: the scan's total must agree)
     const int ncl = (int)ncl_host;
     L.ncl = ncl;
-    GS_CUDA(L.cfirst.ensure(ncl + 1)); GS_CUDA(L.cnt.ensure(ncl + 1)); GS_CUDA(L.ofs.ensure(ncl + 1));
-    GS_CUDA(L.len.ensure(std::max(ncl, 1)));
+    GS_CUDA(grow(L.cfirst, ncl + 1)); GS_CUDA(grow(L.cnt, ncl + 1)); GS_CUDA(grow(L.ofs, ncl + 1));
+    GS_CUDA(grow(L.len, std::max(ncl, 1)));
     k_slab_cfirst<<<blk(n + 1), 256, 0, s>>>(L.head.ptr, L.dest.ptr, L.own_begin, n, L.cfirst.ptr, ncl);
     k_slab_sentinel<<<1, 1, 0, s>>>(L.S.ptr, L.S2.ptr, n_loc, L.cnt.ptr, ncl);
     bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, L.cnt.ptr, L.ofs.ptr, ncl + 1, s);
-    GS_CUDA(L.cub.ensure(bytes));
+    GS_CUDA(grow(L.cub, bytes));
     SlabLists sl = slab_lists(ctx);
     if (int e = slab_list_caps(sl, n_loc, ncl, L.tpl, s)) return fail(GS_ERR_CUDA, cudaGetErrorString((cudaError_t)e));
     long long total = 0;
     GS_CUDA(cudaMemcpyAsync(&total, L.ofs.ptr + ncl, sizeof(total), cudaMemcpyDeviceToHost, s));
     GS_CUDA(cudaStreamSynchronize(s));
     if (total >= (1ll << 31)) return fail(GS_ERR_UNSUPPORTED, "slab lists exceed 2^31 entries");
-    GS_CUDA(L.list.ensure((size_t)std::max<long long>(total, 1)));
+    GS_CUDA(grow(L.list, (size_t)std::max<long long>(total, 1)));
     sl = slab_lists(ctx);
     slab_list_fill(sl, n_loc, ncl, L.tpl, L.own_begin, s);
     GS_CUDA(cudaGetLastError());

@@ -675,41 +675,56 @@ __global__ void __launch_bounds__(kVBB) k_verlet_fill_grp(const float2* __restri
 #pragma unroll
         for (int q = 0; q < kVQ; ++q) { pa[q] = na[q]; pb[q] = nb[q]; }
         if (yy < y_last) row_ranges(yy + 1, na, nb, nA, nB);
-        int A = 0x7fffffff, B = -1;
+        int A = 0x7fffffff, B = -1, span = 0;
 #pragma unroll
         for (int q = 0; q < kVQ; ++q)
-            if (pb[q] > pa[q] || pa[q] != 0) { A = min(A, pa[q]); B = max(B, pb[q]); }
-        for (int base = A; base < B; base += 32) {
-            const int pos = base + lane;
-            float2 f = make_float2(0.0f, 0.0f);
-            if (pos < B) f = Sf[pos];
+            if (pb[q] > pa[q] || pa[q] != 0) { A = min(A, pa[q]); B = max(B, pb[q]); span += pb[q] - pa[q]; }
+        // candidates [a, b) tested against the clusters in qmask, appended in position order
+        auto sweep_range = [&](int a, int b, unsigned qmask) {
+            for (int base = a; base < b; base += 32) {
+                const int pos = base + lane;
+                float2 f = make_float2(0.0f, 0.0f);
+                if (pos < b) f = Sf[pos];
 #if GS_VERLET_FILL_F32X2
-            const unsigned long long fxx = f32x2_splat(f.x), fyy = f32x2_splat(f.y);
+                const unsigned long long fxx = f32x2_splat(f.x), fyy = f32x2_splat(f.y);
 #endif
 #pragma unroll
-            for (int q = 0; q < kVQ; ++q) {
+                for (int q = 0; q < kVQ; ++q) {
+                    if (!((qmask >> q) & 1u)) continue;  // warp-uniform
 #if GS_VERLET_FILL_F32X2
-                // both members at once on the packed FP32 pipe (FADD2 / FMUL2 / FFMA2): the same
-                // roundings as fmaf(dx, dx, dy * dy) per member
-                const unsigned long long dx2 = f32x2_sub(qx2[q], fxx), dy2 = f32x2_sub(qy2[q], fyy);
-                const unsigned long long d22 = f32x2_fma(dx2, dx2, f32x2_mul(dy2, dy2));
-                const float d2 = fminf(fminf(INFINITY, f32x2_lo(d22)), f32x2_hi(d22));
+                    // both members at once on the packed FP32 pipe (FADD2 / FMUL2 / FFMA2): the
+                    // same roundings as fmaf(dx, dx, dy * dy) per member
+                    const unsigned long long dx2 = f32x2_sub(qx2[q], fxx), dy2 = f32x2_sub(qy2[q], fyy);
+                    const unsigned long long d22 = f32x2_fma(dx2, dx2, f32x2_mul(dy2, dy2));
+                    const float d2 = fminf(fminf(INFINITY, f32x2_lo(d22)), f32x2_hi(d22));
 #else
-                float d2 = INFINITY;
+                    float d2 = INFINITY;
 #pragma unroll
-                for (int m = 0; m < kVM; ++m) {
-                    const int t = q * kVM + m;
-                    const float dx = qfx[t] - f.x, dy = qfy[t] - f.y;
-                    d2 = fminf(d2, fmaf(dx, dx, dy * dy));
-                }
+                    for (int m = 0; m < kVM; ++m) {
+                        const int t = q * kVM + m;
+                        const float dx = qfx[t] - f.x, dy = qfy[t] - f.y;
+                        d2 = fminf(d2, fmaf(dx, dx, dy * dy));
+                    }
 #endif
-                const bool acc = (pos >= pa[q]) & (pos < pb[q]) & !(d2 >= rc2f);  // NaN radius: keep
-                const unsigned bal = __ballot_sync(kFull, acc);
-                GS_ASSERT(!acc || (pos < n && wpos[q] + __popc(bal) <= ofs[c0 + q + 1]));
-                const int at = wpos[q] + __popc(bal & lt);
-                if (acc) list[at] = pos;
-                wpos[q] += __popc(bal);
+                    const bool acc = (pos >= pa[q]) & (pos < pb[q]) & !(d2 >= rc2f);  // NaN radius: keep
+                    const unsigned bal = __ballot_sync(kFull, acc);
+                    GS_ASSERT(!acc || (pos < n && wpos[q] + __popc(bal) <= ofs[c0 + q + 1]));
+                    const int at = wpos[q] + __popc(bal & lt);
+                    if (acc) list[at] = pos;
+                    wpos[q] += __popc(bal);
+                }
             }
+        };
+        // clusters far apart in the row (the group wraps to the next cell row: one cluster at the
+        // row's end, the next at its start) would sweep the whole row between them — a warp
+        // hundreds of rounds long that sets the kernel's tail; sweep their ranges one by one
+        // instead (each cluster still gets its candidates in position order: the same lists)
+        if (B - A <= 2 * span + 64) {
+            sweep_range(A, B, (1u << kVQ) - 1u);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kVQ; ++q)
+                if (pb[q] > pa[q]) sweep_range(pa[q], pb[q], 1u << q);
         }
     }
 #pragma unroll
