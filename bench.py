@@ -456,14 +456,19 @@ def main():
 
 
 def _timed(torch, fn, reps):
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    s.record()
-    for _ in range(reps):
+    """(last result, median ms per call): each call between its own pair of events on the stream
+    (the median drops calls a host-side stall of the Python process stretched)."""
+    ts = []
+    out = None
+    for _ in range(max(3, reps)):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
         out = fn()
-    e.record()
-    torch.cuda.synchronize()
-    return out, s.elapsed_time(e) / reps
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return out, statistics.median(ts)
 
 
 def _accepted_pairs(fn, torch):
@@ -516,7 +521,7 @@ def run_extras(a, gs, device, configs, torch, world, rank, dist, sharded_run):
                 # the first calls of a new size allocate the multi-GB list buffer and capture the graphs
                 for _ in range(2):
                     device.evolve(sp, qk, pk, tf, steps)
-                _, ms = _timed(torch, lambda: device.evolve(sp, qk, pk, tf, steps), 3)
+                _, ms = _timed(torch, lambda: device.evolve(sp, qk, pk, tf, steps), 5)
                 _, acc, pair_ms = _accepted_pairs(lambda: device.evolve(sp, qk, pk, tf, steps), torch)
                 # the match loop's conditional graph is captured on its first call: warm it up
                 device.match(sp, wk.q, wk.target, wk.h, wk.epsilon, 1, wk.stop_rule, "max", wk.t_final, wk.steps)
