@@ -306,7 +306,6 @@ int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, c
     GS_CUDA(ctx->v_len.ensure(ncl)); GS_CUDA(ctx->v_inv.ensure(n));
     GS_CUDA(ctx->v_flags.ensure(4)); GS_CUDA(ctx->v_over.ensure(1));
     GS_CUDA(ctx->v_scan.ensure(verlet_scan_bytes(ncl)));
-    if (ctx->v_dx.cap < (size_t)n) GS_CUDA(ctx->v_dx.ensure(n));  // displacements for the relative rebuild trigger
     {
         const size_t box = 4 * (size_t)cell_cap(n);
         if (ctx->v_box.cap < box) {
@@ -548,7 +547,7 @@ void verlet_sweep(gs_context* ctx, const SysConst& sc, const CellWs& w, unsigned
 VerletFuse verlet_fuse(gs_context* ctx, const SysConst& sc, cudaStream_t stream) {
     VerletWs v = verlet_ws(ctx, ctx->n, sc.cutoff);
     const double thr = 0.5 * v.skin * sc.cutoff;
-    VerletFuse f{ctx->c_Ss.ptr, ctx->v_inv.ptr, ctx->v_xb.ptr, thr * thr * (1.0 - 1e-9), ctx->v_flags.ptr, {}, 0, nullptr};
+    VerletFuse f{ctx->c_Ss.ptr, ctx->v_inv.ptr, ctx->v_xb.ptr, thr * thr * (1.0 - 1e-9), ctx->v_flags.ptr, {}, 0, 0};
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(stream, &cs);
     if (cs == cudaStreamCaptureStatusActive) {
@@ -611,9 +610,9 @@ void stage(gs_context* ctx, const SysConst& sc, int step, int s, double dt, cuda
         if (!last) {
             VerletFuse f = verlet_fuse(ctx, sc, stream);
             if (ctx->verlet_rel) {  // rebuild on the relative displacement of neighbours (gs_verlet.cu)
-                f.dX = ctx->v_dx.ptr;
+                f.defer = 1;
                 launch_finish_verlet(sc, fa, f, stream);
-                launch_verlet_trigger(w, v, n, ctx->v_dx.ptr, ctx->v_box.ptr, (int64_t)ctx->v_box.cap, f.cond,
+                launch_verlet_trigger(w, v, n, ctx->v_box.ptr, (int64_t)ctx->v_box.cap, f.cond,
                                       f.use_cond, stream);
                 ctx->launches++;
             } else {
@@ -647,7 +646,7 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
             P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes, (double)ctx->verlet_call,
             P(ctx->v_cnt.ptr), P(ctx->v_ofs.ptr), P(ctx->v_len.ptr), P(ctx->v_inv.ptr), P(ctx->v_list.ptr), (double)ctx->v_list.cap, P(ctx->v_xb.ptr),
             P(ctx->v_flags.ptr), P(ctx->v_over.ptr), P(ctx->v_scan.ptr), ctx->verlet_skin, (double)ctx->verlet_fuse_max_n,
-            P(ctx->v_dx.ptr), P(ctx->v_box.ptr), (double)ctx->v_box.cap, (double)ctx->verlet_rel};
+            P(ctx->v_box.ptr), (double)ctx->v_box.cap, (double)ctx->verlet_rel};
 }
 
 // integrator.py:95-119 as one CUDA graph (4 x steps stages, ~2 kernels per dense stage and
@@ -910,7 +909,7 @@ int gs_destroy(gs_context* ctx) {
     if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_inv.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
-    ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release(); ctx->v_dx.release(); ctx->v_box.release();
+    ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release(); ctx->v_box.release();
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Ss2.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     gs_p2p_close(ctx);

@@ -133,11 +133,12 @@ int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n
 // Ss <- S in sorted order and the rebuild decision (force: no gather, rebuild) -> IF condition / flags[3].
 void verlet_gather(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, int force,
                    cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream);
-// The rebuild decision of large clouds from the stage's displacements dX (sorted slots, written by
-// the separate list epilogue): relative displacement of neighbours over coarse cells of edge 2 rl
-// (gs_verlet.cu k_verlet_trigger) -> flags[3] / the next stage's IF condition.  box: box_cap u32
-// (4 per coarse cell) of scratch, empty between calls (verlet_box_reset once at allocation).
-void launch_verlet_trigger(const CellWs& w, const VerletWs& v, int64_t n, const double2* dX, unsigned* box,
+// The rebuild decision of large clouds from the stage's displacements (the sorted records w.Ss the
+// separate list epilogue wrote, against the build positions v.Xb): relative displacement of
+// neighbours over coarse cells of edge 2 rl (gs_verlet.cu k_verlet_trigger) -> flags[3] / the next
+// stage's IF condition.  box: box_cap u32 (4 per coarse cell) of scratch, empty between calls
+// (verlet_box_reset once at allocation).
+void launch_verlet_trigger(const CellWs& w, const VerletWs& v, int64_t n, unsigned* box,
                            int64_t box_cap, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream);
 void verlet_box_reset(unsigned* box, int64_t cells, cudaStream_t stream);
 // Raw pair sums of all n rows from the lists -> part[i] (original index).

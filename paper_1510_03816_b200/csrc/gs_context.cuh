@@ -151,7 +151,6 @@ struct gs_context {
     double verlet_skin = -1.0;          // GS_B200_SKIN (< 0: by n, see verlet_ws)
     int64_t verlet_fuse_max_n = 131072; // lists: epilogue fused into the sweep below this n (GS_B200_VERLET_FUSE_MAX_N)
     int verlet_rel = 1;                 // large clouds: rebuild on neighbours' relative displacement (GS_B200_VERLET_REL)
-    DevBuf<double2> v_dx;               // displacements since the build (sorted slots)
     DevBuf<unsigned> v_box;             // coarse-cell displacement boxes (k_verlet_trigger)
     double verlet_slack = 1.5;          // list buffer = (1 + slack) x the sizing build (GS_B200_VERLET_SLACK)
     cudaStream_t cap_stream2 = nullptr; // captures the conditional rebuild bodies

@@ -333,12 +333,13 @@ __global__ void __launch_bounds__(256) k_finish_verlet(SysConst sc, FinishArgs a
         const int64_t k = f.inv ? (int64_t)f.inv[i] : li;  // slab path (gs_slab.cu): rows already in sorted order
         GS_ASSERT(k >= 0 && k < a.nrows);
         if (f.Ss) f.Ss[k] = nxt;
-        const double2 b = f.Xb[k];
-        const double dx = nxt.x - b.x, dy = nxt.y - b.y;
-        if (f.dX) f.dX[k] = make_double2(dx, dy);
-        else need = fma(dx, dx, dy * dy) > f.thr2;
+        if (!f.defer) {
+            const double2 b = f.Xb[k];
+            const double dx = nxt.x - b.x, dy = nxt.y - b.y;
+            need = fma(dx, dx, dy * dy) > f.thr2;
+        }
     }
-    if (f.dX) return;  // the trigger kernel decides
+    if (f.defer) return;  // the trigger kernel decides
     if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&f.flags[0], 1u);
     if (threadIdx.x == 0) {
         __threadfence();

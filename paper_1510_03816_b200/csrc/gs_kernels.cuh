@@ -192,8 +192,8 @@ struct VerletFuse {
     unsigned* flags;
     cudaGraphConditionalHandle cond;
     int use_cond;
-    double2* dX;  // non-null: store each particle's displacement since the build (sorted slot) and
-                  // leave the rebuild decision to launch_verlet_trigger (gs_verlet.cu)
+    int defer;    // 1: only store the sorted record; launch_verlet_trigger (gs_verlet.cu) reads it in
+                  // sorted order with the build position and decides
 };
 void launch_finish_verlet(const SysConst& sc, const FinishArgs& a, const VerletFuse& f, cudaStream_t stream);
 // Stage epilogue of rows [row0, row0 + nrows) from the raw row sums of all `world` ranks

@@ -869,7 +869,8 @@ __device__ __forceinline__ float funkey(unsigned k) {
 constexpr unsigned kBoxEmptyMin = 0xffffffffu, kBoxEmptyMax = 0u;
 
 struct TriggerArgs {
-    const double2* dX;
+    const double4* Ss;         // the stage's records in sorted order
+    const double2* Xb;         // their positions at the build
     const unsigned* keys;      // the build's sorted cell keys (cell above GS_CELL_SUBKEY bits)
     const GridParams* gp;
     int64_t n;
@@ -883,6 +884,8 @@ struct TriggerArgs {
     int use_cond;
 };
 
+// Phase 1 (one thread per particle, sorted order): the coarse cells' displacement boxes (or, without
+// coarse cells, the blanket rule straight into flags[0]).
 __global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
     const GridParams g = *t.gp;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -892,7 +895,11 @@ __global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
     const bool coarse = !g.hashed && (int64_t)ncx * ncy * 4 <= t.cap;
     bool need = false;
     double2 d = make_double2(0.0, 0.0);
-    if (valid) d = t.dX[k];
+    if (valid) {
+        const double4 x = t.Ss[k];
+        const double2 b = t.Xb[k];
+        d = make_double2(x.x - b.x, x.y - b.y);
+    }
     if (!coarse) {
         need = valid && fma(d.x, d.x, d.y * d.y) > t.thr2;
     } else {
@@ -916,6 +923,50 @@ __global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
         }
     }
     if (__syncthreads_or(need) && threadIdx.x == 0) atomicOr(&t.flags[0], 1u);
+}
+
+// Phase 2 (grid-stride over the coarse cells, kTrigCheckCtas CTAs): every cell against itself and
+// its forward neighbours, all eight box words loaded before any test (one L2 round trip per
+// cell, where the last CTA of a single kernel used to walk every cell with a dependent load chain
+// — 45 of the 60 us of the C5 trigger); the last CTA empties the boxes and decides.
+constexpr int kTrigCheckCtas = 148;
+__global__ void __launch_bounds__(256) k_verlet_trigger_check(TriggerArgs t) {
+    const GridParams g = *t.gp;
+    const int fct = 2 * max(g.sub, 1);
+    const int ncx = g.hashed ? 1 : (g.nx + fct - 1) / fct, ncy = g.hashed ? 1 : (g.ny + fct - 1) / fct;
+    const bool coarse = !g.hashed && (int64_t)ncx * ncy * 4 <= t.cap;
+    const int ncell = coarse ? ncx * ncy : 0;
+    bool bad = false;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        const uint4 a = __ldcg(reinterpret_cast<const uint4*>(t.box) + c);
+        const int cx = c % ncx, cy = c / ncx;
+        const int nb[4][2] = {{1, 0}, {-1, 1}, {0, 1}, {1, 1}};
+        uint4 e[4];
+        bool ok[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ex = cx + nb[q][0], ey = cy + nb[q][1];
+            ok[q] = ex >= 0 && ex < ncx && ey < ncy;
+            e[q] = ok[q] ? __ldcg(reinterpret_cast<const uint4*>(t.box) + ((int64_t)ey * ncx + ex))
+                         : make_uint4(kBoxEmptyMin, kBoxEmptyMax, kBoxEmptyMin, kBoxEmptyMax);
+        }
+        if (a.x == kBoxEmptyMin) continue;
+        const float ax0 = funkey(a.x), ax1 = funkey(a.y), ay0 = funkey(a.z), ay1 = funkey(a.w);
+        const double mx = fmax(fabs((double)ax0), fabs((double)ax1)), my = fmax(fabs((double)ay0), fabs((double)ay1));
+        bad |= fma(mx, mx, my * my) >= t.mlim2;
+        {   // the cell itself
+            const double wx = (double)ax1 - (double)ax0, wy = (double)ay1 - (double)ay0;
+            bad |= fma(wx, wx, wy * wy) >= t.lim2;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!ok[q] || e[q].x == kBoxEmptyMin) continue;
+            const double wx = (double)fmaxf(ax1, funkey(e[q].y)) - (double)fminf(ax0, funkey(e[q].x));
+            const double wy = (double)fmaxf(ay1, funkey(e[q].w)) - (double)fminf(ay0, funkey(e[q].z));
+            bad |= fma(wx, wx, wy * wy) >= t.lim2;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&t.flags[0], 1u);
     __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
         __threadfence();
@@ -923,39 +974,13 @@ __global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
     }
     __syncthreads();
     if (!s_last) return;
-    // the last CTA: every box is in; check the neighbour pairs, reset the boxes, decide
+    // the last CTA: every check is done; empty the boxes for the next stage and decide
     __threadfence();
-    bool bad = false;
-    if (coarse) {
-        const int ncell = ncx * ncy;
-        for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
-            volatile unsigned* b = t.box + 4 * (int64_t)c;
-            if (b[0] == kBoxEmptyMin) continue;
-            const float ax0 = funkey(b[0]), ax1 = funkey(b[1]), ay0 = funkey(b[2]), ay1 = funkey(b[3]);
-            const double mx = fmax(fabs((double)ax0), fabs((double)ax1)), my = fmax(fabs((double)ay0), fabs((double)ay1));
-            bad |= fma(mx, mx, my * my) >= t.mlim2;
-            const int cx = c % ncx, cy = c / ncx;
-            const int nb[5][2] = {{0, 0}, {1, 0}, {-1, 1}, {0, 1}, {1, 1}};
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                const int ex = cx + nb[q][0], ey = cy + nb[q][1];
-                if (ex < 0 || ex >= ncx || ey >= ncy) continue;
-                volatile unsigned* e = t.box + 4 * ((int64_t)ey * ncx + ex);
-                if (e[0] == kBoxEmptyMin) continue;
-                const double wx = (double)fmaxf(ax1, funkey(e[1])) - (double)fminf(ax0, funkey(e[0]));
-                const double wy = (double)fmaxf(ay1, funkey(e[3])) - (double)fminf(ay0, funkey(e[2]));
-                bad |= fma(wx, wx, wy * wy) >= t.lim2;
-            }
-        }
-        __syncthreads();
-        for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
-            unsigned* b = t.box + 4 * (int64_t)c;
-            b[0] = kBoxEmptyMin; b[1] = kBoxEmptyMax; b[2] = kBoxEmptyMin; b[3] = kBoxEmptyMax;
-        }
-    }
-    const bool any = __syncthreads_or(bad);
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x)
+        reinterpret_cast<uint4*>(t.box)[c] = make_uint4(kBoxEmptyMin, kBoxEmptyMax, kBoxEmptyMin, kBoxEmptyMax);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned dflag = (atomicExch(&t.flags[0], 0u) != 0u || any) ? 1u : 0u;
+        const unsigned dflag = atomicExch(&t.flags[0], 0u) != 0u ? 1u : 0u;
         t.flags[2] = 0u;
         if (t.use_cond) cudaGraphSetConditional(t.cond, dflag);
         t.flags[3] = dflag;
@@ -973,17 +998,18 @@ void verlet_box_reset(unsigned* box, int64_t cells, cudaStream_t stream) {
     if (cells > 0) k_box_reset<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(box, cells);
 }
 
-void launch_verlet_trigger(const CellWs& w, const VerletWs& v, int64_t n, const double2* dX, unsigned* box,
+void launch_verlet_trigger(const CellWs& w, const VerletWs& v, int64_t n, unsigned* box,
                            int64_t box_cap, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream) {
     TriggerArgs t;
-    t.dX = dX; t.keys = w.keys_sorted; t.gp = w.gp; t.n = n; t.box = box; t.cap = box_cap;
+    t.Ss = w.Ss; t.Xb = v.Xb; t.keys = w.keys_sorted; t.gp = w.gp; t.n = n; t.box = box; t.cap = box_cap;
     const double lim = v.skin * v.cutoff, rl = v.cutoff * (1.0 + v.skin), mlim = 0.5 * (2.0 * rl - v.cutoff);
     t.lim2 = lim * lim * (1.0 - 1e-6);
     t.mlim2 = mlim * mlim * (1.0 - 1e-6);
     const double thr = 0.5 * v.skin * v.cutoff;
     t.thr2 = thr * thr * (1.0 - 1e-9);
     t.flags = v.flags; t.cond = cond; t.use_cond = use_cond;
-    k_verlet_trigger<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(t);
+    if (n > 0) k_verlet_trigger<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(t);
+    k_verlet_trigger_check<<<kTrigCheckCtas, 256, 0, stream>>>(t);
 }
 
 namespace {

@@ -28,15 +28,19 @@ def child(out: str, which: str):
     from paper_1510_03816_b200 import configs, device
 
     def timed(fn, reps):
+        """(last result, median ms per call; each call between its own events after 2 warm-ups)"""
         fn()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        s.record()
-        for _ in range(reps):
+        fn()
+        ts = []
+        for _ in range(max(3, reps)):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s.record()
             r = fn()
-        e.record()
-        torch.cuda.synchronize()
-        return r, s.elapsed_time(e) / reps
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e))
+        return r, float(np.median(ts))
 
     res, arrays = {}, {}
     w = configs.c2()
