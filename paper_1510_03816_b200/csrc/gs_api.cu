@@ -291,6 +291,9 @@ VerletWs verlet_ws(gs_context* ctx, int64_t n, double cutoff) {
     v.tpl = verlet_tpl(n);
     v.skin = ctx->verlet_skin >= 0.0 ? ctx->verlet_skin : (n < 131072 ? 0.1 : 0.05);
     v.cutoff = cutoff;
+    // the relative-trigger path (no fused epilogue) adapts the skin to the observed rebuild rate
+    const bool adapt = ctx->skin_adapt && ctx->verlet_rel && ctx->verlet_skin < 0.0 && n >= ctx->verlet_fuse_max_n;
+    v.skin_ctl = adapt && ctx->v_skin.cap >= 2 ? ctx->v_skin.ptr : nullptr;
     v.Ss_pair[0] = ctx->c_Ss.ptr;
     v.Ss_pair[1] = ctx->c_Ss2.cap >= (size_t)(n + 1) ? ctx->c_Ss2.ptr : nullptr;
     return v;
@@ -304,7 +307,7 @@ int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, c
     const bool fresh = ctx->v_flags.cap == 0;
     GS_CUDA(ctx->v_cnt.ensure(ncl + 1)); GS_CUDA(ctx->v_ofs.ensure(ncl + 1)); GS_CUDA(ctx->v_xb.ensure(n));
     GS_CUDA(ctx->v_len.ensure(ncl)); GS_CUDA(ctx->v_inv.ensure(n));
-    GS_CUDA(ctx->v_flags.ensure(4)); GS_CUDA(ctx->v_over.ensure(1));
+    GS_CUDA(ctx->v_flags.ensure(kVerletFlags)); GS_CUDA(ctx->v_over.ensure(1)); GS_CUDA(ctx->v_skin.ensure(2));
     GS_CUDA(ctx->v_scan.ensure(verlet_scan_bytes(ncl)));
     {
         const size_t box = 4 * (size_t)cell_cap(n);
@@ -316,12 +319,15 @@ int ensure_verlet(gs_context* ctx, const double4* S, int64_t n, double cutoff, c
     GS_CUDA(ctx->c_Ss2.ensure(n + 1));  // the ping-pong half of the sorted records (fused epilogue);
                                         // every list build writes the sentinel record [n] into both halves
     if (fresh) {
-        GS_CUDA(cudaMemsetAsync(ctx->v_flags.ptr, 0, 4 * sizeof(unsigned), s));
+        GS_CUDA(cudaMemsetAsync(ctx->v_flags.ptr, 0, kVerletFlags * sizeof(unsigned), s));
         GS_CUDA(cudaMemsetAsync(ctx->v_over.ptr, 0, sizeof(unsigned long long), s));
     }
     GS_CUDA(cudaMemsetAsync(ctx->v_cnt.ptr + ncl, 0, sizeof(long long), s));
-    if (ctx->v_list.cap > 0 && ctx->v_list_n == n && ctx->v_list_cutoff == cutoff) return GS_OK;
     VerletWs v = verlet_ws(ctx, n, cutoff);
+    if (v.skin_ctl) verlet_skin_init(v.skin_ctl, v.skin, s);  // every call starts from the default skin
+    if (ctx->v_list.cap > 0 && ctx->v_list_n == n && ctx->v_list_cutoff == cutoff) return GS_OK;
+    if (v.skin_ctl) v.skin = std::max(v.skin, kSkinMax);  // size for the largest skin it may adapt to
+    v.skin_ctl = nullptr;
     v.cap = 0;  // sizing build: counts and offsets only
     if (int rc = verlet_build(cell_ws(ctx), v, S, n, cutoff, s)) return fail(GS_ERR_CUDA, "verlet sizing build failed");
     long long total = 0;
@@ -646,7 +652,8 @@ std::vector<double> graph_key(gs_context* ctx, const SysConst& sc, double dt, in
             P(ctx->c_nsel.ptr), P(ctx->tbl.ptr), (double)ctx->c_cub_bytes, (double)ctx->verlet_call,
             P(ctx->v_cnt.ptr), P(ctx->v_ofs.ptr), P(ctx->v_len.ptr), P(ctx->v_inv.ptr), P(ctx->v_list.ptr), (double)ctx->v_list.cap, P(ctx->v_xb.ptr),
             P(ctx->v_flags.ptr), P(ctx->v_over.ptr), P(ctx->v_scan.ptr), ctx->verlet_skin, (double)ctx->verlet_fuse_max_n,
-            P(ctx->v_box.ptr), (double)ctx->v_box.cap, (double)ctx->verlet_rel};
+            P(ctx->v_box.ptr), (double)ctx->v_box.cap, (double)ctx->verlet_rel, P(ctx->v_skin.ptr),
+            (double)ctx->skin_adapt};
 }
 
 // integrator.py:95-119 as one CUDA graph (4 x steps stages, ~2 kernels per dense stage and
@@ -870,6 +877,7 @@ int gs_create(gs_context** out, int device) {
     if (const char* g = std::getenv("GS_B200_SKIN")) ctx->verlet_skin = std::atof(g);
     if (const char* g = std::getenv("GS_B200_VERLET_FUSE_MAX_N")) ctx->verlet_fuse_max_n = std::atoll(g);
     if (const char* g = std::getenv("GS_B200_VERLET_REL")) ctx->verlet_rel = std::atoi(g);
+    if (const char* g = std::getenv("GS_B200_SKIN_ADAPT")) ctx->skin_adapt = std::atoi(g);
     if (const char* g = std::getenv("GS_B200_VERLET_SLACK")) ctx->verlet_slack = std::atof(g);  // tests
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     // 2^(j/256), j = 0..255, rounded from long double
@@ -909,7 +917,7 @@ int gs_destroy(gs_context* ctx) {
     if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
     for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
     ctx->v_cnt.release(); ctx->v_list.release(); ctx->v_len.release(); ctx->v_inv.release(); ctx->v_ofs.release(); ctx->v_xb.release(); ctx->v_flags.release();
-    ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release(); ctx->v_box.release();
+    ctx->v_over.release(); ctx->v_scan.release(); ctx->cg.release(); ctx->v_box.release(); ctx->v_skin.release();
     ctx->c_keys.release(); ctx->c_keys_sorted.release(); ctx->c_vals.release(); ctx->c_perm.release();
     ctx->c_start.release(); ctx->c_Ss.release(); ctx->c_Ss2.release(); ctx->c_Sf.release(); ctx->c_bbox.release(); ctx->c_gp.release(); ctx->c_cub.release();
     gs_p2p_close(ctx);

@@ -129,7 +129,8 @@ __device__ GridParams grid_params_of(double mnx, double mny, double mxx, double 
 }
 
 __global__ void k_grid_params(const double* __restrict__ red, int nb, double cutoff, int64_t cap, int sub_max,
-                              GridParams* gp) {
+                              GridParams* gp, const double* __restrict__ skin_ctl, double base_cutoff) {
+    if (skin_ctl) cutoff = base_cutoff * (1.0 + skin_ctl[0]);  // adaptive list skin (gs_verlet.cu)
     __shared__ double s[4][kBB];
     __shared__ int s_bad;
     if (threadIdx.x == 0) s_bad = 0;
@@ -492,11 +493,12 @@ void slab_grid(const double* b4, double cutoff, int64_t n_glob, GridParams* gp, 
     k_grid_from_b4<<<1, 1, 0, stream>>>(b4, cutoff, cell_cap(n_glob), cell_sub_max(), gp);
 }
 
-int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream) {
+int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream,
+               const double* skin_ctl, double base_cutoff) {
     const int nb = (int)std::min<int64_t>(kCellBboxBlocks, (n + kBB - 1) / kBB);
     k_bbox_partial<<<nb, kBB, 0, stream>>>(S, n, w.bbox_red);
     const int64_t cap = cell_cap(n);
-    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, cell_sub_max(), w.gp);
+    k_grid_params<<<1, kBB, 0, stream>>>(w.bbox_red, nb, cutoff, cap, cell_sub_max(), w.gp, skin_ctl, base_cutoff);
     const unsigned blocks = (unsigned)((n + 255) / 256);
     k_cell_keys<<<blocks, 256, 0, stream>>>(S, n, w.gp, w.keys, w.vals);
     int end_bit = 1;

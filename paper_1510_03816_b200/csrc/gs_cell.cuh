@@ -78,7 +78,9 @@ size_t cell_cub_bytes(int64_t n);
 int64_t cell_cap(int64_t n);
 // Builds the grid for the n records of S (positions of the current stage).  Returns a
 // cudaError_t value (0 on success).
-int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream);
+// skin_ctl (device, optional): the grid is built for base_cutoff (1 + skin_ctl[0]) instead of cutoff
+int cell_build(const CellWs& w, const double4* S, int64_t n, double cutoff, cudaStream_t stream,
+               const double* skin_ctl = nullptr, double base_cutoff = 0.0);
 // Raw pair sums of the targets with original index in [row0, row1) -> part[i - row0].
 // `accepted` (nullable) accumulates the number of evaluated pairs (d < cutoff, self included).
 void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t row0, int64_t row1, double4* part,
@@ -89,6 +91,12 @@ void launch_cell_pair(const SysConst& sc, const CellWs& w, int64_t n, int64_t ro
 // Clusters of GS_VERLET_M consecutive sorted particles; one list per cluster of the sorted
 // positions within cutoff (1 + skin) of any member at the last build, reused until a particle has
 // moved half the skin.
+constexpr int kVerletFlags = 8;     // words of VerletWs::flags
+// Adaptive skin (relative trigger path, gs_verlet.cu k_verlet_trigger_check): bounds and the
+// cost ratio (one list build / one pair sweep) of its model.
+constexpr double kSkinMin = 0.03, kSkinMax = 0.12, kSkinCostRatio = 0.67;
+// Device {skin, rate} reset to {skin0, 0} (start of every call: results depend only on the call).
+void verlet_skin_init(double* skin_ctl, double skin0, cudaStream_t stream);
 struct VerletWs {
     long long* cnt;                // ncl + 1 (cnt[ncl] = 0): list capacities (candidate counts, padded)
     long long* ofs;                // ncl + 1: exclusive scan of cnt (ofs[ncl] = entries of the build)
@@ -97,13 +105,16 @@ struct VerletWs {
     int64_t cap;
     double2* Xb;                   // n: positions at the build, sorted order
     int* inv;                      // n: original index -> sorted slot
-    unsigned* flags;               // [0] rebuild wanted, [2] CTA counter, [3] last decision (zero-initialised)
+    unsigned* flags;               // [0] rebuild wanted, [1] builds, [2] CTA counter, [3] last decision,
+                                   // [4] RHS since the build (zero-initialised, kVerletFlags words)
     unsigned long long* overflow;  // entries a build needed beyond cap (0: none)
     void* scan_temp;
     size_t scan_bytes;
     int tpl;                       // pair-sweep lanes per cluster (lists padded to 2 tpl)
     double skin;                   // list radius = cutoff (1 + skin); rebuild at skin * cutoff / 2
     double cutoff;
+    double* skin_ctl;              // device {skin, RHS per unit skin}: the adaptive skin of the relative
+                                   // trigger's path (verlet_skin_adapt); nullptr: the fixed `skin`
     double4* Ss_pair[2];           // both halves of the sorted-record ping-pong: the sentinel goes into each
 };
 // The stage epilogue fused into the list sweep (single rank, all rows): the lane that reduced a

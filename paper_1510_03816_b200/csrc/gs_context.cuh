@@ -149,6 +149,8 @@ struct gs_context {
     double v_list_cutoff = 0.0;
     int verlet_retries = 0;
     double verlet_skin = -1.0;          // GS_B200_SKIN (< 0: by n, see verlet_ws)
+    int skin_adapt = 1;                 // GS_B200_SKIN_ADAPT: adaptive skin on the relative-trigger path
+    DevBuf<double> v_skin;              // its device state {skin, RHS per unit skin}
     int64_t verlet_fuse_max_n = 131072; // lists: epilogue fused into the sweep below this n (GS_B200_VERLET_FUSE_MAX_N)
     int verlet_rel = 1;                 // large clouds: rebuild on neighbours' relative displacement (GS_B200_VERLET_REL)
     DevBuf<unsigned> v_box;             // coarse-cell displacement boxes (k_verlet_trigger)

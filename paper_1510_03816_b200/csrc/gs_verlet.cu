@@ -794,6 +794,12 @@ __global__ void k_verlet_sentinel(double4* Ss, double4* Ss0, double4* Ss1, int64
     if (Ss1) Ss1[n] = far_record(0);
     flags[1] += 1u;  // builds so far (diagnostics)
     flags[2] = 0u;   // decision counter (a failed evolve may have left CTAs uncounted)
+    flags[4] = 0u;   // RHS since the build (the adaptive skin's interval)
+}
+
+__global__ void k_skin_init(double* c, double s0) {
+    c[0] = s0;
+    c[1] = 0.0;
 }
 
 }  // namespace
@@ -824,7 +830,7 @@ size_t verlet_scan_bytes(int64_t ncl) {
 
 int verlet_build(const CellWs& w, const VerletWs& v, const double4* S, int64_t n, double cutoff, cudaStream_t stream) {
     const double rl = cutoff * (1.0 + v.skin);
-    int rc = cell_build(w, S, n, rl, stream);
+    int rc = cell_build(w, S, n, rl, stream, v.skin_ctl, cutoff);
     if (rc) return rc;
     k_verlet_sentinel<<<1, 1, 0, stream>>>(w.Ss, v.Ss_pair[0], v.Ss_pair[1], n, v.flags);
     const int64_t ncl = verlet_clusters(n);
@@ -876,13 +882,42 @@ struct TriggerArgs {
     int64_t n;
     unsigned* box;             // 4 per coarse cell: min x, max x, min y, max y (keys); capacity `cap`
     int64_t cap;
-    double lim2;               // (skin cutoff)^2, slightly reduced
-    double mlim2;              // ((L - cutoff) / 2)^2, slightly reduced
-    double thr2;               // blanket rule (hashed grid): (skin cutoff / 2)^2
+    double skin, cutoff;       // the list's skin (skin_ctl[0] when adaptive) and the kernel cutoff
+    double* skin_ctl;          // adaptive skin {skin, RHS per unit skin} (nullptr: fixed)
     unsigned* flags;
     cudaGraphConditionalHandle cond;
     int use_cond;
 };
+
+// The trigger's thresholds for the current list's skin: lim2 = (skin cutoff)^2, mlim2 =
+// ((L - cutoff) / 2)^2 with L = 2 rl, both slightly reduced; thr2 = the blanket rule's
+// (skin cutoff / 2)^2 (hashed grids).
+struct TriggerLimits {
+    double lim2, mlim2, thr2;
+};
+__device__ __forceinline__ TriggerLimits trigger_limits(const TriggerArgs& t) {
+    const double skin = t.skin_ctl ? t.skin_ctl[0] : t.skin;
+    const double lim = skin * t.cutoff, rl = t.cutoff * (1.0 + skin), mlim = 0.5 * (2.0 * rl - t.cutoff);
+    const double thr = 0.5 * skin * t.cutoff;
+    return TriggerLimits{lim * lim * (1.0 - 1e-6), mlim * mlim * (1.0 - 1e-6), thr * thr * (1.0 - 1e-9)};
+}
+
+// The adaptive skin (relative trigger path): a rebuild after I RHS on a list of skin s observes
+// a = I / s RHS per unit skin (smoothed over the builds); per RHS the sweep costs ~(1 + s)^2 and
+// the builds ~kSkinCostRatio / (a s) sweeps, minimal where s^2 (1 + s) = kSkinCostRatio / (2 a).
+// The next list's skin moves there (Newton), by at most x1.5 per build, within [kSkinMin,
+// kSkinMax].  Measured optimum (tools/skin_scan.py): C5 ~0.1 (a rebuild every ~2.7 RHS at 0.05),
+// C4 0.03-0.05 (every ~9.5 RHS).
+__device__ void verlet_skin_adapt(double* c, unsigned since) {
+    const double s = c[0];
+    const double a_obs = (double)since / s;
+    const double a = c[1] > 0.0 ? 0.5 * (c[1] + a_obs) : a_obs;
+    c[1] = a;
+    const double K = kSkinCostRatio / (2.0 * a);
+    double x = s;
+    for (int it = 0; it < 8; ++it) x -= (x * x * (1.0 + x) - K) / (x * (2.0 + 3.0 * x));
+    c[0] = fmin(fmax(x, fmax(kSkinMin, s / 1.5)), fmin(kSkinMax, s * 1.5));
+}
 
 // Phase 1 (one thread per particle, sorted order): the coarse cells' displacement boxes (or, without
 // coarse cells, the blanket rule straight into flags[0]).
@@ -894,6 +929,7 @@ __global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
     const int ncx = g.hashed ? 1 : (g.nx + fct - 1) / fct, ncy = g.hashed ? 1 : (g.ny + fct - 1) / fct;
     const bool coarse = !g.hashed && (int64_t)ncx * ncy * 4 <= t.cap;
     bool need = false;
+    const TriggerLimits lm = trigger_limits(t);
     double2 d = make_double2(0.0, 0.0);
     if (valid) {
         const double4 x = t.Ss[k];
@@ -901,7 +937,7 @@ __global__ void __launch_bounds__(256) k_verlet_trigger(TriggerArgs t) {
         d = make_double2(x.x - b.x, x.y - b.y);
     }
     if (!coarse) {
-        need = valid && fma(d.x, d.x, d.y * d.y) > t.thr2;
+        need = valid && fma(d.x, d.x, d.y * d.y) > lm.thr2;
     } else {
         int cc = -1;
         if (valid) {
@@ -936,6 +972,7 @@ __global__ void __launch_bounds__(256) k_verlet_trigger_check(TriggerArgs t) {
     const int ncx = g.hashed ? 1 : (g.nx + fct - 1) / fct, ncy = g.hashed ? 1 : (g.ny + fct - 1) / fct;
     const bool coarse = !g.hashed && (int64_t)ncx * ncy * 4 <= t.cap;
     const int ncell = coarse ? ncx * ncy : 0;
+    const TriggerLimits lm = trigger_limits(t);
     bool bad = false;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
         const uint4 a = __ldcg(reinterpret_cast<const uint4*>(t.box) + c);
@@ -953,17 +990,17 @@ __global__ void __launch_bounds__(256) k_verlet_trigger_check(TriggerArgs t) {
         if (a.x == kBoxEmptyMin) continue;
         const float ax0 = funkey(a.x), ax1 = funkey(a.y), ay0 = funkey(a.z), ay1 = funkey(a.w);
         const double mx = fmax(fabs((double)ax0), fabs((double)ax1)), my = fmax(fabs((double)ay0), fabs((double)ay1));
-        bad |= fma(mx, mx, my * my) >= t.mlim2;
+        bad |= fma(mx, mx, my * my) >= lm.mlim2;
         {   // the cell itself
             const double wx = (double)ax1 - (double)ax0, wy = (double)ay1 - (double)ay0;
-            bad |= fma(wx, wx, wy * wy) >= t.lim2;
+            bad |= fma(wx, wx, wy * wy) >= lm.lim2;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (!ok[q] || e[q].x == kBoxEmptyMin) continue;
             const double wx = (double)fmaxf(ax1, funkey(e[q].y)) - (double)fminf(ax0, funkey(e[q].x));
             const double wy = (double)fmaxf(ay1, funkey(e[q].w)) - (double)fminf(ay0, funkey(e[q].z));
-            bad |= fma(wx, wx, wy * wy) >= t.lim2;
+            bad |= fma(wx, wx, wy * wy) >= lm.lim2;
         }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&t.flags[0], 1u);
@@ -982,6 +1019,9 @@ __global__ void __launch_bounds__(256) k_verlet_trigger_check(TriggerArgs t) {
     if (threadIdx.x == 0) {
         const unsigned dflag = atomicExch(&t.flags[0], 0u) != 0u ? 1u : 0u;
         t.flags[2] = 0u;
+        const unsigned since = t.flags[4] + 1u;  // RHS on this list (k_verlet_sentinel zeroes it)
+        t.flags[4] = since;
+        if (dflag && t.skin_ctl) verlet_skin_adapt(t.skin_ctl, since);
         if (t.use_cond) cudaGraphSetConditional(t.cond, dflag);
         t.flags[3] = dflag;
     }
@@ -994,6 +1034,10 @@ __global__ void k_box_reset(unsigned* box, int64_t cells) {
 }
 }  // namespace
 
+void verlet_skin_init(double* skin_ctl, double skin0, cudaStream_t stream) {
+    k_skin_init<<<1, 1, 0, stream>>>(skin_ctl, skin0);
+}
+
 void verlet_box_reset(unsigned* box, int64_t cells, cudaStream_t stream) {
     if (cells > 0) k_box_reset<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(box, cells);
 }
@@ -1002,11 +1046,7 @@ void launch_verlet_trigger(const CellWs& w, const VerletWs& v, int64_t n, unsign
                            int64_t box_cap, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t stream) {
     TriggerArgs t;
     t.Ss = w.Ss; t.Xb = v.Xb; t.keys = w.keys_sorted; t.gp = w.gp; t.n = n; t.box = box; t.cap = box_cap;
-    const double lim = v.skin * v.cutoff, rl = v.cutoff * (1.0 + v.skin), mlim = 0.5 * (2.0 * rl - v.cutoff);
-    t.lim2 = lim * lim * (1.0 - 1e-6);
-    t.mlim2 = mlim * mlim * (1.0 - 1e-6);
-    const double thr = 0.5 * v.skin * v.cutoff;
-    t.thr2 = thr * thr * (1.0 - 1e-9);
+    t.skin = v.skin; t.cutoff = v.cutoff; t.skin_ctl = v.skin_ctl;
     t.flags = v.flags; t.cond = cond; t.use_cond = use_cond;
     if (n > 0) k_verlet_trigger<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(t);
     k_verlet_trigger_check<<<kTrigCheckCtas, 256, 0, stream>>>(t);

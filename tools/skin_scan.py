@@ -1,7 +1,7 @@
 """Whole device matches of C4 / C5 per Verlet skin (one process per skin: GS_B200_SKIN is read
 when the library context is created).
 
-    python tools/skin_scan.py --config C5 --skins 0.04,0.05,0.075,0.1 [--iters 20]
+    python tools/skin_scan.py --config C5 --skins adaptive,default,0.04,0.05,0.075,0.1 [--iters 20]
 
 Prints, per skin, the seconds per feedback iteration of the second whole match in the process
 (the first allocates the list buffer and captures the graphs) and the list builds per iteration.
@@ -54,7 +54,12 @@ def main():
         print(json.dumps(one(a.config, a.iters)))
         return
     for s in a.skins.split(","):
-        env = dict(os.environ, GS_B200_SKIN=s)
+        # "adaptive": the library's adaptive skin; "default": its fixed default; else a fixed skin
+        env = dict(os.environ)
+        if s == "default":
+            env["GS_B200_SKIN_ADAPT"] = "0"
+        elif s != "adaptive":
+            env["GS_B200_SKIN"] = s
         p = subprocess.run([sys.executable, __file__, "--child", "--config", a.config, "--iters", str(a.iters)],
                            env=env, capture_output=True, text=True)
         line = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else p.stderr[-400:]
