@@ -164,3 +164,35 @@ def test_relative_displacement_trigger_rebuilds_less_and_keeps_the_sums(cuda):
     # a stiff clustered flow: three summation orders agree to the rounding its 8 steps amplify
     assert rel(qr, qs) <= 1e-10 and rel(pr, ps) <= 1e-10
     assert rel(qb, qs) <= 1e-10 and rel(pb, ps) <= 1e-10
+
+
+def test_adaptive_skin_follows_the_rebuild_rate_and_keeps_the_sums(cuda):
+    """The relative-trigger path adapts the list skin to the observed rebuild interval
+    (gs_verlet.cu verlet_skin_adapt): the rebuild schedule departs from the fixed default's (here a
+    rebuild every ~9 RHS: the skin narrows and lists are rebuilt more often, each one shorter), the
+    sums agree with the per-RHS cell sweep to rounding, and every call starts from the default
+    skin (two calls on one context are bitwise equal)."""
+    import paper_1510_03816_b200 as gs
+    from paper_1510_03816_b200 import configs, device
+
+    w = configs.c5(30000)
+    rng = np.random.default_rng(11)
+    p = 0.003 * (w.target - w.q) + 1e-3 * rng.standard_normal(w.q.shape)  # noisy
+    spec = gs.SystemSpec(kernel=gs.KernelSpec(alpha=w.alpha), sigma2=w.sigma2)
+    kw = dict(GS_B200_VERLET_FUSE_MAX_N=0, GS_B200_VERLET_REL=1)
+    qa, pa, (ba, _) = _evolve(gs, spec, w.q, p, 20, **kw)
+    qf, pf, (bf, _) = _evolve(gs, spec, w.q, p, 20, GS_B200_SKIN_ADAPT=0, **kw)
+    qs, ps, _ = _evolve(gs, spec, w.q, p, 20, GS_B200_VERLET=0)
+    assert bf >= 8 and ba > bf, (ba, bf)
+    assert rel(qa, qs) <= 1e-10 and rel(pa, ps) <= 1e-10
+    assert rel(qf, qs) <= 1e-10 and rel(pf, ps) <= 1e-10
+    with _Env(**kw):
+        device.set_path("cell")
+        try:
+            q_d = device.as_device(w.q, __import__("torch"))
+            p_d = device.as_device(p, __import__("torch"))
+            r1 = device.evolve(spec, q_d, p_d, 1.0, 20)
+            r2 = device.evolve(spec, q_d, p_d, 1.0, 20)
+        finally:
+            device.set_path("auto")
+    assert bool((r1[0] == r2[0]).all()) and bool((r1[1] == r2[1]).all())
