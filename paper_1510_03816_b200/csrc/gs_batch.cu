@@ -14,7 +14,7 @@ extern "C" {
 // items run one after another through the general path.
 namespace {
 
-constexpr size_t kSmemBudget = 220 * 1024;  // dynamic shared memory one CTA may claim
+constexpr size_t kSmemBudget = 200 * 1024;  // dynamic shared memory one CTA may claim (227 KB - k_small's static)
 
 int upload_items(gs_context* ctx, const std::vector<SmallItem>& items, cudaStream_t s) {
     GS_CUDA(ctx->b_items.ensure(items.size()));

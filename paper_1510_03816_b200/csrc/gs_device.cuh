@@ -11,11 +11,12 @@
 // The reference evaluates exp twice per pair (kernel_value and kernel_derivative) and a
 // sqrt and a divide (kernels.py:130, 159; particles.py:100).  Here one pair costs one
 // MUFU.RSQ64H + one cubic refinement (r and 1/r), and ONE table-driven exp:
-//   2^(y/64) = T[k & 63] * 2^(k >> 6) * e^(u ln2/64),  k = rint(y), u = y - k in [-1/2, 1/2]
-// with a 64-entry table in shared memory (replicated for conflict-free lookups) and a
-// degree-5 polynomial for e^x - 1 on |x| <= ln2/128 (truncation 3.5e-17).  The exp is
-// ~9 FP64-pipe instructions plus integer work; results agree with libm to a few ulp
-// (tests/test_gpu_parity.py).
+//   2^(y/T) = T[k & (T-1)] * 2^(k / T) * e^(u ln2/T),  k = rint(y), u = y - k in [-1/2, 1/2]
+// with a 2^kTblBits-entry table in shared memory (replicated for conflict-free lookups) and a
+// polynomial for e^x - 1 on |x| <= ln2/2^(kTblBits+1): 64 entries with the degree-5 Taylor
+// polynomial (truncation 3.5e-17), or 128 entries with a degree-4 minimax polynomial (error
+// 7.6e-17, one FP64 instruction less per pair; GS_EXP_TBL_BITS).  The exp is ~8-9 FP64-pipe
+// instructions plus integer work; results agree with libm to a few ulp (tests/test_gpu_parity.py).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -43,7 +44,12 @@ namespace gsb {
 constexpr int kFamConical = 0;
 constexpr int kFamGaussian = 1;
 
-constexpr int kTblBits = 6;
+#ifndef GS_EXP_TBL_BITS   // table entries 2^bits: 6 (degree-5 Taylor) or 7 (degree-4 minimax; A/B: C2 dense solve
+                          // 137.2 -> 134.8 ms, C2 cell solve 11.68 -> 11.37, C4 / C5 list RHS 1.685 / 1.222 -> 1.663 / 1.201)
+#define GS_EXP_TBL_BITS 7
+#endif
+constexpr int kTblBits = GS_EXP_TBL_BITS;
+static_assert(kTblBits == 6 || kTblBits == 7, "exp table: 64 or 128 entries");
 constexpr int kTbl = 1 << kTblBits;
 // The table is stored 16 times interleaved (entry j of copy c at [16 j + c]) and lane l reads
 // copy l & 15: a warp's random lookups hit 16 distinct bank pairs per half-warp, i.e. the
@@ -51,11 +57,22 @@ constexpr int kTbl = 1 << kTblBits;
 constexpr int kTblRep = 16;
 constexpr int kTblWords = kTbl * kTblRep;
 constexpr double kLn2 = 0.69314718055994530941723212145818;
+// e1(u) = e^(u ln2 / kTbl) - 1 = u (C1 + u (C2 + u (C3 + u (C4 [+ u C5])))) on |u| <= 1/2
+#if GS_EXP_TBL_BITS == 6   // Taylor, degree 5
+constexpr int kExpDeg = 5;
 constexpr double kC1 = kLn2 / kTbl;
 constexpr double kC2 = kC1 * kC1 / 2.0;
 constexpr double kC3 = kC1 * kC1 * kC1 / 6.0;
 constexpr double kC4 = kC1 * kC1 * kC1 * kC1 / 24.0;
 constexpr double kC5 = kC1 * kC1 * kC1 * kC1 * kC1 / 120.0;
+#else                      // minimax (Remez in 60-digit arithmetic, tools/exp_minimax.py), degree 4
+constexpr int kExpDeg = 4;
+constexpr double kC1 = 0.005415212348123815;
+constexpr double kC2 = 1.4662262387640288e-05;
+constexpr double kC3 = 2.6466433568944648e-08;
+constexpr double kC4 = 3.583032962059034e-11;
+constexpr double kC5 = 0.0;
+#endif
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr int kKMin = -1020 * kTbl;                 // below: G underflows (flush to 0)
 
@@ -99,7 +116,7 @@ constexpr int kMagicHi = 0x43380000;
 // The integer side is written for the fewest instructions: `tb` is the
 // 32-bit shared-memory byte address of this lane's table copy (lane_table_addr), so a lookup is
 // one AND + one shift-add; the range test is two compares on the words of s; the exponent goes
-// into the table value's high word as ((lo(s) >> 6) << 20) (lo(s) = k + 2^30 and 2^30 / 64 << 20
+// into the table value's high word as ((lo(s) >> kTblBits) << 20) (lo(s) = k + 2^30 and 2^30 / kTbl << 20
 // vanishes mod 2^32).  (Zeroing only the high word on the out-of-range side was tried: for the
 // far padding records u = y - kd is huge and the polynomial overflows to inf, inf * 0 = NaN.)
 constexpr unsigned kLoMin = (1u << 30) + (unsigned)kKMin;  // lo(s) >= kLoMin <=> k >= kKMin
@@ -115,14 +132,15 @@ __device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb)
     // (and + mad), exponent ((lo >> 6) << 20 added to the table value's high word: shr + mad),
     // range test (two chained compares: one predicate)
     unsigned addr, sh;
-    asm("{\n\t.reg .b32 x;\n\tand.b32 x, %1, 63;\n\tmad.lo.u32 %0, x, 128, %2;\n\t}" : "=r"(addr) : "r"(lo), "r"(tb));
-    asm("shr.u32 %0, %1, 6;" : "=r"(sh) : "r"(lo));
+    asm("{\n\t.reg .b32 x;\n\tand.b32 x, %1, %3;\n\tmad.lo.u32 %0, x, 128, %2;\n\t}"
+        : "=r"(addr) : "r"(lo), "r"(tb), "n"(kTbl - 1));
+    asm("shr.u32 %0, %1, %2;" : "=r"(sh) : "r"(lo), "n"(kTblBits));
     double t;
     asm("ld.shared.f64 %0, [%1];" : "=d"(t) : "r"(addr));
     unsigned th;
     asm("mad.lo.u32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(sh), "r"((unsigned)__double2hiint(t)));
-    const double e1 = u * fma(fma(fma(fma(gs_cb[kCbC5], u, gs_cb[kCbC4]), u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u,
-                              gs_cb[kCbC1]);
+    const double p4 = kExpDeg == 5 ? fma(gs_cb[kCbC5], u, gs_cb[kCbC4]) : gs_cb[kCbC4];
+    const double e1 = u * fma(fma(fma(p4, u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u, gs_cb[kCbC1]);
     const double tn = __hiloint2double((int)th, __double2loint(t));
     const double g = fma(tn, e1, tn);
     double r;

@@ -605,7 +605,10 @@ static int launch_small_cluster(int fam, const SmallArgs& a, const double* tbl_d
         case 8: kern = con ? k_small<kFamConical, 8> : k_small<kFamGaussian, 8>; break;
         default: return (int)cudaErrorInvalidValue;
     }
-    if (smem > 48 * 1024) {
+    // static (exp table, slots) + dynamic above the 48 KB default: opt in for the dynamic part
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return (int)cudaErrorInvalidValue;
+    if (smem + fa.sharedSizeBytes > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
     }
