@@ -190,7 +190,12 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
     for (int k = threadIdx.x; k < G * kDB; k += kST) s_acc[k] = zero4;
     table_bulk_wait(&s_tbar);
 
+#ifdef GS_SYM_EMPTY  // A/B probe: prologue + partial writes only (the per-CTA fixed cost)
+    if (pre) tile_wait(&s_rbar, 0);  // no copy in flight into a retiring CTA
+    for (int ib = 0; ib < 0; ++ib) {
+#else
     for (int ib = 0; ib < G; ++ib) {
+#endif
         const long long I = SI * G + ib;
         if (I >= nb) break;
         const int64_t i0 = I * kDB + r0, i1 = I * kDB + r1;
