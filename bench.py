@@ -415,7 +415,11 @@ def main():
 
     extras = {}
     if not a.no_extras:
-        extras = run_extras(a, gs, device, configs, torch, world, rank, dist, solver is not None)
+        try:  # secondary figures must never cost the headline line
+            extras = run_extras(a, gs, device, configs, torch, world, rank, dist, solver is not None)
+        except Exception as exc:  # noqa: BLE001
+            extras = {"error": f"{type(exc).__name__}: {exc}"}
+            print(f"bench: extras failed on rank {rank}: {extras['error']}", file=sys.stderr, flush=True)
     if rank == 0:
         cpu = cpu_baseline_port(w, w.alpha, None if a.no_extras else configs.c1())
         kernel = ("gsb::k_dense_sym (symmetric, 1 GPU) / gsb::k_dense_partial (row shards)" if a.path == "dense"
@@ -564,23 +568,31 @@ def run_extras(a, gs, device, configs, torch, world, rank, dist, sharded_run):
 
     sc = {}
     for name, path, steps in (("C3", "dense", 2), ("C5", "cell", 4)):
-        wk = configs.CONFIGS[name]()
-        sp = gs.SystemSpec(kernel=gs.KernelSpec(alpha=wk.alpha), sigma2=wk.sigma2)
-        pk = wk.p if wk.p is not None else wk.h * (wk.target - wk.q)
-        device.set_path(path)
-        solver = sharded.ShardedSolver(sp)
-        qk, pkd = torch.from_numpy(wk.q).cuda(), torch.from_numpy(np.ascontiguousarray(pk)).cuda()
-        tf = steps * wk.t_final / wk.steps
-        solver.evolve(qk, pkd, tf, steps)
-        dist.barrier()
-        _, ms = _timed(torch, lambda: solver.evolve(qk, pkd, tf, steps), 1)
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sc[name] = {"ms_per_rhs": float(t[0]) / (4 * steps), "path": path, "rk_steps": steps,
-                    "pairs_per_rhs": float(wk.n) ** 2 if path == "dense" else None}
+        try:
+            sc[name] = _scaling_workload(name, path, steps, gs, device, configs, sharded, torch, dist)
+        except Exception as exc:  # noqa: BLE001  (every rank takes the same path: no collective is left waiting)
+            sc[name] = {"error": f"{type(exc).__name__}: {exc}", "path": path}
     device.set_path(a.path)
     out["scaling"] = sc
     return out
+
+
+def _scaling_workload(name, path, steps, gs, device, configs, sharded, torch, dist):
+    """ms per RHS (max over ranks) of a short evolve of a BASELINE scaling workload at this N."""
+    wk = configs.CONFIGS[name]()
+    sp = gs.SystemSpec(kernel=gs.KernelSpec(alpha=wk.alpha), sigma2=wk.sigma2)
+    pk = wk.p if wk.p is not None else wk.h * (wk.target - wk.q)
+    device.set_path(path)
+    solver = sharded.ShardedSolver(sp)
+    qk, pkd = torch.from_numpy(wk.q).cuda(), torch.from_numpy(np.ascontiguousarray(pk)).cuda()
+    tf = steps * wk.t_final / wk.steps
+    solver.evolve(qk, pkd, tf, steps)
+    dist.barrier()
+    _, ms = _timed(torch, lambda: solver.evolve(qk, pkd, tf, steps), 1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"ms_per_rhs": float(t[0]) / (4 * steps), "path": path, "rk_steps": steps,
+            "pairs_per_rhs": float(wk.n) ** 2 if path == "dense" else None}
 
 
 if __name__ == "__main__":
