@@ -237,8 +237,9 @@ def cpu_baseline_port(w, spec_alpha, c1=None):
 
 
 def implemented_fp64_per_pair(path_kind: str):
-    """FP64-pipe instructions per ordered pair of the dominant kernel, counted in the SASS of the
-    library actually loaded (tools/sass_loops.py; cuobjdump ships with the CUDA toolkit)."""
+    """(FP64-pipe instructions per ordered pair of the dominant kernel, the operand-read ceiling of
+    its loop's FP64 instruction mix), both from the SASS of the library actually loaded
+    (tools/sass_loops.py; cuobjdump ships with the CUDA toolkit)."""
     try:
         sys.path.insert(0, os.path.join(REPO, "tools"))
         import sass_loops
@@ -246,10 +247,12 @@ def implemented_fp64_per_pair(path_kind: str):
         from paper_1510_03816_b200 import _native as N
 
         if path_kind == "dense":
-            return sass_loops.fp64_per_pair(N.LIB_PATH, r"k_dense_symILi0E", True)[0]
-        return sass_loops.fp64_per_pair(N.LIB_PATH, r"k_verlet_pairILi0ELi\d+ELb0E", False)[0]
+            w, loop = sass_loops.fp64_per_pair(N.LIB_PATH, r"k_dense_symILi0E", True)
+        else:
+            w, loop = sass_loops.fp64_per_pair(N.LIB_PATH, r"k_verlet_pairILi0ELi\d+ELb0E", False)
+        return w, (sass_loops.operand_read_ceiling(loop) if loop else None)
     except Exception:
-        return None
+        return None, None
 
 
 # ---------------------------------------------------------------------------------------------
@@ -383,7 +386,7 @@ def main():
     # -- roofline of the dominant kernel (the pair kernel), from the profiled pass
     ach_pairs = pairs_per_launch / (pair_ms_avg / 1e3) if pair_ms_avg > 0 else 0.0
     path_kind = "dense" if a.path == "dense" else "cell"
-    w_impl = implemented_fp64_per_pair(path_kind)
+    w_impl, op_ceiling = implemented_fp64_per_pair(path_kind)
     best = None
     for _ in range(3):
         pms, pfl = ctypes.c_double(), ctypes.c_double()
@@ -439,6 +442,10 @@ def main():
                 "basis": "FP64-pipe utilisation: implemented FP64 instructions per ordered pair (counted in the "
                          "loaded library's SASS) x pairs/s x 2 flops, against the FP64 peak measured live",
                 "fp64_slots_per_pair_implemented": w_impl,
+                "operand_read_ceiling": op_ceiling,
+                "operand_read_ceiling_basis": "a DFMA with three fresh 64-bit register operands holds the FP64 pipe's "
+                                              "issue ~3.2 cycles instead of 2 (tools/issue_probe2.cu); share of the pipe "
+                                              "this kernel's SASS mix can reach",
                 "peak_source": "measured live: gs_fp64_peak_probe (DFMA chains on all SMs, best of 3)",
                 "w45": {"work_per_pair": f"{W_ALG} DP-pipe slots = {2 * W_ALG} flop-equivalents (SURVEY.md §8(d) "
                                          "libm formulation)",
