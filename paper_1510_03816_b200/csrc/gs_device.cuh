@@ -70,7 +70,19 @@ constexpr int kExpDeg = 4;
 constexpr double kC1 = 0.005415212348123815;
 constexpr double kC2 = 1.4662262387640288e-05;
 constexpr double kC3 = 2.6466433568944648e-08;
+#ifndef GS_EXP_C4_IMM
+#define GS_EXP_C4_IMM 1
+#endif
+#if GS_EXP_C4_IMM
+// C4 rounded to a double whose low word is zero (0x3DC3B2AC00000000, relative change 2.5e-7: 5.7e-19
+// on e^x): the first Horner step fma(C4, u, C3) then carries C4 as a 32-bit immediate and C3 in one
+// register — two fresh 64-bit register operands.  With both constants in registers (what ptxas makes
+// of two constant-bank operands in one instruction) the DFMA reads three and holds the FP64 pipe's
+// issue ~3.2 cycles instead of 2 (tools/issue_probe2.cu).
+constexpr double kC4 = 3.583033869603014e-11;
+#else
 constexpr double kC4 = 3.583032962059034e-11;
+#endif
 constexpr double kC5 = 0.0;
 #endif
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
@@ -139,7 +151,11 @@ __device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb)
     asm("ld.shared.f64 %0, [%1];" : "=d"(t) : "r"(addr));
     unsigned th;
     asm("mad.lo.u32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(sh), "r"((unsigned)__double2hiint(t)));
+#if GS_EXP_C4_IMM && GS_EXP_TBL_BITS != 6
+    const double p4 = kC4;  // a literal: the immediate form
+#else
     const double p4 = kExpDeg == 5 ? fma(gs_cb[kCbC5], u, gs_cb[kCbC4]) : gs_cb[kCbC4];
+#endif
     const double e1 = u * fma(fma(fma(p4, u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u, gs_cb[kCbC1]);
     const double tn = __hiloint2double((int)th, __double2loint(t));
     const double g = fma(tn, e1, tn);

@@ -60,6 +60,9 @@ constexpr int kTplB = 32;    // list-build lanes per cluster: one warp (warp-uni
 #define GS_VERLET_DEPTH 128   // A/B (C2 100-step solve, ms): lanes 4 -> 13.6, 8 -> 14.1, 16 -> 14.3, 2 -> 16.1
 #endif
 constexpr int kVM = GS_VERLET_M;
+#ifndef GS_VERLET_UNIFORM
+#define GS_VERLET_UNIFORM 1
+#endif
 
 struct Acc {
     double qx, qy, px, py;
@@ -192,8 +195,19 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     int2 jc = ldl(e + 2 * step);
     double4 c0, c1;
     table_bulk_wait(&s_tbar);
+#if GS_VERLET_UNIFORM
+    // warp-uniform trip count (the longest list of the warp's clusters; a warp runs that long
+    // anyway): lanes past their own list sweep the sentinel (exact zeros), and the loop's branches
+    // and loop-invariant FP64 operands become uniform (constants stay out of the vector registers:
+    // a DFMA with three vector-register operands costs ~3.2 instead of 2 pipe cycles)
+    const int trips = __reduce_max_sync(kFull, (int)((end - beg) / step));
+    for (int t = 0; t < trips; t += 3) {
+#else
+    const int trips = 0;
     while (true) {
+        const int t = -3;
         if (e >= end) break;
+#endif
         asm volatile("prefetch.global.L2 [%0];" ::"l"(list + e + GS_VERLET_PF * step));
         GS_ASSERT(jc.x >= 0 && jc.x <= n && jc.y >= 0 && jc.y <= n);
         c0 = Ss[jc.x]; c1 = Ss[jc.y];
@@ -204,7 +218,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
             vbody<FAM, COUNT>(me[m], a1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
         }
         e += step;
-        if (e >= end) break;
+        if (GS_VERLET_UNIFORM ? t + 1 >= trips : e >= end) break;
         a0 = Ss[jc.x]; a1 = Ss[jc.y];
         jc = ldl(e + 3 * step);
 #pragma unroll
@@ -213,7 +227,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
             vbody<FAM, COUNT>(me[m], b1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
         }
         e += step;
-        if (e >= end) break;
+        if (GS_VERLET_UNIFORM ? t + 2 >= trips : e >= end) break;
         b0 = Ss[jc.x]; b1 = Ss[jc.y];
         jc = ldl(e + 3 * step);
 #pragma unroll

@@ -59,7 +59,7 @@ def _fp64_reads(body) -> dict:
         if not m or m.group(1).split(".")[0] not in ("DFMA", "DMUL", "DADD"):
             continue
         srcs = [a.strip().lstrip("-|").rstrip("|") for a in m.group(2).split(",")][1:]
-        n = sum(1 for a in srcs if re.match(r"R\d+", a) and ".reuse" not in a)
+        n = len({a for a in srcs if re.match(r"R\d+", a) and ".reuse" not in a})  # distinct registers
         hist[n] = hist.get(n, 0) + 1
     return hist
 
