@@ -135,7 +135,8 @@ constexpr unsigned kLoMin = (1u << 30) + (unsigned)kKMin;  // lo(s) >= kLoMin <=
 // The argument is y = x k, never rounded on its own: the exact product enters the magic-constant
 // rounding and the reduced argument u = x k - rint(x k) through fused multiply-adds (what nvcc's
 // contraction made of the y + M / y - kd form anyway; written out so the rounding is explicit).
-__device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb) {
+template <bool SELECT>
+__device__ __forceinline__ double exp2_tbl_core(double x, double k, unsigned tb) {
     const double s = fma(x, k, gs_cb[kCbMagicK]);
     const double kd = s - gs_cb[kCbMagicK];
     const double u = fma(x, k, -kd);
@@ -159,11 +160,40 @@ __device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb)
     const double e1 = u * fma(fma(fma(p4, u, gs_cb[kCbC3]), u, gs_cb[kCbC2]), u, gs_cb[kCbC1]);
     const double tn = __hiloint2double((int)th, __double2loint(t));
     const double g = fma(tn, e1, tn);
+    if (!SELECT) return g;  // the caller keeps x k inside [kKMin + kTbl, 0] (pair_clamp_hi)
     double r;
     asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %1, %2;\n\tsetp.eq.and.u32 p, %3, %4, p;\n\t"
         "selp.f64 %0, %5, 0d0000000000000000, p;\n\t}"
         : "=d"(r) : "r"(lo), "n"(kLoMin), "r"(hi), "n"(kMagicHi), "d"(g));
     return r;
+}
+
+__device__ __forceinline__ double exp2_tbl_fast(double x, double k, unsigned tb) {
+    return exp2_tbl_core<true>(x, k, tb);
+}
+
+// Range handling of the hot pair loops without the select (GS_PAIR_CLAMP): instead of testing the
+// rounded exponent argument after the fact (two compares + a 64-bit select = 4 instructions per
+// pair), d^2 is clamped from above by ONE integer min on its high word before the rsqrt, at the
+// d^2 where G = 2^-1019: every farther pair then evaluates G ~ 2^-1019 (x its momentum: < 1e-300
+// absolute, where the reference holds subnormals or 0) instead of exactly 0, the argument stays
+// inside the table exp's range, and the far padding records (p = 0) still contribute exact zeros.
+// The clamp replaces the high word only: the clamped value lies within 2^-20 below the cap.
+// Valid wherever the lean core itself is (d = 0 pairs need cap >> 1e-200: alpha > ~1e-103).
+// A/B (session 6): the list sweep gains (44.5 -> 42.5 instructions per pair, C4 / C5 list RHS 1.594 /
+// 1.159 -> 1.584 / 1.151 ms, bitwise unchanged: only the sentinel is ever clamped there); the
+// symmetric dense kernel loses (47.4 -> 45.4 instructions per pair but 160 -> 168 registers and a
+// worse schedule: C2 solve 134.7 -> 137.4 ms), so it keeps the select (GS_PAIR_CLAMP_SYM=0).
+#ifndef GS_PAIR_CLAMP
+#define GS_PAIR_CLAMP 1
+#endif
+#ifndef GS_PAIR_CLAMP_SYM
+#define GS_PAIR_CLAMP_SYM 0
+#endif
+__device__ __forceinline__ int pair_clamp_hi(int fam, double k1) {
+    const double lim = (1019.0 * kTbl) / fabs(k1);  // d (conical) or d^2 (gaussian) with G = 2^-1019
+    const double cap = fam == kFamConical ? lim * lim : lim;
+    return min(max(__double2hiint(cap) - 1, 0x00100000), 0x7fefffff);
 }
 static_assert(kTblRep * 8 == 128, "lane copies interleave in 128-byte rows (exp2_tbl_fast)");
 
@@ -237,10 +267,22 @@ __device__ __forceinline__ void pair_core(double dx, double dy, double pdot, con
 // integer op per pair); a minimum <= hi(1e-200) means a pair with d^2 within 2^-20 of the offset
 // (d < ~1e-103, in practice d == 0) and triggers the exact re-scan.
 template <int FAM>
-__device__ __forceinline__ void pair_core_hi(double dx, double dy, double pdot, unsigned tb, double k1, double& g,
-                                             double& c, int& r2hi) {
-    const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
+__device__ __forceinline__ void pair_core_hi(double dx, double dy, double pdot, unsigned tb, double k1, int caphi,
+                                             double& g, double& c, int& r2hi) {
+    double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
     r2hi = __double2hiint(r2);
+#if GS_PAIR_CLAMP_SYM
+    r2 = __hiloint2double(min(r2hi, caphi), __double2loint(r2));
+    if (FAM == kFamConical) {
+        const double rs = rsqrt_refined(r2);
+        g = exp2_tbl_core<false>(r2 * rs, k1, tb);
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl_core<false>(r2, k1, tb);
+        c = pdot * g;
+    }
+    return;
+#endif
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
         g = exp2_tbl_fast(r2 * rs, k1, tb);

@@ -80,13 +80,13 @@ __device__ __forceinline__ void one_sided(const double4& me, const double4& s, c
 
 template <int FAM>
 __device__ __forceinline__ void two_sided(const double4& me, const double4& s, const double* tbl, unsigned tb,
-                                          double k1, Acc& a, Acc& j, int& nz) {
+                                          double k1, int caphi, Acc& a, Acc& j, int& nz) {
     const double dx = me.x - s.x, dy = me.y - s.y;
     const double pdot = fma(me.z, s.z, me.w * s.w);
     double g, c;
 #if GS_SYM_ZMIN
     int h;
-    pair_core_hi<FAM>(dx, dy, pdot, tb, k1, g, c, h);
+    pair_core_hi<FAM>(dx, dy, pdot, tb, k1, caphi, g, c, h);
     nz = min(nz, h);  // nz: the minimum high word of d^2 (see pair_core_hi)
 #else
     int z;
@@ -165,6 +165,7 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
     block_wait(wait);  // multi-GPU peer exchange: every rank's records of the previous stage are in S
     const double* tbl = lane_table(s_tbl);
     const unsigned tb = lane_table_addr(s_tbl);
+    const int caphi = pair_clamp_hi(FAM, k1);
 
     // CTA -> superblock pair (SI, SJ), SI <= SJ, row-major over the upper triangle
     const long long t = cta0 + blockIdx.x;
@@ -249,10 +250,10 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
                 for (int step = 0; step < 32; step += 2) {
                     const double4 sa = rot[step];
                     const double4 sb = rot[step + 1];
-                    two_sided<FAM>(me0, sa, tbl, tb, k1, a0, j, nz0);
-                    two_sided<FAM>(me1, sa, tbl, tb, k1, a1, j, nz1);
-                    two_sided<FAM>(me0, sb, tbl, tb, k1, a0, jb2, nz0);
-                    two_sided<FAM>(me1, sb, tbl, tb, k1, a1, jb2, nz1);
+                    two_sided<FAM>(me0, sa, tbl, tb, k1, caphi, a0, j, nz0);
+                    two_sided<FAM>(me1, sa, tbl, tb, k1, caphi, a1, j, nz1);
+                    two_sided<FAM>(me0, sb, tbl, tb, k1, caphi, a0, jb2, nz0);
+                    two_sided<FAM>(me1, sb, tbl, tb, k1, caphi, a1, jb2, nz1);
                     const int src = (lane + 2) & 31;
                     j.qx = __shfl_sync(kFull, j.qx, src);
                     j.qy = __shfl_sync(kFull, j.qy, src);
@@ -274,8 +275,8 @@ __global__ void GS_SYM_BOUNDS k_dense_sym(const double4* __restrict__ S, int64_t
 #pragma unroll 4
                 for (int step = 0; step < 32; ++step) {
                     const double4 s = rot[step];
-                    two_sided<FAM>(me0, s, tbl, tb, k1, a0, j, nz0);
-                    two_sided<FAM>(me1, s, tbl, tb, k1, a1, j, nz1);
+                    two_sided<FAM>(me0, s, tbl, tb, k1, caphi, a0, j, nz0);
+                    two_sided<FAM>(me1, s, tbl, tb, k1, caphi, a1, j, nz1);
                     const int src = (lane + 1) & 31;
                     j.qx = __shfl_sync(kFull, j.qx, src);
                     j.qy = __shfl_sync(kFull, j.qy, src);

@@ -89,19 +89,38 @@ __device__ __forceinline__ double vexp(double x, double k, unsigned tb, bool in)
 
 template <int FAM, bool COUNT>
 __device__ __forceinline__ void vbody(const double4& me, const double4& s, const double* __restrict__ tbl, unsigned tb,
-                                      double k1, long long rc2b, Acc& a, int& nz, int& nin) {
+                                      double k1, int caphi, long long rc2b, Acc& a, int& nz, int& nin) {
     const double dx = me.x - s.x, dy = me.y - s.y;
     const double pdot = fma(me.z, s.z, me.w * s.w);
-    const double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
+    double r2 = fma(dx, dx, fma(dy, dy, gs_cb[kCbTinyR2]));
     const long long r2b = __double_as_longlong(r2);
 #if GS_VERLET_NOMASK  // A/B: sum every list pair (skin pairs add their sub-2^-53 terms)
     const bool in = COUNT ? r2b < rc2b : true;
 #else
     const bool in = r2b < rc2b;
 #endif
+#if GS_PAIR_CLAMP && GS_VERLET_NOMASK
+    // list pairs lie within rl of their target; only the sentinel (far, p = 0) is out of the table
+    // exp's range: the clamp of d^2 (pair_clamp_hi) replaces the exp's range select.  The d == 0
+    // count reads the clamped high word (the cap lies far above 1e-200), so d^2 is clamped in place.
+    const int r2h = min(__double2hiint(r2), caphi);
+    r2 = __hiloint2double(r2h, __double2loint(r2));
+    nz += r2h == __double2hiint(kTinyR2);
+#else
     nz += __double2hiint(r2) == __double2hiint(kTinyR2);
+#endif
     if (COUNT) nin += in;
     double g, c;
+#if GS_PAIR_CLAMP && GS_VERLET_NOMASK
+    if (FAM == kFamConical) {
+        const double rs = rsqrt_refined(r2);
+        g = exp2_tbl_core<false>(r2 * rs, k1, tb);
+        c = (pdot * g) * rs;
+    } else {
+        g = exp2_tbl_core<false>(r2, k1, tb);
+        c = pdot * g;
+    }
+#else
     if (FAM == kFamConical) {
         const double rs = rsqrt_refined(r2);
         g = vexp<FAM>(r2 * rs, k1, tb, in);
@@ -110,6 +129,7 @@ __device__ __forceinline__ void vbody(const double4& me, const double4& s, const
         g = vexp<FAM>(r2, k1, tb, in);
         c = pdot * g;
     }
+#endif
     a.qx = fma(g, s.z, a.qx);
     a.qy = fma(g, s.w, a.qy);
     a.px = fma(c, dx, a.px);
@@ -152,6 +172,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     __syncthreads();
     const double* tbl = lane_table(s_tbl);
     const unsigned tb = lane_table_addr(s_tbl);
+    const int caphi = pair_clamp_hi(FAM, k1);
 
     const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
     const int64_t c = cl0 + (int64_t)blockIdx.x * (kVB / TPL) + threadIdx.x / TPL;
@@ -214,8 +235,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         jc = ldl(e + 3 * step);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            vbody<FAM, COUNT>(me[m], a0, tbl, tb, k1, rc2b, a[m], nz[m], nin);
-            vbody<FAM, COUNT>(me[m], a1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], a0, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], a1, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
         }
         e += step;
         if (GS_VERLET_UNIFORM ? t + 1 >= trips : e >= end) break;
@@ -223,8 +244,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         jc = ldl(e + 3 * step);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            vbody<FAM, COUNT>(me[m], b0, tbl, tb, k1, rc2b, a[m], nz[m], nin);
-            vbody<FAM, COUNT>(me[m], b1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], b0, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], b1, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
         }
         e += step;
         if (GS_VERLET_UNIFORM ? t + 2 >= trips : e >= end) break;
@@ -232,8 +253,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         jc = ldl(e + 3 * step);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
-            vbody<FAM, COUNT>(me[m], c0, tbl, tb, k1, rc2b, a[m], nz[m], nin);
-            vbody<FAM, COUNT>(me[m], c1, tbl, tb, k1, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], c0, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
+            vbody<FAM, COUNT>(me[m], c1, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
         }
         e += step;
     }
