@@ -63,6 +63,9 @@ constexpr int kVM = GS_VERLET_M;
 #ifndef GS_VERLET_UNIFORM
 #define GS_VERLET_UNIFORM 1
 #endif
+#ifndef GS_VERLET_BALANCE
+#define GS_VERLET_BALANCE 1
+#endif
 
 struct Acc {
     double qx, qy, px, py;
@@ -175,7 +178,33 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     const int caphi = pair_clamp_hi(FAM, k1);
 
     const int sub = (TPL > 1) ? (int)(threadIdx.x % TPL) : 0;
+#if GS_VERLET_BALANCE
+    // A warp runs to the longest list among its 32 / TPL clusters (28 of 32 lanes busy on C5).  The
+    // CTA's kVB / TPL consecutive clusters are dealt to the lane groups in order of list length
+    // (ties by index), so a warp's clusters have nearly equal lists; each cluster keeps its lanes'
+    // split and summation order — the results are bitwise those of the natural assignment — and
+    // the CTA still works on one contiguous run of the sorted order (source records shared in L1).
+    constexpr int kSlots = kVB / TPL;
+    __shared__ int s_len[kSlots];
+    __shared__ unsigned char s_slot[kSlots];
+    const int slot0 = threadIdx.x / TPL;
+    const int64_t cbase = cl0 + (int64_t)blockIdx.x * kSlots;
+    if (sub == 0) s_len[slot0] = (cbase + slot0 < cl1) ? len[cbase + slot0] : -1;
+    __syncthreads();
+    if (sub == 0) {
+        const int mine = s_len[slot0];
+        int rank = 0;
+        for (int k = 0; k < kSlots; ++k) {
+            const int o = s_len[k];
+            rank += (o > mine) || (o == mine && k < slot0);
+        }
+        s_slot[rank] = (unsigned char)slot0;
+    }
+    __syncthreads();
+    const int64_t c = cbase + s_slot[slot0];
+#else
     const int64_t c = cl0 + (int64_t)blockIdx.x * (kVB / TPL) + threadIdx.x / TPL;
+#endif
     const bool valid = c < cl1;
     // members: sorted positions first .. first + cnt - 1 (slab: clusters restart at every cell row,
     // cfirst[c]; otherwise c * M)
