@@ -66,6 +66,9 @@ constexpr int kVM = GS_VERLET_M;
 #ifndef GS_VERLET_BALANCE
 #define GS_VERLET_BALANCE 1
 #endif
+#ifndef GS_VERLET_LIST2
+#define GS_VERLET_LIST2 1
+#endif
 
 struct Acc {
     double qx, qy, px, py;
@@ -186,10 +189,15 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     // the CTA still works on one contiguous run of the sorted order (source records shared in L1).
     constexpr int kSlots = kVB / TPL;
     __shared__ int s_len[kSlots];
+    __shared__ long long s_ofs[kSlots];  // loaded beside the lengths: one global round trip less before the first list entry
     __shared__ unsigned char s_slot[kSlots];
     const int slot0 = threadIdx.x / TPL;
     const int64_t cbase = cl0 + (int64_t)blockIdx.x * kSlots;
-    if (sub == 0) s_len[slot0] = (cbase + slot0 < cl1) ? len[cbase + slot0] : -1;
+    if (sub == 0) {
+        const bool in = cbase + slot0 < cl1;
+        s_len[slot0] = in ? len[cbase + slot0] : -1;
+        s_ofs[slot0] = in ? ofs[cbase + slot0] : 0;
+    }
     __syncthreads();
     if (sub == 0) {
         const int mine = s_len[slot0];
@@ -201,7 +209,8 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         s_slot[rank] = (unsigned char)slot0;
     }
     __syncthreads();
-    const int64_t c = cbase + s_slot[slot0];
+    const int myslot = s_slot[slot0];
+    const int64_t c = cbase + myslot;
 #else
     const int64_t c = cl0 + (int64_t)blockIdx.x * (kVB / TPL) + threadIdx.x / TPL;
 #endif
@@ -227,7 +236,11 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         nz[m] = 0;
     }
     int nin = 0;
+#if GS_VERLET_BALANCE
+    const long long beg = valid ? s_ofs[myslot] : 0, end = valid ? beg + s_len[myslot] : 0;
+#else
     const long long beg = valid ? ofs[c] : 0, end = valid ? beg + len[c] : 0;
+#endif
     // software pipeline: source records two trips ahead (unrolled by three, so the prefetched
     // records rotate through three register sets without moves), list entries three trips ahead,
     // and an L2 prefetch of the list GS_VERLET_PF trips ahead.  Past the end the sentinel n is
@@ -243,6 +256,15 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
     j = ldl(e + step);
     double4 b0 = Ss[j.x], b1 = Ss[j.y];
     int2 jc = ldl(e + 2 * step);
+#if GS_VERLET_LIST2
+    // a second list entry in flight: an entry is loaded two trips before it addresses its records
+    // (with one, the address computation waited on the entry loaded one trip earlier: long
+    // scoreboard on 10 % of the sweep's stall samples)
+    int2 jd = ldl(e + 3 * step);
+#define GS_V_NEXT(k) jc = jd; jd = ldl(e + ((k) + 1) * step)
+#else
+#define GS_V_NEXT(k) jc = ldl(e + (k) * step)
+#endif
     double4 c0, c1;
     table_bulk_wait(&s_tbar);
 #if GS_VERLET_UNIFORM
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(list + e + GS_VERLET_PF * step));
         GS_ASSERT(jc.x >= 0 && jc.x <= n && jc.y >= 0 && jc.y <= n);
         c0 = Ss[jc.x]; c1 = Ss[jc.y];
-        jc = ldl(e + 3 * step);
+        GS_V_NEXT(3);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
             vbody<FAM, COUNT>(me[m], a0, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
@@ -270,7 +292,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         e += step;
         if (GS_VERLET_UNIFORM ? t + 1 >= trips : e >= end) break;
         a0 = Ss[jc.x]; a1 = Ss[jc.y];
-        jc = ldl(e + 3 * step);
+        GS_V_NEXT(3);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
             vbody<FAM, COUNT>(me[m], b0, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
@@ -279,7 +301,7 @@ __global__ void __launch_bounds__(kVB, GS_VERLET_MINB)
         e += step;
         if (GS_VERLET_UNIFORM ? t + 2 >= trips : e >= end) break;
         b0 = Ss[jc.x]; b1 = Ss[jc.y];
-        jc = ldl(e + 3 * step);
+        GS_V_NEXT(3);
 #pragma unroll
         for (int m = 0; m < kVM; ++m) {
             vbody<FAM, COUNT>(me[m], c0, tbl, tb, k1, caphi, rc2b, a[m], nz[m], nin);
