@@ -44,7 +44,9 @@ constexpr int kST = 64;  // threads per CTA
 #define GS_SYM_MINB 6  // A/B on C2 (one source per step): 6 -> 0.374 ms, 8 -> 0.377, 10 -> 0.391, 12 -> 0.401
 #endif
 #ifndef GS_SYM_SB        // superblock count above which blocks are grouped (A/B builds)
-#define GS_SYM_SB 128  // A/B on C2 (ms per 100-step solve): 128 -> 152.8, 64 -> 165.4, 32 -> 178.7
+#define GS_SYM_SB 256  // A/B on C2 (ms per 100-step solve): 128 -> 152.8, 64 -> 165.4, 32 -> 178.7; on C3 (N = 131072,
+                       // ms per RHS, 16 KB exp table): 128 (G = 8: 57 KB of shared memory, 3 CTAs/SM) -> 23.44,
+                       // 256 (G = 4, 5 CTAs/SM; 1 GB of partials, 0.17 ms of k_finish) -> 20.90
 #endif
 #ifndef GS_SYM_UNROLL     // unroll of the two-source rotation loop (16 trips)
 #define GS_SYM_UNROLL 4  // A/B on C2 (ms per 100-step solve, bulk-copy prologue, 152-160 regs): 1 -> 138.1,
