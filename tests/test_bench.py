@@ -51,3 +51,22 @@ def test_reference_arm_pool_is_the_reference_rhs():
     dp = np.concatenate([got[b][1] for b in sorted(got)])
     wq, wp = restate.rhs(k, 0.0, w.q, w.p)
     assert np.array_equal(dq, wq) and np.allclose(dp, wp, rtol=0, atol=1e-15 * np.abs(wp).max())
+
+
+def test_roofline_counts_come_from_the_built_library():
+    """bench.py's FP64 instructions per ordered pair and operand-read ceiling are read from the SASS
+    of the library actually built (tools/sass_loops.py, cuobjdump; no GPU needed)."""
+    import shutil
+
+    import pytest
+
+    if not (shutil.which("cuobjdump") or os.path.exists("/usr/local/cuda/bin/cuobjdump")):
+        pytest.skip("cuobjdump not installed")
+    sys.path.insert(0, REPO)
+    import bench
+
+    for kind, lo, hi in (("dense", 12.0, 20.0), ("cell", 20.0, 32.0)):
+        w, ceiling = bench.implemented_fp64_per_pair(kind)
+        assert w is not None and lo <= w <= hi, (kind, w)
+        # a mix of 2-cycle and ~3.2-cycle FP64 instructions: between 2 / 3.2 and 1
+        assert ceiling is not None and 0.625 <= ceiling <= 1.0, (kind, ceiling)
